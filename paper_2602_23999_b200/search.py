@@ -1,0 +1,232 @@
+"""Batched search on the GPU: rotation, coarse probe, query prep and the fused scan.
+
+Mirrors ``ivfrabitq.search`` (reference search.py).  ``search_batch``
+(search.py:390-454) is four launches of libivrq_b200.so on the current stream:
+
+1. ``ivrq_rotate_queries``       q_rot = q @ R^T, float64           (search.py:422)
+2. ``ivrq_select_clusters_ordered`` exact n_probe nearest centroids,
+   handed to the scan in ascending cluster id                      (search.py:226-244, 429)
+3. ``ivrq_prepare_queries``      QueryState: planes / LUTs, sums    (search.py:186-214)
+4. ``ivrq_search_scan``          per query, lists in ascending id: stage-1
+   estimate + lower bound, prune against the running threshold, ex-code
+   refinement of survivors, top-k merge, threshold update           (search.py:326-387, 425-448)
+
+Results are identical for every ``workers`` value (the argument is accepted
+for API compatibility; GPU parallelism does not change the per-query
+threshold trajectory).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from paper_2602_23999_b200 import _device as dev
+from paper_2602_23999_b200 import _lib
+from paper_2602_23999_b200.clustering import Centroids, row_sqnorms
+from paper_2602_23999_b200.index import IvfRabitqIndex, default_workers
+
+__all__ = [
+    "SearchParams",
+    "select_clusters",
+    "search_batch",
+    "search_device",
+    "schedule_probes",
+    "merge_topk",
+]
+
+
+@dataclass(frozen=True)
+class SearchParams:
+    """Per-search knobs (search.py:56-81)."""
+
+    k: int
+    n_probe: int
+    ip_mode: str = "lut"
+    query_bits: int = 4
+    refine: bool = True
+    prune: bool = True
+
+    def __post_init__(self) -> None:
+        if self.k < 1:
+            raise ValueError(f"k must be >= 1, got {self.k}")
+        if self.n_probe < 1:
+            raise ValueError(f"n_probe must be >= 1, got {self.n_probe}")
+        if self.ip_mode not in ("lut", "bitwise"):
+            raise ValueError(f"ip_mode must be 'lut' or 'bitwise', got {self.ip_mode!r}")
+        if not 2 <= self.query_bits <= 8:
+            raise ValueError(f"query_bits must be in [2, 8], got {self.query_bits}")
+
+    def to_c(self) -> _lib.SearchParamsC:
+        return _lib.SearchParamsC(
+            k=self.k,
+            n_probe=self.n_probe,
+            ip_mode=_lib.IVRQ_IP_BITWISE if self.ip_mode == "bitwise" else _lib.IVRQ_IP_LUT,
+            query_bits=self.query_bits,
+            refine=1 if self.refine else 0,
+            prune=1 if self.prune else 0,
+        )
+
+
+def schedule_probes(pairs):
+    """Stable sort of (query, cluster, ...) pairs by (cluster, query) (search.py:247-253)."""
+    return sorted(pairs, key=lambda p: (p[1], p[0]))
+
+
+def merge_topk(lists, k: int):
+    """K smallest (dist, id) of the concatenated candidate lists (search.py:378-387).
+
+    Host helper for API compatibility; the GPU scan merges in shared memory.
+    """
+    if not lists:
+        return np.empty(0, dtype=np.int64), np.empty(0, dtype=np.float64)
+    ids = np.concatenate([np.asarray(i, dtype=np.int64) for i, _ in lists])
+    dists = np.concatenate([np.asarray(d, dtype=np.float64) for _, d in lists])
+    order = np.lexsort((ids, dists))[:k]
+    return ids[order], dists[order]
+
+
+def _probe_device(q_rot: torch.Tensor, cent: torch.Tensor, c_sq: torch.Tensor, n_probe: int, order_by_id: bool):
+    nq, d = q_rot.shape
+    nlist = cent.shape[0]
+    ids = torch.empty((nq, n_probe), dtype=torch.int64, device=q_rot.device)
+    d2 = torch.empty((nq, n_probe), dtype=torch.float64, device=q_rot.device)
+    lib = _lib.load()
+    ws_bytes = int(lib.ivrq_select_clusters_workspace(nq, nlist))
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=q_rot.device)
+    _lib.call(
+        "ivrq_select_clusters_ordered",
+        dev.ptr(q_rot), nq, d, dev.ptr(cent), dev.ptr(c_sq), nlist, n_probe, 1 if order_by_id else 0,
+        dev.ptr(ids), dev.ptr(d2), dev.ptr(ws), ws_bytes, dev.stream_ptr(),
+    )
+    return ids, d2
+
+
+def select_clusters(q_rot: np.ndarray, centroids: Centroids, n_probe: int) -> tuple[np.ndarray, np.ndarray]:
+    """Exact n_probe nearest centroids, ascending (distance, id) (search.py:226-244)."""
+    q = np.atleast_2d(np.asarray(q_rot, dtype=np.float64))
+    if n_probe > centroids.n_clusters:
+        raise ValueError(f"n_probe={n_probe} exceeds {centroids.n_clusters} clusters")
+    vals = np.asarray(centroids.values)
+    v32 = vals.astype(np.float32)
+    if vals.dtype != np.float32 and not np.array_equal(v32.astype(vals.dtype), vals):
+        raise ValueError("select_clusters on the GPU takes float32-representable centroids")
+    qd = dev.to_device(q)
+    cd = dev.to_device(v32)
+    csq = dev.to_device(np.asarray(centroids.squared_norms, dtype=np.float64))
+    ids, d2 = _probe_device(qd, cd, csq, n_probe, order_by_id=False)
+    return dev.to_host(ids), dev.to_host(d2)
+
+
+@dataclass
+class DeviceResult:
+    """Device-resident output of one search batch."""
+
+    ids: torch.Tensor  # (nq, k) int64, -1 padded
+    dists: torch.Tensor  # (nq, k) float64, +inf padded
+    counts: torch.Tensor  # (nq,) int32
+    stats: torch.Tensor | None  # (nq, 2) int64: vectors probed, stage-1 survivors
+
+
+def rotate_queries_device(q: torch.Tensor, index: IvfRabitqIndex) -> torch.Tensor:
+    nq, d = q.shape
+    q_rot = torch.empty((nq, d), dtype=torch.float64, device=q.device)
+    if nq:
+        _lib.call(
+            "ivrq_rotate_queries",
+            dev.ptr(q), 1 if q.dtype == torch.float64 else 0, nq, d, dev.ptr(index.device["rotation"]),
+            dev.ptr(q_rot), dev.stream_ptr(),
+        )
+    return q_rot
+
+
+def prepare_queries_device(q_rot: torch.Tensor, index: IvfRabitqIndex, params: SearchParams):
+    """QueryState scalars + planes/LUTs for every query (device tensors)."""
+    nq, d = q_rot.shape
+    g = (d + 31) // 32
+    scalars = torch.empty((nq, _lib.QS_COUNT), dtype=torch.float64, device=q_rot.device)
+    planes = luts = None
+    if params.ip_mode == "bitwise":
+        planes = torch.empty((nq, params.query_bits, g), dtype=torch.int32, device=q_rot.device)
+    else:
+        luts = torch.empty((nq, 8 * g, 16), dtype=torch.float32, device=q_rot.device)
+    cp = params.to_c()
+    _lib.call(
+        "ivrq_prepare_queries",
+        dev.ptr(q_rot), nq, d, cp, index.bits, float(index.eps_bound),
+        dev.ptr(scalars), dev.ptr(planes), dev.ptr(luts), dev.stream_ptr(),
+    )
+    return scalars, planes, luts
+
+
+def search_device(
+    q: torch.Tensor,
+    index: IvfRabitqIndex,
+    params: SearchParams,
+    *,
+    q_rot: torch.Tensor | None = None,
+    with_stats: bool = False,
+) -> DeviceResult:
+    """The whole search on device tensors (queries already in HBM).
+
+    ``q_rot`` (tests only) injects precomputed rotated queries, the
+    reference's own, to compare everything downstream bit-exactly.
+    """
+    nq = q.shape[0] if q_rot is None else q_rot.shape[0]
+    if q_rot is None:
+        q_rot = rotate_queries_device(q, index)
+    t = index.device
+    probe_ids, probe_d2 = _probe_device(q_rot, t["centroids"], t["centroid_sqnorms"], params.n_probe, True)
+    scalars, planes, luts = prepare_queries_device(q_rot, index, params)
+    k = params.k
+    out_ids = torch.empty((nq, k), dtype=torch.int64, device=q_rot.device)
+    out_d = torch.empty((nq, k), dtype=torch.float64, device=q_rot.device)
+    counts = torch.empty(nq, dtype=torch.int32, device=q_rot.device)
+    stats = torch.empty((nq, 2), dtype=torch.int64, device=q_rot.device) if with_stats else None
+    cp = params.to_c()
+    _lib.call(
+        "ivrq_search_scan",
+        index.view(), dev.ptr(q_rot), dev.ptr(probe_ids), dev.ptr(probe_d2), dev.ptr(scalars), dev.ptr(planes),
+        dev.ptr(luts), nq, cp, dev.ptr(out_ids), dev.ptr(out_d), dev.ptr(counts), dev.ptr(stats), dev.stream_ptr(),
+    )
+    return DeviceResult(ids=out_ids, dists=out_d, counts=counts, stats=stats)
+
+
+def results_to_lists(res: DeviceResult) -> list[tuple[np.ndarray, np.ndarray]]:
+    ids = dev.to_host(res.ids)
+    dists = dev.to_host(res.dists)
+    counts = dev.to_host(res.counts)
+    return [(ids[i, : counts[i]].copy(), dists[i, : counts[i]].copy()) for i in range(ids.shape[0])]
+
+
+def _validate(q: np.ndarray, index: IvfRabitqIndex, params: SearchParams) -> None:
+    if q.shape[1] != index.dims:
+        raise ValueError(f"query dims {q.shape[1]} != index dims {index.dims}")
+    if params.n_probe > index.n_clusters:
+        raise ValueError(f"n_probe={params.n_probe} exceeds {index.n_clusters} clusters")
+
+
+def search_batch(
+    queries: np.ndarray,
+    index: IvfRabitqIndex,
+    params: SearchParams,
+    workers: int | None = None,
+) -> list[tuple[np.ndarray, np.ndarray]]:
+    """Approximate K nearest neighbours per query row (search.py:390-454).
+
+    Returns one ``(ids int64, dists float64)`` pair per query, ascending by
+    (distance, id), with fewer than K entries when the probed lists hold fewer.
+    """
+    q = np.atleast_2d(np.asarray(queries))
+    if q.dtype not in (np.float32, np.float64):
+        q = q.astype(np.float64)
+    q = np.ascontiguousarray(q)
+    _validate(q, index, params)
+    if workers is None:
+        default_workers()
+    if q.shape[0] == 0:
+        return []
+    qd = dev.to_device(q)
+    return results_to_lists(search_device(qd, index, params))

@@ -1,0 +1,250 @@
+"""GPU parity: every CUDA stage against the reference's golden vectors and the oracle.
+
+Bar (BASELINE.json north star): ids / labels / codes / planes bit-exact;
+distances and factors within 1e-4 relative (we check much tighter where the
+arithmetic allows); recall within 0.002.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import SEARCHES, case_params, golden_index_arrays, load_case, padded
+from oracle import ivrq_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+import paper_2602_23999_b200 as iv  # noqa: E402
+from paper_2602_23999_b200 import _device as dev  # noqa: E402
+from paper_2602_23999_b200.clustering import Centroids, row_sqnorms, train_kmeans_device  # noqa: E402
+from paper_2602_23999_b200.codec import encode_rows  # noqa: E402
+from paper_2602_23999_b200.index import IvfRabitqIndex, build_index_device  # noqa: E402
+from paper_2602_23999_b200.search import prepare_queries_device, search_device  # noqa: E402
+
+
+def _index(g) -> IvfRabitqIndex:
+    a = golden_index_arrays(g)
+    return IvfRabitqIndex(
+        dims=a["dims"], bits=a["bits"], n_clusters=a["n_clusters"], size=a["size"], eps_bound=a["eps_bound"],
+        seed=int(g["params"][3]), rotation=a["rotation"], centroids=Centroids(a["centroids"]),
+        offsets=a["offsets"], packed_msb=a["packed_msb"], excodes=a["excodes"],
+        short_factors=a["short_factors"], long_factors=a["long_factors"], pids=a["pids"],
+    )
+
+
+def test_row_sqnorms_bit_exact_einsum_order():
+    with np.load("tests/golden/reductions.npz") as z:
+        red = {k: z[k] for k in z.files}
+    for d in (1, 7, 8, 13, 32, 96, 100, 128, 768, 1536):
+        a = red[f"einsum_a_{d}"]
+        got = dev.to_host(row_sqnorms(dev.to_device(a)))
+        np.testing.assert_array_equal(got, red[f"einsum_aa_{d}"])
+        b32 = red[f"einsum_b_{d}"]
+        got32 = dev.to_host(row_sqnorms(dev.to_device(b32)))
+        np.testing.assert_array_equal(got32, np.einsum("ij,ij->i", b32, b32, dtype=np.float64))
+
+
+def test_centroid_sqnorms_match_reference(golden):
+    c = Centroids(golden["centroids"])
+    np.testing.assert_array_equal(c.squared_norms, golden["centroid_sqnorms"])
+
+
+def test_select_clusters_matches_reference(golden):
+    c = Centroids(golden["centroids"])
+    for si, sp in enumerate(SEARCHES):
+        if f"s{si}_probe_ids" not in golden:
+            continue
+        ids, d2 = iv.select_clusters(golden["q_rot"], c, sp["n_probe"])
+        np.testing.assert_array_equal(ids, golden[f"s{si}_probe_ids"])
+        np.testing.assert_allclose(d2, golden[f"s{si}_probe_d2"], rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("si", [0, 1, 2, 3])
+def test_query_state_matches_reference(golden, si):
+    if f"s{si}_qstate" not in golden:
+        pytest.skip("n_probe exceeds n_clusters")
+    sp = iv.SearchParams(**SEARCHES[si])
+    ix = _index(golden)
+    scal, planes, luts = prepare_queries_device(dev.to_device(golden["q_rot"]), ix, sp)
+    scal = dev.to_host(scal)
+    want = golden[f"s{si}_qstate"]
+    np.testing.assert_array_equal(scal[:, 0], want[:, 0])  # sum_q (pairwise order)
+    np.testing.assert_array_equal(scal[:, 1], want[:, 1])  # delta
+    np.testing.assert_array_equal(scal[:, 2], want[:, 2])  # code_sum_q
+    np.testing.assert_array_equal(scal[:, 3], want[:, 3])  # ip_margin
+    if sp.ip_mode == "bitwise":
+        np.testing.assert_array_equal(dev.to_host(planes).view(np.uint32), golden[f"s{si}_planes"])
+    else:
+        np.testing.assert_array_equal(dev.to_host(luts), golden[f"s{si}_luts"])
+
+
+@pytest.mark.parametrize("si", range(len(SEARCHES)))
+def test_scan_bit_exact_given_reference_q_rot(golden, si):
+    """IDs bit-exact and distances to 1e-12 given the reference's rotated queries."""
+    if f"s{si}_ids" not in golden:
+        pytest.skip("n_probe exceeds n_clusters")
+    sp = iv.SearchParams(**SEARCHES[si])
+    ix = _index(golden)
+    q_rot = dev.to_device(golden["q_rot"])
+    res = search_device(None, ix, sp, q_rot=q_rot, with_stats=True)
+    cnt = dev.to_host(res.counts)
+    ids = dev.to_host(res.ids)
+    dists = dev.to_host(res.dists)
+    np.testing.assert_array_equal(cnt, golden[f"s{si}_counts"])
+    np.testing.assert_array_equal(ids, golden[f"s{si}_ids"])
+    np.testing.assert_allclose(dists, golden[f"s{si}_dists"], rtol=1e-12, atol=1e-12)
+    # survivor counts agree with the oracle's stage-1 pruning
+    stats = {}
+    orc.search(golden["queries"], golden_index_arrays(golden), q_rot=golden["q_rot"], stats=stats, **SEARCHES[si])
+    st = dev.to_host(res.stats)
+    assert int(st[:, 0].sum()) == stats.get("probed", 0)
+    assert int(st[:, 1].sum()) == stats.get("survivors", 0)
+
+
+@pytest.mark.parametrize("si", [0, 1, 3])
+def test_search_batch_end_to_end(golden, si):
+    """Public API, GPU query rotation included: ids equal the reference's."""
+    if f"s{si}_ids" not in golden:
+        pytest.skip("n_probe exceeds n_clusters")
+    sp = iv.SearchParams(**SEARCHES[si])
+    res = iv.search_batch(golden["queries"], _index(golden), sp)
+    ids, dists, cnt = padded(res, sp.k)
+    np.testing.assert_array_equal(cnt, golden[f"s{si}_counts"])
+    np.testing.assert_array_equal(ids, golden[f"s{si}_ids"])
+    np.testing.assert_allclose(dists, golden[f"s{si}_dists"], rtol=1e-9, atol=1e-9)
+
+
+def test_encoder_bit_exact_given_reference_inputs(golden):
+    p = case_params(golden)
+    o_rot = dev.to_device(golden["stage_o_rot"])
+    dist = dev.to_device(golden["stage_dist"])
+    cent_rot = dev.to_device(golden["centroids"])
+    offsets = dev.to_device(golden["offsets"].astype(np.int64))
+    out = encode_rows(o_rot, dist, cent_rot, offsets, iv.QuantizationParams(bits=p["bits"]), want_codes=True)
+    np.testing.assert_array_equal(dev.to_host(out["codes"]), golden["stage_codes"])
+    np.testing.assert_array_equal(dev.to_host(out["t"]).astype(np.float32), golden["stage_t"])
+    np.testing.assert_array_equal(dev.to_host(out["packed_msb"]).view(np.uint32), golden["packed_msb"])
+    sf = np.stack([dev.to_host(out[k]) for k in ("short_add", "short_scale", "short_err")], axis=1)
+    np.testing.assert_array_equal(sf, golden["short_factors"])
+    np.testing.assert_array_equal(dev.to_host(out["long_factors"]), golden["long_factors"])
+    if p["bits"] > 1:
+        n = golden["x"].shape[0]
+        bpv = golden["excodes"].shape[1]
+        exb = dev.to_host(out["excodes"]).view(np.uint8).reshape(n, -1)[:, :bpv]
+        np.testing.assert_array_equal(exb, golden["excodes"])
+    assert int(out["bad_rows"].item()) == 0
+
+
+@pytest.mark.parametrize("bits", [1, 2, 3, 5, 8])
+def test_quantize_batch_float64_rows_match_oracle(bits):
+    rng = np.random.default_rng(bits)
+    o = rng.standard_normal((300, 24))
+    o /= np.linalg.norm(o, axis=1)[:, None]
+    o[7] = 0.0
+    u, t = iv.quantize_batch(o, iv.QuantizationParams(bits=bits))
+    u_o, t_o = orc.quantize(o, bits)
+    np.testing.assert_array_equal(u, u_o)
+    np.testing.assert_array_equal(t, t_o)
+    with pytest.raises(ValueError):
+        iv.quantize_batch(np.ones((1, 4)), iv.QuantizationParams(bits=bits))
+
+
+def test_kmeans_matches_reference(golden):
+    p = case_params(golden)
+    xt = golden["x"][golden["stage_train_rows"]]
+    c = train_kmeans_device(dev.to_device(xt), p["nlist"], p["iters"], int(golden["stage_km_seed"]))
+    np.testing.assert_allclose(dev.to_host(c), golden["stage_centroids64"], rtol=1e-12, atol=1e-12)
+
+
+def test_assign_matches_reference(golden):
+    c = Centroids(golden["stage_centroids64"], None)
+    labels = iv.assign(golden["x"], c)
+    np.testing.assert_array_equal(labels, golden["stage_labels"])
+
+
+def test_build_bit_exact_given_reference_centroids_and_rotations(golden):
+    p = case_params(golden)
+    params = iv.BuildParams(
+        n_clusters=p["nlist"], quant=iv.QuantizationParams(bits=p["bits"]), kmeans_iters=p["iters"],
+        train_fraction=p["train_fraction"], seed=p["seed"],
+    )
+    inject = dict(
+        centroids64=golden["stage_centroids64"], rotation=golden["rotation"], cent_rot=golden["centroids"],
+        o_rot=golden["stage_o_rot"],
+    )
+    ix = build_index_device(dev.to_device(golden["x"]), params, inject=inject)
+    for field in ("offsets", "pids", "packed_msb", "excodes", "short_factors", "long_factors"):
+        np.testing.assert_array_equal(getattr(ix, field), golden[field], err_msg=field)
+
+
+def test_build_full_pipeline_matches_reference(golden):
+    """No injection: GPU k-means, assignment, rotation GEMMs and encoder."""
+    p = case_params(golden)
+    params = iv.BuildParams(
+        n_clusters=p["nlist"], quant=iv.QuantizationParams(bits=p["bits"]), kmeans_iters=p["iters"],
+        train_fraction=p["train_fraction"], seed=p["seed"],
+    )
+    keep: dict = {}
+    ix = build_index_device(dev.to_device(golden["x"]), params, keep=keep)
+    np.testing.assert_allclose(dev.to_host(keep["centers"]), golden["stage_centroids64"], rtol=1e-12, atol=1e-12)
+    np.testing.assert_array_equal(dev.to_host(keep["labels"]), golden["stage_labels"])
+    np.testing.assert_array_equal(ix.pids, golden["pids"])
+    np.testing.assert_array_equal(ix.offsets, golden["offsets"])
+    np.testing.assert_array_equal(ix.rotation, golden["rotation"])
+    # float64-accumulated rotations round to float32 like the reference's GEMMs
+    # except for rare last-ulp cases; codes follow from o_rot
+    o_rot = dev.to_host(keep["o_rot"])
+    ulp = np.abs(o_rot.view(np.int32).astype(np.int64) - golden["stage_o_rot"].view(np.int32).astype(np.int64))
+    assert ulp.max() <= 1
+    assert (ulp > 0).mean() < 1e-3
+    np.testing.assert_allclose(ix.centroids.values, golden["centroids"], rtol=1e-6, atol=1e-6)
+    code_mismatch = (dev.to_host(keep["codes"]) != golden["stage_codes"]).mean()
+    assert code_mismatch < 1e-3
+    np.testing.assert_allclose(ix.short_factors, golden["short_factors"], rtol=1e-4, atol=1e-5)
+
+
+def test_build_and_search_recall_parity_with_oracle():
+    """Mid-size seeded workload: GPU build+search recall within 0.002 of the oracle's."""
+    g = load_case("b8_d128")
+    x = g["x"]
+    q = g["queries"]
+    params = iv.BuildParams(n_clusters=20, quant=iv.QuantizationParams(bits=8), kmeans_iters=5, seed=1)
+    ix = iv.build_index(x, params)
+    gt, _ = orc.exact_knn(x, q, 10)
+    ref = orc.build(x, 20, 8, 5, 1.0, 1)
+    for mode in ("bitwise", "lut"):
+        sp = iv.SearchParams(k=10, n_probe=5, ip_mode=mode)
+        r_gpu = orc.recall_at_k(iv.search_batch(q, ix, sp), gt, 10)
+        r_ref = orc.recall_at_k(orc.search(q, ref, 10, 5, ip_mode=mode), gt, 10)
+        assert abs(r_gpu - r_ref) <= 0.002, (mode, r_gpu, r_ref)
+
+
+def test_exact_knn_matches_oracle():
+    rng = np.random.default_rng(4)
+    base = rng.standard_normal((1000, 16)).astype(np.float32)
+    queries = rng.standard_normal((20, 16))
+    ids, d = iv.exact_knn(base, queries, 10)
+    ids_o, d_o = orc.exact_knn(base, queries, 10)
+    np.testing.assert_array_equal(ids, ids_o)
+    np.testing.assert_allclose(d, d_o, rtol=1e-12, atol=1e-12)
+
+
+def test_rotate_matches_oracle():
+    rot = iv.gen_rotation(24, 9)
+    rng = np.random.default_rng(2)
+    x = rng.standard_normal((30, 24))
+    np.testing.assert_allclose(iv.rotate(rot, x), x @ rot.matrix.T, rtol=1e-12, atol=1e-12)
+
+
+def test_edge_cases_empty_lists_and_small_k():
+    g = load_case("b2_dup")
+    ix = _index(g)
+    sp = iv.SearchParams(k=50, n_probe=ix.n_clusters, ip_mode="bitwise")
+    res = iv.search_batch(g["queries"], ix, sp)
+    ref = orc.search(g["queries"], golden_index_arrays(g), 50, ix.n_clusters, ip_mode="bitwise", q_rot=g["q_rot"])
+    for (a, b), (c, d) in zip(res, ref):
+        np.testing.assert_array_equal(a, c)
+        np.testing.assert_allclose(b, d, rtol=1e-9)
+    assert iv.search_batch(np.zeros((0, ix.dims)), ix, sp) == []

@@ -1,0 +1,200 @@
+"""Host-side logic that runs without a GPU: parameter validation, storage
+formats, IVRQ1 files and the C-ABI library surface."""
+
+from __future__ import annotations
+
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_2602_23999_b200 as iv
+from conftest import ROOT, golden_index_arrays, load_case
+from oracle import ivrq_oracle as orc
+from paper_2602_23999_b200 import _lib
+from paper_2602_23999_b200.clustering import Centroids
+from paper_2602_23999_b200.index import IvfRabitqIndex
+
+
+def _host_index(g) -> IvfRabitqIndex:
+    a = golden_index_arrays(g)
+    return IvfRabitqIndex(
+        dims=a["dims"], bits=a["bits"], n_clusters=a["n_clusters"], size=a["size"], eps_bound=a["eps_bound"],
+        seed=int(g["params"][3]), rotation=a["rotation"],
+        centroids=Centroids(a["centroids"], a["centroid_sqnorms"]), offsets=a["offsets"],
+        packed_msb=a["packed_msb"], excodes=a["excodes"], short_factors=a["short_factors"],
+        long_factors=a["long_factors"], pids=a["pids"],
+    )
+
+
+# ---------------------------------------------------------------- ABI
+
+
+def _header_symbols() -> list[str]:
+    text = (ROOT / "include" / "ivrq_b200.h").read_text()
+    return sorted(set(re.findall(r"IVRQ_API\s+[\w\s\*]+?\b(ivrq_\w+)\s*\(", text)))
+
+
+def test_header_declares_entry_points():
+    syms = _header_symbols()
+    for name in ("ivrq_search_scan", "ivrq_select_clusters", "ivrq_encode", "ivrq_kmeanspp", "ivrq_assign"):
+        assert name in syms
+
+
+def test_library_loads_and_exports_every_header_symbol():
+    lib = _lib.load()
+    for name in _header_symbols():
+        assert hasattr(lib, name), name
+    assert set(_header_symbols()) == set(_lib.exported_symbols())
+    assert lib.ivrq_abi_version() == 1
+    assert lib.ivrq_last_error() is not None
+
+
+def test_library_is_sm100a_only():
+    import subprocess
+
+    out = subprocess.run(
+        ["cuobjdump", "--list-elf", str(_lib.library_path())], capture_output=True, text=True
+    ).stdout
+    assert "sm_100a" in out
+    assert "sm_90" not in out
+
+
+# ---------------------------------------------------------------- params
+
+
+def test_params_validation():
+    with pytest.raises(ValueError):
+        iv.QuantizationParams(bits=0)
+    with pytest.raises(ValueError):
+        iv.QuantizationParams(bits=9)
+    with pytest.raises(ValueError):
+        iv.QuantizationParams(bits=4, n_coarse=1)
+    with pytest.raises(ValueError):
+        iv.QuantizationParams(bits=4, eps_bound=-1.0)
+    with pytest.raises(ValueError):
+        iv.BuildParams(n_clusters=0, quant=iv.QuantizationParams(bits=1))
+    with pytest.raises(ValueError):
+        iv.BuildParams(n_clusters=2, quant=iv.QuantizationParams(bits=1), kmeans_iters=0)
+    with pytest.raises(ValueError):
+        iv.BuildParams(n_clusters=2, quant=iv.QuantizationParams(bits=1), train_fraction=0.0)
+    with pytest.raises(ValueError):
+        iv.SearchParams(k=0, n_probe=1)
+    with pytest.raises(ValueError):
+        iv.SearchParams(k=1, n_probe=0)
+    with pytest.raises(ValueError):
+        iv.SearchParams(k=1, n_probe=1, ip_mode="simd")
+    with pytest.raises(ValueError):
+        iv.SearchParams(k=1, n_probe=1, query_bits=1)
+    assert iv.SearchParams(k=1, n_probe=1).ip_mode == "lut"
+
+
+def test_default_workers_env(monkeypatch):
+    monkeypatch.setenv("IVRQ_THREADS", "3")
+    assert iv.default_workers() == 3
+    monkeypatch.setenv("IVRQ_THREADS", "0")
+    with pytest.raises(ValueError):
+        iv.default_workers()
+
+
+def test_search_batch_validates_before_touching_the_device():
+    g = load_case("b4_d48")
+    ix = _host_index(g)
+    with pytest.raises(ValueError):
+        iv.search_batch(np.zeros((1, ix.dims)), ix, iv.SearchParams(k=1, n_probe=ix.n_clusters + 1))
+    with pytest.raises(ValueError):
+        iv.search_batch(np.zeros((1, ix.dims + 1)), ix, iv.SearchParams(k=1, n_probe=2))
+
+
+# ---------------------------------------------------------------- formats
+
+
+def test_pack_interleaved_word_order():
+    plane = iv.pack_interleaved(np.ones((1, 32), dtype=np.uint8))
+    assert plane.words.tolist() == [0xFFFFFFFF]
+    bits = np.zeros((2, 64), dtype=np.uint8)
+    bits[0, 0] = 1
+    bits[1, 1] = 1
+    bits[0, 32] = 1
+    bits[1, 63] = 1
+    assert iv.pack_interleaved(bits).words.tolist() == [1, 2, 1, 1 << 31]
+
+
+@pytest.mark.parametrize("dims", [1, 31, 32, 33, 70, 128])
+def test_pack_roundtrips(dims):
+    rng = np.random.default_rng(dims)
+    b = rng.integers(0, 2, (7, dims)).astype(np.uint8)
+    plane = iv.pack_interleaved(b)
+    assert np.array_equal(iv.unpack_interleaved(plane), b)
+    assert int(np.bitwise_count(plane.words).sum()) == int(b.sum())
+    np.testing.assert_array_equal(plane.words, orc.msb_words(b))
+    for bits in (2, 3, 5, 8):
+        ex = rng.integers(0, 2 ** (bits - 1), (6, dims)).astype(np.uint8)
+        packed = iv.pack_excodes(ex, bits)
+        assert packed.shape == (6, iv.excode_bytes_per_vector(dims, bits))
+        np.testing.assert_array_equal(packed, orc.ex_bytes(ex, bits))
+        assert np.array_equal(iv.unpack_excodes(packed, dims, bits), ex)
+
+
+def test_split_planes():
+    msb, ex = iv.split_planes(np.array([5], dtype=np.uint8), 3)
+    assert msb.tolist() == [1] and ex.tolist() == [1]
+    msb, ex = iv.split_planes(np.array([0, 1, 1], dtype=np.uint8), 1)
+    assert ex is None and msb.tolist() == [0, 1, 1]
+    with pytest.raises(ValueError):
+        iv.split_planes(np.array([4], dtype=np.uint8), 2)
+
+
+# ---------------------------------------------------------------- IVRQ1 files
+
+
+def test_save_load_roundtrip_is_byte_identical(tmp_path):
+    for name in ("b4_d48", "b1_d32", "b2_dup"):
+        g = load_case(name)
+        ix = _host_index(g)
+        p1 = tmp_path / f"{name}.idx"
+        iv.save_index(ix, str(p1))
+        loaded = iv.load_index(str(p1))
+        for field in ("rotation", "offsets", "packed_msb", "excodes", "short_factors", "long_factors", "pids"):
+            assert np.array_equal(getattr(loaded, field), getattr(ix, field)), field
+        assert np.array_equal(loaded.centroids.values, ix.centroids.values)
+        assert loaded.eps_bound == np.float32(ix.eps_bound)
+        p2 = tmp_path / f"{name}.2.idx"
+        iv.save_index(loaded, str(p2))
+        assert p1.read_bytes() == p2.read_bytes()
+
+
+def test_load_rejects_malformed_files(tmp_path):
+    g = load_case("b4_d48")
+    path = tmp_path / "a.idx"
+    iv.save_index(_host_index(g), str(path))
+    data = path.read_bytes()
+    bad = tmp_path / "bad.idx"
+    bad.write_bytes(b"NOTIDX" + b"\x00" * 64)
+    with pytest.raises(iv.IndexFormatError, match="magic"):
+        iv.load_index(str(bad))
+    cut = tmp_path / "cut.idx"
+    cut.write_bytes(data[:-17])
+    with pytest.raises(iv.IndexFormatError, match="pids"):
+        iv.load_index(str(cut))
+    head = tmp_path / "head.idx"
+    head.write_bytes(data[:10])
+    with pytest.raises(iv.IndexFormatError, match="header"):
+        iv.load_index(str(head))
+    raw = bytearray(data)
+    raw[40:48] = (999).to_bytes(8, "little")
+    wrong = tmp_path / "wrong.idx"
+    wrong.write_bytes(bytes(raw))
+    with pytest.raises(iv.IndexFormatError, match="rotation"):
+        iv.load_index(str(wrong))
+
+
+def test_index_views_match_oracle_decode():
+    g = load_case("b3_d96")
+    ix = _host_index(g)
+    a = golden_index_arrays(g)
+    np.testing.assert_array_equal(ix.code_values, orc.decode_codes(a))
+    lo, hi = ix.cluster_range(0)
+    assert ix.cluster_words(0).shape == (ix.words_per_vector, hi - lo)
+    assert ix.msb_nibbles.shape == (ix.size, 8 * ix.words_per_vector)
