@@ -585,7 +585,9 @@ extern "C" int ivrq_rotate_queries(const void* q, int q_is_f64, int64_t nq, int3
 }
 
 static int64_t probe_chunk_rows(int64_t nq, int32_t n_clusters) {
-  const int64_t budget = (int64_t)256 << 20;  // bytes of distance matrix per pass
+  // bytes of distance matrix per pass: enough for >= 256 query rows so the
+  // GEMM tiles stay full even when "clusters" are a whole base set (exact k-NN)
+  const int64_t budget = std::max<int64_t>((int64_t)256 << 20, (int64_t)256 * n_clusters * 8);
   int64_t rows = budget / ((int64_t)n_clusters * 8);
   rows = std::max<int64_t>(rows, 1);
   return std::min<int64_t>(rows, std::max<int64_t>(nq, 1));

@@ -168,18 +168,32 @@ def search_device(
     *,
     q_rot: torch.Tensor | None = None,
     with_stats: bool = False,
+    events: dict[str, torch.cuda.Event] | None = None,
 ) -> DeviceResult:
     """The whole search on device tensors (queries already in HBM).
 
     ``q_rot`` (tests only) injects precomputed rotated queries, the
     reference's own, to compare everything downstream bit-exactly.
+    ``events`` (bench only) receives CUDA events recorded on the current
+    stream at the stage boundaries: start, rotated, probed, prepared, scanned.
     """
+
+    def mark(name: str) -> None:
+        if events is not None:
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record()
+            events[name] = ev
+
+    mark("start")
     nq = q.shape[0] if q_rot is None else q_rot.shape[0]
     if q_rot is None:
         q_rot = rotate_queries_device(q, index)
+    mark("rotated")
     t = index.device
     probe_ids, probe_d2 = _probe_device(q_rot, t["centroids"], t["centroid_sqnorms"], params.n_probe, True)
+    mark("probed")
     scalars, planes, luts = prepare_queries_device(q_rot, index, params)
+    mark("prepared")
     k = params.k
     out_ids = torch.empty((nq, k), dtype=torch.int64, device=q_rot.device)
     out_d = torch.empty((nq, k), dtype=torch.float64, device=q_rot.device)
@@ -191,6 +205,7 @@ def search_device(
         index.view(), dev.ptr(q_rot), dev.ptr(probe_ids), dev.ptr(probe_d2), dev.ptr(scalars), dev.ptr(planes),
         dev.ptr(luts), nq, cp, dev.ptr(out_ids), dev.ptr(out_d), dev.ptr(counts), dev.ptr(stats), dev.stream_ptr(),
     )
+    mark("scanned")
     return DeviceResult(ids=out_ids, dists=out_d, counts=counts, stats=stats)
 
 
