@@ -7,6 +7,7 @@
 
 #include "ivrq_common.cuh"
 #include "ivrq_gemm.cuh"
+#include "ivrq_rowchain.cuh"
 
 namespace ivrq {
 
@@ -21,46 +22,32 @@ static int dalloc(T** p, size_t count, cudaStream_t s, const char* what) {
 // ============================================================ k-means++ seeding
 // d2[i] = einsum((x_i - c)^2) with c = centers[j] (float64 of an x row),
 // optionally min-ed into the existing d2 (clustering.py:66-67, 77-78).
-__global__ void kpp_update_kernel(const float* __restrict__ x, int64_t n, int d, const double* __restrict__ center,
-                                  double* __restrict__ d2, int init, const int* __restrict__ halt) {
+__global__ void __launch_bounds__(rowchain::THREADS) kpp_update_kernel(const float* __restrict__ x, int64_t n, int d,
+                                                                       const double* __restrict__ center,
+                                                                       double* __restrict__ d2, int init,
+                                                                       const int* __restrict__ halt) {
+  using namespace rowchain;
   if (halt && *halt) return;
-  constexpr int ROWS = 64, CH = 64;
-  __shared__ double tile[ROWS][CH + 1];
+  __shared__ Tile<float> tile;
   __shared__ double cs[CH];
   const int64_t row0 = (int64_t)blockIdx.x * ROWS;
-  const int r = threadIdx.x;
-  EinsumAcc acc;
+  const int r = threadIdx.x >> 1, lane = threadIdx.x & 1;
+  const bool vec = (d % 4 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
+  auto src = [&](int64_t gr) { return x + gr * d; };
+  double acc = 0.0;
   for (int c0 = 0; c0 < d; c0 += CH) {
     const int cw = min(CH, d - c0);
     __syncthreads();
-    for (int idx = threadIdx.x; idx < ROWS * CH; idx += blockDim.x) {
-      int rr = idx / CH, cc = idx % CH;
-      int64_t gr = row0 + rr;
-      tile[rr][cc] = (gr < n && cc < cw) ? (double)x[gr * d + c0 + cc] : 0.0;
-    }
+    stage_tile(tile, src, row0, n, c0, cw, vec);
     if (threadIdx.x < CH) cs[threadIdx.x] = threadIdx.x < cw ? center[c0 + threadIdx.x] : 0.0;
     __syncthreads();
-    if (row0 + r < n) {
-      int i = 0;
-      for (; i + 8 <= cw; i += 8) {
-        double p[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          double df = dsub(tile[r][i + q], cs[i + q]);
-          p[q] = dmul(df, df);
-        }
-        acc.block8(p);
-      }
-      for (; i < cw; i += 2) {
-        double d0 = dsub(tile[r][i], cs[i]);
-        bool has1 = (i + 1) < cw;
-        double d1 = has1 ? dsub(tile[r][i + 1], cs[i + 1]) : 0.0;
-        acc.pair(dmul(d0, d0), dmul(d1, d1), has1);
-      }
-    }
+    acc = chain_chunk(acc, lane, cw, [&](int k) {
+      const double df = dsub((double)tile.v[r][k], cs[k]);
+      return dmul(df, df);
+    });
   }
-  if (row0 + r < n) {
-    double v = acc.result();
+  const double v = finish(acc);
+  if (lane == 0 && row0 + r < n) {
     if (init) d2[row0 + r] = v;
     else d2[row0 + r] = dmin(d2[row0 + r], v);  // np.minimum(d2, new, out=d2)
   }
@@ -112,28 +99,52 @@ __global__ void __launch_bounds__(1024) kpp_select_kernel(
     }
     const double target = dmul(draws[j], total);
     if (exact_scan) {
+      // NumPy's sequential cumsum, walked by one thread out of shared memory
+      // while the rest of the block streams the next chunk in.
+      constexpr int SC = 2048;
+      __shared__ double sbuf[2][SC];
+      __shared__ int s_found;
       if (tid == 0) {
-        double cs = 0.0;
-        int64_t idx = n;
-        int64_t i = 0;
-        for (; i + 4 <= n; i += 4) {
-          double a0 = d2[i], a1 = d2[i + 1], a2 = d2[i + 2], a3 = d2[i + 3];
-          cs = dadd(cs, a0);
-          if (cs >= target) { idx = i; break; }
-          cs = dadd(cs, a1);
-          if (cs >= target) { idx = i + 1; break; }
-          cs = dadd(cs, a2);
-          if (cs >= target) { idx = i + 2; break; }
-          cs = dadd(cs, a3);
-          if (cs >= target) { idx = i + 3; break; }
-        }
-        if (idx == n) {
-          for (; i < n; ++i) {
-            cs = dadd(cs, d2[i]);
-            if (cs >= target) { idx = i; break; }
+        s_found = 0;
+        s_idx = n - 1;
+      }
+      double cs = 0.0;
+      for (int64_t i = tid; i < min((int64_t)SC, n); i += blockDim.x) sbuf[0][i] = d2[i];
+      __syncthreads();
+      int cur = 0;
+      for (int64_t base = 0; base < n; base += SC) {
+        const int64_t nb = base + SC;
+        if (tid >= 32) {
+          for (int64_t i = nb + tid - 32; i < min(nb + SC, n); i += blockDim.x - 32) sbuf[cur ^ 1][i - nb] = d2[i];
+        } else if (tid == 0) {
+          const int len = (int)min((int64_t)SC, n - base);
+          const double* b = sbuf[cur];
+          int hit = -1;
+          int i = 0;
+          for (; i + 4 <= len; i += 4) {
+            const double v0 = b[i], v1 = b[i + 1], v2 = b[i + 2], v3 = b[i + 3];
+            cs = dadd(cs, v0);
+            if (cs >= target) { hit = i; break; }
+            cs = dadd(cs, v1);
+            if (cs >= target) { hit = i + 1; break; }
+            cs = dadd(cs, v2);
+            if (cs >= target) { hit = i + 2; break; }
+            cs = dadd(cs, v3);
+            if (cs >= target) { hit = i + 3; break; }
+          }
+          if (hit < 0)
+            for (; i < len; ++i) {
+              cs = dadd(cs, b[i]);
+              if (cs >= target) { hit = i; break; }
+            }
+          if (hit >= 0) {
+            s_found = 1;
+            s_idx = min(base + hit, n - 1);
           }
         }
-        s_idx = idx < n - 1 ? idx : n - 1;
+        __syncthreads();
+        if (s_found) break;
+        cur ^= 1;
       }
     } else {
       // blocked scan: 1024-element blocks summed sequentially, then a
@@ -338,40 +349,33 @@ __global__ void update_kernel(const float* __restrict__ x, int64_t n, const int6
 
 // ============================================================ normalise + rotate
 // dist[r] = sqrt(einsum(diff, diff)), diff = x[order[r]] - cent32[labels[order[r]]]
-__global__ void resid_norm_kernel(const float* __restrict__ x, const int64_t* __restrict__ order,
-                                  const int32_t* __restrict__ labels, const float* __restrict__ cent, int64_t n, int d,
-                                  double* __restrict__ dist) {
-  const int lane = threadIdx.x & 31;
-  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (r >= n) return;
-  // the einsum chain is sequential: lanes 0/1 own the two accumulators; the
-  // other lanes only prefetch.
-  const int64_t s = order ? order[r] : r;
-  const float* xr = x + s * d;
-  const float* cr = cent + (int64_t)labels[s] * d;
+__global__ void __launch_bounds__(rowchain::THREADS) resid_norm_kernel(const float* __restrict__ x,
+                                                                       const int64_t* __restrict__ order,
+                                                                       const int32_t* __restrict__ labels,
+                                                                       const float* __restrict__ cent, int64_t n,
+                                                                       int d, double* __restrict__ dist) {
+  using namespace rowchain;
+  __shared__ Tile<float> tx, tc;
+  const int64_t row0 = (int64_t)blockIdx.x * ROWS;
+  const int r = threadIdx.x >> 1, lane = threadIdx.x & 1;
+  const bool vec = (d % 4 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(cent) & 15) == 0);
+  auto srcx = [&](int64_t gr) { return x + (order ? order[gr] : gr) * d; };
+  auto srcc = [&](int64_t gr) { return cent + (int64_t)labels[order ? order[gr] : gr] * d; };
   double acc = 0.0;
-  if (lane < 2) {
-    int i = 0;
-    for (; i + 8 <= d; i += 8) {
-#pragma unroll
-      for (int blk = 3; blk >= 0; --blk) {
-        int kk = i + 2 * blk + lane;
-        double df = dsub((double)xr[kk], (double)cr[kk]);
-        acc = dadd(dmul(df, df), acc);
-      }
-    }
-    for (; i < d; i += 2) {
-      int kk = i + lane;
-      double p = 0.0;
-      if (kk < d) {
-        double df = dsub((double)xr[kk], (double)cr[kk]);
-        p = dmul(df, df);
-      }
-      acc = dadd(p, acc);
-    }
+  for (int c0 = 0; c0 < d; c0 += CH) {
+    const int cw = min(CH, d - c0);
+    __syncthreads();
+    stage_tile(tx, srcx, row0, n, c0, cw, vec);
+    stage_tile(tc, srcc, row0, n, c0, cw, vec);
+    __syncthreads();
+    acc = chain_chunk(acc, lane, cw, [&](int k) {
+      const double df = dsub((double)tx.v[r][k], (double)tc.v[r][k]);
+      return dmul(df, df);
+    });
   }
-  double a1 = __shfl_sync(0xffffffffu, acc, 1);
-  if (lane == 0) dist[r] = dsqrt(dadd(0.0, dadd(acc, a1)));
+  const double v = finish(acc);
+  if (lane == 0 && row0 + r < n) dist[row0 + r] = dsqrt(v);
 }
 
 struct ResidLoader {
@@ -790,20 +794,20 @@ extern "C" int ivrq_kmeanspp(const float* x, int64_t n, int32_t d, int32_t n_clu
   cudaMemsetAsync(halt, 0, sizeof(int), s);
   const int64_t exact_max = 1 << 20;
   const int exact = n <= exact_max ? 1 : 0;
-  const unsigned ub = (unsigned)ceil_div(n, 64);
+  const unsigned ub = (unsigned)ceil_div(n, rowchain::ROWS);
   int j = j_begin;
   if (j == 0) {
     // centers[0] = x[first]; d2 = |x - c0|^2
     kpp_select_kernel<<<1, 1024, 0, s>>>(x, n, d, d2, nodes, dl, dr, dlb, nlevels, nleaf, tree.root, draws, 1, 0,
                                          centers, zero_step, halt, exact, bsums);
-    kpp_update_kernel<<<ub, 64, 0, s>>>(x, n, d, centers, d2, 1, halt);
+    kpp_update_kernel<<<ub, rowchain::THREADS, 0, s>>>(x, n, d, centers, d2, 1, halt);
     j = 1;
   }
   for (; j < j_end; ++j) {
     kpp_leaf_kernel<<<(unsigned)ceil_div(nleaf, 256), 256, 0, s>>>(d2, dls, dll, nleaf, nodes, halt);
     kpp_select_kernel<<<1, 1024, 0, s>>>(x, n, d, d2, nodes, dl, dr, dlb, nlevels, nleaf, tree.root, draws,
                                          draw_kind, j, centers, zero_step, halt, exact, bsums);
-    kpp_update_kernel<<<ub, 64, 0, s>>>(x, n, d, centers + (int64_t)j * d, d2, 0, halt);
+    kpp_update_kernel<<<ub, rowchain::THREADS, 0, s>>>(x, n, d, centers + (int64_t)j * d, d2, 0, halt);
   }
   IVRQ_TRY(check_launch("ivrq_kmeanspp"));
   cudaFreeAsync(dls, s);
@@ -883,7 +887,8 @@ extern "C" int ivrq_normalize_rotate(const float* x, const int64_t* order, const
   if (n < 0 || d <= 0) return fail(IVRQ_EINVAL, "ivrq_normalize_rotate: bad sizes");
   if (n == 0) return IVRQ_OK;
   cudaStream_t s = as_stream(stream);
-  resid_norm_kernel<<<(unsigned)ceil_div(n, 8), 256, 0, s>>>(x, order, labels, cent32, n, d, dist);
+  resid_norm_kernel<<<(unsigned)ceil_div(n, rowchain::ROWS), rowchain::THREADS, 0, s>>>(x, order, labels, cent32, n, d,
+                                                                                        dist);
   IVRQ_TRY(check_launch("ivrq_normalize_rotate(norm)"));
   ResidLoader la{x, order, labels, cent32, dist, d};
   gemm::RowMajor<float> lb{rotation, d, d};

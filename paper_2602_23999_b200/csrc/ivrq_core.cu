@@ -1,5 +1,6 @@
 // Error state, device queries and the einsum-order row norms.
 #include "ivrq_common.cuh"
+#include "ivrq_rowchain.cuh"
 
 namespace ivrq {
 
@@ -20,47 +21,30 @@ int check_launch(const char* what) {
   return IVRQ_OK;
 }
 
-// Row-wise einsum("ij,ij->i") with each row staged through shared memory so
-// global loads stay coalesced; one thread owns one row's 2-lane chain.
+// Row-wise einsum("ij,ij->i", x, x): NumPy's two accumulator lanes run on two
+// threads per row over 128-bit staged tiles (ivrq_rowchain.cuh).
 template <typename T>
-__global__ void row_sqnorm_kernel(const T* __restrict__ x, int64_t n, int d, double* __restrict__ out) {
-  constexpr int ROWS = 64;
-  constexpr int CH = 64;  // dims per chunk (multiple of 8 keeps einsum blocks whole)
-  __shared__ double tile[ROWS][CH + 1];
+__global__ void __launch_bounds__(rowchain::THREADS) row_sqnorm_kernel(const T* __restrict__ x, int64_t n, int d,
+                                                                      double* __restrict__ out) {
+  using namespace rowchain;
+  __shared__ Tile<T> tile;
   const int64_t row0 = (int64_t)blockIdx.x * ROWS;
-  const int r = threadIdx.x;  // blockDim.x == ROWS
-  EinsumAcc acc;
+  const int r = threadIdx.x >> 1, lane = threadIdx.x & 1;
+  const bool vec = (d % Tile<T>::VEC == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
+  auto src = [&](int64_t gr) { return x + gr * d; };
+  double acc = 0.0;
   for (int c0 = 0; c0 < d; c0 += CH) {
     const int cw = min(CH, d - c0);
     __syncthreads();
-    for (int idx = threadIdx.x; idx < ROWS * CH; idx += blockDim.x) {
-      int rr = idx / CH, cc = idx % CH;
-      int64_t gr = row0 + rr;
-      double v = 0.0;
-      if (gr < n && cc < cw) v = (double)x[gr * d + c0 + cc];
-      tile[rr][cc] = v;
-    }
+    stage_tile(tile, src, row0, n, c0, cw, vec);
     __syncthreads();
-    if (row0 + r < n) {
-      int i = 0;
-      for (; i + 8 <= cw; i += 8) {
-        double p[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          double v = tile[r][i + k];
-          p[k] = dmul(v, v);
-        }
-        acc.block8(p);
-      }
-      for (; i < cw; i += 2) {
-        double v0 = tile[r][i];
-        bool has1 = (i + 1) < cw;
-        double v1 = has1 ? tile[r][i + 1] : 0.0;
-        acc.pair(dmul(v0, v0), dmul(v1, v1), has1);
-      }
-    }
+    acc = chain_chunk(acc, lane, cw, [&](int k) {
+      const double v = (double)tile.v[r][k];
+      return dmul(v, v);
+    });
   }
-  if (row0 + r < n) out[row0 + r] = acc.result();
+  const double res = finish(acc);
+  if (lane == 0 && row0 + r < n) out[row0 + r] = res;
 }
 
 }  // namespace ivrq
@@ -83,11 +67,11 @@ extern "C" int ivrq_row_sqnorms(const void* x, int x_is_f64, int64_t n, int32_t 
                                 void* stream) {
   if (n < 0 || d < 0) return fail(IVRQ_EINVAL, "ivrq_row_sqnorms: negative size");
   if (n == 0) return IVRQ_OK;
-  dim3 grid((unsigned)ceil_div(n, 64));
+  dim3 grid((unsigned)ceil_div(n, rowchain::ROWS));
   if (x_is_f64)
-    row_sqnorm_kernel<double><<<grid, 64, 0, as_stream(stream)>>>((const double*)x, n, d, out);
+    row_sqnorm_kernel<double><<<grid, rowchain::THREADS, 0, as_stream(stream)>>>((const double*)x, n, d, out);
   else
-    row_sqnorm_kernel<float><<<grid, 64, 0, as_stream(stream)>>>((const float*)x, n, d, out);
+    row_sqnorm_kernel<float><<<grid, rowchain::THREADS, 0, as_stream(stream)>>>((const float*)x, n, d, out);
   return check_launch("ivrq_row_sqnorms");
 }
 

@@ -1,0 +1,635 @@
+// The fused two-stage list scan + top-k (search.py:326-387 inside the
+// per-query loop 425-448).  One CTA per query visits the query's probed
+// lists in ascending cluster id; within a list:
+//   stage 1  every vector: binary inner product (AND+POPC against the query's
+//            bit planes, or 4-bit LUT lookups), float64 estimate + lower bound,
+//            prune lb2 <= T with T the K-th best distance before this list;
+//   stage 2  survivors: full-code inner product <u, q_rot> in float64 and the
+//            refined estimate;
+//   merge    survivors into the running (dist, pid) top-k; after the list
+//            T := pool[k-1] once the pool holds k entries.
+// The threshold trajectory, and therefore every prune decision, is the
+// reference's.  k <= 32 keeps per-warp top-32 queues in registers (bitonic
+// shuffle networks); larger k falls back to a block-wide bitonic sort.
+#include "ivrq_common.cuh"
+
+namespace ivrq {
+namespace scan {
+
+constexpr int THREADS = 256;
+constexpr int WARPS = THREADS / 32;
+constexpr int CHUNK = 1024;            // vectors of one list per stage-1 pass
+constexpr int VPT = CHUNK / THREADS;   // vectors per thread per pass
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int64_t NO_ID = 0x7fffffffffffffffLL;
+
+struct Args {
+  ivrq_index_view ix;
+  const double* q_rot;
+  const int64_t* probe_ids;
+  const double* probe_d2;
+  const double* scalars;
+  const uint32_t* planes;
+  const float* luts;
+  int64_t nq;
+  int k, nprobe, qbits, prune;
+  int g, eb, exw;
+  int sort_n;  // big-k path: power of two >= CHUNK + k
+  int64_t* out_ids;
+  double* out_dists;
+  int32_t* out_counts;
+  int64_t* stats;
+};
+
+__device__ __forceinline__ double dinf() { return __longlong_as_double(0x7ff0000000000000LL); }
+
+// ------------------------------------------------------------ per-query state in smem
+struct QueryCtx {
+  double delta, half_code, ipm, kb_sum;
+};
+
+// ------------------------------------------------------------ stage 1
+// Fills s_cv (row within list) / s_cd (stage-1 estimate) with the survivors of
+// vectors [c0, c0+cn) of the list; returns the count via s_ncand.
+template <int MODE>
+__device__ __forceinline__ void stage1_chunk(const Args& a, const QueryCtx& qc, const uint32_t* __restrict__ words,
+                                             int64_t lo, int64_t n_c, int64_t c0, int cn, double d_qc2, double sq,
+                                             double T_list, const uint32_t* s_planes8, const float* s_lut,
+                                             int32_t* s_cv, double* s_cd, int* s_ncand) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int g = a.g;
+  double ipb[VPT];
+  if (MODE == IVRQ_IP_BITWISE) {
+    int pos[VPT], last[VPT];
+#pragma unroll
+    for (int u = 0; u < VPT; ++u) pos[u] = last[u] = 0;
+    const int qb = a.qbits;
+    for (int gi = 0; gi < g; ++gi) {
+      const uint4 pa = *reinterpret_cast<const uint4*>(s_planes8 + gi * 8);
+      const uint4 pb = *reinterpret_cast<const uint4*>(s_planes8 + gi * 8 + 4);
+      const uint32_t pl[8] = {pa.x, pa.y, pa.z, pa.w, pb.x, pb.y, pb.z, pb.w};
+      const uint32_t* wrow = words + (int64_t)gi * n_c + c0;
+#pragma unroll
+      for (int u = 0; u < VPT; ++u) {
+        const int vi = tid + u * THREADS;
+        const uint32_t w = vi < cn ? __ldg(wrow + vi) : 0u;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (j < qb) {
+            const int c = __popc(w & pl[j]);
+            pos[u] += c << j;
+            if (j == qb - 1) last[u] += c;
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < VPT; ++u) ipb[u] = dmul(qc.delta, (double)(pos[u] - (last[u] << qb)));
+  } else {
+    double acc[VPT];
+#pragma unroll
+    for (int u = 0; u < VPT; ++u) acc[u] = 0.0;
+    for (int gi = 0; gi < g; ++gi) {
+      const uint32_t* wrow = words + (int64_t)gi * n_c + c0;
+      const float* lrow = s_lut + gi * 8 * 16;
+#pragma unroll
+      for (int u = 0; u < VPT; ++u) {
+        const int vi = tid + u * THREADS;
+        const uint32_t w = vi < cn ? __ldg(wrow + vi) : 0u;
+#pragma unroll
+        for (int s = 0; s < 8; ++s) acc[u] = dadd(acc[u], (double)lrow[s * 16 + ((w >> (4 * s)) & 15u)]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < VPT; ++u) ipb[u] = acc[u];
+  }
+#pragma unroll
+  for (int u = 0; u < VPT; ++u) {
+    const int vi = tid + u * THREADS;
+    bool keep = false;
+    double est2 = 0.0;
+    if (vi < cn) {
+      const int64_t row = lo + c0 + vi;
+      const double add = (double)__ldg(a.ix.short_add + row);
+      const double scale = (double)__ldg(a.ix.short_scale + row);
+      const double ip_signed = dsub(ipb[u], qc.half_code);
+      est2 = dmax(dsub(dadd(add, d_qc2), dmul(scale, ip_signed)), 0.0);
+      if (est2 <= T_list) {
+        keep = true;  // lb2 <= est2 <= T
+      } else {
+        const double err = (double)__ldg(a.ix.short_err + row);
+        double margin = dmul(err, sq);
+        if (qc.ipm != 0.0) {
+          const double sm = dmul(scale, qc.ipm);
+          margin = dsqrt(dadd(dmul(margin, margin), dmul(sm, sm)));
+        }
+        keep = dmax(dsub(est2, margin), 0.0) <= T_list;
+      }
+    }
+    const unsigned kb = __ballot_sync(FULL, keep);
+    int base = 0;
+    if (lane == 0 && kb) base = atomicAdd(s_ncand, __popc(kb));
+    base = __shfl_sync(FULL, base, 0);
+    if (keep) {
+      const int p = base + __popc(kb & ((1u << lane) - 1u));
+      s_cv[p] = vi;
+      s_cd[p] = est2;
+    }
+  }
+}
+
+// ------------------------------------------------------------ stage 2
+// Extract the 32 ex-code fields (eb bits each, LSB-first) of one 32-dim group
+// and accumulate sum_i u_i * q_i with u_i = msb_i << eb | ex_i.
+template <int EB>
+__device__ __forceinline__ double group_dot(const uint32_t* __restrict__ exg, uint32_t msb, const double* q) {
+  double acc = 0.0;
+  if constexpr (EB == 0) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) acc = fma((double)((msb >> i) & 1u), q[i], acc);
+  } else {
+    uint32_t w[EB + 1];
+#pragma unroll
+    for (int i = 0; i < EB; ++i) w[i] = __ldg(exg + i);
+    w[EB] = 0u;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      constexpr uint32_t mask = (1u << EB) - 1u;
+      const int bit = i * EB;
+      const int wi = bit >> 5, off = bit & 31;
+      const uint64_t win = ((uint64_t)w[wi + 1] << 32) | (uint64_t)w[wi];
+      const uint32_t field = (uint32_t)(win >> off) & mask;
+      const uint32_t u = ((((msb >> i) & 1u)) << EB) | field;
+      acc = fma((double)u, q[i], acc);
+    }
+  }
+  return acc;
+}
+
+// Refined distance of every candidate (in place in s_cd) (search.py:313-323).
+template <int EB>
+__device__ __forceinline__ void refine_chunk(const Args& a, const QueryCtx& qc, const uint32_t* __restrict__ words,
+                                             int64_t lo, int64_t n_c, int64_t c0, double d_qc2, const double* s_q,
+                                             const int32_t* s_cv, double* s_cd, int ncand) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int g = a.g;
+  int lpc = 1;
+  while (lpc < g && lpc < 32) lpc <<= 1;
+  const int cpw = 32 / lpc;  // candidates per warp per step
+  const int sub = lane / lpc, sl = lane % lpc;
+  for (int cb = wid * cpw; cb < ncand; cb += WARPS * cpw) {
+    const int ci = cb + sub;
+    double acc = 0.0;
+    int64_t row = 0;
+    if (ci < ncand) {
+      const int64_t v = c0 + s_cv[ci];
+      row = lo + v;
+      const uint32_t* exrow = a.ix.excodes + row * a.exw;
+      for (int gi = sl; gi < g; gi += lpc) {
+        const uint32_t msb = __ldg(words + (int64_t)gi * n_c + v);
+        acc += group_dot<EB>(exrow + gi * EB, msb, s_q + gi * 32);
+      }
+    }
+    for (int o = lpc >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
+    if (ci < ncand && sl == 0) {
+      const float2 lf = __ldg(reinterpret_cast<const float2*>(a.ix.long_factors) + row);
+      s_cd[ci] = dmax(dsub(dadd((double)lf.x, d_qc2), dmul((double)lf.y, dsub(acc, qc.kb_sum))), 0.0);
+    }
+  }
+}
+
+// ------------------------------------------------------------ warp top-32 queues
+__device__ __forceinline__ void cmpx(double& d, int64_t& id, int stride, bool take_min) {
+  const double od = __shfl_xor_sync(FULL, d, stride);
+  const int64_t oi = __shfl_xor_sync(FULL, id, stride);
+  const bool other_less = key_less(od, oi, d, id);
+  if (take_min ? other_less : key_less(d, id, od, oi)) {
+    d = od;
+    id = oi;
+  }
+}
+
+__device__ __forceinline__ void warp_sort32(double& d, int64_t& id) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      const bool up = (lane & size) == 0;
+      const bool lower = (lane & stride) == 0;
+      cmpx(d, id, stride, lower == up);
+    }
+  }
+}
+
+// q (sorted ascending) := 32 smallest of q ∪ b (b sorted ascending), sorted.
+__device__ __forceinline__ void warp_merge32(double& qd, int64_t& qi, double bd, int64_t bi) {
+  const int lane = threadIdx.x & 31;
+  const double rd = __shfl_sync(FULL, bd, 31 - lane);
+  const int64_t ri = __shfl_sync(FULL, bi, 31 - lane);
+  if (key_less(rd, ri, qd, qi)) {
+    qd = rd;
+    qi = ri;
+  }
+#pragma unroll
+  for (int stride = 16; stride > 0; stride >>= 1) cmpx(qd, qi, stride, (lane & stride) == 0);
+}
+
+// ------------------------------------------------------------ common prologue
+struct Smem {
+  double* s_q;
+  uint32_t* s_planes8;
+  float* s_lut;
+  double* s_cd;
+  int32_t* s_cv;
+  double* s_pool_d;
+  int64_t* s_pool_i;
+  double* s_sortk;
+  int64_t* s_sorti;
+};
+
+template <int MODE, bool REFINE>
+__device__ __forceinline__ Smem carve(const Args& a, unsigned char* smem, bool bigk) {
+  Smem s{};
+  const int g = a.g;
+  unsigned char* p = smem;
+  s.s_q = reinterpret_cast<double*>(p);
+  p += REFINE ? sizeof(double) * 32 * g : 0;
+  s.s_cd = reinterpret_cast<double*>(p);
+  p += sizeof(double) * CHUNK;
+  s.s_pool_d = reinterpret_cast<double*>(p);
+  p += sizeof(double) * (bigk ? a.k : 32);
+  s.s_pool_i = reinterpret_cast<int64_t*>(p);
+  p += sizeof(int64_t) * (bigk ? a.k : 32);
+  s.s_sortk = reinterpret_cast<double*>(p);  // big k: sort buffer; small k: per-warp queues
+  p += sizeof(double) * (bigk ? a.sort_n : WARPS * 32);
+  s.s_sorti = reinterpret_cast<int64_t*>(p);
+  p += sizeof(int64_t) * (bigk ? a.sort_n : WARPS * 32);
+  s.s_cv = reinterpret_cast<int32_t*>(p);
+  p += sizeof(int32_t) * CHUNK;
+  s.s_planes8 = reinterpret_cast<uint32_t*>(p);
+  p += MODE == IVRQ_IP_BITWISE ? sizeof(uint32_t) * 8 * g : 0;
+  s.s_lut = reinterpret_cast<float*>(p);
+  return s;
+}
+
+size_t smem_bytes(const Args& a, int mode, bool refine, bool bigk) {
+  size_t b = 0;
+  b += refine ? sizeof(double) * 32 * a.g : 0;
+  b += sizeof(double) * CHUNK;
+  b += (sizeof(double) + sizeof(int64_t)) * (bigk ? a.k : 32);
+  b += (sizeof(double) + sizeof(int64_t)) * (bigk ? a.sort_n : WARPS * 32);
+  b += sizeof(int32_t) * CHUNK;
+  b += mode == IVRQ_IP_BITWISE ? sizeof(uint32_t) * 8 * a.g : sizeof(float) * 8 * a.g * 16;
+  return b + 16;
+}
+
+template <int MODE, bool REFINE>
+__device__ __forceinline__ QueryCtx load_query(const Args& a, const Smem& s, int64_t q) {
+  const int g = a.g, d = a.ix.dims, tid = threadIdx.x;
+  if (REFINE)
+    for (int i = tid; i < 32 * g; i += THREADS) s.s_q[i] = i < d ? a.q_rot[q * d + i] : 0.0;
+  if (MODE == IVRQ_IP_BITWISE) {
+    for (int i = tid; i < 8 * g; i += THREADS) {
+      const int gi = i / 8, j = i % 8;
+      s.s_planes8[i] = j < a.qbits ? a.planes[(q * a.qbits + j) * g + gi] : 0u;
+    }
+  } else {
+    for (int i = tid; i < 8 * g * 16; i += THREADS) s.s_lut[i] = a.luts[q * 8 * g * 16 + i];
+  }
+  const double* sc = a.scalars + q * IVRQ_QS_COUNT;
+  QueryCtx qc;
+  qc.delta = sc[IVRQ_QS_DELTA];
+  qc.half_code = sc[IVRQ_QS_HALF_CODE];
+  qc.ipm = sc[IVRQ_QS_IP_MARGIN];
+  qc.kb_sum = sc[IVRQ_QS_KB_SUM];
+  return qc;
+}
+
+// ------------------------------------------------------------ kernel, k <= 32
+template <int MODE, int EB, bool REFINE>
+__global__ void __launch_bounds__(THREADS) scan_kernel(Args a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ int s_ncand;
+  __shared__ double s_T;
+  __shared__ int s_pool_n;
+  __shared__ long long s_probed, s_surv;
+  const int64_t q = blockIdx.x;
+  if (q >= a.nq) return;
+  const int k = a.k;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const Smem s = carve<MODE, REFINE>(a, smem, false);
+  const QueryCtx qc = load_query<MODE, REFINE>(a, s, q);
+  if (tid < 32) {
+    s.s_pool_d[tid] = dinf();
+    s.s_pool_i[tid] = NO_ID;
+  }
+  if (tid == 0) {
+    s_T = dinf();
+    s_pool_n = 0;
+    s_probed = 0;
+    s_surv = 0;
+  }
+  __syncthreads();
+  const int64_t* pid_list = a.probe_ids + q * a.nprobe;
+  const double* pd2_list = a.probe_d2 + q * a.nprobe;
+  for (int p = 0; p < a.nprobe; ++p) {  // ascending cluster id (search.py:429)
+    const int64_t c = pid_list[p];
+    const double d_qc2 = pd2_list[p];
+    const int64_t lo = a.ix.offsets[c], n_c = a.ix.offsets[c + 1] - lo;
+    if (n_c == 0) continue;
+    const double T_list = a.prune ? s_T : dinf();
+    const bool pool_full = s_pool_n >= k;
+    const double pk_d = pool_full ? s.s_pool_d[k - 1] : dinf();
+    const int64_t pk_i = pool_full ? s.s_pool_i[k - 1] : NO_ID;
+    const double sq = dsqrt(d_qc2);
+    const uint32_t* words = a.ix.packed_msb + (int64_t)a.g * lo;
+    double qd = dinf();  // this warp's top-32 queue (lane i = i-th smallest)
+    int64_t qi = NO_ID;
+    bool any_cand = false;
+    for (int64_t c0 = 0; c0 < n_c; c0 += CHUNK) {
+      const int cn = (int)min((int64_t)CHUNK, n_c - c0);
+      if (tid == 0) s_ncand = 0;
+      __syncthreads();
+      stage1_chunk<MODE>(a, qc, words, lo, n_c, c0, cn, d_qc2, sq, T_list, s.s_planes8, s.s_lut, s.s_cv, s.s_cd,
+                         &s_ncand);
+      __syncthreads();
+      const int ncand = s_ncand;
+      if (tid == 0) {
+        s_probed += cn;
+        s_surv += ncand;
+      }
+      if (ncand == 0) continue;
+      any_cand = true;
+      if (REFINE) {
+        refine_chunk<EB>(a, qc, words, lo, n_c, c0, d_qc2, s.s_q, s.s_cv, s.s_cd, ncand);
+        __syncthreads();
+      }
+      // each warp folds its share of the candidates into its queue
+      for (int cb = wid * 32; cb < ncand; cb += THREADS) {
+        const int ci = cb + lane;
+        double d = dinf();
+        int64_t id = NO_ID;
+        if (ci < ncand) {
+          d = s.s_cd[ci];
+          id = (int64_t)__ldg(a.ix.pids + lo + c0 + s.s_cv[ci]);
+        }
+        const double wk_d = __shfl_sync(FULL, qd, k - 1);
+        const int64_t wk_i = __shfl_sync(FULL, qi, k - 1);
+        const bool pass = key_less(d, id, wk_d, wk_i) && key_less(d, id, pk_d, pk_i);
+        if (!__any_sync(FULL, pass)) continue;
+        if (!pass) {
+          d = dinf();
+          id = NO_ID;
+        }
+        warp_sort32(d, id);
+        warp_merge32(qd, qi, d, id);
+      }
+    }
+    if (!__syncthreads_or(any_cand)) continue;
+    // fold the warp queues into the pool (warp 0), then move the threshold
+    s.s_sortk[wid * 32 + lane] = qd;
+    s.s_sorti[wid * 32 + lane] = qi;
+    __syncthreads();
+    if (wid == 0) {
+      double pd = s.s_pool_d[lane];
+      int64_t pi = s.s_pool_i[lane];
+      for (int w = 0; w < WARPS; ++w) {
+        if (s.s_sorti[w * 32] == NO_ID) continue;
+        warp_merge32(pd, pi, s.s_sortk[w * 32 + lane], s.s_sorti[w * 32 + lane]);
+      }
+      s.s_pool_d[lane] = pd;
+      s.s_pool_i[lane] = pi;
+      const int cnt = __popc(__ballot_sync(FULL, lane < k && pi != NO_ID));
+      const double kd = __shfl_sync(FULL, pd, k - 1);
+      if (lane == 0) {
+        s_pool_n = cnt;
+        if (cnt >= k) s_T = kd;  // search.py:444-447
+      }
+    }
+    __syncthreads();
+  }
+  const int pn = s_pool_n;
+  for (int i = tid; i < k; i += THREADS) {
+    a.out_ids[q * k + i] = i < pn ? s.s_pool_i[i] : -1;
+    a.out_dists[q * k + i] = i < pn ? s.s_pool_d[i] : dinf();
+  }
+  if (tid == 0) {
+    a.out_counts[q] = pn;
+    if (a.stats) {
+      a.stats[2 * q] = s_probed;
+      a.stats[2 * q + 1] = s_surv;
+    }
+  }
+}
+
+// ------------------------------------------------------------ kernel, k > 32
+// block-wide bitonic sort (ascending (key, id)) of n (power of two) entries
+__device__ void bitonic_sort(double* key, int64_t* id, int n) {
+  for (int size = 2; size <= n; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      __syncthreads();
+      for (int t = threadIdx.x; t < (n >> 1); t += blockDim.x) {
+        const int lo = 2 * t - (t & (stride - 1));
+        const int hi = lo + stride;
+        const bool up = ((lo & size) == 0);
+        const double kl = key[lo], kh = key[hi];
+        const int64_t il = id[lo], ih = id[hi];
+        const bool swap = up ? key_less(kh, ih, kl, il) : key_less(kl, il, kh, ih);
+        if (swap) {
+          key[lo] = kh;
+          key[hi] = kl;
+          id[lo] = ih;
+          id[hi] = il;
+        }
+      }
+    }
+  }
+  __syncthreads();
+}
+
+template <int MODE, int EB, bool REFINE>
+__global__ void __launch_bounds__(THREADS) scan_kernel_bigk(Args a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ int s_ncand, s_nfilt, s_pool_n;
+  __shared__ double s_T;
+  __shared__ long long s_probed, s_surv;
+  const int64_t q = blockIdx.x;
+  if (q >= a.nq) return;
+  const int k = a.k;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const Smem s = carve<MODE, REFINE>(a, smem, true);
+  const QueryCtx qc = load_query<MODE, REFINE>(a, s, q);
+  if (tid == 0) {
+    s_pool_n = 0;
+    s_T = dinf();
+    s_probed = 0;
+    s_surv = 0;
+  }
+  __syncthreads();
+  const int64_t* pid_list = a.probe_ids + q * a.nprobe;
+  const double* pd2_list = a.probe_d2 + q * a.nprobe;
+  for (int p = 0; p < a.nprobe; ++p) {
+    const int64_t c = pid_list[p];
+    const double d_qc2 = pd2_list[p];
+    const int64_t lo = a.ix.offsets[c], n_c = a.ix.offsets[c + 1] - lo;
+    if (n_c == 0) continue;
+    const double T_list = a.prune ? s_T : dinf();
+    const double sq = dsqrt(d_qc2);
+    const uint32_t* words = a.ix.packed_msb + (int64_t)a.g * lo;
+    for (int64_t c0 = 0; c0 < n_c; c0 += CHUNK) {
+      const int cn = (int)min((int64_t)CHUNK, n_c - c0);
+      if (tid == 0) s_ncand = 0;
+      __syncthreads();
+      stage1_chunk<MODE>(a, qc, words, lo, n_c, c0, cn, d_qc2, sq, T_list, s.s_planes8, s.s_lut, s.s_cv, s.s_cd,
+                         &s_ncand);
+      __syncthreads();
+      const int ncand = s_ncand;
+      if (tid == 0) {
+        s_probed += cn;
+        s_surv += ncand;
+      }
+      if (ncand == 0) continue;
+      if (REFINE) {
+        refine_chunk<EB>(a, qc, words, lo, n_c, c0, d_qc2, s.s_q, s.s_cv, s.s_cd, ncand);
+        __syncthreads();
+      }
+      if (tid == 0) s_nfilt = 0;
+      __syncthreads();
+      const int pn = s_pool_n;
+      const bool full = pn >= k;
+      const double kd = full ? s.s_pool_d[k - 1] : 0.0;
+      const int64_t kid = full ? s.s_pool_i[k - 1] : 0;
+      for (int cb = 0; cb < ncand; cb += THREADS) {
+        const int ci = cb + tid;
+        bool pass = false;
+        double dist = 0.0;
+        int64_t pid = 0;
+        if (ci < ncand) {
+          dist = s.s_cd[ci];
+          pid = (int64_t)__ldg(a.ix.pids + lo + c0 + s.s_cv[ci]);
+          pass = !full || key_less(dist, pid, kd, kid);
+        }
+        const unsigned pb = __ballot_sync(FULL, pass);
+        int base = 0;
+        if (lane == 0 && pb) base = atomicAdd(&s_nfilt, __popc(pb));
+        base = __shfl_sync(FULL, base, 0);
+        if (pass) {
+          const int pos = pn + base + __popc(pb & ((1u << lane) - 1u));
+          s.s_sortk[pos] = dist;
+          s.s_sorti[pos] = pid;
+        }
+      }
+      __syncthreads();
+      const int m = s_nfilt;
+      if (m > 0) {
+        for (int i = tid; i < pn; i += THREADS) {
+          s.s_sortk[i] = s.s_pool_d[i];
+          s.s_sorti[i] = s.s_pool_i[i];
+        }
+        const int tot = pn + m;
+        int n2 = 1;
+        while (n2 < tot) n2 <<= 1;
+        for (int i = tot + tid; i < n2; i += THREADS) {
+          s.s_sortk[i] = dinf();
+          s.s_sorti[i] = NO_ID;
+        }
+        bitonic_sort(s.s_sortk, s.s_sorti, n2);
+        const int newn = min(tot, k);
+        for (int i = tid; i < newn; i += THREADS) {
+          s.s_pool_d[i] = s.s_sortk[i];
+          s.s_pool_i[i] = s.s_sorti[i];
+        }
+        __syncthreads();
+        if (tid == 0) s_pool_n = newn;
+      }
+      __syncthreads();
+    }
+    if (tid == 0 && s_pool_n >= k) s_T = s.s_pool_d[k - 1];
+    __syncthreads();
+  }
+  const int pn = s_pool_n;
+  for (int i = tid; i < k; i += THREADS) {
+    a.out_ids[q * k + i] = i < pn ? s.s_pool_i[i] : -1;
+    a.out_dists[q * k + i] = i < pn ? s.s_pool_d[i] : dinf();
+  }
+  if (tid == 0) {
+    a.out_counts[q] = pn;
+    if (a.stats) {
+      a.stats[2 * q] = s_probed;
+      a.stats[2 * q + 1] = s_surv;
+    }
+  }
+}
+
+template <int MODE, int EB, bool REFINE>
+int launch_t(const Args& a, cudaStream_t s) {
+  const bool bigk = a.k > 32;
+  const size_t sm = smem_bytes(a, MODE, REFINE, bigk);
+  auto kern = bigk ? scan_kernel_bigk<MODE, EB, REFINE> : scan_kernel<MODE, EB, REFINE>;
+  if (sm > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return fail(IVRQ_EUNSUP, "ivrq_search_scan: shared memory request too large");
+  }
+  kern<<<(unsigned)a.nq, THREADS, sm, s>>>(a);
+  return check_launch("ivrq_search_scan");
+}
+
+template <int MODE>
+int launch_mode(const Args& a, bool refine, cudaStream_t s) {
+  if (!refine) return launch_t<MODE, 0, false>(a, s);
+  switch (a.eb) {
+    case 1: return launch_t<MODE, 1, true>(a, s);
+    case 2: return launch_t<MODE, 2, true>(a, s);
+    case 3: return launch_t<MODE, 3, true>(a, s);
+    case 4: return launch_t<MODE, 4, true>(a, s);
+    case 5: return launch_t<MODE, 5, true>(a, s);
+    case 6: return launch_t<MODE, 6, true>(a, s);
+    case 7: return launch_t<MODE, 7, true>(a, s);
+    default: return fail(IVRQ_EUNSUP, "ivrq_search_scan: bits out of range");
+  }
+}
+
+}  // namespace scan
+}  // namespace ivrq
+
+using namespace ivrq;
+
+extern "C" int ivrq_search_scan(const ivrq_index_view* index, const double* q_rot, const int64_t* probe_ids,
+                                const double* probe_d2, const double* scalars, const uint32_t* planes,
+                                const float* luts, int64_t nq, const ivrq_search_params* params,
+                                int64_t* out_ids, double* out_dists, int32_t* out_counts, int64_t* stats,
+                                void* stream) {
+  if (!index || !params) return fail(IVRQ_EINVAL, "ivrq_search_scan: null argument");
+  if (params->k < 1) return fail(IVRQ_EINVAL, "k must be >= 1");
+  if (params->k > 4096) return fail(IVRQ_EUNSUP, "ivrq_search_scan: k > 4096 not supported");
+  if (index->bits < 1 || index->bits > 8) return fail(IVRQ_EINVAL, "index bits out of range");
+  if (nq == 0) return IVRQ_OK;
+  scan::Args a{};
+  a.ix = *index;
+  a.q_rot = q_rot;
+  a.probe_ids = probe_ids;
+  a.probe_d2 = probe_d2;
+  a.scalars = scalars;
+  a.planes = planes;
+  a.luts = luts;
+  a.nq = nq;
+  a.k = params->k;
+  a.nprobe = params->n_probe;
+  a.qbits = params->query_bits;
+  a.prune = params->prune;
+  a.g = words_per_vector(index->dims);
+  a.eb = index->bits - 1;
+  a.exw = a.eb * a.g;
+  int n2 = 1;
+  while (n2 < scan::CHUNK + a.k) n2 <<= 1;
+  a.sort_n = n2;
+  a.out_ids = out_ids;
+  a.out_dists = out_dists;
+  a.out_counts = out_counts;
+  a.stats = stats;
+  const bool refine = params->refine && index->bits >= 2;
+  cudaStream_t s = as_stream(stream);
+  if (params->ip_mode == IVRQ_IP_BITWISE) return scan::launch_mode<IVRQ_IP_BITWISE>(a, refine, s);
+  return scan::launch_mode<IVRQ_IP_LUT>(a, refine, s);
+}
