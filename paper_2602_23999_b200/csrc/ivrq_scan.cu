@@ -18,7 +18,7 @@ namespace scan {
 
 constexpr int THREADS = 256;
 constexpr int WARPS = THREADS / 32;
-constexpr int CHUNK = 1024;            // vectors of one list per stage-1 pass
+constexpr int CHUNK = 512;             // vectors of one list per stage-1 pass
 constexpr int VPT = CHUNK / THREADS;   // vectors per thread per pass
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int64_t NO_ID = 0x7fffffffffffffffLL;
@@ -43,6 +43,10 @@ struct Args {
 
 __device__ __forceinline__ double dinf() { return __longlong_as_double(0x7ff0000000000000LL); }
 
+// rotated query in smem, transposed: element (group gi, dim i) at i * qstride + gi,
+// so the lanes of a refine (one 32-dim group each) read consecutive words
+__host__ __device__ __forceinline__ int qstride(int g) { return g | 1; }
+
 // ------------------------------------------------------------ per-query state in smem
 struct QueryCtx {
   double delta, half_code, ipm, kb_sum;
@@ -51,7 +55,7 @@ struct QueryCtx {
 // ------------------------------------------------------------ stage 1
 // Fills s_cv (row within list) / s_cd (stage-1 estimate) with the survivors of
 // vectors [c0, c0+cn) of the list; returns the count via s_ncand.
-template <int MODE>
+template <int MODE, int QB>
 __device__ __forceinline__ void stage1_chunk(const Args& a, const QueryCtx& qc, const uint32_t* __restrict__ words,
                                              int64_t lo, int64_t n_c, int64_t c0, int cn, double d_qc2, double sq,
                                              double T_list, const uint32_t* s_planes8, const float* s_lut,
@@ -63,22 +67,29 @@ __device__ __forceinline__ void stage1_chunk(const Args& a, const QueryCtx& qc, 
     int pos[VPT], last[VPT];
 #pragma unroll
     for (int u = 0; u < VPT; ++u) pos[u] = last[u] = 0;
-    const int qb = a.qbits;
+    const int qb = QB ? QB : a.qbits;
     for (int gi = 0; gi < g; ++gi) {
       const uint4 pa = *reinterpret_cast<const uint4*>(s_planes8 + gi * 8);
-      const uint4 pb = *reinterpret_cast<const uint4*>(s_planes8 + gi * 8 + 4);
+      uint4 pb = make_uint4(0u, 0u, 0u, 0u);
+      if (QB == 0 || QB > 4) pb = *reinterpret_cast<const uint4*>(s_planes8 + gi * 8 + 4);
       const uint32_t pl[8] = {pa.x, pa.y, pa.z, pa.w, pb.x, pb.y, pb.z, pb.w};
       const uint32_t* wrow = words + (int64_t)gi * n_c + c0;
 #pragma unroll
       for (int u = 0; u < VPT; ++u) {
         const int vi = tid + u * THREADS;
         const uint32_t w = vi < cn ? __ldg(wrow + vi) : 0u;
+        if (QB) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          if (j < qb) {
-            const int c = __popc(w & pl[j]);
-            pos[u] += c << j;
-            if (j == qb - 1) last[u] += c;
+          for (int j = 0; j < QB; ++j) pos[u] += __popc(w & pl[j]) << j;
+          last[u] += __popc(w & pl[QB - 1]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            if (j < qb) {
+              const int c = __popc(w & pl[j]);
+              pos[u] += c << j;
+              if (j == qb - 1) last[u] += c;
+            }
           }
         }
       }
@@ -120,10 +131,23 @@ __device__ __forceinline__ void stage1_chunk(const Args& a, const QueryCtx& qc, 
         const double err = (double)__ldg(a.ix.short_err + row);
         double margin = dmul(err, sq);
         if (qc.ipm != 0.0) {
+          // margin = sqrt(margin^2 + (scale*ipm)^2); decide lb2 <= T from the
+          // squares when the answer is unambiguous by a wide (2^-38) margin,
+          // otherwise evaluate the reference expression exactly.
           const double sm = dmul(scale, qc.ipm);
-          margin = dsqrt(dadd(dmul(margin, margin), dmul(sm, sm)));
+          const double S = dadd(dmul(margin, margin), dmul(sm, sm));
+          const double gap = dsub(est2, T_list);
+          const double g2 = dmul(gap, gap);
+          if (S >= g2 * (1.0 + 0x1p-38)) {
+            keep = true;
+          } else if (S <= g2 * (1.0 - 0x1p-38) && gap > T_list * 0x1p-12) {
+            keep = false;
+          } else {
+            keep = dmax(dsub(est2, dsqrt(S)), 0.0) <= T_list;
+          }
+        } else {
+          keep = dmax(dsub(est2, margin), 0.0) <= T_list;
         }
-        keep = dmax(dsub(est2, margin), 0.0) <= T_list;
       }
     }
     const unsigned kb = __ballot_sync(FULL, keep);
@@ -141,12 +165,19 @@ __device__ __forceinline__ void stage1_chunk(const Args& a, const QueryCtx& qc, 
 // ------------------------------------------------------------ stage 2
 // Extract the 32 ex-code fields (eb bits each, LSB-first) of one 32-dim group
 // and accumulate sum_i u_i * q_i with u_i = msb_i << eb | ex_i.
+// u -> double without the quarter-rate I2F.F64: 2^52 + u has u in its low
+// mantissa bits, so one exact DADD recovers u.
+__device__ __forceinline__ double u2d(uint32_t u) {
+  return __dsub_rn(__hiloint2double(0x43300000, (int)u), 4503599627370496.0);
+}
+
+// q points at dim 0 of the group in the transposed query (stride qs between dims).
 template <int EB>
-__device__ __forceinline__ double group_dot(const uint32_t* __restrict__ exg, uint32_t msb, const double* q) {
+__device__ __forceinline__ double group_dot(const uint32_t* __restrict__ exg, uint32_t msb, const double* q, int qs) {
   double acc = 0.0;
   if constexpr (EB == 0) {
 #pragma unroll
-    for (int i = 0; i < 32; ++i) acc = fma((double)((msb >> i) & 1u), q[i], acc);
+    for (int i = 0; i < 32; ++i) acc = fma(u2d((msb >> i) & 1u), q[i * qs], acc);
   } else {
     uint32_t w[EB + 1];
 #pragma unroll
@@ -160,7 +191,7 @@ __device__ __forceinline__ double group_dot(const uint32_t* __restrict__ exg, ui
       const uint64_t win = ((uint64_t)w[wi + 1] << 32) | (uint64_t)w[wi];
       const uint32_t field = (uint32_t)(win >> off) & mask;
       const uint32_t u = ((((msb >> i) & 1u)) << EB) | field;
-      acc = fma((double)u, q[i], acc);
+      acc = fma(u2d(u), q[i * qs], acc);
     }
   }
   return acc;
@@ -187,7 +218,7 @@ __device__ __forceinline__ void refine_chunk(const Args& a, const QueryCtx& qc, 
       const uint32_t* exrow = a.ix.excodes + row * a.exw;
       for (int gi = sl; gi < g; gi += lpc) {
         const uint32_t msb = __ldg(words + (int64_t)gi * n_c + v);
-        acc += group_dot<EB>(exrow + gi * EB, msb, s_q + gi * 32);
+        acc += group_dot<EB>(exrow + gi * EB, msb, s_q + gi, qstride(g));
       }
     }
     for (int o = lpc >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
@@ -254,7 +285,7 @@ __device__ __forceinline__ Smem carve(const Args& a, unsigned char* smem, bool b
   const int g = a.g;
   unsigned char* p = smem;
   s.s_q = reinterpret_cast<double*>(p);
-  p += REFINE ? sizeof(double) * 32 * g : 0;
+  p += REFINE ? sizeof(double) * 32 * qstride(g) : 0;
   s.s_cd = reinterpret_cast<double*>(p);
   p += sizeof(double) * CHUNK;
   s.s_pool_d = reinterpret_cast<double*>(p);
@@ -275,7 +306,7 @@ __device__ __forceinline__ Smem carve(const Args& a, unsigned char* smem, bool b
 
 size_t smem_bytes(const Args& a, int mode, bool refine, bool bigk) {
   size_t b = 0;
-  b += refine ? sizeof(double) * 32 * a.g : 0;
+  b += refine ? sizeof(double) * 32 * qstride(a.g) : 0;
   b += sizeof(double) * CHUNK;
   b += (sizeof(double) + sizeof(int64_t)) * (bigk ? a.k : 32);
   b += (sizeof(double) + sizeof(int64_t)) * (bigk ? a.sort_n : WARPS * 32);
@@ -288,7 +319,10 @@ template <int MODE, bool REFINE>
 __device__ __forceinline__ QueryCtx load_query(const Args& a, const Smem& s, int64_t q) {
   const int g = a.g, d = a.ix.dims, tid = threadIdx.x;
   if (REFINE)
-    for (int i = tid; i < 32 * g; i += THREADS) s.s_q[i] = i < d ? a.q_rot[q * d + i] : 0.0;
+    for (int i = tid; i < 32 * qstride(g); i += THREADS) {
+      const int dim = (i % qstride(g)) * 32 + i / qstride(g);
+      s.s_q[i] = (i % qstride(g)) < g && dim < d ? a.q_rot[q * d + dim] : 0.0;
+    }
   if (MODE == IVRQ_IP_BITWISE) {
     for (int i = tid; i < 8 * g; i += THREADS) {
       const int gi = i / 8, j = i % 8;
@@ -307,7 +341,7 @@ __device__ __forceinline__ QueryCtx load_query(const Args& a, const Smem& s, int
 }
 
 // ------------------------------------------------------------ kernel, k <= 32
-template <int MODE, int EB, bool REFINE>
+template <int MODE, int EB, bool REFINE, int QB>
 __global__ void __launch_bounds__(THREADS) scan_kernel(Args a) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int s_ncand;
@@ -351,7 +385,7 @@ __global__ void __launch_bounds__(THREADS) scan_kernel(Args a) {
       const int cn = (int)min((int64_t)CHUNK, n_c - c0);
       if (tid == 0) s_ncand = 0;
       __syncthreads();
-      stage1_chunk<MODE>(a, qc, words, lo, n_c, c0, cn, d_qc2, sq, T_list, s.s_planes8, s.s_lut, s.s_cv, s.s_cd,
+      stage1_chunk<MODE, QB>(a, qc, words, lo, n_c, c0, cn, d_qc2, sq, T_list, s.s_planes8, s.s_lut, s.s_cv, s.s_cd,
                          &s_ncand);
       __syncthreads();
       const int ncand = s_ncand;
@@ -448,7 +482,7 @@ __device__ void bitonic_sort(double* key, int64_t* id, int n) {
   __syncthreads();
 }
 
-template <int MODE, int EB, bool REFINE>
+template <int MODE, int EB, bool REFINE, int QB>
 __global__ void __launch_bounds__(THREADS) scan_kernel_bigk(Args a) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int s_ncand, s_nfilt, s_pool_n;
@@ -481,7 +515,7 @@ __global__ void __launch_bounds__(THREADS) scan_kernel_bigk(Args a) {
       const int cn = (int)min((int64_t)CHUNK, n_c - c0);
       if (tid == 0) s_ncand = 0;
       __syncthreads();
-      stage1_chunk<MODE>(a, qc, words, lo, n_c, c0, cn, d_qc2, sq, T_list, s.s_planes8, s.s_lut, s.s_cv, s.s_cd,
+      stage1_chunk<MODE, QB>(a, qc, words, lo, n_c, c0, cn, d_qc2, sq, T_list, s.s_planes8, s.s_lut, s.s_cv, s.s_cd,
                          &s_ncand);
       __syncthreads();
       const int ncand = s_ncand;
@@ -566,7 +600,9 @@ template <int MODE, int EB, bool REFINE>
 int launch_t(const Args& a, cudaStream_t s) {
   const bool bigk = a.k > 32;
   const size_t sm = smem_bytes(a, MODE, REFINE, bigk);
-  auto kern = bigk ? scan_kernel_bigk<MODE, EB, REFINE> : scan_kernel<MODE, EB, REFINE>;
+  const bool qb4 = MODE == IVRQ_IP_BITWISE && a.qbits == 4;  // the SearchParams default
+  auto kern = bigk ? (qb4 ? scan_kernel_bigk<MODE, EB, REFINE, 4> : scan_kernel_bigk<MODE, EB, REFINE, 0>)
+                   : (qb4 ? scan_kernel<MODE, EB, REFINE, 4> : scan_kernel<MODE, EB, REFINE, 0>);
   if (sm > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return fail(IVRQ_EUNSUP, "ivrq_search_scan: shared memory request too large");
