@@ -21,11 +21,14 @@
  *                                             (codec.py:98-115, index.py:114-118)
  *   short_add/short_scale/short_err float[size]   SoA split of short_factors
  *   long_factors float2[size]                 (add, scale)  (index.py:104)
- *   excodes     uint32[size*exw], exw=(bits-1)*g  per-vector LSB-first bit stream
- *                                             of the (bits-1)-bit ex-codes, i.e.
- *                                             the IVRQ1 excodes row zero-padded to
- *                                             a whole number of 32-dim groups
- *                                             (codec.py:432-444)
+ *   rcodes      uint8 [size*rcode_bytes]      full unsigned codes u = msb<<(bits-1) | ex
+ *                                             per vector for the tensor-core refine:
+ *                                             kpad = round_up(dims, 64); bits >= 5:
+ *                                             one byte per dim (kpad bytes); 2 <= bits
+ *                                             <= 4: two dims per byte, dim 2j in the
+ *                                             low nibble (kpad/2 bytes); none for
+ *                                             bits == 1.  The IVRQ1 ex-codes
+ *                                             (codec.py:432-444) are u's low bits.
  *   pids        int64 [size]                  original row ids (index.py:105)
  *   centroids   float [n_clusters*dims]       rotated centroids (index.py:235)
  *   centroid_sqnorms double[n_clusters]       einsum-order squared norms
@@ -74,7 +77,8 @@ typedef struct {
   const float* short_scale;
   const float* short_err;
   const float* long_factors;
-  const uint32_t* excodes;
+  const uint8_t* rcodes;
+  int64_t rcode_bytes; /* row stride of rcodes, ivrq_rcode_row_bytes(dims, bits) */
   const int64_t* pids;
   const float* centroids;
   const double* centroid_sqnorms;
@@ -99,6 +103,7 @@ enum {
   IVRQ_QS_IP_MARGIN = 3,  /* ip_margin (search.py:213)                         */
   IVRQ_QS_KB_SUM = 4,     /* k_b * sum_q used by the refine (search.py:323)    */
   IVRQ_QS_HALF_CODE = 5,  /* 0.5 * code_sum_q (search.py:281)                  */
+  IVRQ_QS_SLICE_EXP = 6,  /* e: q_rot ~ sum_s slice_s * 128^(7-s) * 2^(e-55)   */
   IVRQ_QS_COUNT = 8
 };
 
@@ -107,6 +112,9 @@ IVRQ_API int ivrq_abi_version(void);
 IVRQ_API const char* ivrq_last_error(void);
 /* Number of SMs of `device` (synchronous; for host-side grid sizing). */
 IVRQ_API int ivrq_device_sm_count(int device, int* out);
+
+/* Bytes per vector of the rcodes layout (0 for bits == 1). */
+IVRQ_API int64_t ivrq_rcode_row_bytes(int32_t dims, int32_t bits);
 
 /* Row-wise np.einsum("ij,ij->i", X, X) in float64, bit-exact to NumPy's
  * 2-lane reduction order.  Replaces Centroids.from_values
@@ -145,24 +153,31 @@ IVRQ_API int ivrq_select_clusters_ordered(const double* q_rot, int64_t nq, int32
 
 /* Per-query state (_prepare_from_rotated, search.py:186-214; build_luts 115-132).
  * scalars: double[nq*IVRQ_QS_COUNT]; planes: uint32[nq*query_bits*g] (bitwise
- * mode, else may be NULL); luts: float[nq*8*g*16] (lut mode, else may be NULL). */
+ * mode, else may be NULL); luts: float[nq*8*g*16] (lut mode, else may be NULL);
+ * qslices: int8[nq*8*kpad] (refine of a multi-bit index, else may be NULL):
+ * q_rot as a 55-bit fixed-point number split into 8 balanced base-128 digits,
+ * laid out in the K order of the refine's int8 MMA fragments. */
 IVRQ_API int ivrq_prepare_queries(const double* q_rot, int64_t nq, int32_t dims,
                          const ivrq_search_params* params, int32_t index_bits, double eps_bound,
-                         double* scalars, uint32_t* planes, float* luts, void* stream);
+                         double* scalars, uint32_t* planes, float* luts, int8_t* qslices,
+                         void* stream);
 
 /* The fused two-stage list scan + top-k (the per-query loop of search_batch,
  * search.py:425-448, with cluster_local_search 326-375 and merge_topk 378-387).
  * Each query visits its probed lists in ascending cluster id and carries its
  * pruning threshold from list to list exactly as the reference does.
- * probe_ids/probe_d2: [nq*n_probe] as written by ivrq_select_clusters.
+ * probe_ids/probe_d2: [nq*n_probe] as written by ivrq_select_clusters_ordered
+ * (ascending id).  scalars/planes/luts/qslices come from ivrq_prepare_queries;
+ * q_rot is not read (the refine uses the exact digit slices of q_rot).
  * Outputs: out_ids int64[nq*k], out_dists double[nq*k] (ascending (dist, id)),
  * out_counts int32[nq]; stats (may be NULL) int64[nq*2] = (vectors probed,
  * stage-1 survivors) per query. */
-IVRQ_API int ivrq_search_scan(const ivrq_index_view* index, const double* q_rot, const int64_t* probe_ids,
-                     const double* probe_d2, const double* scalars, const uint32_t* planes,
-                     const float* luts, int64_t nq, const ivrq_search_params* params,
-                     int64_t* out_ids, double* out_dists, int32_t* out_counts, int64_t* stats,
-                     void* stream);
+IVRQ_API int ivrq_search_scan(const ivrq_index_view* index, const double* q_rot,
+                              const int64_t* probe_ids, const double* probe_d2,
+                              const double* scalars, const uint32_t* planes, const float* luts,
+                              const int8_t* qslices, int64_t nq, const ivrq_search_params* params,
+                              int64_t* out_ids, double* out_dists, int32_t* out_counts,
+                              int64_t* stats, void* stream);
 
 /* ---------------------------------------------------------------- build */
 /* k-means++ seeding (_kmeans_pp_init, clustering.py:60-79) on x float[n*d]
@@ -219,20 +234,26 @@ IVRQ_API int ivrq_normalize_rotate(const float* x, const int64_t* order, const i
 IVRQ_API int ivrq_rotate_rows_f32(const float* x, int64_t n, int32_t d, const float* rotation, float* out,
                          void* stream);
 
+/* rcodes of an index given in IVRQ1 arrays (load_index path): u rebuilt from the
+ * interleaved MSB plane and the ex-code byte stream (excodes uint8[n*bpv]). */
+IVRQ_API int ivrq_make_rcodes(const uint32_t* packed_msb, const int64_t* offsets, int32_t n_clusters,
+                              const uint8_t* excodes, int64_t n, int32_t d, int32_t bits,
+                              uint8_t* rcodes, void* stream);
+
 /* RaBitQ encoder, one warp per vector (quantize_batch codec.py:204-244,
  * split_planes 306-319, compute_factors_batch 322-380, pack_interleaved 404-413,
  * pack_excodes 432-444), writing the device list layout directly.
  * o_rot float[n*d] or double[n*d] (o_is_f64; the grid search runs in that
  * dtype exactly like NumPy does), unit or zero rows in CSR order, dist double[n], cent_rot
  * float[n_clusters*d], offsets int64[n_clusters+1].
- * Outputs: packed_msb, excodes (NULL when bits == 1), short SoA, long float2,
+ * Outputs: packed_msb, rcodes (NULL when bits == 1), short SoA, long float2,
  * optionally codes uint8[n*d] (full unsigned codes u) and t float[n].
  * bad_rows (device int32[1], caller-initialised 0) counts rows whose norm
  * differs from 1 by more than 1e-4 (_check_unit_rows, codec.py:154-160). */
 IVRQ_API int ivrq_encode(const void* o_rot, int32_t o_is_f64, const double* dist, const float* cent_rot,
                 const int64_t* offsets, int32_t n_clusters, int64_t n, int32_t d, int32_t bits,
                 int32_t n_coarse, int32_t n_fine, double eps_bound, uint32_t* packed_msb,
-                uint32_t* excodes, float* short_add, float* short_scale, float* short_err,
+                uint8_t* rcodes, float* short_add, float* short_scale, float* short_err,
                 float* long_factors, uint8_t* codes, double* t_out, int32_t* bad_rows,
                 void* stream);
 

@@ -25,7 +25,7 @@ IVRQ_EUNSUP = -4
 IVRQ_IP_LUT = 0
 IVRQ_IP_BITWISE = 1
 
-QS_SUM_Q, QS_DELTA, QS_CODE_SUM, QS_IP_MARGIN, QS_KB_SUM, QS_HALF_CODE = range(6)
+QS_SUM_Q, QS_DELTA, QS_CODE_SUM, QS_IP_MARGIN, QS_KB_SUM, QS_HALF_CODE, QS_SLICE_EXP = range(7)
 QS_COUNT = 8
 
 
@@ -43,7 +43,8 @@ class IndexView(ctypes.Structure):
         ("short_scale", c_void_p),
         ("short_err", c_void_p),
         ("long_factors", c_void_p),
-        ("excodes", c_void_p),
+        ("rcodes", c_void_p),
+        ("rcode_bytes", c_int64),
         ("pids", c_void_p),
         ("centroids", c_void_p),
         ("centroid_sqnorms", c_void_p),
@@ -83,12 +84,14 @@ _SIGNATURES: dict[str, tuple[object, list[object]]] = {
     ),
     "ivrq_prepare_queries": (
         c_int,
-        [P, c_int64, c_int32, POINTER(SearchParamsC), c_int32, c_double, P, P, P, P],
+        [P, c_int64, c_int32, POINTER(SearchParamsC), c_int32, c_double, P, P, P, P, P],
     ),
     "ivrq_search_scan": (
         c_int,
-        [POINTER(IndexView), P, P, P, P, P, P, c_int64, POINTER(SearchParamsC), P, P, P, P, P],
+        [POINTER(IndexView), P, P, P, P, P, P, P, c_int64, POINTER(SearchParamsC), P, P, P, P, P],
     ),
+    "ivrq_rcode_row_bytes": (c_int64, [c_int32, c_int32]),
+    "ivrq_make_rcodes": (c_int, [P, P, c_int32, P, c_int64, c_int32, c_int32, P, P]),
     "ivrq_kmeanspp": (
         c_int,
         [P, c_int64, c_int32, c_int32, c_int32, c_int32, P, c_int32, P, P, P, P],

@@ -33,6 +33,7 @@ __all__ = [
     "quantize_batch",
     "quantize_vector",
     "encode_rows",
+    "rcode_row_bytes",
 ]
 
 
@@ -156,6 +157,38 @@ def unpack_excodes(packed: np.ndarray, dims: int, bits: int) -> np.ndarray:
     return out
 
 
+# ---------------------------------------------------------------- refine code rows
+
+
+def kpad64(dims: int) -> int:
+    return (dims + 63) // 64 * 64
+
+
+def rcode_row_bytes(dims: int, bits: int) -> int:
+    """Bytes per vector of the device ``rcodes`` rows (see include/ivrq_b200.h)."""
+    if bits <= 1:
+        return 0
+    return kpad64(dims) // 2 if bits <= 4 else kpad64(dims)
+
+
+def codes_from_rcodes(rcodes: np.ndarray, dims: int, bits: int) -> np.ndarray:
+    """Full unsigned codes (n, dims) from rcodes rows (host view)."""
+    rc = np.asarray(rcodes, dtype=np.uint8).reshape(-1, rcode_row_bytes(dims, bits))
+    if bits <= 4:
+        u = np.empty((rc.shape[0], rc.shape[1] * 2), dtype=np.uint8)
+        u[:, 0::2] = rc & 15
+        u[:, 1::2] = rc >> 4
+    else:
+        u = rc
+    return np.ascontiguousarray(u[:, :dims])
+
+
+def excodes_from_rcodes(rcodes: np.ndarray, dims: int, bits: int) -> np.ndarray:
+    """IVRQ1 ex-code bytes (codec.py:432-444) derived from rcodes rows."""
+    u = codes_from_rcodes(rcodes, dims, bits)
+    return pack_excodes(u & np.uint8((1 << (bits - 1)) - 1), bits)
+
+
 # ---------------------------------------------------------------- GPU encoder
 
 
@@ -169,7 +202,7 @@ def encode_rows(
 ) -> dict[str, torch.Tensor]:
     """Run the warp-per-vector encoder over CSR-ordered rows (device tensors).
 
-    Returns the device list layout (packed_msb, excodes words, short SoA, long
+    Returns the device list layout (packed_msb, rcodes rows, short SoA, long
     float2) plus optionally the full codes ``u`` and factors ``t``.
     """
     n, d = o_rot.shape
@@ -179,7 +212,7 @@ def encode_rows(
     device = o_rot.device
     out = {
         "packed_msb": torch.empty(n * g, dtype=torch.int32, device=device),
-        "excodes": torch.empty(n * eb * g if eb else 0, dtype=torch.int32, device=device),
+        "rcodes": torch.empty(n * rcode_row_bytes(d, params.bits), dtype=torch.uint8, device=device),
         "short_add": torch.empty(n, dtype=torch.float32, device=device),
         "short_scale": torch.empty(n, dtype=torch.float32, device=device),
         "short_err": torch.empty(n, dtype=torch.float32, device=device),
@@ -204,7 +237,7 @@ def encode_rows(
         params.n_fine,
         float(params.eps_bound),
         dev.ptr(out["packed_msb"]),
-        dev.ptr(out["excodes"]) if eb else None,
+        dev.ptr(out["rcodes"]) if eb else None,
         dev.ptr(out["short_add"]),
         dev.ptr(out["short_scale"]),
         dev.ptr(out["short_err"]),

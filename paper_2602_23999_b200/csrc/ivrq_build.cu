@@ -492,7 +492,8 @@ __device__ __forceinline__ void warp_best(double& v, int& s) {
 
 struct Out {
   uint32_t* packed;
-  uint32_t* ex;
+  uint8_t* rc;
+  int64_t rb;
   float* sadd;
   float* sscale;
   float* serr;
@@ -514,7 +515,7 @@ __global__ void __launch_bounds__(WARPS * 32) encode_kernel(const T* __restrict_
   const int eb = bits - 1;
   T* so = reinterpret_cast<T*>(esm) + (size_t)w * g * 32;
   uint8_t* su = reinterpret_cast<uint8_t*>(reinterpret_cast<T*>(esm) + (size_t)WARPS * g * 32) + (size_t)w * g * 32;
-  __shared__ uint32_t exw_s[WARPS][8];
+
   const int64_t r = (int64_t)blockIdx.x * WARPS + w;
   if (r >= n) return;
   // cluster of row r: last c with offsets[c] <= r (non-empty)
@@ -616,20 +617,19 @@ __global__ void __launch_bounds__(WARPS * 32) encode_kernel(const T* __restrict_
     unsigned word = __ballot_sync(0xffffffffu, bit);
     if (lane == 0) out.packed[g * lo + (int64_t)gi * n_c + v] = word;
   }
-  // ---- pack ex-codes: LSB-first bit stream per vector (codec.py:432-444)
+  // ---- full codes for the tensor-core refine (rcodes layout, ivrq_b200.h);
+  // the IVRQ1 ex-codes (codec.py:432-444) are their low bits.
   if (eb > 0) {
-    const int exw = eb * g;
-    for (int gi = 0; gi < g; ++gi) {
-      if (lane < 8) exw_s[w][lane] = 0u;
-      __syncwarp();
-      int dim = gi * 32 + lane;
-      uint32_t field = dim < d ? (uint32_t)(su[dim] & ((1 << eb) - 1)) : 0u;
-      int bit = lane * eb, wi = bit >> 5, off = bit & 31;
-      atomicOr(&exw_s[w][wi], field << off);
-      if (off + eb > 32) atomicOr(&exw_s[w][wi + 1], field >> (32 - off));
-      __syncwarp();
-      if (lane < eb) out.ex[r * exw + gi * eb + lane] = exw_s[w][lane];
-      __syncwarp();
+    const int kp = kpad64(d);
+    uint8_t* dst = out.rc + r * out.rb;
+    if (rcode_nibbles(bits)) {
+      for (int j = lane; j < kp / 2; j += 32) {
+        const int d0 = 2 * j, d1 = 2 * j + 1;
+        const uint32_t lo4 = d0 < d ? su[d0] : 0u, hi4 = d1 < d ? su[d1] : 0u;
+        dst[j] = (uint8_t)(lo4 | (hi4 << 4));
+      }
+    } else {
+      for (int j = lane; j < kp; j += 32) dst[j] = j < d ? su[j] : (uint8_t)0;
     }
   }
   // ---- factors (codec.py:355-379): five einsums, lanes 2e / 2e+1 own the
@@ -908,14 +908,15 @@ extern "C" int ivrq_rotate_rows_f32(const float* x, int64_t n, int32_t d, const 
 extern "C" int ivrq_encode(const void* o_rot, int32_t o_is_f64, const double* dist, const float* cent_rot,
                            const int64_t* offsets, int32_t n_clusters, int64_t n, int32_t d, int32_t bits,
                            int32_t n_coarse, int32_t n_fine, double eps_bound, uint32_t* packed_msb,
-                           uint32_t* excodes, float* short_add, float* short_scale, float* short_err,
+                           uint8_t* rcodes, float* short_add, float* short_scale, float* short_err,
                            float* long_factors, uint8_t* codes, double* t_out, int32_t* bad_rows, void* stream) {
   if (bits < 1 || bits > 8) return fail(IVRQ_EINVAL, "bits must be in [1, 8]");
   if (n_coarse < 2 || n_fine < 2) return fail(IVRQ_EINVAL, "n_coarse and n_fine must both be >= 2");
-  if (bits > 1 && !excodes) return fail(IVRQ_EINVAL, "ivrq_encode: excodes required for bits > 1");
+  if (bits > 1 && !rcodes) return fail(IVRQ_EINVAL, "ivrq_encode: rcodes required for bits > 1");
   if (n == 0) return IVRQ_OK;
   if (d > 4096) return fail(IVRQ_EUNSUP, "ivrq_encode: dims > 4096");
-  enc::Out out{packed_msb, excodes, short_add, short_scale, short_err, long_factors, codes, t_out, bad_rows};
+  enc::Out out{packed_msb, rcodes, rcode_row_bytes_of(d, bits), short_add, short_scale, short_err, long_factors,
+               codes, t_out, bad_rows};
   const int g = words_per_vector(d);
   cudaStream_t s = as_stream(stream);
   const unsigned grid = (unsigned)ceil_div(n, enc::WARPS);
@@ -933,4 +934,53 @@ extern "C" int ivrq_encode(const void* o_rot, int32_t o_is_f64, const double* di
                                                                 out);
   }
   return check_launch("ivrq_encode");
+}
+
+// ============================================================ rcodes from IVRQ1 arrays
+namespace ivrq {
+// One warp per row: u = msb << eb | ex with msb from the interleaved plane of
+// the row's list and ex from the LSB-first ex-code byte stream.
+__global__ void make_rcodes_kernel(const uint32_t* __restrict__ packed, const int64_t* __restrict__ offsets, int nlist,
+                                   const uint8_t* __restrict__ ex, int64_t n, int d, int bits,
+                                   uint8_t* __restrict__ rc) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= n) return;
+  int lo_c = 0, hi_c = nlist;
+  while (hi_c - lo_c > 1) {
+    const int mid = (lo_c + hi_c) >> 1;
+    if (offsets[mid] <= r) lo_c = mid; else hi_c = mid;
+  }
+  const int64_t lo = offsets[lo_c], n_c = offsets[lo_c + 1] - lo, v = r - lo;
+  const int g = words_per_vector(d), eb = bits - 1;
+  const int64_t bpv = ((int64_t)d * eb + 7) / 8;
+  const uint8_t* exr = ex + r * bpv;
+  auto code = [&](int dim) -> uint32_t {
+    if (dim >= d) return 0u;
+    const uint32_t msb = (packed[(int64_t)g * lo + (int64_t)(dim >> 5) * n_c + v] >> (dim & 31)) & 1u;
+    uint32_t e = 0;
+    for (int b = 0; b < eb; ++b) {
+      const int64_t bit = (int64_t)dim * eb + b;
+      e |= (uint32_t)((exr[bit >> 3] >> (bit & 7)) & 1) << b;
+    }
+    return (msb << eb) | e;
+  };
+  const int kp = kpad64(d);
+  uint8_t* dst = rc + r * rcode_row_bytes_of(d, bits);
+  if (rcode_nibbles(bits)) {
+    for (int j = lane; j < kp / 2; j += 32) dst[j] = (uint8_t)(code(2 * j) | (code(2 * j + 1) << 4));
+  } else {
+    for (int j = lane; j < kp; j += 32) dst[j] = (uint8_t)code(j);
+  }
+}
+}  // namespace ivrq
+
+extern "C" int ivrq_make_rcodes(const uint32_t* packed_msb, const int64_t* offsets, int32_t n_clusters,
+                                const uint8_t* excodes, int64_t n, int32_t d, int32_t bits, uint8_t* rcodes,
+                                void* stream) {
+  if (bits < 2 || bits > 8 || d <= 0 || n < 0) return fail(IVRQ_EINVAL, "ivrq_make_rcodes: bad sizes");
+  if (n == 0) return IVRQ_OK;
+  make_rcodes_kernel<<<(unsigned)ceil_div(n, 8), 256, 0, as_stream(stream)>>>(packed_msb, offsets, n_clusters,
+                                                                              excodes, n, d, bits, rcodes);
+  return check_launch("ivrq_make_rcodes");
 }

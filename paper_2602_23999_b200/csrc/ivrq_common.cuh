@@ -41,6 +41,27 @@ constexpr int kWarp = 32;
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 __host__ __device__ inline int words_per_vector(int dims) { return (dims + 31) / 32; }
 
+// ------------------------------------------------------------------ refine code layout
+// rcodes rows hold the full unsigned code u per dim for the int8 MMA refine:
+// K is padded to a multiple of 64 (two m16n8k32 steps); bits <= 4 packs two
+// dims per byte (dim 2j low nibble), bits >= 5 one dim per byte.
+__host__ __device__ inline int kpad64(int dims) { return (dims + 63) / 64 * 64; }
+__host__ __device__ inline bool rcode_nibbles(int bits) { return bits <= 4; }
+__host__ __device__ inline int64_t rcode_row_bytes_of(int dims, int bits) {
+  if (bits <= 1) return 0;
+  return rcode_nibbles(bits) ? kpad64(dims) / 2 : kpad64(dims);
+}
+// MMA K position -> dimension.  Lane t4 of a quad loads 16 codes per pair of
+// k-steps (one 128-bit load of bytes, or one 64-bit load of nibbles); the
+// fragment registers a0/a2 (k ranges 4t4.., 16+4t4..) are filled from them as
+// below, and the query slices are laid out in the same K order.
+__host__ __device__ inline int refine_kdim(int k, bool nibbles) {
+  const int s = k >> 5, w = k & 31, t4 = (w & 15) >> 2, j = w & 3, half = w >> 4;
+  const int p = s >> 1, odd = s & 1;
+  const int base = 16 * (4 * p + t4) + 8 * odd;
+  return nibbles ? base + 2 * j + half : base + 4 * half + j;
+}
+
 // ------------------------------------------------------------------ exact fp64 ops
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }

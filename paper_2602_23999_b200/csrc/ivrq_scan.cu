@@ -4,8 +4,10 @@
 //   stage 1  every vector: binary inner product (AND+POPC against the query's
 //            bit planes, or 4-bit LUT lookups), float64 estimate + lower bound,
 //            prune lb2 <= T with T the K-th best distance before this list;
-//   stage 2  survivors: full-code inner product <u, q_rot> in float64 and the
-//            refined estimate;
+//   stage 2  survivors: full-code inner product <u, q_rot> on the int8 tensor
+//            cores (mma.sync m16n8k32: 16 survivors x 8 digit slices of the
+//            query), combined exactly in integers and rounded once to float64;
+//            then the refined estimate;
 //   merge    survivors into the running (dist, pid) top-k; after the list
 //            T := pool[k-1] once the pool holds k entries.
 // The threshold trajectory, and therefore every prune decision, is the
@@ -20,20 +22,22 @@ constexpr int THREADS = 256;
 constexpr int WARPS = THREADS / 32;
 constexpr int CHUNK = 512;             // vectors of one list per stage-1 pass
 constexpr int VPT = CHUNK / THREADS;   // vectors per thread per pass
+constexpr int SLICES = 8;              // base-128 digits of the query (refine)
+constexpr int SPAD = 16;               // slice row padding (bank spread)
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int64_t NO_ID = 0x7fffffffffffffffLL;
 
 struct Args {
   ivrq_index_view ix;
-  const double* q_rot;
   const int64_t* probe_ids;
   const double* probe_d2;
   const double* scalars;
   const uint32_t* planes;
   const float* luts;
+  const int8_t* qslices;
   int64_t nq;
   int k, nprobe, qbits, prune;
-  int g, eb, exw;
+  int g, kpad;
   int sort_n;  // big-k path: power of two >= CHUNK + k
   int64_t* out_ids;
   double* out_dists;
@@ -43,13 +47,9 @@ struct Args {
 
 __device__ __forceinline__ double dinf() { return __longlong_as_double(0x7ff0000000000000LL); }
 
-// rotated query in smem, transposed: element (group gi, dim i) at i * qstride + gi,
-// so the lanes of a refine (one 32-dim group each) read consecutive words
-__host__ __device__ __forceinline__ int qstride(int g) { return g | 1; }
-
-// ------------------------------------------------------------ per-query state in smem
 struct QueryCtx {
   double delta, half_code, ipm, kb_sum;
+  int sexp;
 };
 
 // ------------------------------------------------------------ stage 1
@@ -163,68 +163,88 @@ __device__ __forceinline__ void stage1_chunk(const Args& a, const QueryCtx& qc, 
 }
 
 // ------------------------------------------------------------ stage 2
-// Extract the 32 ex-code fields (eb bits each, LSB-first) of one 32-dim group
-// and accumulate sum_i u_i * q_i with u_i = msb_i << eb | ex_i.
-// u -> double without the quarter-rate I2F.F64: 2^52 + u has u in its low
-// mantissa bits, so one exact DADD recovers u.
-__device__ __forceinline__ double u2d(uint32_t u) {
-  return __dsub_rn(__hiloint2double(0x43300000, (int)u), 4503599627370496.0);
+__device__ __forceinline__ void mma_u8s8(int (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                                         uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+      : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
-// q points at dim 0 of the group in the transposed query (stride qs between dims).
-template <int EB>
-__device__ __forceinline__ double group_dot(const uint32_t* __restrict__ exg, uint32_t msb, const double* q, int qs) {
-  double acc = 0.0;
-  if constexpr (EB == 0) {
-#pragma unroll
-    for (int i = 0; i < 32; ++i) acc = fma(u2d((msb >> i) & 1u), q[i * qs], acc);
-  } else {
-    uint32_t w[EB + 1];
-#pragma unroll
-    for (int i = 0; i < EB; ++i) w[i] = __ldg(exg + i);
-    w[EB] = 0u;
-#pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      constexpr uint32_t mask = (1u << EB) - 1u;
-      const int bit = i * EB;
-      const int wi = bit >> 5, off = bit & 31;
-      const uint64_t win = ((uint64_t)w[wi + 1] << 32) | (uint64_t)w[wi];
-      const uint32_t field = (uint32_t)(win >> off) & mask;
-      const uint32_t u = ((((msb >> i) & 1u)) << EB) | field;
-      acc = fma(u2d(u), q[i * qs], acc);
-    }
-  }
-  return acc;
-}
-
-// Refined distance of every candidate (in place in s_cd) (search.py:313-323).
-template <int EB>
-__device__ __forceinline__ void refine_chunk(const Args& a, const QueryCtx& qc, const uint32_t* __restrict__ words,
-                                             int64_t lo, int64_t n_c, int64_t c0, double d_qc2, const double* s_q,
-                                             const int32_t* s_cv, double* s_cd, int ncand) {
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int g = a.g;
-  int lpc = 1;
-  while (lpc < g && lpc < 32) lpc <<= 1;
-  const int cpw = 32 / lpc;  // candidates per warp per step
-  const int sub = lane / lpc, sl = lane % lpc;
-  for (int cb = wid * cpw; cb < ncand; cb += WARPS * cpw) {
-    const int ci = cb + sub;
-    double acc = 0.0;
-    int64_t row = 0;
-    if (ci < ncand) {
-      const int64_t v = c0 + s_cv[ci];
-      row = lo + v;
-      const uint32_t* exrow = a.ix.excodes + row * a.exw;
-      for (int gi = sl; gi < g; gi += lpc) {
-        const uint32_t msb = __ldg(words + (int64_t)gi * n_c + v);
-        acc += group_dot<EB>(exrow + gi * EB, msb, s_q + gi, qstride(g));
+// Refined distance of every candidate, in place in s_cd (search.py:313-323):
+//   ip_u = <u, q_rot> = 2^(e-54) * sum_s 128^(7-s) * <u, D_s>
+// with the int32 dot products <u, D_s> from the tensor cores (exact), the
+// digit sum assembled in int64 (exact) and rounded once to float64.
+template <bool NIB>
+__device__ __forceinline__ void refine_chunk(const Args& a, const QueryCtx& qc, int64_t lo, int64_t c0, double d_qc2,
+                                             const int8_t* s_slices, const int32_t* s_cv, double* s_cd, int ncand) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int gid = lane >> 2, t4 = lane & 3;
+  const int kp = a.kpad, ss = kp + SPAD;
+  const int64_t rb = a.ix.rcode_bytes;
+  const uint8_t* __restrict__ rc = a.ix.rcodes;
+  const int8_t* sl = s_slices + gid * ss + 4 * t4;  // this lane's B column (slice gid)
+  for (int cb = wid * 16; cb < ncand; cb += WARPS * 16) {
+    const int i0 = cb + gid, i1 = cb + gid + 8;
+    const int64_t r0 = lo + c0 + s_cv[min(i0, ncand - 1)];
+    const int64_t r1 = lo + c0 + s_cv[min(i1, ncand - 1)];
+    const uint8_t* row0 = rc + r0 * rb;
+    const uint8_t* row1 = rc + r1 * rb;
+    int c[4] = {0, 0, 0, 0};
+    for (int p = 0; p < kp / 64; ++p) {
+      uint32_t a0s0, a2s0, a0s1, a2s1, a1s0, a3s0, a1s1, a3s1;
+      if (NIB) {
+        const uint2 x0 = __ldg(reinterpret_cast<const uint2*>(row0 + 8 * (4 * p + t4)));
+        const uint2 x1 = __ldg(reinterpret_cast<const uint2*>(row1 + 8 * (4 * p + t4)));
+        a0s0 = x0.x & 0x0F0F0F0Fu;
+        a2s0 = (x0.x >> 4) & 0x0F0F0F0Fu;
+        a0s1 = x0.y & 0x0F0F0F0Fu;
+        a2s1 = (x0.y >> 4) & 0x0F0F0F0Fu;
+        a1s0 = x1.x & 0x0F0F0F0Fu;
+        a3s0 = (x1.x >> 4) & 0x0F0F0F0Fu;
+        a1s1 = x1.y & 0x0F0F0F0Fu;
+        a3s1 = (x1.y >> 4) & 0x0F0F0F0Fu;
+      } else {
+        const uint4 x0 = __ldg(reinterpret_cast<const uint4*>(row0 + 16 * (4 * p + t4)));
+        const uint4 x1 = __ldg(reinterpret_cast<const uint4*>(row1 + 16 * (4 * p + t4)));
+        a0s0 = x0.x;
+        a2s0 = x0.y;
+        a0s1 = x0.z;
+        a2s1 = x0.w;
+        a1s0 = x1.x;
+        a3s0 = x1.y;
+        a1s1 = x1.z;
+        a3s1 = x1.w;
       }
+      const int kb0 = 64 * p, kb1 = 64 * p + 32;
+      const uint32_t b00 = *reinterpret_cast<const uint32_t*>(sl + kb0);
+      const uint32_t b10 = *reinterpret_cast<const uint32_t*>(sl + kb0 + 16);
+      const uint32_t b01 = *reinterpret_cast<const uint32_t*>(sl + kb1);
+      const uint32_t b11 = *reinterpret_cast<const uint32_t*>(sl + kb1 + 16);
+      mma_u8s8(c, a0s0, a1s0, a2s0, a3s0, b00, b10);
+      mma_u8s8(c, a0s1, a1s1, a2s1, a3s1, b01, b11);
     }
-    for (int o = lpc >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
-    if (ci < ncand && sl == 0) {
-      const float2 lf = __ldg(reinterpret_cast<const float2*>(a.ix.long_factors) + row);
-      s_cd[ci] = dmax(dsub(dadd((double)lf.x, d_qc2), dmul((double)lf.y, dsub(acc, qc.kb_sum))), 0.0);
+    // c0,c1: row gid, slices 2t4, 2t4+1; c2,c3: row gid+8.  Slices 0-3 form
+    // the high int64 half (weights 128^3..1), slices 4-7 the low half.
+    const long long w0 = (t4 & 1) ? 128LL : 2097152LL;  // 128^3 or 128 (first slice of the pair)
+    const long long w1 = (t4 & 1) ? 1LL : 16384LL;
+    long long p0 = (long long)c[0] * w0 + (long long)c[1] * w1;
+    long long p1 = (long long)c[2] * w0 + (long long)c[3] * w1;
+    p0 += __shfl_xor_sync(FULL, p0, 1);
+    p1 += __shfl_xor_sync(FULL, p1, 1);
+    const long long q0 = __shfl_xor_sync(FULL, p0, 2);  // lane t4=0 receives the low half
+    const long long q1 = __shfl_xor_sync(FULL, p1, 2);
+    if (t4 == 0) {
+      const double hi_s = ldexp(1.0, qc.sexp - 26), lo_s = ldexp(1.0, qc.sexp - 54);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int ci = h ? i1 : i0;
+        if (ci >= ncand) continue;
+        const long long hi = h ? p1 : p0, lw = h ? q1 : q0;
+        const double ip = dadd(dmul((double)hi, hi_s), dmul((double)lw, lo_s));
+        const float2 lf = __ldg(reinterpret_cast<const float2*>(a.ix.long_factors) + (h ? r1 : r0));
+        s_cd[ci] = dmax(dsub(dadd((double)lf.x, d_qc2), dmul((double)lf.y, dsub(ip, qc.kb_sum))), 0.0);
+      }
     }
   }
 }
@@ -268,7 +288,7 @@ __device__ __forceinline__ void warp_merge32(double& qd, int64_t& qi, double bd,
 
 // ------------------------------------------------------------ common prologue
 struct Smem {
-  double* s_q;
+  int8_t* s_slices;
   uint32_t* s_planes8;
   float* s_lut;
   double* s_cd;
@@ -284,8 +304,6 @@ __device__ __forceinline__ Smem carve(const Args& a, unsigned char* smem, bool b
   Smem s{};
   const int g = a.g;
   unsigned char* p = smem;
-  s.s_q = reinterpret_cast<double*>(p);
-  p += REFINE ? sizeof(double) * 32 * qstride(g) : 0;
   s.s_cd = reinterpret_cast<double*>(p);
   p += sizeof(double) * CHUNK;
   s.s_pool_d = reinterpret_cast<double*>(p);
@@ -301,28 +319,33 @@ __device__ __forceinline__ Smem carve(const Args& a, unsigned char* smem, bool b
   s.s_planes8 = reinterpret_cast<uint32_t*>(p);
   p += MODE == IVRQ_IP_BITWISE ? sizeof(uint32_t) * 8 * g : 0;
   s.s_lut = reinterpret_cast<float*>(p);
+  p += MODE == IVRQ_IP_LUT ? sizeof(float) * 8 * g * 16 : 0;
+  s.s_slices = reinterpret_cast<int8_t*>(p);
   return s;
 }
 
 size_t smem_bytes(const Args& a, int mode, bool refine, bool bigk) {
   size_t b = 0;
-  b += refine ? sizeof(double) * 32 * qstride(a.g) : 0;
   b += sizeof(double) * CHUNK;
   b += (sizeof(double) + sizeof(int64_t)) * (bigk ? a.k : 32);
   b += (sizeof(double) + sizeof(int64_t)) * (bigk ? a.sort_n : WARPS * 32);
   b += sizeof(int32_t) * CHUNK;
   b += mode == IVRQ_IP_BITWISE ? sizeof(uint32_t) * 8 * a.g : sizeof(float) * 8 * a.g * 16;
+  b += refine ? (size_t)SLICES * (a.kpad + SPAD) : 0;
   return b + 16;
 }
 
 template <int MODE, bool REFINE>
 __device__ __forceinline__ QueryCtx load_query(const Args& a, const Smem& s, int64_t q) {
-  const int g = a.g, d = a.ix.dims, tid = threadIdx.x;
-  if (REFINE)
-    for (int i = tid; i < 32 * qstride(g); i += THREADS) {
-      const int dim = (i % qstride(g)) * 32 + i / qstride(g);
-      s.s_q[i] = (i % qstride(g)) < g && dim < d ? a.q_rot[q * d + dim] : 0.0;
+  const int g = a.g, tid = threadIdx.x;
+  if (REFINE) {
+    const int kp = a.kpad, ss = kp + SPAD;
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(a.qslices + q * SLICES * (int64_t)kp);
+    for (int i = tid; i < SLICES * kp / 4; i += THREADS) {
+      const int sidx = (4 * i) / kp, k = (4 * i) % kp;
+      *reinterpret_cast<uint32_t*>(s.s_slices + sidx * ss + k) = src[i];
     }
+  }
   if (MODE == IVRQ_IP_BITWISE) {
     for (int i = tid; i < 8 * g; i += THREADS) {
       const int gi = i / 8, j = i % 8;
@@ -337,12 +360,13 @@ __device__ __forceinline__ QueryCtx load_query(const Args& a, const Smem& s, int
   qc.half_code = sc[IVRQ_QS_HALF_CODE];
   qc.ipm = sc[IVRQ_QS_IP_MARGIN];
   qc.kb_sum = sc[IVRQ_QS_KB_SUM];
+  qc.sexp = REFINE ? (int)sc[IVRQ_QS_SLICE_EXP] : 0;
   return qc;
 }
 
 // ------------------------------------------------------------ kernel, k <= 32
-template <int MODE, int EB, bool REFINE, int QB>
-__global__ void __launch_bounds__(THREADS) scan_kernel(Args a) {
+template <int MODE, bool REFINE, bool NIB, int QB>
+__global__ void __launch_bounds__(THREADS, 3) scan_kernel(Args a) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int s_ncand;
   __shared__ double s_T;
@@ -386,7 +410,7 @@ __global__ void __launch_bounds__(THREADS) scan_kernel(Args a) {
       if (tid == 0) s_ncand = 0;
       __syncthreads();
       stage1_chunk<MODE, QB>(a, qc, words, lo, n_c, c0, cn, d_qc2, sq, T_list, s.s_planes8, s.s_lut, s.s_cv, s.s_cd,
-                         &s_ncand);
+                             &s_ncand);
       __syncthreads();
       const int ncand = s_ncand;
       if (tid == 0) {
@@ -396,7 +420,7 @@ __global__ void __launch_bounds__(THREADS) scan_kernel(Args a) {
       if (ncand == 0) continue;
       any_cand = true;
       if (REFINE) {
-        refine_chunk<EB>(a, qc, words, lo, n_c, c0, d_qc2, s.s_q, s.s_cv, s.s_cd, ncand);
+        refine_chunk<NIB>(a, qc, lo, c0, d_qc2, s.s_slices, s.s_cv, s.s_cd, ncand);
         __syncthreads();
       }
       // each warp folds its share of the candidates into its queue
@@ -482,7 +506,7 @@ __device__ void bitonic_sort(double* key, int64_t* id, int n) {
   __syncthreads();
 }
 
-template <int MODE, int EB, bool REFINE, int QB>
+template <int MODE, bool REFINE, bool NIB, int QB>
 __global__ void __launch_bounds__(THREADS) scan_kernel_bigk(Args a) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int s_ncand, s_nfilt, s_pool_n;
@@ -516,7 +540,7 @@ __global__ void __launch_bounds__(THREADS) scan_kernel_bigk(Args a) {
       if (tid == 0) s_ncand = 0;
       __syncthreads();
       stage1_chunk<MODE, QB>(a, qc, words, lo, n_c, c0, cn, d_qc2, sq, T_list, s.s_planes8, s.s_lut, s.s_cv, s.s_cd,
-                         &s_ncand);
+                             &s_ncand);
       __syncthreads();
       const int ncand = s_ncand;
       if (tid == 0) {
@@ -525,7 +549,7 @@ __global__ void __launch_bounds__(THREADS) scan_kernel_bigk(Args a) {
       }
       if (ncand == 0) continue;
       if (REFINE) {
-        refine_chunk<EB>(a, qc, words, lo, n_c, c0, d_qc2, s.s_q, s.s_cv, s.s_cd, ncand);
+        refine_chunk<NIB>(a, qc, lo, c0, d_qc2, s.s_slices, s.s_cv, s.s_cd, ncand);
         __syncthreads();
       }
       if (tid == 0) s_nfilt = 0;
@@ -596,13 +620,13 @@ __global__ void __launch_bounds__(THREADS) scan_kernel_bigk(Args a) {
   }
 }
 
-template <int MODE, int EB, bool REFINE>
+template <int MODE, bool REFINE, bool NIB>
 int launch_t(const Args& a, cudaStream_t s) {
   const bool bigk = a.k > 32;
   const size_t sm = smem_bytes(a, MODE, REFINE, bigk);
   const bool qb4 = MODE == IVRQ_IP_BITWISE && a.qbits == 4;  // the SearchParams default
-  auto kern = bigk ? (qb4 ? scan_kernel_bigk<MODE, EB, REFINE, 4> : scan_kernel_bigk<MODE, EB, REFINE, 0>)
-                   : (qb4 ? scan_kernel<MODE, EB, REFINE, 4> : scan_kernel<MODE, EB, REFINE, 0>);
+  auto kern = bigk ? (qb4 ? scan_kernel_bigk<MODE, REFINE, NIB, 4> : scan_kernel_bigk<MODE, REFINE, NIB, 0>)
+                   : (qb4 ? scan_kernel<MODE, REFINE, NIB, 4> : scan_kernel<MODE, REFINE, NIB, 0>);
   if (sm > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return fail(IVRQ_EUNSUP, "ivrq_search_scan: shared memory request too large");
@@ -612,18 +636,9 @@ int launch_t(const Args& a, cudaStream_t s) {
 }
 
 template <int MODE>
-int launch_mode(const Args& a, bool refine, cudaStream_t s) {
-  if (!refine) return launch_t<MODE, 0, false>(a, s);
-  switch (a.eb) {
-    case 1: return launch_t<MODE, 1, true>(a, s);
-    case 2: return launch_t<MODE, 2, true>(a, s);
-    case 3: return launch_t<MODE, 3, true>(a, s);
-    case 4: return launch_t<MODE, 4, true>(a, s);
-    case 5: return launch_t<MODE, 5, true>(a, s);
-    case 6: return launch_t<MODE, 6, true>(a, s);
-    case 7: return launch_t<MODE, 7, true>(a, s);
-    default: return fail(IVRQ_EUNSUP, "ivrq_search_scan: bits out of range");
-  }
+int launch_mode(const Args& a, bool refine, bool nib, cudaStream_t s) {
+  if (!refine) return launch_t<MODE, false, false>(a, s);
+  return nib ? launch_t<MODE, true, true>(a, s) : launch_t<MODE, true, false>(a, s);
 }
 
 }  // namespace scan
@@ -633,30 +648,32 @@ using namespace ivrq;
 
 extern "C" int ivrq_search_scan(const ivrq_index_view* index, const double* q_rot, const int64_t* probe_ids,
                                 const double* probe_d2, const double* scalars, const uint32_t* planes,
-                                const float* luts, int64_t nq, const ivrq_search_params* params,
-                                int64_t* out_ids, double* out_dists, int32_t* out_counts, int64_t* stats,
-                                void* stream) {
+                                const float* luts, const int8_t* qslices, int64_t nq,
+                                const ivrq_search_params* params, int64_t* out_ids, double* out_dists,
+                                int32_t* out_counts, int64_t* stats, void* stream) {
+  (void)q_rot;
   if (!index || !params) return fail(IVRQ_EINVAL, "ivrq_search_scan: null argument");
   if (params->k < 1) return fail(IVRQ_EINVAL, "k must be >= 1");
   if (params->k > 4096) return fail(IVRQ_EUNSUP, "ivrq_search_scan: k > 4096 not supported");
   if (index->bits < 1 || index->bits > 8) return fail(IVRQ_EINVAL, "index bits out of range");
+  const bool refine = params->refine && index->bits >= 2;
+  if (refine && (!qslices || !index->rcodes)) return fail(IVRQ_EINVAL, "refine needs qslices and rcodes");
   if (nq == 0) return IVRQ_OK;
   scan::Args a{};
   a.ix = *index;
-  a.q_rot = q_rot;
   a.probe_ids = probe_ids;
   a.probe_d2 = probe_d2;
   a.scalars = scalars;
   a.planes = planes;
   a.luts = luts;
+  a.qslices = qslices;
   a.nq = nq;
   a.k = params->k;
   a.nprobe = params->n_probe;
   a.qbits = params->query_bits;
   a.prune = params->prune;
   a.g = words_per_vector(index->dims);
-  a.eb = index->bits - 1;
-  a.exw = a.eb * a.g;
+  a.kpad = kpad64(index->dims);
   int n2 = 1;
   while (n2 < scan::CHUNK + a.k) n2 <<= 1;
   a.sort_n = n2;
@@ -664,8 +681,8 @@ extern "C" int ivrq_search_scan(const ivrq_index_view* index, const double* q_ro
   a.out_dists = out_dists;
   a.out_counts = out_counts;
   a.stats = stats;
-  const bool refine = params->refine && index->bits >= 2;
+  const bool nib = rcode_nibbles(index->bits);
   cudaStream_t s = as_stream(stream);
-  if (params->ip_mode == IVRQ_IP_BITWISE) return scan::launch_mode<IVRQ_IP_BITWISE>(a, refine, s);
-  return scan::launch_mode<IVRQ_IP_LUT>(a, refine, s);
+  if (params->ip_mode == IVRQ_IP_BITWISE) return scan::launch_mode<IVRQ_IP_BITWISE>(a, refine, nib, s);
+  return scan::launch_mode<IVRQ_IP_LUT>(a, refine, nib, s);
 }

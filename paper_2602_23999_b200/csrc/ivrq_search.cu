@@ -156,7 +156,7 @@ __global__ void __launch_bounds__(256) probe_select_kernel(const double* __restr
 // and build_luts (search.py:115-132).
 __global__ void prepare_kernel(const double* __restrict__ q_rot, int64_t nq, int d, int mode, int qbits,
                                int index_bits, double eps_bound, double* __restrict__ scalars,
-                               uint32_t* __restrict__ planes, float* __restrict__ luts) {
+                               uint32_t* __restrict__ planes, float* __restrict__ luts, int8_t* __restrict__ qslices) {
   const int lane = threadIdx.x & 31;
   const int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (q >= nq) return;
@@ -167,6 +167,29 @@ __global__ void prepare_kernel(const double* __restrict__ q_rot, int64_t nq, int
   sum_q = __shfl_sync(0xffffffffu, sum_q, 0);
   const double k_b = ((double)((1 << index_bits) - 1)) / 2.0;
   double* sc = scalars + q * IVRQ_QS_COUNT;
+  if (qslices) {
+    // q_rot as Q * 2^(e-54), |Q| < 2^54, Q = sum_s D_s 128^(7-s) with balanced
+    // digits D_s in [-64, 63]; stored per slice in the refine's K order.
+    double mx = 0.0;
+    for (int i = lane; i < d; i += 32) mx = dmax(mx, fabs(x[i]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = dmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    int e = 0;
+    if (mx > 0.0) frexp(mx, &e);  // mx < 2^e
+    const int kp = kpad64(d);
+    const bool nib = rcode_nibbles(index_bits);
+    int8_t* out = qslices + q * 8 * (int64_t)kp;
+    for (int k = lane; k < kp; k += 32) {
+      const int dim = refine_kdim(k, nib);
+      long long Q = dim < d ? llrint(ldexp(x[dim], 54 - e)) : 0;
+      for (int s = 7; s >= 0; --s) {
+        const long long r = ((Q + 64) & 127) - 64;
+        out[s * kp + k] = (int8_t)r;
+        Q = (Q - r) >> 7;
+      }
+    }
+    if (lane == 0) sc[IVRQ_QS_SLICE_EXP] = (double)e;
+  }
   if (mode == IVRQ_IP_LUT) {
     // L[j][key] = float32(sum over set bits i of key of q[4j+i]), dims padded with 0
     const int nblk = 8 * g;
@@ -304,15 +327,20 @@ extern "C" int ivrq_select_clusters_ordered(const double* q_rot, int64_t nq, int
 
 extern "C" int ivrq_prepare_queries(const double* q_rot, int64_t nq, int32_t dims,
                                     const ivrq_search_params* params, int32_t index_bits, double eps_bound,
-                                    double* scalars, uint32_t* planes, float* luts, void* stream) {
+                                    double* scalars, uint32_t* planes, float* luts, int8_t* qslices,
+                                    void* stream) {
   if (!params) return fail(IVRQ_EINVAL, "ivrq_prepare_queries: null params");
   if (params->ip_mode == IVRQ_IP_BITWISE && (params->query_bits < 2 || params->query_bits > 8))
     return fail(IVRQ_EINVAL, "query_bits must be in [2, 8]");
   if (params->ip_mode == IVRQ_IP_BITWISE && !planes) return fail(IVRQ_EINVAL, "bitwise mode needs planes");
   if (params->ip_mode == IVRQ_IP_LUT && !luts) return fail(IVRQ_EINVAL, "lut mode needs luts");
+  if (params->refine && index_bits >= 2 && !qslices) return fail(IVRQ_EINVAL, "refine needs qslices");
   if (nq == 0) return IVRQ_OK;
   const int wpb = 4;
   prepare_kernel<<<(unsigned)ceil_div(nq, wpb), wpb * 32, 0, as_stream(stream)>>>(
-      q_rot, nq, dims, params->ip_mode, params->query_bits, index_bits, eps_bound, scalars, planes, luts);
+      q_rot, nq, dims, params->ip_mode, params->query_bits, index_bits, eps_bound, scalars, planes, luts,
+      (params->refine && index_bits >= 2) ? qslices : nullptr);
   return check_launch("ivrq_prepare_queries");
 }
+
+extern "C" int64_t ivrq_rcode_row_bytes(int32_t dims, int32_t bits) { return rcode_row_bytes_of(dims, bits); }

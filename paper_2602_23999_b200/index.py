@@ -35,6 +35,8 @@ from paper_2602_23999_b200.codec import (
     QuantizationParams,
     encode_rows,
     excode_bytes_per_vector,
+    excodes_from_rcodes,
+    rcode_row_bytes,
     unpack_excodes,
     unpack_interleaved,
 )
@@ -184,10 +186,6 @@ class IvfRabitqIndex:
         n = self.size
         sf = np.asarray(self._host["short_factors"], dtype=np.float32).reshape(n, 3)
         lf = np.asarray(self._host["long_factors"], dtype=np.float32).reshape(n, 2)
-        ex_words = np.zeros((n, eb * g * 4), dtype=np.uint8)
-        if eb:
-            bpv = excode_bytes_per_vector(self.dims, self.bits)
-            ex_words[:, :bpv] = np.asarray(self._host["excodes"], dtype=np.uint8).reshape(n, bpv)
         cent = self.centroids
         cvals = np.ascontiguousarray(np.asarray(cent.values, dtype=np.float32))
         out = {
@@ -197,12 +195,22 @@ class IvfRabitqIndex:
             "short_scale": dev.to_device(np.ascontiguousarray(sf[:, 1]), d),
             "short_err": dev.to_device(np.ascontiguousarray(sf[:, 2]), d),
             "long_factors": dev.to_device(np.ascontiguousarray(lf), d),
-            "excodes": dev.to_device(ex_words.view(np.uint32).reshape(-1), d),
             "pids": dev.to_device(np.asarray(self._host["pids"], dtype=np.uint64), d),
             "centroids": dev.to_device(cvals, d),
             "rotation": dev.to_device(np.asarray(self._host["rotation"], dtype=np.float32), d),
         }
         out["centroid_sqnorms"] = dev.to_device(np.asarray(cent.squared_norms, dtype=np.float64), d)
+        rb = rcode_row_bytes(self.dims, self.bits)
+        out["rcodes"] = torch.empty(n * rb, dtype=torch.uint8, device=d)
+        if eb and n:
+            bpv = excode_bytes_per_vector(self.dims, self.bits)
+            ex = dev.to_device(np.ascontiguousarray(np.asarray(self._host["excodes"], dtype=np.uint8).reshape(n, bpv)), d)
+            _lib.call(
+                "ivrq_make_rcodes",
+                dev.ptr(out["packed_msb"]), dev.ptr(out["offsets"]), self.n_clusters, dev.ptr(ex),
+                n, self.dims, self.bits, dev.ptr(out["rcodes"]), dev.stream_ptr(),
+            )
+        del g
         return out
 
     def view(self) -> _lib.IndexView:
@@ -222,7 +230,8 @@ class IvfRabitqIndex:
                 short_scale=dev.ptr(t["short_scale"]),
                 short_err=dev.ptr(t["short_err"]),
                 long_factors=dev.ptr(t["long_factors"]),
-                excodes=dev.ptr(t["excodes"]),
+                rcodes=dev.ptr(t["rcodes"]),
+                rcode_bytes=rcode_row_bytes(self.dims, self.bits),
                 pids=dev.ptr(t["pids"]),
                 centroids=dev.ptr(t["centroids"]),
                 centroid_sqnorms=dev.ptr(t["centroid_sqnorms"]),
@@ -245,12 +254,10 @@ class IvfRabitqIndex:
         elif name == "packed_msb":
             a = dev.to_host(t["packed_msb"]).view(np.uint32)
         elif name == "excodes":
-            bpv = excode_bytes_per_vector(self.dims, self.bits)
-            words = dev.to_host(t["excodes"]).view(np.uint32)
-            if bpv == 0:
+            if self.bits == 1:
                 a = np.zeros((n, 0), dtype=np.uint8)
             else:
-                a = np.ascontiguousarray(words.view(np.uint8).reshape(n, -1)[:, :bpv])
+                a = excodes_from_rcodes(dev.to_host(t["rcodes"]), self.dims, self.bits)
         elif name == "short_factors":
             a = np.stack(
                 [dev.to_host(t["short_add"]), dev.to_host(t["short_scale"]), dev.to_host(t["short_err"])], axis=1
@@ -397,7 +404,7 @@ def build_index_device(
         "short_scale": enc["short_scale"],
         "short_err": enc["short_err"],
         "long_factors": enc["long_factors"],
-        "excodes": enc["excodes"],
+        "rcodes": enc["rcodes"],
         "pids": order,
         "centroids": cent_rot,
         "centroid_sqnorms": row_sqnorms(cent_rot),

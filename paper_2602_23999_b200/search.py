@@ -147,7 +147,10 @@ def prepare_queries_device(q_rot: torch.Tensor, index: IvfRabitqIndex, params: S
     nq, d = q_rot.shape
     g = (d + 31) // 32
     scalars = torch.empty((nq, _lib.QS_COUNT), dtype=torch.float64, device=q_rot.device)
-    planes = luts = None
+    planes = luts = qslices = None
+    if params.refine and index.bits >= 2:
+        kpad = (d + 63) // 64 * 64
+        qslices = torch.empty((nq, 8, kpad), dtype=torch.int8, device=q_rot.device)
     if params.ip_mode == "bitwise":
         planes = torch.empty((nq, params.query_bits, g), dtype=torch.int32, device=q_rot.device)
     else:
@@ -156,9 +159,9 @@ def prepare_queries_device(q_rot: torch.Tensor, index: IvfRabitqIndex, params: S
     _lib.call(
         "ivrq_prepare_queries",
         dev.ptr(q_rot), nq, d, cp, index.bits, float(index.eps_bound),
-        dev.ptr(scalars), dev.ptr(planes), dev.ptr(luts), dev.stream_ptr(),
+        dev.ptr(scalars), dev.ptr(planes), dev.ptr(luts), dev.ptr(qslices), dev.stream_ptr(),
     )
-    return scalars, planes, luts
+    return scalars, planes, luts, qslices
 
 
 def search_device(
@@ -192,7 +195,7 @@ def search_device(
     t = index.device
     probe_ids, probe_d2 = _probe_device(q_rot, t["centroids"], t["centroid_sqnorms"], params.n_probe, True)
     mark("probed")
-    scalars, planes, luts = prepare_queries_device(q_rot, index, params)
+    scalars, planes, luts, qslices = prepare_queries_device(q_rot, index, params)
     mark("prepared")
     k = params.k
     out_ids = torch.empty((nq, k), dtype=torch.int64, device=q_rot.device)
@@ -203,7 +206,8 @@ def search_device(
     _lib.call(
         "ivrq_search_scan",
         index.view(), dev.ptr(q_rot), dev.ptr(probe_ids), dev.ptr(probe_d2), dev.ptr(scalars), dev.ptr(planes),
-        dev.ptr(luts), nq, cp, dev.ptr(out_ids), dev.ptr(out_d), dev.ptr(counts), dev.ptr(stats), dev.stream_ptr(),
+        dev.ptr(luts), dev.ptr(qslices), nq, cp, dev.ptr(out_ids), dev.ptr(out_d), dev.ptr(counts), dev.ptr(stats),
+        dev.stream_ptr(),
     )
     mark("scanned")
     return DeviceResult(ids=out_ids, dists=out_d, counts=counts, stats=stats)

@@ -67,7 +67,7 @@ def test_query_state_matches_reference(golden, si):
         pytest.skip("n_probe exceeds n_clusters")
     sp = iv.SearchParams(**SEARCHES[si])
     ix = _index(golden)
-    scal, planes, luts = prepare_queries_device(dev.to_device(golden["q_rot"]), ix, sp)
+    scal, planes, luts, _ = prepare_queries_device(dev.to_device(golden["q_rot"]), ix, sp)
     scal = dev.to_host(scal)
     want = golden[f"s{si}_qstate"]
     np.testing.assert_array_equal(scal[:, 0], want[:, 0])  # sum_q (pairwise order)
@@ -130,10 +130,11 @@ def test_encoder_bit_exact_given_reference_inputs(golden):
     np.testing.assert_array_equal(sf, golden["short_factors"])
     np.testing.assert_array_equal(dev.to_host(out["long_factors"]), golden["long_factors"])
     if p["bits"] > 1:
-        n = golden["x"].shape[0]
-        bpv = golden["excodes"].shape[1]
-        exb = dev.to_host(out["excodes"]).view(np.uint8).reshape(n, -1)[:, :bpv]
-        np.testing.assert_array_equal(exb, golden["excodes"])
+        from paper_2602_23999_b200.codec import codes_from_rcodes, excodes_from_rcodes
+
+        rc = dev.to_host(out["rcodes"])
+        np.testing.assert_array_equal(codes_from_rcodes(rc, golden["x"].shape[1], p["bits"]), golden["stage_codes"])
+        np.testing.assert_array_equal(excodes_from_rcodes(rc, golden["x"].shape[1], p["bits"]), golden["excodes"])
     assert int(out["bad_rows"].item()) == 0
 
 
