@@ -35,6 +35,7 @@ struct Args {
   const uint32_t* planes;
   const float* luts;
   const int8_t* qslices;
+  const int64_t* qorder;  // CTA -> query (queries grouped by first probed list)
   int64_t nq;
   int k, nprobe, qbits, prune;
   int g, kpad;
@@ -68,30 +69,42 @@ __device__ __forceinline__ void stage1_chunk(const Args& a, const QueryCtx& qc, 
 #pragma unroll
     for (int u = 0; u < VPT; ++u) pos[u] = last[u] = 0;
     const int qb = QB ? QB : a.qbits;
-    for (int gi = 0; gi < g; ++gi) {
+    constexpr int GB = 8;  // 32-dim groups whose words are in flight together
+    for (int g0 = 0; g0 < g; g0 += GB) {
+      uint32_t wv[GB][VPT];
+#pragma unroll
+      for (int j = 0; j < GB; ++j)
+#pragma unroll
+        for (int u = 0; u < VPT; ++u) {
+          const int vi = tid + u * THREADS;
+          wv[j][u] = (g0 + j < g && vi < cn) ? __ldg(words + (int64_t)(g0 + j) * n_c + c0 + vi) : 0u;
+        }
+#pragma unroll
+      for (int j = 0; j < GB; ++j) {
+      const int gi = g0 + j;
+      if (gi >= g) break;
       const uint4 pa = *reinterpret_cast<const uint4*>(s_planes8 + gi * 8);
       uint4 pb = make_uint4(0u, 0u, 0u, 0u);
       if (QB == 0 || QB > 4) pb = *reinterpret_cast<const uint4*>(s_planes8 + gi * 8 + 4);
       const uint32_t pl[8] = {pa.x, pa.y, pa.z, pa.w, pb.x, pb.y, pb.z, pb.w};
-      const uint32_t* wrow = words + (int64_t)gi * n_c + c0;
 #pragma unroll
       for (int u = 0; u < VPT; ++u) {
-        const int vi = tid + u * THREADS;
-        const uint32_t w = vi < cn ? __ldg(wrow + vi) : 0u;
+        const uint32_t w = wv[j][u];
         if (QB) {
 #pragma unroll
-          for (int j = 0; j < QB; ++j) pos[u] += __popc(w & pl[j]) << j;
+          for (int b = 0; b < QB; ++b) pos[u] += __popc(w & pl[b]) << b;
           last[u] += __popc(w & pl[QB - 1]);
         } else {
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            if (j < qb) {
-              const int c = __popc(w & pl[j]);
-              pos[u] += c << j;
-              if (j == qb - 1) last[u] += c;
+          for (int b = 0; b < 8; ++b) {
+            if (b < qb) {
+              const int c = __popc(w & pl[b]);
+              pos[u] += c << b;
+              if (b == qb - 1) last[u] += c;
             }
           }
         }
+      }
       }
     }
 #pragma unroll
@@ -366,14 +379,14 @@ __device__ __forceinline__ QueryCtx load_query(const Args& a, const Smem& s, int
 
 // ------------------------------------------------------------ kernel, k <= 32
 template <int MODE, bool REFINE, bool NIB, int QB>
-__global__ void __launch_bounds__(THREADS, 3) scan_kernel(Args a) {
+__global__ void __launch_bounds__(THREADS, 4) scan_kernel(Args a) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int s_ncand;
   __shared__ double s_T;
   __shared__ int s_pool_n;
   __shared__ long long s_probed, s_surv;
-  const int64_t q = blockIdx.x;
-  if (q >= a.nq) return;
+  if (blockIdx.x >= a.nq) return;
+  const int64_t q = a.qorder ? a.qorder[blockIdx.x] : (int64_t)blockIdx.x;
   const int k = a.k;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const Smem s = carve<MODE, REFINE>(a, smem, false);
@@ -426,15 +439,15 @@ __global__ void __launch_bounds__(THREADS, 3) scan_kernel(Args a) {
       // each warp folds its share of the candidates into its queue
       for (int cb = wid * 32; cb < ncand; cb += THREADS) {
         const int ci = cb + lane;
-        double d = dinf();
-        int64_t id = NO_ID;
-        if (ci < ncand) {
-          d = s.s_cd[ci];
-          id = (int64_t)__ldg(a.ix.pids + lo + c0 + s.s_cv[ci]);
-        }
+        const double d0 = ci < ncand ? s.s_cd[ci] : dinf();
         const double wk_d = __shfl_sync(FULL, qd, k - 1);
         const int64_t wk_i = __shfl_sync(FULL, qi, k - 1);
-        const bool pass = key_less(d, id, wk_d, wk_i) && key_less(d, id, pk_d, pk_i);
+        // the pid is only needed when the distance can enter the queue
+        const bool maybe = d0 <= wk_d && d0 <= pk_d && ci < ncand;
+        if (!__any_sync(FULL, maybe)) continue;
+        double d = d0;
+        int64_t id = maybe ? (int64_t)__ldg(a.ix.pids + lo + c0 + s.s_cv[ci]) : NO_ID;
+        const bool pass = maybe && key_less(d, id, wk_d, wk_i) && key_less(d, id, pk_d, pk_i);
         if (!__any_sync(FULL, pass)) continue;
         if (!pass) {
           d = dinf();
@@ -512,8 +525,8 @@ __global__ void __launch_bounds__(THREADS) scan_kernel_bigk(Args a) {
   __shared__ int s_ncand, s_nfilt, s_pool_n;
   __shared__ double s_T;
   __shared__ long long s_probed, s_surv;
-  const int64_t q = blockIdx.x;
-  if (q >= a.nq) return;
+  if (blockIdx.x >= a.nq) return;
+  const int64_t q = a.qorder ? a.qorder[blockIdx.x] : (int64_t)blockIdx.x;
   const int k = a.k;
   const int tid = threadIdx.x, lane = tid & 31;
   const Smem s = carve<MODE, REFINE>(a, smem, true);
@@ -620,6 +633,12 @@ __global__ void __launch_bounds__(THREADS) scan_kernel_bigk(Args a) {
   }
 }
 
+__global__ void first_probe_kernel(const int64_t* __restrict__ probe_ids, int64_t nq, int nprobe,
+                                   int32_t* __restrict__ first) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < nq) first[q] = (int32_t)probe_ids[q * nprobe];  // ids are ascending per query
+}
+
 template <int MODE, bool REFINE, bool NIB>
 int launch_t(const Args& a, cudaStream_t s) {
   const bool bigk = a.k > 32;
@@ -683,6 +702,29 @@ extern "C" int ivrq_search_scan(const ivrq_index_view* index, const double* q_ro
   a.stats = stats;
   const bool nib = rcode_nibbles(index->bits);
   cudaStream_t s = as_stream(stream);
-  if (params->ip_mode == IVRQ_IP_BITWISE) return scan::launch_mode<IVRQ_IP_BITWISE>(a, refine, nib, s);
-  return scan::launch_mode<IVRQ_IP_LUT>(a, refine, nib, s);
+  // Schedule queries grouped by their first (lowest-id) probed list: that list
+  // is refined in full (the threshold is still +inf), so neighbours in the
+  // grid share it through L2.  Results do not depend on the order.
+  int32_t* first = nullptr;
+  int64_t *cnt = nullptr, *off = nullptr, *order = nullptr;
+  if (nq > 1 && index->n_clusters > 1) {
+    if (cudaMallocAsync(reinterpret_cast<void**>(&first), nq * sizeof(int32_t), s) != cudaSuccess ||
+        cudaMallocAsync(reinterpret_cast<void**>(&cnt), index->n_clusters * sizeof(int64_t), s) != cudaSuccess ||
+        cudaMallocAsync(reinterpret_cast<void**>(&off), (index->n_clusters + 1) * sizeof(int64_t), s) != cudaSuccess ||
+        cudaMallocAsync(reinterpret_cast<void**>(&order), nq * sizeof(int64_t), s) != cudaSuccess)
+      return fail(IVRQ_ENOMEM, "ivrq_search_scan: workspace allocation failed");
+    scan::first_probe_kernel<<<(unsigned)ceil_div(nq, 256), 256, 0, s>>>(probe_ids, nq, a.nprobe, first);
+    IVRQ_TRY(check_launch("ivrq_search_scan(order)"));
+    IVRQ_TRY(ivrq_counting_sort(first, nq, index->n_clusters, cnt, off, order, stream));
+    a.qorder = order;
+  }
+  const int rc = params->ip_mode == IVRQ_IP_BITWISE ? scan::launch_mode<IVRQ_IP_BITWISE>(a, refine, nib, s)
+                                                    : scan::launch_mode<IVRQ_IP_LUT>(a, refine, nib, s);
+  if (first) {
+    cudaFreeAsync(first, s);
+    cudaFreeAsync(cnt, s);
+    cudaFreeAsync(off, s);
+    cudaFreeAsync(order, s);
+  }
+  return rc;
 }
