@@ -13,6 +13,8 @@
 // The threshold trajectory, and therefore every prune decision, is the
 // reference's.  k <= 32 keeps per-warp top-32 queues in registers (bitonic
 // shuffle networks); larger k falls back to a block-wide bitonic sort.
+#include <cstdlib>
+
 #include "ivrq_common.cuh"
 
 namespace ivrq {
@@ -707,7 +709,9 @@ extern "C" int ivrq_search_scan(const ivrq_index_view* index, const double* q_ro
   // grid share it through L2.  Results do not depend on the order.
   int32_t* first = nullptr;
   int64_t *cnt = nullptr, *off = nullptr, *order = nullptr;
-  if (nq > 1 && index->n_clusters > 1) {
+  const char* ord_env = getenv("IVRQ_SCAN_ORDER");
+  const bool grouped = ord_env ? atoi(ord_env) != 0 : true;
+  if (grouped && nq > 1 && index->n_clusters > 1) {
     if (cudaMallocAsync(reinterpret_cast<void**>(&first), nq * sizeof(int32_t), s) != cudaSuccess ||
         cudaMallocAsync(reinterpret_cast<void**>(&cnt), index->n_clusters * sizeof(int64_t), s) != cudaSuccess ||
         cudaMallocAsync(reinterpret_cast<void**>(&off), (index->n_clusters + 1) * sizeof(int64_t), s) != cudaSuccess ||

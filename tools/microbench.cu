@@ -79,7 +79,7 @@ float time_it(F f) {
   return ms;
 }
 
-int main() {
+int main1() {
   int sms;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   int clk;
@@ -104,3 +104,59 @@ int main() {
   printf("%s\n", cudaGetErrorString(e));
   return 0;
 }
+
+// fp64 tensor core (DMMA) rates: m8n8k4 and m16n8k16
+__global__ void k_dmma884(double* out, double seed) {
+  double a = seed + threadIdx.x, b = seed * 0.5;
+  double c[4][2] = {};
+  for (int i = 0; i < ITERS / 4; ++i) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                   : "+d"(c[j][0]), "+d"(c[j][1]) : "d"(a), "d"(b));
+  }
+  double s = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) s += c[j][0] + c[j][1];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+__global__ void k_dmma16816(double* out, double seed) {
+  double a[8], b[4];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) a[i] = seed + i;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) b[i] = seed * i;
+  double c[2][4] = {};
+  for (int i = 0; i < ITERS / 16; ++i) {
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+      asm volatile(
+          "mma.sync.aligned.m16n8k16.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7,%8,%9,%10,%11}, "
+          "{%12,%13,%14,%15}, {%0,%1,%2,%3};\n"
+          : "+d"(c[j][0]), "+d"(c[j][1]), "+d"(c[j][2]), "+d"(c[j][3])
+          : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(a[4]), "d"(a[5]), "d"(a[6]), "d"(a[7]), "d"(b[0]),
+            "d"(b[1]), "d"(b[2]), "d"(b[3]));
+  }
+  double s = 0;
+#pragma unroll
+  for (int j = 0; j < 2; ++j) s += c[j][0] + c[j][1] + c[j][2] + c[j][3];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+int main2() {
+  int sms, clk;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
+  const int blocks = sms * 8, threads = 256;
+  void* buf;
+  cudaMalloc(&buf, (size_t)blocks * threads * 8);
+  double warps = (double)blocks * threads / 32;
+  float ms = time_it([&] { k_dmma884<<<blocks, threads>>>((double*)buf, 1.0); });
+  double macs = warps * (ITERS / 4) * 4 * (8.0 * 8 * 4);
+  printf("DMMA 884  %8.2f TMAC/s = %6.1f MAC/clk/SM\n", macs / ms / 1e9, macs / (ms * 1e-3) / sms / (clk * 1e3));
+  ms = time_it([&] { k_dmma16816<<<blocks, threads>>>((double*)buf, 1.0); });
+  macs = warps * (ITERS / 16) * 2 * (16.0 * 8 * 16);
+  printf("DMMA16816 %8.2f TMAC/s = %6.1f MAC/clk/SM\n", macs / ms / 1e9, macs / (ms * 1e-3) / sms / (clk * 1e3));
+  printf("%s\n", cudaGetErrorString(cudaGetLastError()));
+  return 0;
+}
+int main() { main1(); return main2(); }
