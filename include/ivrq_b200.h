@@ -179,6 +179,27 @@ IVRQ_API int ivrq_search_scan(const ivrq_index_view* index, const double* q_rot,
                               int64_t* out_ids, double* out_dists, int32_t* out_counts,
                               int64_t* stats, void* stream);
 
+/* List-sharded scan: the index holds global clusters [list_lo, list_hi) renumbered
+ * from 0; probes outside the range are skipped.  init_ids/init_dists/init_counts
+ * (all NULL or all given; [nq*k] ascending, counts [nq]) seed each query's pool and
+ * threshold -- shard g continuing the ascending-id walk of shard g-1 reproduces
+ * search.py:429-447 exactly across GPUs. */
+IVRQ_API int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list_lo, int64_t list_hi,
+                                    const double* q_rot, const int64_t* probe_ids,
+                                    const double* probe_d2, const double* scalars,
+                                    const uint32_t* planes, const float* luts, const int8_t* qslices,
+                                    int64_t nq, const ivrq_search_params* params,
+                                    const int64_t* init_ids, const double* init_dists,
+                                    const int32_t* init_counts, int64_t* out_ids, double* out_dists,
+                                    int32_t* out_counts, int64_t* stats, void* stream);
+
+/* Merge `parts` (<= 16) per-query top-k lists laid out [parts][nq][k] (ascending,
+ * counts [parts][nq]) into the k best by (dist, id) (merge_topk, search.py:378-387):
+ * the all-gather merge of list-sharded search. */
+IVRQ_API int ivrq_merge_topk(const int64_t* ids, const double* dists, const int32_t* counts,
+                             int64_t nq, int32_t parts, int32_t k, int64_t* out_ids,
+                             double* out_dists, int32_t* out_counts, void* stream);
+
 /* ---------------------------------------------------------------- build */
 /* k-means++ seeding (_kmeans_pp_init, clustering.py:60-79) on x float[n*d]
  * (values are upcast to float64 exactly as the reference does).  Runs steps

@@ -339,8 +339,13 @@ def decode_codes(ix: dict) -> np.ndarray:
 
 
 def search(queries, ix: dict, k: int, n_probe: int, ip_mode="lut", query_bits=4, refine=True, prune=True, q_rot=None,
-           codes=None, stats=None):
-    """Per-query two-stage scan, lists in ascending id with a carried threshold (search.py:390-454)."""
+           codes=None, stats=None, list_range=None, init=None):
+    """Per-query two-stage scan, lists in ascending id with a carried threshold (search.py:390-454).
+
+    Shard semantics for the multi-GPU tests: ``list_range=(lo, hi)`` restricts
+    the walk to those cluster ids; ``init`` = [(ids, dists)] per query seeds
+    each pool (and its threshold) as if the lower-id lists had been visited.
+    """
     q = np.ascontiguousarray(np.atleast_2d(queries), dtype=np.float64)
     if q_rot is None:
         q_rot = q @ np.asarray(ix["rotation"]).T.astype(np.float64)
@@ -360,9 +365,14 @@ def search(queries, ix: dict, k: int, n_probe: int, ip_mode="lut", query_bits=4,
         st = query_state(q_rot[qi], ip_mode, query_bits, ix["eps_bound"])
         pool_i = np.empty(0, dtype=np.int64)
         pool_d = np.empty(0)
-        thr = math.inf
+        if init is not None:
+            pool_i = np.asarray(init[qi][0], dtype=np.int64)
+            pool_d = np.asarray(init[qi][1], dtype=np.float64)
+        thr = float(pool_d[k - 1]) if pool_i.size >= k else math.inf
         for j in np.argsort(sel[qi], kind="stable"):
             c = int(sel[qi, j])
+            if list_range is not None and not (list_range[0] <= c < list_range[1]):
+                continue
             dq = float(d2[qi, j])
             lo, hi = int(off[c]), int(off[c + 1])
             if hi == lo:

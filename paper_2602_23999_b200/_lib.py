@@ -90,6 +90,12 @@ _SIGNATURES: dict[str, tuple[object, list[object]]] = {
         c_int,
         [POINTER(IndexView), P, P, P, P, P, P, P, c_int64, POINTER(SearchParamsC), P, P, P, P, P],
     ),
+    "ivrq_search_scan_shard": (
+        c_int,
+        [POINTER(IndexView), c_int64, c_int64, P, P, P, P, P, P, P, c_int64, POINTER(SearchParamsC),
+         P, P, P, P, P, P, P, P],
+    ),
+    "ivrq_merge_topk": (c_int, [P, P, P, c_int64, c_int32, c_int32, P, P, P, P]),
     "ivrq_rcode_row_bytes": (c_int64, [c_int32, c_int32]),
     "ivrq_make_rcodes": (c_int, [P, P, c_int32, P, c_int64, c_int32, c_int32, P, P]),
     "ivrq_kmeanspp": (

@@ -40,6 +40,10 @@ struct Args {
   const int64_t* qorder;  // CTA -> query (queries grouped by first probed list)
   int64_t nq;
   int k, nprobe, qbits, prune;
+  int64_t list_lo, list_hi;  // global cluster ids held by this (shard of the) index
+  const int64_t* init_ids;   // optional pool carried in (exact ascending-id chain)
+  const double* init_dists;
+  const int32_t* init_counts;
   int g, kpad;
   int sort_n;  // big-k path: power of two >= CHUNK + k
   int64_t* out_ids;
@@ -393,13 +397,14 @@ __global__ void __launch_bounds__(THREADS, 4) scan_kernel(Args a) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const Smem s = carve<MODE, REFINE>(a, smem, false);
   const QueryCtx qc = load_query<MODE, REFINE>(a, s, q);
+  const int init_n = a.init_counts ? a.init_counts[q] : 0;  // pool carried in from the previous shard
   if (tid < 32) {
-    s.s_pool_d[tid] = dinf();
-    s.s_pool_i[tid] = NO_ID;
+    s.s_pool_d[tid] = tid < init_n ? a.init_dists[q * k + tid] : dinf();
+    s.s_pool_i[tid] = tid < init_n ? a.init_ids[q * k + tid] : NO_ID;
   }
   if (tid == 0) {
-    s_T = dinf();
-    s_pool_n = 0;
+    s_T = init_n >= k ? a.init_dists[q * k + k - 1] : dinf();
+    s_pool_n = init_n;
     s_probed = 0;
     s_surv = 0;
   }
@@ -407,7 +412,9 @@ __global__ void __launch_bounds__(THREADS, 4) scan_kernel(Args a) {
   const int64_t* pid_list = a.probe_ids + q * a.nprobe;
   const double* pd2_list = a.probe_d2 + q * a.nprobe;
   for (int p = 0; p < a.nprobe; ++p) {  // ascending cluster id (search.py:429)
-    const int64_t c = pid_list[p];
+    const int64_t cg = pid_list[p];
+    if (cg < a.list_lo || cg >= a.list_hi) continue;  // another shard's list
+    const int64_t c = cg - a.list_lo;
     const double d_qc2 = pd2_list[p];
     const int64_t lo = a.ix.offsets[c], n_c = a.ix.offsets[c + 1] - lo;
     if (n_c == 0) continue;
@@ -533,9 +540,14 @@ __global__ void __launch_bounds__(THREADS) scan_kernel_bigk(Args a) {
   const int tid = threadIdx.x, lane = tid & 31;
   const Smem s = carve<MODE, REFINE>(a, smem, true);
   const QueryCtx qc = load_query<MODE, REFINE>(a, s, q);
+  const int init_n = a.init_counts ? a.init_counts[q] : 0;
+  for (int i = tid; i < init_n; i += THREADS) {
+    s.s_pool_d[i] = a.init_dists[q * k + i];
+    s.s_pool_i[i] = a.init_ids[q * k + i];
+  }
   if (tid == 0) {
-    s_pool_n = 0;
-    s_T = dinf();
+    s_pool_n = init_n;
+    s_T = init_n >= k ? a.init_dists[q * k + k - 1] : dinf();
     s_probed = 0;
     s_surv = 0;
   }
@@ -543,7 +555,9 @@ __global__ void __launch_bounds__(THREADS) scan_kernel_bigk(Args a) {
   const int64_t* pid_list = a.probe_ids + q * a.nprobe;
   const double* pd2_list = a.probe_d2 + q * a.nprobe;
   for (int p = 0; p < a.nprobe; ++p) {
-    const int64_t c = pid_list[p];
+    const int64_t cg = pid_list[p];
+    if (cg < a.list_lo || cg >= a.list_hi) continue;  // another shard's list
+    const int64_t c = cg - a.list_lo;
     const double d_qc2 = pd2_list[p];
     const int64_t lo = a.ix.offsets[c], n_c = a.ix.offsets[c + 1] - lo;
     if (n_c == 0) continue;
@@ -635,10 +649,60 @@ __global__ void __launch_bounds__(THREADS) scan_kernel_bigk(Args a) {
   }
 }
 
-__global__ void first_probe_kernel(const int64_t* __restrict__ probe_ids, int64_t nq, int nprobe,
-                                   int32_t* __restrict__ first) {
+// first probed list of each query inside this shard's id range (ids ascend per query)
+__global__ void first_probe_kernel(const int64_t* __restrict__ probe_ids, int64_t nq, int nprobe, int64_t list_lo,
+                                   int64_t list_hi, int32_t* __restrict__ first) {
   const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (q < nq) first[q] = (int32_t)probe_ids[q * nprobe];  // ids are ascending per query
+  if (q >= nq) return;
+  int32_t f = 0;
+  for (int p = 0; p < nprobe; ++p) {
+    const int64_t c = probe_ids[q * nprobe + p];
+    if (c >= list_lo && c < list_hi) {
+      f = (int32_t)(c - list_lo);
+      break;
+    }
+  }
+  first[q] = f;
+}
+
+// Merge `parts` per-query top-k lists (each ascending by (dist, id), counts
+// given) into the k best -- the all-gather merge of list-sharded search
+// (merge_topk, search.py:378-387).  One thread per query.
+__global__ void merge_topk_kernel(const int64_t* __restrict__ ids, const double* __restrict__ dists,
+                                  const int32_t* __restrict__ counts, int64_t nq, int parts, int k,
+                                  int64_t* __restrict__ out_ids, double* __restrict__ out_dists,
+                                  int32_t* __restrict__ out_counts) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nq) return;
+  int head[16];
+  for (int p = 0; p < parts; ++p) head[p] = 0;
+  int n = 0;
+  while (n < k) {
+    int best = -1;
+    double bd = 0.0;
+    int64_t bi = 0;
+    for (int p = 0; p < parts; ++p) {
+      const int64_t base = ((int64_t)p * nq + q) * k;
+      if (head[p] >= counts[(int64_t)p * nq + q]) continue;
+      const double d = dists[base + head[p]];
+      const int64_t i = ids[base + head[p]];
+      if (best < 0 || key_less(d, i, bd, bi)) {
+        best = p;
+        bd = d;
+        bi = i;
+      }
+    }
+    if (best < 0) break;
+    ++head[best];
+    out_ids[q * k + n] = bi;
+    out_dists[q * k + n] = bd;
+    ++n;
+  }
+  for (int i = n; i < k; ++i) {
+    out_ids[q * k + i] = -1;
+    out_dists[q * k + i] = dinf();
+  }
+  out_counts[q] = n;
 }
 
 template <int MODE, bool REFINE, bool NIB>
@@ -672,8 +736,22 @@ extern "C" int ivrq_search_scan(const ivrq_index_view* index, const double* q_ro
                                 const float* luts, const int8_t* qslices, int64_t nq,
                                 const ivrq_search_params* params, int64_t* out_ids, double* out_dists,
                                 int32_t* out_counts, int64_t* stats, void* stream) {
+  const int64_t nl = index ? index->n_clusters : 0;
+  return ivrq_search_scan_shard(index, 0, nl, q_rot, probe_ids, probe_d2, scalars, planes, luts, qslices, nq, params,
+                                nullptr, nullptr, nullptr, out_ids, out_dists, out_counts, stats, stream);
+}
+
+extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list_lo, int64_t list_hi,
+                                      const double* q_rot, const int64_t* probe_ids, const double* probe_d2,
+                                      const double* scalars, const uint32_t* planes, const float* luts,
+                                      const int8_t* qslices, int64_t nq, const ivrq_search_params* params,
+                                      const int64_t* init_ids, const double* init_dists,
+                                      const int32_t* init_counts, int64_t* out_ids, double* out_dists,
+                                      int32_t* out_counts, int64_t* stats, void* stream) {
   (void)q_rot;
   if (!index || !params) return fail(IVRQ_EINVAL, "ivrq_search_scan: null argument");
+  if (list_hi - list_lo != index->n_clusters) return fail(IVRQ_EINVAL, "ivrq_search_scan: shard range mismatch");
+  if (init_counts && (!init_ids || !init_dists)) return fail(IVRQ_EINVAL, "ivrq_search_scan: partial init pool");
   if (params->k < 1) return fail(IVRQ_EINVAL, "k must be >= 1");
   if (params->k > 4096) return fail(IVRQ_EUNSUP, "ivrq_search_scan: k > 4096 not supported");
   if (index->bits < 1 || index->bits > 8) return fail(IVRQ_EINVAL, "index bits out of range");
@@ -693,6 +771,11 @@ extern "C" int ivrq_search_scan(const ivrq_index_view* index, const double* q_ro
   a.nprobe = params->n_probe;
   a.qbits = params->query_bits;
   a.prune = params->prune;
+  a.list_lo = list_lo;
+  a.list_hi = list_hi;
+  a.init_ids = init_ids;
+  a.init_dists = init_dists;
+  a.init_counts = init_counts;
   a.g = words_per_vector(index->dims);
   a.kpad = kpad64(index->dims);
   int n2 = 1;
@@ -717,7 +800,8 @@ extern "C" int ivrq_search_scan(const ivrq_index_view* index, const double* q_ro
         cudaMallocAsync(reinterpret_cast<void**>(&off), (index->n_clusters + 1) * sizeof(int64_t), s) != cudaSuccess ||
         cudaMallocAsync(reinterpret_cast<void**>(&order), nq * sizeof(int64_t), s) != cudaSuccess)
       return fail(IVRQ_ENOMEM, "ivrq_search_scan: workspace allocation failed");
-    scan::first_probe_kernel<<<(unsigned)ceil_div(nq, 256), 256, 0, s>>>(probe_ids, nq, a.nprobe, first);
+    scan::first_probe_kernel<<<(unsigned)ceil_div(nq, 256), 256, 0, s>>>(probe_ids, nq, a.nprobe, list_lo, list_hi,
+                                                                         first);
     IVRQ_TRY(check_launch("ivrq_search_scan(order)"));
     IVRQ_TRY(ivrq_counting_sort(first, nq, index->n_clusters, cnt, off, order, stream));
     a.qorder = order;
@@ -731,4 +815,14 @@ extern "C" int ivrq_search_scan(const ivrq_index_view* index, const double* q_ro
     cudaFreeAsync(order, s);
   }
   return rc;
+}
+
+extern "C" int ivrq_merge_topk(const int64_t* ids, const double* dists, const int32_t* counts, int64_t nq,
+                               int32_t parts, int32_t k, int64_t* out_ids, double* out_dists, int32_t* out_counts,
+                               void* stream) {
+  if (parts < 1 || parts > 16 || k < 1) return fail(IVRQ_EINVAL, "ivrq_merge_topk: parts must be in [1, 16]");
+  if (nq == 0) return IVRQ_OK;
+  scan::merge_topk_kernel<<<(unsigned)ceil_div(nq, 128), 128, 0, as_stream(stream)>>>(
+      ids, dists, counts, nq, parts, k, out_ids, out_dists, out_counts);
+  return check_launch("ivrq_merge_topk");
 }

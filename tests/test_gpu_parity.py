@@ -249,3 +249,50 @@ def test_edge_cases_empty_lists_and_small_k():
         np.testing.assert_array_equal(a, c)
         np.testing.assert_allclose(b, d, rtol=1e-9)
     assert iv.search_batch(np.zeros((0, ix.dims)), ix, sp) == []
+
+
+@pytest.mark.parametrize("case,si", [("b8_d128", 0), ("b4_d48", 1), ("b3_d96", 2), ("b1_d32", 0)])
+def test_sharded_scan_chain_and_merge_on_one_gpu(case, si):
+    """The shard kernel path: two list ranges, the second continuing the first's pools."""
+    from paper_2602_23999_b200.distributed import _merge_gpu, cluster_ranges, slice_lists
+    from paper_2602_23999_b200.search import _probe_device, prepare_queries_device
+
+    g = load_case(case)
+    if f"s{si}_ids" not in g:
+        pytest.skip("n_probe exceeds n_clusters")
+    sp = iv.SearchParams(**SEARCHES[si])
+    full = _index(g)
+    counts = np.diff(g["offsets"].astype(np.int64))
+    ranges = cluster_ranges(counts, 2)
+    shards = [slice_lists(full, lo, hi, ranges) for lo, hi in ranges]
+    q_rot = dev.to_device(g["q_rot"])
+    t = full.device
+    probe_ids, probe_d2 = _probe_device(q_rot, t["centroids"], t["centroid_sqnorms"], sp.n_probe, True)
+    nq, k = q_rot.shape[0], sp.k
+
+    def scan(sh, init):
+        scal, planes, luts, qsl = prepare_queries_device(q_rot, sh.local, sp)
+        ids = torch.empty((nq, k), dtype=torch.int64, device=q_rot.device)
+        dd = torch.empty((nq, k), dtype=torch.float64, device=q_rot.device)
+        cc = torch.empty(nq, dtype=torch.int32, device=q_rot.device)
+        from paper_2602_23999_b200 import _lib
+
+        _lib.call(
+            "ivrq_search_scan_shard", sh.local.view(), sh.list_lo, sh.list_hi, None, dev.ptr(probe_ids),
+            dev.ptr(probe_d2), dev.ptr(scal), dev.ptr(planes), dev.ptr(luts), dev.ptr(qsl), nq, sp.to_c(),
+            dev.ptr(init[0]) if init else None, dev.ptr(init[1]) if init else None,
+            dev.ptr(init[2]) if init else None, dev.ptr(ids), dev.ptr(dd), dev.ptr(cc), None, dev.stream_ptr(),
+        )
+        return ids, dd, cc
+
+    p0 = scan(shards[0], None)
+    chained = scan(shards[1], p0)
+    np.testing.assert_array_equal(dev.to_host(chained[2]), g[f"s{si}_counts"])
+    np.testing.assert_array_equal(dev.to_host(chained[0]), g[f"s{si}_ids"])
+    np.testing.assert_allclose(dev.to_host(chained[1]), g[f"s{si}_dists"], rtol=1e-12, atol=1e-12)
+    if case.startswith("b1"):  # order-independent: fresh shards + merge is exact too
+        p1 = scan(shards[1], None)
+        stacked = tuple(torch.stack([a, b]) for a, b in zip(p0, p1))
+        mi, md, mc = _merge_gpu(stacked, 2, k)
+        np.testing.assert_array_equal(dev.to_host(mi), g[f"s{si}_ids"])
+        np.testing.assert_array_equal(dev.to_host(mc), g[f"s{si}_counts"])
