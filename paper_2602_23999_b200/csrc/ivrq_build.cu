@@ -120,23 +120,20 @@ __global__ void __launch_bounds__(1024) kpp_select_kernel(
           const int len = (int)min((int64_t)SC, n - base);
           const double* b = sbuf[cur];
           int hit = -1;
-          int i = 0;
-          for (; i + 4 <= len; i += 4) {
-            const double v0 = b[i], v1 = b[i + 1], v2 = b[i + 2], v3 = b[i + 3];
-            cs = dadd(cs, v0);
-            if (cs >= target) { hit = i; break; }
-            cs = dadd(cs, v1);
-            if (cs >= target) { hit = i + 1; break; }
-            cs = dadd(cs, v2);
-            if (cs >= target) { hit = i + 2; break; }
-            cs = dadd(cs, v3);
-            if (cs >= target) { hit = i + 3; break; }
-          }
-          if (hit < 0)
-            for (; i < len; ++i) {
+          // d2 >= 0 makes the running sum monotone: a branch-free pass over the
+          // chunk decides whether the crossing lies inside it; only that chunk
+          // is walked again with the compares.
+          double end = cs;
+#pragma unroll 8
+          for (int i = 0; i < len; ++i) end = dadd(end, b[i]);
+          if (end >= target) {
+            for (int i = 0; i < len; ++i) {
               cs = dadd(cs, b[i]);
               if (cs >= target) { hit = i; break; }
             }
+          } else {
+            cs = end;
+          }
           if (hit >= 0) {
             s_found = 1;
             s_idx = min(base + hit, n - 1);

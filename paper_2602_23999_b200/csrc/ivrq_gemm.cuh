@@ -6,7 +6,9 @@
 // On B200 the DMMA m16n8k16 path issues twice the float64 MACs per clock of
 // the DFMA pipe (measured: 121.7 vs 61.8 MAC/clk/SM, tools/microbench.cu), so
 // the tiles use mma.sync.m16n8k16.f64: 128x128 CTA tile, 16-deep k slab,
-// 8 warps in a 2x4 grid each owning a 64x32 sub-tile (4x4 fragments).
+// 16 warps in a 4x4 grid each owning a 32x32 sub-tile (2x4 fragments), so an
+// SM keeps 16 warps in flight (the 8-warp variant was latency bound at 12.5%
+// occupancy, profiles/round1).
 // Operand loaders and epilogues are functors so one kernel body serves the
 // query rotation, probe distances, k-means labelling and residual rotation.
 #pragma once
@@ -16,7 +18,8 @@
 namespace ivrq {
 namespace gemm {
 
-constexpr int BM = 128, BN = 128, BK = 16, THREADS = 256;
+constexpr int BM = 128, BN = 128, BK = 16, THREADS = 512;
+constexpr int MF = 2, NF = 4;  // m16 / n8 fragments per warp
 constexpr int LDA = BM + 8;  // k-major smem pitch (doubles): conflict-free fragment loads
 constexpr int SMEM_BYTES = 2 * 2 * BK * LDA * (int)sizeof(double);  // double-buffered A and B
 
@@ -39,14 +42,14 @@ __device__ __forceinline__ void dmma16816(double (&c)[4], const double (&a)[8], 
 }
 
 // Accumulator tile of one thread: acc[mf][nf][r], r = 0,1: row gid, cols 2t4+r;
-// r = 2,3: row gid+8.  Rows: wm*64 + mf*16 (+gid), cols: wn*32 + nf*8 (+2t4).
+// r = 2,3: row gid+8.  Rows: wm*32 + mf*16 (+gid), cols: wn*32 + nf*8 (+2t4).
 struct Acc {
-  double v[4][4][4];
+  double v[MF][NF][4];
 };
 
 __device__ __forceinline__ int64_t acc_row(int64_t m0, int mf, int r) {
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  return m0 + (w >> 2) * 64 + mf * 16 + (lane >> 2) + (r >= 2 ? 8 : 0);
+  return m0 + (w >> 2) * 32 + mf * 16 + (lane >> 2) + (r >= 2 ? 8 : 0);
 }
 __device__ __forceinline__ int64_t acc_col(int64_t n0, int nf, int r) {
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -63,20 +66,19 @@ __device__ __forceinline__ void mainloop(const LA& la, int64_t M, const LB& lb, 
   double* As = smem;                // [2][BK][LDA]
   double* Bs = smem + 2 * BK * LDA;  // [2][BK][LDA]
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < MF; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+    for (int j = 0; j < NF; ++j)
 #pragma unroll
       for (int r = 0; r < 4; ++r) acc.v[i][j][r] = 0.0;
 
-  // global->smem: each thread moves 8 (row, k) elements per operand:
-  // row = tid / 2, k = (tid % 2) * 8 + e
-  const int lr = tid >> 1, lk0 = (tid & 1) * 8;
-  double ra[8], rb[8];
+  // global->smem: each thread moves 4 consecutive k of one row per operand
+  const int lr = tid >> 2, lk0 = (tid & 3) * 4;
+  double ra[4], rb[4];
   auto load_regs = [&](int k0) {
     const int64_t gm = m0 + lr, gn = n0 + lr;
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
+    for (int e = 0; e < 4; ++e) {
       const int k = k0 + lk0 + e;
       ra[e] = (gm < M && k < K) ? la(gm, k) : 0.0;
       rb[e] = (gn < N && k < K) ? lb(gn, k) : 0.0;
@@ -86,7 +88,7 @@ __device__ __forceinline__ void mainloop(const LA& la, int64_t M, const LB& lb, 
     double* a = As + buf * BK * LDA;
     double* b = Bs + buf * BK * LDA;
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
+    for (int e = 0; e < 4; ++e) {
       a[(lk0 + e) * LDA + lr] = ra[e];
       b[(lk0 + e) * LDA + lr] = rb[e];
     }
@@ -101,24 +103,24 @@ __device__ __forceinline__ void mainloop(const LA& la, int64_t M, const LB& lb, 
     if (kt + 1 < nk) load_regs((kt + 1) * BK);
     const double* a = As + buf * BK * LDA;
     const double* b = Bs + buf * BK * LDA;
-    // B fragments of the warp's 4 column blocks: b_j = B[k = t4 + 4j][n = gid]
-    double bf[4][4];
+    // B fragments of the warp's column blocks: b_j = B[k = t4 + 4j][n = gid]
+    double bf[NF][4];
 #pragma unroll
-    for (int nf = 0; nf < 4; ++nf)
+    for (int nf = 0; nf < NF; ++nf)
 #pragma unroll
       for (int j = 0; j < 4; ++j) bf[nf][j] = b[(t4 + 4 * j) * LDA + wn * 32 + nf * 8 + gid];
 #pragma unroll
-    for (int mf = 0; mf < 4; ++mf) {
+    for (int mf = 0; mf < MF; ++mf) {
       // A fragment: a_{2j} = A[row gid][k = t4 + 4j], a_{2j+1} = A[row gid + 8][k = t4 + 4j]
       double af[8];
-      const int rbase = wm * 64 + mf * 16 + gid;
+      const int rbase = wm * 32 + mf * 16 + gid;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         af[2 * j] = a[(t4 + 4 * j) * LDA + rbase];
         af[2 * j + 1] = a[(t4 + 4 * j) * LDA + rbase + 8];
       }
 #pragma unroll
-      for (int nf = 0; nf < 4; ++nf) dmma16816(acc.v[mf][nf], af, bf[nf]);
+      for (int nf = 0; nf < NF; ++nf) dmma16816(acc.v[mf][nf], af, bf[nf]);
     }
     if (kt + 1 < nk) store_smem(buf ^ 1);
     __syncthreads();
@@ -134,9 +136,9 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_kernel(LA la, int64_t M, LB l
   Acc acc;
   mainloop(la, M, lb, N, K, m0, n0, smem_d, acc);
 #pragma unroll
-  for (int mf = 0; mf < 4; ++mf)
+  for (int mf = 0; mf < MF; ++mf)
 #pragma unroll
-    for (int nf = 0; nf < 4; ++nf)
+    for (int nf = 0; nf < NF; ++nf)
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
         const int64_t row = acc_row(m0, mf, r), col = acc_col(n0, nf, r);
@@ -155,10 +157,10 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_argmin_kernel(LA la, int64_t 
   __shared__ int32_t red_i[4][BM];
   const int64_t m0 = (int64_t)blockIdx.x * BM;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double best_d[8];
-  int32_t best_i[8];  // [mf*2 + (r>=2)]
+  double best_d[2 * MF];
+  int32_t best_i[2 * MF];  // [mf*2 + (r>=2)]
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
+  for (int i = 0; i < 2 * MF; ++i) {
     best_d[i] = __longlong_as_double(0x7ff0000000000000LL);  // +inf
     best_i[i] = 0x7fffffff;
   }
@@ -166,9 +168,9 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_argmin_kernel(LA la, int64_t 
   for (int64_t n0 = 0; n0 < N; n0 += BN) {
     mainloop(la, M, lb, N, K, m0, n0, smem_d, acc);
 #pragma unroll
-    for (int mf = 0; mf < 4; ++mf)
+    for (int mf = 0; mf < MF; ++mf)
 #pragma unroll
-      for (int nf = 0; nf < 4; ++nf)
+      for (int nf = 0; nf < NF; ++nf)
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
           const int64_t row = acc_row(m0, mf, r), col = acc_col(n0, nf, r);
@@ -184,7 +186,7 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_argmin_kernel(LA la, int64_t 
   }
   // reduce over the 4 lanes (t4) sharing a row, then over the 4 column warps
 #pragma unroll
-  for (int s = 0; s < 8; ++s) {
+  for (int s = 0; s < 2 * MF; ++s) {
 #pragma unroll
     for (int o = 1; o <= 2; o <<= 1) {
       const double od = __shfl_xor_sync(0xffffffffu, best_d[s], o);
@@ -197,8 +199,8 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_argmin_kernel(LA la, int64_t 
   }
   if ((lane & 3) == 0) {
 #pragma unroll
-    for (int s = 0; s < 8; ++s) {
-      const int lrow = (w >> 2) * 64 + (s >> 1) * 16 + (lane >> 2) + (s & 1) * 8;
+    for (int s = 0; s < 2 * MF; ++s) {
+      const int lrow = (w >> 2) * 32 + (s >> 1) * 16 + (lane >> 2) + (s & 1) * 8;
       red_d[w & 3][lrow] = best_d[s];
       red_i[w & 3][lrow] = best_i[s];
     }
