@@ -38,6 +38,7 @@ struct Args {
   const float* luts;
   const int8_t* qslices;
   const int64_t* qorder;  // CTA -> query (queries grouped by first probed list)
+  int skip_first;         // the first in-range probe was handled by first_list_kernel
   int64_t nq;
   int k, nprobe, qbits, prune;
   int64_t list_lo, list_hi;  // global cluster ids held by this (shard of the) index
@@ -405,15 +406,21 @@ __global__ void __launch_bounds__(THREADS, 4) scan_kernel(Args a) {
   if (tid == 0) {
     s_T = init_n >= k ? a.init_dists[q * k + k - 1] : dinf();
     s_pool_n = init_n;
-    s_probed = 0;
-    s_surv = 0;
+    // after the first-list phase the first list's counts are already in stats
+    s_probed = (a.skip_first && a.stats) ? a.stats[2 * q] : 0;
+    s_surv = (a.skip_first && a.stats) ? a.stats[2 * q + 1] : 0;
   }
   __syncthreads();
   const int64_t* pid_list = a.probe_ids + q * a.nprobe;
   const double* pd2_list = a.probe_d2 + q * a.nprobe;
+  bool first_pending = a.skip_first != 0;
   for (int p = 0; p < a.nprobe; ++p) {  // ascending cluster id (search.py:429)
     const int64_t cg = pid_list[p];
     if (cg < a.list_lo || cg >= a.list_hi) continue;  // another shard's list
+    if (first_pending) {  // scanned by first_list_kernel
+      first_pending = false;
+      continue;
+    }
     const int64_t c = cg - a.list_lo;
     const double d_qc2 = pd2_list[p];
     const int64_t lo = a.ix.offsets[c], n_c = a.ix.offsets[c + 1] - lo;
@@ -649,12 +656,222 @@ __global__ void __launch_bounds__(THREADS) scan_kernel_bigk(Args a) {
   }
 }
 
+// ------------------------------------------------------------ first-list phase
+// Each query's first (lowest-id) probed list is scanned with the threshold at
+// +inf (search.py:435 before any merge): every vector survives and is refined.
+// That is the bulk of all refines, and queries sharing a first list can share
+// one pass over its codes: one CTA takes a list and up to QG of the queries
+// whose first list it is, streams the list's rcodes once through the int8
+// tensor cores against all their digit slices, and leaves each query's pool
+// after that list.  scan_kernel then continues from those pools.
+constexpr int QG = 8;
+
+struct FArgs {
+  ivrq_index_view ix;
+  int64_t list_lo, list_hi;
+  const int64_t* probe_ids;
+  const double* probe_d2;
+  int nprobe;
+  const double* scalars;
+  const int8_t* qslices;
+  int kpad;
+  const int64_t* qorder;  // queries sorted by first list (local id), bucket nlist = none
+  const int64_t* qoff;    // [nlist + 2] start of each bucket in qorder
+  const int32_t* gpre;    // [nlist + 1] prefix sum of ceil(bucket size / QG)
+  int nlist, k;
+  int64_t* pool_ids;
+  double* pool_d;
+  int32_t* pool_n;
+  int64_t* stats;
+};
+
+__global__ void group_prefix_kernel(const int64_t* __restrict__ qoff, int nlist, int32_t* __restrict__ gpre) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  int32_t s = 0;
+  gpre[0] = 0;
+  for (int c = 0; c < nlist; ++c) {
+    s += (int32_t)((qoff[c + 1] - qoff[c] + QG - 1) / QG);
+    gpre[c + 1] = s;
+  }
+}
+
+template <bool NIB>
+__global__ void __launch_bounds__(THREADS) first_list_kernel(FArgs a) {
+  extern __shared__ __align__(16) unsigned char fsm[];
+  __shared__ double s_qd[WARPS][32];
+  __shared__ int64_t s_qi[WARPS][32];
+  __shared__ int64_t s_q[QG];
+  __shared__ double s_dq[QG], s_kb[QG];
+  __shared__ int s_e[QG];
+  const int b = blockIdx.x;
+  if (b >= a.gpre[a.nlist]) return;
+  int lo_c = 0, hi_c = a.nlist;  // gpre[lo_c] <= b < gpre[hi_c]
+  while (hi_c - lo_c > 1) {
+    const int mid = (lo_c + hi_c) >> 1;
+    if (a.gpre[mid] <= b) lo_c = mid; else hi_c = mid;
+  }
+  const int c = lo_c;
+  const int64_t qs = a.qoff[c] + (int64_t)(b - a.gpre[c]) * QG;
+  const int nqg = (int)min((int64_t)QG, a.qoff[c + 1] - qs);
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int gid = lane >> 2, t4 = lane & 3;
+  const int kp = a.kpad, ss = kp + SPAD, k = a.k;
+  int8_t* s_sl = reinterpret_cast<int8_t*>(fsm);  // [QG][SLICES][ss]
+  if (tid < QG) {
+    int64_t q = -1;
+    double dq = 0.0;
+    if (tid < nqg) {
+      q = a.qorder[qs + tid];
+      for (int p = 0; p < a.nprobe; ++p) {  // the first in-range probe is list c
+        if (a.probe_ids[q * a.nprobe + p] == c + a.list_lo) {
+          dq = a.probe_d2[q * a.nprobe + p];
+          break;
+        }
+      }
+      s_kb[tid] = a.scalars[q * IVRQ_QS_COUNT + IVRQ_QS_KB_SUM];
+      s_e[tid] = (int)a.scalars[q * IVRQ_QS_COUNT + IVRQ_QS_SLICE_EXP];
+    }
+    s_q[tid] = q;
+    s_dq[tid] = dq;
+  }
+  __syncthreads();
+  for (int i = tid; i < nqg * SLICES * kp / 4; i += THREADS) {
+    const int j = (4 * i) / (SLICES * kp), rem = (4 * i) % (SLICES * kp);
+    const int sidx = rem / kp, kk = rem % kp;
+    *reinterpret_cast<uint32_t*>(s_sl + (j * SLICES + sidx) * ss + kk) =
+        reinterpret_cast<const uint32_t*>(a.qslices + s_q[j] * SLICES * (int64_t)kp)[rem / 4];
+  }
+  __syncthreads();
+  const int64_t lo = a.ix.offsets[c], n_c = a.ix.offsets[c + 1] - lo;
+  const int64_t rb = a.ix.rcode_bytes;
+  double qd[QG];
+  int64_t qi[QG];
+#pragma unroll
+  for (int j = 0; j < QG; ++j) {
+    qd[j] = dinf();
+    qi[j] = NO_ID;
+  }
+  for (int64_t t0 = (int64_t)wid * 16; t0 < n_c; t0 += WARPS * 16) {
+    const int64_t v0 = min(t0 + gid, n_c - 1), v1 = min(t0 + gid + 8, n_c - 1);
+    const uint8_t* row0 = a.ix.rcodes + (lo + v0) * rb;
+    const uint8_t* row1 = a.ix.rcodes + (lo + v1) * rb;
+    int acc[QG][4];
+#pragma unroll
+    for (int j = 0; j < QG; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0;
+    for (int p = 0; p < kp / 64; ++p) {
+      uint32_t a0s0, a2s0, a0s1, a2s1, a1s0, a3s0, a1s1, a3s1;
+      if (NIB) {
+        const uint2 x0 = __ldg(reinterpret_cast<const uint2*>(row0 + 8 * (4 * p + t4)));
+        const uint2 x1 = __ldg(reinterpret_cast<const uint2*>(row1 + 8 * (4 * p + t4)));
+        a0s0 = x0.x & 0x0F0F0F0Fu;
+        a2s0 = (x0.x >> 4) & 0x0F0F0F0Fu;
+        a0s1 = x0.y & 0x0F0F0F0Fu;
+        a2s1 = (x0.y >> 4) & 0x0F0F0F0Fu;
+        a1s0 = x1.x & 0x0F0F0F0Fu;
+        a3s0 = (x1.x >> 4) & 0x0F0F0F0Fu;
+        a1s1 = x1.y & 0x0F0F0F0Fu;
+        a3s1 = (x1.y >> 4) & 0x0F0F0F0Fu;
+      } else {
+        const uint4 x0 = __ldg(reinterpret_cast<const uint4*>(row0 + 16 * (4 * p + t4)));
+        const uint4 x1 = __ldg(reinterpret_cast<const uint4*>(row1 + 16 * (4 * p + t4)));
+        a0s0 = x0.x;
+        a2s0 = x0.y;
+        a0s1 = x0.z;
+        a2s1 = x0.w;
+        a1s0 = x1.x;
+        a3s0 = x1.y;
+        a1s1 = x1.z;
+        a3s1 = x1.w;
+      }
+#pragma unroll
+      for (int j = 0; j < QG; ++j) {
+        if (j < nqg) {
+          const int8_t* sl = s_sl + (j * SLICES + gid) * ss + 4 * t4 + 64 * p;
+          const uint32_t b00 = *reinterpret_cast<const uint32_t*>(sl);
+          const uint32_t b10 = *reinterpret_cast<const uint32_t*>(sl + 16);
+          const uint32_t b01 = *reinterpret_cast<const uint32_t*>(sl + 32);
+          const uint32_t b11 = *reinterpret_cast<const uint32_t*>(sl + 48);
+          mma_u8s8(acc[j], a0s0, a1s0, a2s0, a3s0, b00, b10);
+          mma_u8s8(acc[j], a0s1, a1s1, a2s1, a3s1, b01, b11);
+        }
+      }
+    }
+    // rows of this tile as candidate lanes 0..15 (lane L <- row t0 + L)
+    const int L = lane & 15;
+    const bool row_ok = lane < 16 && t0 + L < n_c;
+    const long long w0 = (t4 & 1) ? 128LL : 2097152LL;
+    const long long w1 = (t4 & 1) ? 1LL : 16384LL;
+    float2 lf = make_float2(0.f, 0.f);
+    if (row_ok) lf = __ldg(reinterpret_cast<const float2*>(a.ix.long_factors) + lo + t0 + L);
+#pragma unroll
+    for (int j = 0; j < QG; ++j) {
+      if (j >= nqg) continue;
+      long long p0 = (long long)acc[j][0] * w0 + (long long)acc[j][1] * w1;
+      long long p1 = (long long)acc[j][2] * w0 + (long long)acc[j][3] * w1;
+      p0 += __shfl_xor_sync(FULL, p0, 1);
+      p1 += __shfl_xor_sync(FULL, p1, 1);
+      const long long l0 = __shfl_xor_sync(FULL, p0, 2);
+      const long long l1 = __shfl_xor_sync(FULL, p1, 2);
+      const int src = (L & 7) * 4;  // lane t4 == 0 of group (row & 7) holds the sums
+      const long long hi0 = __shfl_sync(FULL, p0, src), hi1 = __shfl_sync(FULL, p1, src);
+      const long long lw0 = __shfl_sync(FULL, l0, src), lw1 = __shfl_sync(FULL, l1, src);
+      double d = dinf();
+      if (row_ok) {
+        const long long hi = (L >= 8) ? hi1 : hi0, lw = (L >= 8) ? lw1 : lw0;
+        const double ip = dadd(dmul((double)hi, ldexp(1.0, s_e[j] - 26)), dmul((double)lw, ldexp(1.0, s_e[j] - 54)));
+        d = dmax(dsub(dadd((double)lf.x, s_dq[j]), dmul((double)lf.y, dsub(ip, s_kb[j]))), 0.0);
+      }
+      const double kd = __shfl_sync(FULL, qd[j], k - 1);
+      const int64_t ki = __shfl_sync(FULL, qi[j], k - 1);
+      const bool maybe = row_ok && d <= kd;
+      if (!__any_sync(FULL, maybe)) continue;
+      int64_t id = maybe ? (int64_t)__ldg(a.ix.pids + lo + t0 + L) : NO_ID;
+      const bool pass = maybe && key_less(d, id, kd, ki);
+      if (!__any_sync(FULL, pass)) continue;
+      double dd = pass ? d : dinf();
+      if (!pass) id = NO_ID;
+      warp_sort32(dd, id);
+      warp_merge32(qd[j], qi[j], dd, id);
+    }
+  }
+  // fold the 8 warp queues of each query into its pool
+#pragma unroll
+  for (int j = 0; j < QG; ++j) {
+    if (j >= nqg) break;
+    s_qd[wid][lane] = qd[j];
+    s_qi[wid][lane] = qi[j];
+    __syncthreads();
+    if (wid == 0) {
+      double pd = s_qd[0][lane];
+      int64_t pi = s_qi[0][lane];
+      for (int w = 1; w < WARPS; ++w) {
+        if (s_qi[w][0] == NO_ID) continue;
+        warp_merge32(pd, pi, s_qd[w][lane], s_qi[w][lane]);
+      }
+      const int64_t q = s_q[j];
+      if (lane < k) {
+        a.pool_ids[q * k + lane] = pi;
+        a.pool_d[q * k + lane] = pd;
+      }
+      const int cnt = __popc(__ballot_sync(FULL, lane < k && pi != NO_ID));
+      if (lane == 0) {
+        a.pool_n[q] = cnt;
+        if (a.stats) {
+          a.stats[2 * q] = n_c;
+          a.stats[2 * q + 1] = n_c;
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // first probed list of each query inside this shard's id range (ids ascend per query)
 __global__ void first_probe_kernel(const int64_t* __restrict__ probe_ids, int64_t nq, int nprobe, int64_t list_lo,
                                    int64_t list_hi, int32_t* __restrict__ first) {
   const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= nq) return;
-  int32_t f = 0;
+  int32_t f = (int32_t)(list_hi - list_lo);  // bucket "no list of this shard"
   for (int p = 0; p < nprobe; ++p) {
     const int64_t c = probe_ids[q * nprobe + p];
     if (c >= list_lo && c < list_hi) {
@@ -794,17 +1011,65 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
   int64_t *cnt = nullptr, *off = nullptr, *order = nullptr;
   const char* ord_env = getenv("IVRQ_SCAN_ORDER");
   const bool grouped = ord_env ? atoi(ord_env) != 0 : true;
-  if (grouped && nq > 1 && index->n_clusters > 1) {
+  const int64_t nl = index->n_clusters;
+  int32_t* gpre = nullptr;
+  int64_t* pool_ids = nullptr;
+  double* pool_d = nullptr;
+  int32_t* pool_n = nullptr;
+  const char* fl_env = getenv("IVRQ_FIRST_LIST");
+  const bool first_phase = grouped && refine && a.k <= 32 && !init_counts && (fl_env ? atoi(fl_env) != 0 : true);
+  if (grouped && nq > 1 && nl >= 1) {
     if (cudaMallocAsync(reinterpret_cast<void**>(&first), nq * sizeof(int32_t), s) != cudaSuccess ||
-        cudaMallocAsync(reinterpret_cast<void**>(&cnt), index->n_clusters * sizeof(int64_t), s) != cudaSuccess ||
-        cudaMallocAsync(reinterpret_cast<void**>(&off), (index->n_clusters + 1) * sizeof(int64_t), s) != cudaSuccess ||
+        cudaMallocAsync(reinterpret_cast<void**>(&cnt), (nl + 1) * sizeof(int64_t), s) != cudaSuccess ||
+        cudaMallocAsync(reinterpret_cast<void**>(&off), (nl + 2) * sizeof(int64_t), s) != cudaSuccess ||
         cudaMallocAsync(reinterpret_cast<void**>(&order), nq * sizeof(int64_t), s) != cudaSuccess)
       return fail(IVRQ_ENOMEM, "ivrq_search_scan: workspace allocation failed");
     scan::first_probe_kernel<<<(unsigned)ceil_div(nq, 256), 256, 0, s>>>(probe_ids, nq, a.nprobe, list_lo, list_hi,
                                                                          first);
     IVRQ_TRY(check_launch("ivrq_search_scan(order)"));
-    IVRQ_TRY(ivrq_counting_sort(first, nq, index->n_clusters, cnt, off, order, stream));
+    IVRQ_TRY(ivrq_counting_sort(first, nq, (int32_t)(nl + 1), cnt, off, order, stream));
     a.qorder = order;
+    if (first_phase) {
+      if (cudaMallocAsync(reinterpret_cast<void**>(&gpre), (nl + 1) * sizeof(int32_t), s) != cudaSuccess ||
+          cudaMallocAsync(reinterpret_cast<void**>(&pool_ids), nq * a.k * sizeof(int64_t), s) != cudaSuccess ||
+          cudaMallocAsync(reinterpret_cast<void**>(&pool_d), nq * a.k * sizeof(double), s) != cudaSuccess ||
+          cudaMallocAsync(reinterpret_cast<void**>(&pool_n), nq * sizeof(int32_t), s) != cudaSuccess)
+        return fail(IVRQ_ENOMEM, "ivrq_search_scan: workspace allocation failed");
+      cudaMemsetAsync(pool_n, 0, nq * sizeof(int32_t), s);
+      if (stats) cudaMemsetAsync(stats, 0, 2 * nq * sizeof(int64_t), s);
+      scan::group_prefix_kernel<<<1, 1, 0, s>>>(off, (int)nl, gpre);
+      scan::FArgs fa{};
+      fa.ix = *index;
+      fa.list_lo = list_lo;
+      fa.list_hi = list_hi;
+      fa.probe_ids = probe_ids;
+      fa.probe_d2 = probe_d2;
+      fa.nprobe = a.nprobe;
+      fa.scalars = scalars;
+      fa.qslices = qslices;
+      fa.kpad = a.kpad;
+      fa.qorder = order;
+      fa.qoff = off;
+      fa.gpre = gpre;
+      fa.nlist = (int)nl;
+      fa.k = a.k;
+      fa.pool_ids = pool_ids;
+      fa.pool_d = pool_d;
+      fa.pool_n = pool_n;
+      fa.stats = stats;
+      const size_t fsm = (size_t)scan::QG * scan::SLICES * (a.kpad + scan::SPAD);
+      auto fk = nib ? scan::first_list_kernel<true> : scan::first_list_kernel<false>;
+      if (fsm > 48 * 1024 &&
+          cudaFuncSetAttribute(fk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm) != cudaSuccess)
+        return fail(IVRQ_EUNSUP, "ivrq_search_scan: dims too large for the first-list phase");
+      const unsigned grid = (unsigned)(ceil_div(nq, scan::QG) + nl);
+      fk<<<grid, scan::THREADS, fsm, s>>>(fa);
+      IVRQ_TRY(check_launch("ivrq_search_scan(first lists)"));
+      a.init_ids = pool_ids;
+      a.init_dists = pool_d;
+      a.init_counts = pool_n;
+      a.skip_first = 1;
+    }
   }
   const int rc = params->ip_mode == IVRQ_IP_BITWISE ? scan::launch_mode<IVRQ_IP_BITWISE>(a, refine, nib, s)
                                                     : scan::launch_mode<IVRQ_IP_LUT>(a, refine, nib, s);
@@ -813,6 +1078,12 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
     cudaFreeAsync(cnt, s);
     cudaFreeAsync(off, s);
     cudaFreeAsync(order, s);
+  }
+  if (gpre) {
+    cudaFreeAsync(gpre, s);
+    cudaFreeAsync(pool_ids, s);
+    cudaFreeAsync(pool_d, s);
+    cudaFreeAsync(pool_n, s);
   }
   return rc;
 }
