@@ -306,6 +306,42 @@ __device__ __forceinline__ void warp_merge32(double& qd, int64_t& qi, double bd,
   for (int stride = 16; stride > 0; stride >>= 1) cmpx(qd, qi, stride, (lane & stride) == 0);
 }
 
+// Fold this warp's candidates (d, id) where `pass` into the sorted queue.
+// Few passers: insert one at a time (position by ballot, shift by shfl_up);
+// many (a filling queue): sort the batch and merge.
+__device__ __forceinline__ void warp_fold(double& qd, int64_t& qi, double d, int64_t id, bool pass, int k) {
+  const int lane = threadIdx.x & 31;
+  unsigned m = __ballot_sync(FULL, pass);
+  if (__popc(m) > 6) {
+    if (!pass) {
+      d = dinf();
+      id = NO_ID;
+    }
+    warp_sort32(d, id);
+    warp_merge32(qd, qi, d, id);
+    return;
+  }
+  while (m) {
+    const int src = __ffs(m) - 1;
+    m &= m - 1;
+    const double xd = __shfl_sync(FULL, d, src);
+    const int64_t xi = __shfl_sync(FULL, id, src);
+    const double kd = __shfl_sync(FULL, qd, k - 1);
+    const int64_t ki = __shfl_sync(FULL, qi, k - 1);
+    if (!key_less(xd, xi, kd, ki)) continue;  // the queue moved on
+    const int pos = __popc(__ballot_sync(FULL, key_less(qd, qi, xd, xi)));
+    const double ud = __shfl_up_sync(FULL, qd, 1);
+    const int64_t ui = __shfl_up_sync(FULL, qi, 1);
+    if (lane > pos) {
+      qd = ud;
+      qi = ui;
+    } else if (lane == pos) {
+      qd = xd;
+      qi = xi;
+    }
+  }
+}
+
 // ------------------------------------------------------------ common prologue
 struct Smem {
   int8_t* s_slices;
@@ -465,12 +501,7 @@ __global__ void __launch_bounds__(THREADS, 4) scan_kernel(Args a) {
         int64_t id = maybe ? (int64_t)__ldg(a.ix.pids + lo + c0 + s.s_cv[ci]) : NO_ID;
         const bool pass = maybe && key_less(d, id, wk_d, wk_i) && key_less(d, id, pk_d, pk_i);
         if (!__any_sync(FULL, pass)) continue;
-        if (!pass) {
-          d = dinf();
-          id = NO_ID;
-        }
-        warp_sort32(d, id);
-        warp_merge32(qd, qi, d, id);
+        warp_fold(qd, qi, d, id, pass, k);
       }
     }
     if (!__syncthreads_or(any_cand)) continue;
@@ -701,8 +732,9 @@ __global__ void __launch_bounds__(THREADS) first_list_kernel(FArgs a) {
   __shared__ double s_qd[WARPS][32];
   __shared__ int64_t s_qi[WARPS][32];
   __shared__ int64_t s_q[QG];
-  __shared__ double s_dq[QG], s_kb[QG];
+  __shared__ double s_dq[QG], s_kb[QG], s_hs[QG], s_ls[QG];
   __shared__ int s_e[QG];
+  __shared__ unsigned long long s_bnd[QG];  // bits of a bound on each query's k-th distance
   const int b = blockIdx.x;
   if (b >= a.gpre[a.nlist]) return;
   int lo_c = 0, hi_c = a.nlist;  // gpre[lo_c] <= b < gpre[hi_c]
@@ -730,9 +762,12 @@ __global__ void __launch_bounds__(THREADS) first_list_kernel(FArgs a) {
       }
       s_kb[tid] = a.scalars[q * IVRQ_QS_COUNT + IVRQ_QS_KB_SUM];
       s_e[tid] = (int)a.scalars[q * IVRQ_QS_COUNT + IVRQ_QS_SLICE_EXP];
+      s_hs[tid] = ldexp(1.0, s_e[tid] - 26);
+      s_ls[tid] = ldexp(1.0, s_e[tid] - 54);
     }
     s_q[tid] = q;
     s_dq[tid] = dq;
+    s_bnd[tid] = 0x7ff0000000000000ULL;  // +inf
   }
   __syncthreads();
   for (int i = tid; i < nqg * SLICES * kp / 4; i += THREADS) {
@@ -818,20 +853,23 @@ __global__ void __launch_bounds__(THREADS) first_list_kernel(FArgs a) {
       double d = dinf();
       if (row_ok) {
         const long long hi = (L >= 8) ? hi1 : hi0, lw = (L >= 8) ? lw1 : lw0;
-        const double ip = dadd(dmul((double)hi, ldexp(1.0, s_e[j] - 26)), dmul((double)lw, ldexp(1.0, s_e[j] - 54)));
+        const double ip = dadd(dmul((double)hi, s_hs[j]), dmul((double)lw, s_ls[j]));
         d = dmax(dsub(dadd((double)lf.x, s_dq[j]), dmul((double)lf.y, dsub(ip, s_kb[j]))), 0.0);
       }
       const double kd = __shfl_sync(FULL, qd[j], k - 1);
       const int64_t ki = __shfl_sync(FULL, qi[j], k - 1);
-      const bool maybe = row_ok && d <= kd;
+      // any warp holding k candidates bounds the query's k-th distance
+      const double bound = __longlong_as_double((long long)*(volatile unsigned long long*)&s_bnd[j]);
+      const bool maybe = row_ok && d <= kd && d <= bound;
       if (!__any_sync(FULL, maybe)) continue;
       int64_t id = maybe ? (int64_t)__ldg(a.ix.pids + lo + t0 + L) : NO_ID;
       const bool pass = maybe && key_less(d, id, kd, ki);
       if (!__any_sync(FULL, pass)) continue;
-      double dd = pass ? d : dinf();
-      if (!pass) id = NO_ID;
-      warp_sort32(dd, id);
-      warp_merge32(qd[j], qi[j], dd, id);
+      warp_fold(qd[j], qi[j], d, id, pass, k);
+      const int64_t full_i = __shfl_sync(FULL, qi[j], k - 1);
+      const double full_d = __shfl_sync(FULL, qd[j], k - 1);
+      if (lane == 0 && full_i != NO_ID)
+        atomicMin(&s_bnd[j], (unsigned long long)__double_as_longlong(full_d));
     }
   }
   // fold the 8 warp queues of each query into its pool
