@@ -222,6 +222,12 @@ def run_ours(args, cfg_name: str) -> dict:
     torch.cuda.synchronize()
     build_s = time.perf_counter() - tb
     log(f"[bench] build {build_s:.2f}s")
+    build_stages: dict = {}
+    if args.build_breakdown:
+        del index
+        torch.cuda.empty_cache()
+        index = build_index_device(x, params, timings=build_stages)
+        log(f"[bench] build stages {build_stages}")
     # ---- ground truth + nprobe choice
     tg = time.perf_counter()
     n_gt = NQ if args.gt_queries <= 0 else min(NQ, args.gt_queries)
@@ -332,6 +338,7 @@ def run_ours(args, cfg_name: str) -> dict:
             "recall_queries": n_gt,
             "nprobe_sweep": sweep,
             "build_seconds": round(build_s, 3),
+            "build_stage_seconds": {k2: round(v, 3) for k2, v in build_stages.items()},
             "build_params": {"kmeans_iters": 25, "train_fraction": round(params.train_fraction, 5), "seed": 0},
             "stage_ms_per_step": {k2: round(v / args.steps, 4) for k2, v in stage_ms.items()},
             "l2": "flushed (256 MB write) between timed steps",
@@ -495,6 +502,7 @@ def main() -> None:
     ap.add_argument("--ref-nprobe", type=int, default=8)
     ap.add_argument("--ref-queries-per-step", type=int, default=64)
     ap.add_argument("--gt-queries", type=int, default=0, help="queries with exact ground truth (0 = all)")
+    ap.add_argument("--build-breakdown", action="store_true", help="rebuild once with per-stage timings")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":

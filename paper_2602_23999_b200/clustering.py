@@ -135,14 +135,22 @@ def _kmeanspp_device(x: torch.Tensor, n_clusters: int, seed: int) -> torch.Tenso
     return centers
 
 
-def train_kmeans_device(x: torch.Tensor, n_clusters: int, iters: int, seed: int) -> torch.Tensor:
+def train_kmeans_device(x: torch.Tensor, n_clusters: int, iters: int, seed: int,
+                        timings: dict | None = None) -> torch.Tensor:
     """Lloyd's k-means with k-means++ seeding on float32 device rows; returns float64 centres."""
+    import time
+
     n, d = x.shape
     if n_clusters < 1 or n_clusters > n:
         raise ValueError(f"n_clusters must be in [1, {n}], got {n_clusters}")
     if iters < 1:
         raise ValueError(f"iters must be >= 1, got {iters}")
+    t0 = time.perf_counter()
     centers = _kmeanspp_device(x, n_clusters, seed)
+    if timings is not None:
+        torch.cuda.synchronize()
+        timings["kmeans_pp"] = time.perf_counter() - t0
+        t0 = time.perf_counter()
     n_empty = torch.zeros(1, dtype=torch.int32, device=x.device)
     for _ in range(iters):
         c_sq = row_sqnorms(centers)
@@ -159,6 +167,9 @@ def train_kmeans_device(x: torch.Tensor, n_clusters: int, iters: int, seed: int)
             dev.ptr(x), n, dev.ptr(order), dev.ptr(offsets), n_clusters, d, dev.ptr(new_centers), dev.stream_ptr(),
         )
         centers = new_centers
+    if timings is not None:
+        torch.cuda.synchronize()
+        timings["lloyd"] = time.perf_counter() - t0
     return centers
 
 

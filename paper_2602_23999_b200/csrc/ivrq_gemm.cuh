@@ -131,8 +131,9 @@ __device__ __forceinline__ void mainloop(const LA& la, int64_t M, const LB& lb, 
 template <typename LA, typename LB, typename EPI>
 __global__ void __launch_bounds__(THREADS, 1) gemm_kernel(LA la, int64_t M, LB lb, int64_t N, int K, EPI epi) {
   extern __shared__ __align__(16) double smem_d[];
-  const int64_t m0 = (int64_t)blockIdx.y * BM;
-  const int64_t n0 = (int64_t)blockIdx.x * BN;
+  // row tiles on grid.x (up to 2^31-1: N = 10M rows is 78K tiles), column tiles on grid.y
+  const int64_t m0 = (int64_t)blockIdx.x * BM;
+  const int64_t n0 = (int64_t)blockIdx.y * BN;
   Acc acc;
   mainloop(la, M, lb, N, K, m0, n0, smem_d, acc);
 #pragma unroll
@@ -232,7 +233,8 @@ inline int launch_gemm(const LA& la, int64_t M, const LB& lb, int64_t N, int K, 
   if (M == 0 || N == 0) return IVRQ_OK;
   auto kern = gemm_kernel<LA, LB, EPI>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-  dim3 grid((unsigned)ceil_div(N, BN), (unsigned)ceil_div(M, BM));
+  if (ceil_div(N, BN) > 65535) return fail(IVRQ_EUNSUP, std::string(what) + ": too many column tiles");
+  dim3 grid((unsigned)ceil_div(M, BM), (unsigned)ceil_div(N, BN));
   kern<<<grid, THREADS, SMEM_BYTES, s>>>(la, M, lb, N, K, epi);
   return check_launch(what);
 }

@@ -338,6 +338,7 @@ def build_index_device(
     *,
     inject: dict | None = None,
     keep: dict | None = None,
+    timings: dict | None = None,
 ) -> IvfRabitqIndex:
     """Build from float32 rows already on the device (the bench's resident path).
 
@@ -345,8 +346,20 @@ def build_index_device(
     reference's own -- ``centroids64`` (float64 (k, d)), ``rotation`` (float32),
     ``cent_rot`` (float32), ``o_rot`` (float32, CSR order) -- to check the
     downstream stages bit-exactly "given identical rotated vectors and
-    centroids".  ``keep`` receives intermediate device tensors when given.
+    centroids".  ``keep`` receives intermediate device tensors when given;
+    ``timings`` (bench) receives per-stage seconds (synchronising between stages).
     """
+    import time
+
+    t_last = [time.perf_counter()]
+
+    def tick(name: str) -> None:
+        if timings is not None:
+            torch.cuda.synchronize()
+            now = time.perf_counter()
+            timings[name] = timings.get(name, 0.0) + now - t_last[0]
+            t_last[0] = now
+
     inject = inject or {}
     n, dims = x.shape
     quant = params.quant
@@ -363,10 +376,12 @@ def build_index_device(
         else:
             x_train = x
         km_seed = int(seeds[1].generate_state(1)[0])
-        centers = train_kmeans_device(x_train, params.n_clusters, params.kmeans_iters, km_seed)
+        centers = train_kmeans_device(x_train, params.n_clusters, params.kmeans_iters, km_seed, timings=timings)
+        t_last[0] = time.perf_counter()
     c_sq = row_sqnorms(centers)
     labels = assign_device(x, centers, c_sq)
     counts, offsets, order = counting_sort(labels, params.n_clusters)
+    tick("assign_csr")
 
     if "rotation" in inject:
         rot32_np = np.asarray(inject["rotation"], dtype=np.float32)
@@ -391,7 +406,9 @@ def build_index_device(
     )
     if "o_rot" in inject:
         o_rot = dev.to_device(np.asarray(inject["o_rot"], dtype=np.float32), device)
+    tick("rotations")
     enc = encode_rows(o_rot, dist, cent_rot, offsets, quant, want_codes=keep is not None)
+    tick("encode")
     if keep is not None:
         keep.update(
             centers=centers, labels=labels, counts=counts, offsets=offsets, order=order,
