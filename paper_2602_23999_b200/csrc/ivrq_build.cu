@@ -416,6 +416,17 @@ struct ResidLoader {
     double df = dsub((double)x[s * d + k], (double)cent[(int64_t)labels[s] * d + k]);
     return ddiv(df, dd);
   }
+  __device__ __forceinline__ void load8(int64_t r, int k, int K, double (&out)[8]) const {
+    const int64_t s = order ? order[r] : r;
+    const double dd = dist[r];
+    const float* xr = x + s * d;
+    const float* cr = cent + (int64_t)labels[s] * d;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int kk = k + e;
+      out[e] = (kk < K && dd != 0.0) ? ddiv(dsub((double)xr[kk], (double)cr[kk]), dd) : 0.0;
+    }
+  }
 };
 
 struct StoreF32 {

@@ -5,7 +5,7 @@
 // the discrete outputs (labels, probes, codes) needs float64 accumulation.
 // On B200 the DMMA m16n8k16 path issues twice the float64 MACs per clock of
 // the DFMA pipe (measured: 121.7 vs 61.8 MAC/clk/SM, tools/microbench.cu), so
-// the tiles use mma.sync.m16n8k16.f64: 128x128 CTA tile, 16-deep k slab,
+// the tiles use mma.sync.m16n8k16.f64: 128x128 CTA tile, 32-deep k slab,
 // 16 warps in a 4x4 grid each owning a 32x32 sub-tile (2x4 fragments), so an
 // SM keeps 16 warps in flight (the 8-warp variant was latency bound at 12.5%
 // occupancy, profiles/round1).
@@ -13,23 +13,49 @@
 // query rotation, probe distances, k-means labelling and residual rotation.
 #pragma once
 
+#include <algorithm>
+
 #include "ivrq_common.cuh"
 
 namespace ivrq {
 namespace gemm {
 
-constexpr int BM = 128, BN = 128, BK = 16, THREADS = 512;
+constexpr int BM = 128, BN = 128, BK = 32, THREADS = 512;
 constexpr int MF = 2, NF = 4;  // m16 / n8 fragments per warp
 constexpr int LDA = BM + 8;  // k-major smem pitch (doubles): conflict-free fragment loads
 constexpr int SMEM_BYTES = 2 * 2 * BK * LDA * (int)sizeof(double);  // double-buffered A and B
 
 // Row-major [rows x ld] operand of element type T (float or double).
+// load8: 8 consecutive k of row r as float64, through 128-bit loads when aligned.
 template <typename T>
 struct RowMajor {
   const T* p;
   int64_t rows;
   int64_t ld;
   __device__ __forceinline__ double operator()(int64_t r, int k) const { return (double)p[r * ld + k]; }
+  __device__ __forceinline__ void load8(int64_t r, int k, int K, double (&out)[8]) const {
+    const T* src = p + r * ld + k;
+    constexpr int W = 16 / sizeof(T);
+    if (k + 8 <= K && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+#pragma unroll
+      for (int v = 0; v < 8 / W; ++v) {
+        if constexpr (sizeof(T) == 4) {
+          const float4 f = __ldg(reinterpret_cast<const float4*>(src) + v);
+          out[4 * v] = f.x;
+          out[4 * v + 1] = f.y;
+          out[4 * v + 2] = f.z;
+          out[4 * v + 3] = f.w;
+        } else {
+          const double2 f = __ldg(reinterpret_cast<const double2*>(src) + v);
+          out[2 * v] = f.x;
+          out[2 * v + 1] = f.y;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) out[e] = (k + e < K) ? (double)src[e] : 0.0;
+    }
+  }
 };
 
 __device__ __forceinline__ void dmma16816(double (&c)[4], const double (&a)[8], const double (&b)[4]) {
@@ -72,23 +98,29 @@ __device__ __forceinline__ void mainloop(const LA& la, int64_t M, const LB& lb, 
 #pragma unroll
       for (int r = 0; r < 4; ++r) acc.v[i][j][r] = 0.0;
 
-  // global->smem: each thread moves 4 consecutive k of one row per operand
-  const int lr = tid >> 2, lk0 = (tid & 3) * 4;
-  double ra[4], rb[4];
+  // global->smem: each thread moves 8 consecutive k of one row per operand
+  const int lr = tid >> 2, lk0 = (tid & 3) * 8;
+  double ra[8], rb[8];
   auto load_regs = [&](int k0) {
     const int64_t gm = m0 + lr, gn = n0 + lr;
+    if (gm < M) {
+      la.load8(gm, k0 + lk0, K, ra);
+    } else {
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int k = k0 + lk0 + e;
-      ra[e] = (gm < M && k < K) ? la(gm, k) : 0.0;
-      rb[e] = (gn < N && k < K) ? lb(gn, k) : 0.0;
+      for (int e = 0; e < 8; ++e) ra[e] = 0.0;
+    }
+    if (gn < N) {
+      lb.load8(gn, k0 + lk0, K, rb);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) rb[e] = 0.0;
     }
   };
   auto store_smem = [&](int buf) {
     double* a = As + buf * BK * LDA;
     double* b = Bs + buf * BK * LDA;
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
+    for (int e = 0; e < 8; ++e) {
       a[(lk0 + e) * LDA + lr] = ra[e];
       b[(lk0 + e) * LDA + lr] = rb[e];
     }
@@ -101,26 +133,29 @@ __device__ __forceinline__ void mainloop(const LA& la, int64_t M, const LB& lb, 
   for (int kt = 0; kt < nk; ++kt) {
     const int buf = kt & 1;
     if (kt + 1 < nk) load_regs((kt + 1) * BK);
-    const double* a = As + buf * BK * LDA;
-    const double* b = Bs + buf * BK * LDA;
-    // B fragments of the warp's column blocks: b_j = B[k = t4 + 4j][n = gid]
-    double bf[NF][4];
 #pragma unroll
-    for (int nf = 0; nf < NF; ++nf)
+    for (int ks = 0; ks < BK / 16; ++ks) {
+      const double* a = As + buf * BK * LDA + ks * 16 * LDA;
+      const double* b = Bs + buf * BK * LDA + ks * 16 * LDA;
+      // B fragments of the warp's column blocks: b_j = B[k = t4 + 4j][n = gid]
+      double bf[NF][4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) bf[nf][j] = b[(t4 + 4 * j) * LDA + wn * 32 + nf * 8 + gid];
+      for (int nf = 0; nf < NF; ++nf)
 #pragma unroll
-    for (int mf = 0; mf < MF; ++mf) {
-      // A fragment: a_{2j} = A[row gid][k = t4 + 4j], a_{2j+1} = A[row gid + 8][k = t4 + 4j]
-      double af[8];
-      const int rbase = wm * 32 + mf * 16 + gid;
+        for (int j = 0; j < 4; ++j) bf[nf][j] = b[(t4 + 4 * j) * LDA + wn * 32 + nf * 8 + gid];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        af[2 * j] = a[(t4 + 4 * j) * LDA + rbase];
-        af[2 * j + 1] = a[(t4 + 4 * j) * LDA + rbase + 8];
+      for (int mf = 0; mf < MF; ++mf) {
+        // A fragment: a_{2j} = A[row gid][k = t4 + 4j], a_{2j+1} = A[row gid + 8][k = t4 + 4j]
+        double af[8];
+        const int rbase = wm * 32 + mf * 16 + gid;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          af[2 * j] = a[(t4 + 4 * j) * LDA + rbase];
+          af[2 * j + 1] = a[(t4 + 4 * j) * LDA + rbase + 8];
+        }
+#pragma unroll
+        for (int nf = 0; nf < NF; ++nf) dmma16816(acc.v[mf][nf], af, bf[nf]);
       }
-#pragma unroll
-      for (int nf = 0; nf < NF; ++nf) dmma16816(acc.v[mf][nf], af, bf[nf]);
     }
     if (kt + 1 < nk) store_smem(buf ^ 1);
     __syncthreads();
@@ -129,11 +164,13 @@ __device__ __forceinline__ void mainloop(const LA& la, int64_t M, const LB& lb, 
 
 // Plain tiled GEMM: grid (ceil(N/BN), ceil(M/BM)); epilogue(row, col, acc).
 template <typename LA, typename LB, typename EPI>
-__global__ void __launch_bounds__(THREADS, 1) gemm_kernel(LA la, int64_t M, LB lb, int64_t N, int K, EPI epi) {
+__global__ void __launch_bounds__(THREADS, 1) gemm_kernel(LA la, int64_t M, LB lb, int64_t N, int K, EPI epi,
+                                                          int64_t n_base) {
   extern __shared__ __align__(16) double smem_d[];
-  // row tiles on grid.x (up to 2^31-1: N = 10M rows is 78K tiles), column tiles on grid.y
+  // row tiles on grid.x (up to 2^31-1: 10M rows is 78K tiles), column tiles on
+  // grid.y (launched in slices of 65535 tiles from n_base)
   const int64_t m0 = (int64_t)blockIdx.x * BM;
-  const int64_t n0 = (int64_t)blockIdx.y * BN;
+  const int64_t n0 = n_base + (int64_t)blockIdx.y * BN;
   Acc acc;
   mainloop(la, M, lb, N, K, m0, n0, smem_d, acc);
 #pragma unroll
@@ -233,9 +270,11 @@ inline int launch_gemm(const LA& la, int64_t M, const LB& lb, int64_t N, int K, 
   if (M == 0 || N == 0) return IVRQ_OK;
   auto kern = gemm_kernel<LA, LB, EPI>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-  if (ceil_div(N, BN) > 65535) return fail(IVRQ_EUNSUP, std::string(what) + ": too many column tiles");
-  dim3 grid((unsigned)ceil_div(M, BM), (unsigned)ceil_div(N, BN));
-  kern<<<grid, THREADS, SMEM_BYTES, s>>>(la, M, lb, N, K, epi);
+  const int64_t nt = ceil_div(N, BN);
+  for (int64_t t0 = 0; t0 < nt; t0 += 65535) {
+    dim3 grid((unsigned)ceil_div(M, BM), (unsigned)std::min<int64_t>(65535, nt - t0));
+    kern<<<grid, THREADS, SMEM_BYTES, s>>>(la, M, lb, N, K, epi, t0 * BN);
+  }
   return check_launch(what);
 }
 
