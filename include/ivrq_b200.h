@@ -68,7 +68,7 @@ typedef struct {
   int32_t dims;
   int32_t bits;
   int32_t n_clusters;
-  int32_t reserved0;
+  int32_t max_list;    /* largest inverted list (rows); 0 = unknown (the scan then reads it back) */
   int64_t size;
   double eps_bound;
   const int64_t* offsets;

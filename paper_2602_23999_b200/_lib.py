@@ -34,7 +34,7 @@ class IndexView(ctypes.Structure):
         ("dims", c_int32),
         ("bits", c_int32),
         ("n_clusters", c_int32),
-        ("reserved0", c_int32),
+        ("max_list", c_int32),
         ("size", c_int64),
         ("eps_bound", c_double),
         ("offsets", c_void_p),

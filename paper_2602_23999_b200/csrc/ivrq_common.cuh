@@ -27,6 +27,11 @@ namespace ivrq {
 void set_error(const std::string& msg);
 int fail(int code, const std::string& msg);
 int check_launch(const char* what);
+// Keep freed stream-ordered (cudaMallocAsync) memory in the device's default
+// pool across synchronisations instead of returning it to the driver, so the
+// per-call workspaces of the search do not re-map pages every call.
+void retain_async_pool(cudaStream_t s);
+int sm_count_of_current_device();
 
 #define IVRQ_TRY(expr)              \
   do {                              \

@@ -21,6 +21,25 @@ int check_launch(const char* what) {
   return IVRQ_OK;
 }
 
+void retain_async_pool(cudaStream_t) {
+  static thread_local int done_mask = 0;  // devices 0..31 handled by this thread
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev >= 32 || (done_mask >> dev) & 1) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = ~0ULL;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done_mask |= 1 << dev;
+}
+
+int sm_count_of_current_device() {
+  int dev = 0, v = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) return 148;
+  return v;
+}
+
 // Row-wise einsum("ij,ij->i", x, x): NumPy's two accumulator lanes run on two
 // threads per row over 128-bit staged tiles (ivrq_rowchain.cuh).
 template <typename T>

@@ -14,6 +14,7 @@
 // reference's.  k <= 32 keeps per-warp top-32 queues in registers (bitonic
 // shuffle networks); larger k falls back to a block-wide bitonic sort.
 #include <cstdlib>
+#include <type_traits>
 
 #include "ivrq_common.cuh"
 
@@ -28,6 +29,13 @@ constexpr int SLICES = 8;              // base-128 digits of the query (refine)
 constexpr int SPAD = 16;               // slice row padding (bank spread)
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int64_t NO_ID = 0x7fffffffffffffffLL;
+// list-major stage-1 tiles (ip_tile_kernel)
+constexpr int TQ = 64;   // queries per tile: 4 m16 tiles, every warp
+constexpr int TV = 256;  // vectors per tile: 8 warps x 4 n8 tiles
+constexpr int TQ_PAD = 16;
+
+// ip row of a (list, query) pair: n_c rounded up to 8 elements
+__host__ __device__ inline int64_t ip_row_stride(int64_t n_c) { return (n_c + 7) & ~int64_t(7); }
 
 struct Args {
   ivrq_index_view ix;
@@ -51,6 +59,10 @@ struct Args {
   double* out_dists;
   int32_t* out_counts;
   int64_t* stats;
+  // stage-1 inner products precomputed list-major (ip_tile_kernel), or null
+  const void* ipbuf;
+  const int32_t* pslot;      // [nq * nprobe] slot of (q, p) in its list's bucket
+  const int64_t* pair_base;  // [nlist + 1]
 };
 
 __device__ __forceinline__ double dinf() { return __longlong_as_double(0x7ff0000000000000LL); }
@@ -63,15 +75,23 @@ struct QueryCtx {
 // ------------------------------------------------------------ stage 1
 // Fills s_cv (row within list) / s_cd (stage-1 estimate) with the survivors of
 // vectors [c0, c0+cn) of the list; returns the count via s_ncand.
-template <int MODE, int QB>
+template <int MODE, int QB, int IPB>
 __device__ __forceinline__ void stage1_chunk(const Args& a, const QueryCtx& qc, const uint32_t* __restrict__ words,
                                              int64_t lo, int64_t n_c, int64_t c0, int cn, double d_qc2, double sq,
                                              double T_list, const uint32_t* s_planes8, const float* s_lut,
-                                             int32_t* s_cv, double* s_cd, int* s_ncand) {
+                                             int32_t* s_cv, double* s_cd, int* s_ncand, const void* iprow) {
   const int tid = threadIdx.x, lane = tid & 31;
   const int g = a.g;
   double ipb[VPT];
-  if (MODE == IVRQ_IP_BITWISE) {
+  if (IPB) {  // integer inner products from ip_tile_kernel (same integer as the popcount sum below)
+    using IPT = typename std::conditional<IPB == 2, int16_t, int32_t>::type;
+    const IPT* r = reinterpret_cast<const IPT*>(iprow) + c0;
+#pragma unroll
+    for (int u = 0; u < VPT; ++u) {
+      const int vi = tid + u * THREADS;
+      ipb[u] = dmul(qc.delta, (double)(vi < cn ? (int)__ldg(r + vi) : 0));
+    }
+  } else if (MODE == IVRQ_IP_BITWISE) {
     int pos[VPT], last[VPT];
 #pragma unroll
     for (int u = 0; u < VPT; ++u) pos[u] = last[u] = 0;
@@ -421,7 +441,7 @@ __device__ __forceinline__ QueryCtx load_query(const Args& a, const Smem& s, int
 }
 
 // ------------------------------------------------------------ kernel, k <= 32
-template <int MODE, bool REFINE, bool NIB, int QB>
+template <int MODE, bool REFINE, bool NIB, int QB, int IPB>
 __global__ void __launch_bounds__(THREADS, 4) scan_kernel(Args a) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int s_ncand;
@@ -467,6 +487,11 @@ __global__ void __launch_bounds__(THREADS, 4) scan_kernel(Args a) {
     const int64_t pk_i = pool_full ? s.s_pool_i[k - 1] : NO_ID;
     const double sq = dsqrt(d_qc2);
     const uint32_t* words = a.ix.packed_msb + (int64_t)a.g * lo;
+    const void* iprow = nullptr;
+    if (IPB) {
+      const int64_t slot = a.pslot[q * a.nprobe + p];
+      iprow = reinterpret_cast<const char*>(a.ipbuf) + IPB * (a.pair_base[c] + slot * ip_row_stride(n_c));
+    }
     double qd = dinf();  // this warp's top-32 queue (lane i = i-th smallest)
     int64_t qi = NO_ID;
     bool any_cand = false;
@@ -474,8 +499,8 @@ __global__ void __launch_bounds__(THREADS, 4) scan_kernel(Args a) {
       const int cn = (int)min((int64_t)CHUNK, n_c - c0);
       if (tid == 0) s_ncand = 0;
       __syncthreads();
-      stage1_chunk<MODE, QB>(a, qc, words, lo, n_c, c0, cn, d_qc2, sq, T_list, s.s_planes8, s.s_lut, s.s_cv, s.s_cd,
-                             &s_ncand);
+      stage1_chunk<MODE, QB, IPB>(a, qc, words, lo, n_c, c0, cn, d_qc2, sq, T_list, s.s_planes8, s.s_lut, s.s_cv,
+                                  s.s_cd, &s_ncand, iprow);
       __syncthreads();
       const int ncand = s_ncand;
       if (tid == 0) {
@@ -606,8 +631,8 @@ __global__ void __launch_bounds__(THREADS) scan_kernel_bigk(Args a) {
       const int cn = (int)min((int64_t)CHUNK, n_c - c0);
       if (tid == 0) s_ncand = 0;
       __syncthreads();
-      stage1_chunk<MODE, QB>(a, qc, words, lo, n_c, c0, cn, d_qc2, sq, T_list, s.s_planes8, s.s_lut, s.s_cv, s.s_cd,
-                             &s_ncand);
+      stage1_chunk<MODE, QB, 0>(a, qc, words, lo, n_c, c0, cn, d_qc2, sq, T_list, s.s_planes8, s.s_lut, s.s_cv,
+                                s.s_cd, &s_ncand, nullptr);
       __syncthreads();
       const int ncand = s_ncand;
       if (tid == 0) {
@@ -904,6 +929,272 @@ __global__ void __launch_bounds__(THREADS) first_list_kernel(FArgs a) {
   }
 }
 
+// ------------------------------------------------------------ stage-1 inner products, list-major, int8 tensor cores
+// ip_bitwise (search.py:163-183) is sum_j w_j sum_g popc(word & plane_j) with
+// w_j the two's-complement weights of the query_bits planes, i.e. exactly the
+// integer dot product sum_d bit[v,d] * qhat[q,d] of the 1-bit code with the
+// quantized query.  For every (list, query probing it) pair that the
+// per-query pass will scan, ip_tile_kernel computes that dot for every vector
+// of the list as an int8 GEMM on mma.sync m16n8k32 (u8 0/1 codes x s8 qhat,
+// int32 accumulate: exact), reading each list's codes once per 64 queries
+// instead of once per query.  The per-query pass then reads 2 bytes per
+// (pair, vector) and replays the reference's threshold order unchanged.
+//
+// ip buffer layout: pair (list c, slot s) owns the row
+//   ipbuf[pair_base[c] + s * rs(c) + v],  rs(c) = n_c rounded up to 8,
+// slots numbered in the stable (list, query, probe) order of the pair sort.
+
+struct IpArgs {
+  ivrq_index_view ix;
+  const uint32_t* planes;
+  int qbits, g, nprobe, nlist;
+  const int64_t* porder;    // pair indices (q * nprobe + p) sorted by list
+  const int64_t* poff;      // [nlist + 2] bucket starts in porder
+  const int64_t* pair_base; // [nlist + 1] element offset of each list's rows
+  const int32_t* tpre;      // [nlist + 1] prefix of tiles per list
+  void* ipbuf;              // int16 or int32 elements
+};
+
+__device__ __forceinline__ void mma_s8u8(int (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k32.row.col.s32.s8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+      : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// 4 code bits (dims 4i..4i+3 of a word) -> 4 bytes of 0/1
+__device__ __forceinline__ uint32_t nib_bytes(uint32_t w, int shift) {
+  return (((w >> shift) & 0xFu) * 0x00204081u) & 0x01010101u;
+}
+
+template <typename IPT>
+__device__ __forceinline__ void ip_tile(const IpArgs& a, int b, int8_t* sq);
+
+// persistent: the CTAs stride over the tiles (their count is only known on device)
+template <typename IPT>
+__global__ void __launch_bounds__(THREADS, 2) ip_tile_kernel(IpArgs a) {
+  extern __shared__ __align__(16) unsigned char ism[];
+  const int total = a.tpre[a.nlist];
+  for (int b = blockIdx.x; b < total; b += gridDim.x) {
+    ip_tile<IPT>(a, b, reinterpret_cast<int8_t*>(ism));
+    __syncthreads();  // qhat tile is rewritten by the next tile
+  }
+}
+
+template <typename IPT>
+__device__ __forceinline__ void ip_tile(const IpArgs& a, int b, int8_t* sq) {
+  int lo_c = 0, hi_c = a.nlist;  // tpre[lo_c] <= b < tpre[hi_c]
+  while (hi_c - lo_c > 1) {
+    const int mid = (lo_c + hi_c) >> 1;
+    if (a.tpre[mid] <= b) lo_c = mid; else hi_c = mid;
+  }
+  const int c = lo_c;
+  const int64_t lo = a.ix.offsets[c], n_c = a.ix.offsets[c + 1] - lo;
+  const int64_t nv_t = ceil_div(n_c, TV);
+  const int local = b - a.tpre[c];
+  const int qt = (int)(local / nv_t);
+  const int64_t v0 = (local % nv_t) * TV;
+  const int64_t pb = a.poff[c] + (int64_t)qt * TQ;
+  const int nqt = (int)min((int64_t)TQ, a.poff[c + 1] - pb);
+  const int g = a.g, qb = a.qbits;
+  const int ldq = 32 * g + TQ_PAD;  // bytes per query row of qhat
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  // qhat[q][32*gi + i] = sum_j w_j * bit_i(plane_j[gi]), rows >= nqt zero
+  for (int it = tid; it < TQ * g; it += THREADS) {
+    const int r = it / g, gi = it % g;
+    uint32_t pl[8];
+    const int64_t q = r < nqt ? a.porder[pb + r] / a.nprobe : -1;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) pl[j] = (q >= 0 && j < qb) ? __ldg(a.planes + (q * qb + j) * g + gi) : 0u;
+    uint32_t* dst = reinterpret_cast<uint32_t*>(sq + r * ldq + 32 * gi);
+#pragma unroll
+    for (int w4 = 0; w4 < 8; ++w4) {
+      uint32_t packed = 0;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int i = 4 * w4 + e;
+        int v = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (j < qb) v |= (int)((pl[j] >> i) & 1u) << j;
+        v = (v << (32 - qb)) >> (32 - qb);  // two's complement of qb bits
+        packed |= ((uint32_t)v & 0xFFu) << (8 * e);
+      }
+      dst[w4] = packed;
+    }
+  }
+  __syncthreads();
+  const int gid = lane >> 2, t4 = lane & 3;
+  const int nmt = (nqt + 15) >> 4;  // warp-uniform
+  const uint32_t* words = a.ix.packed_msb + (int64_t)g * lo;
+  int acc[4][4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = acc[i][j][2] = acc[i][j][3] = 0;
+  const int64_t vw = v0 + wid * 32;  // this warp's 32 vectors
+  if (vw < n_c) {
+    int64_t vrow[4];
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) vrow[nt] = vw + nt * 8 + gid;
+    uint32_t wnext[4];
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) wnext[nt] = vrow[nt] < n_c ? __ldg(words + vrow[nt]) : 0u;
+    for (int gi = 0; gi < g; ++gi) {
+      uint32_t wcur[4];
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        wcur[nt] = wnext[nt];
+        wnext[nt] = (gi + 1 < g && vrow[nt] < n_c) ? __ldg(words + (int64_t)(gi + 1) * n_c + vrow[nt]) : 0u;
+      }
+      uint32_t bf[4][2];
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        bf[nt][0] = nib_bytes(wcur[nt], 4 * t4);
+        bf[nt][1] = nib_bytes(wcur[nt], 16 + 4 * t4);
+      }
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) {
+        if (mt < nmt) {
+          const int8_t* r0 = sq + (mt * 16 + gid) * ldq + 32 * gi + 4 * t4;
+          const int8_t* r1 = r0 + 8 * ldq;
+          uint32_t af[4];
+          af[0] = *reinterpret_cast<const uint32_t*>(r0);
+          af[1] = *reinterpret_cast<const uint32_t*>(r1);
+          af[2] = *reinterpret_cast<const uint32_t*>(r0 + 16);
+          af[3] = *reinterpret_cast<const uint32_t*>(r1 + 16);
+#pragma unroll
+          for (int nt = 0; nt < 4; ++nt) mma_s8u8(acc[mt][nt], af, bf[nt][0], bf[nt][1]);
+        }
+      }
+    }
+    const int64_t rs = ip_row_stride(n_c);
+    IPT* base = reinterpret_cast<IPT*>(a.ipbuf) + a.pair_base[c] + (int64_t)qt * TQ * rs;
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt) {
+      if (mt >= nmt) continue;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int r = mt * 16 + gid + 8 * h;
+        if (r >= nqt) continue;
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) {
+          const int64_t v = vw + nt * 8 + 2 * t4;  // even; v + 1 stays inside the padded row
+          if (v >= n_c) continue;
+          IPT* dst = base + (int64_t)r * rs + v;
+          const int x0 = acc[mt][nt][2 * h], x1 = acc[mt][nt][2 * h + 1];
+          if constexpr (sizeof(IPT) == 2) {
+            *reinterpret_cast<uint32_t*>(dst) = ((uint32_t)x0 & 0xFFFFu) | ((uint32_t)x1 << 16);
+          } else {
+            *reinterpret_cast<int2*>(dst) = make_int2(x0, x1);
+          }
+        }
+      }
+    }
+  }
+}
+
+// pair keys: list of every in-range probe the per-query pass scans (the first
+// in-range probe is excluded when the first-list phase handles it)
+__global__ void pair_key_kernel(const int64_t* __restrict__ probe_ids, int64_t nq, int nprobe, int64_t list_lo,
+                                int64_t list_hi, int skip_first, int32_t* __restrict__ keys) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nq) return;
+  const int32_t none = (int32_t)(list_hi - list_lo);
+  bool first = skip_first != 0;
+  for (int p = 0; p < nprobe; ++p) {
+    const int64_t cg = probe_ids[q * nprobe + p];
+    int32_t key = none;
+    if (cg >= list_lo && cg < list_hi) {
+      if (first) first = false;
+      else key = (int32_t)(cg - list_lo);
+    }
+    keys[q * nprobe + p] = key;
+  }
+}
+
+// slot of each pair inside its list's bucket
+__global__ void pair_slot_kernel(const int64_t* __restrict__ porder, const int64_t* __restrict__ poff,
+                                 const int32_t* __restrict__ keys, int64_t npairs, int32_t none,
+                                 int32_t* __restrict__ pslot) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= npairs) return;
+  const int64_t pr = porder[i];
+  const int32_t c = keys[pr];
+  pslot[pr] = c < none ? (int32_t)(i - poff[c]) : -1;
+}
+
+// pair_base (elements) and tile prefix over the lists; one block.
+// totals[0] = ip elements, totals[1] = tiles.
+__global__ void __launch_bounds__(1024) pair_plan_kernel(const int64_t* __restrict__ offsets,
+                                                         const int64_t* __restrict__ poff, int nlist,
+                                                         int64_t* __restrict__ pair_base, int32_t* __restrict__ tpre,
+                                                         int64_t* __restrict__ totals) {
+  __shared__ int64_t s_e[32], s_t[32];
+  __shared__ int64_t s_run_e, s_run_t;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid == 0) {
+    s_run_e = 0;
+    s_run_t = 0;
+  }
+  __syncthreads();
+  for (int c0 = 0; c0 < nlist; c0 += 1024) {
+    const int c = c0 + tid;
+    int64_t e = 0, t = 0;
+    if (c < nlist) {
+      const int64_t n_c = offsets[c + 1] - offsets[c], cnt = poff[c + 1] - poff[c];
+      e = cnt * ip_row_stride(n_c);
+      t = (n_c > 0 && cnt > 0) ? ceil_div(cnt, TQ) * ceil_div(n_c, TV) : 0;
+    }
+    int64_t ie = e, it = t;  // inclusive warp scans
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t xe = __shfl_up_sync(FULL, ie, o), xt = __shfl_up_sync(FULL, it, o);
+      if (lane >= o) {
+        ie += xe;
+        it += xt;
+      }
+    }
+    if (lane == 31) {
+      s_e[wid] = ie;
+      s_t[wid] = it;
+    }
+    __syncthreads();
+    if (wid == 0) {
+      int64_t we = s_e[lane], wt = s_t[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int64_t xe = __shfl_up_sync(FULL, we, o), xt = __shfl_up_sync(FULL, wt, o);
+        if (lane >= o) {
+          we += xe;
+          wt += xt;
+        }
+      }
+      s_e[lane] = we;  // inclusive over warps
+      s_t[lane] = wt;
+    }
+    __syncthreads();
+    const int64_t before_e = s_run_e + (wid ? s_e[wid - 1] : 0) + ie - e;
+    const int64_t before_t = s_run_t + (wid ? s_t[wid - 1] : 0) + it - t;
+    if (c < nlist) {
+      pair_base[c] = before_e;
+      tpre[c] = (int32_t)before_t;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      s_run_e += s_e[31];
+      s_run_t += s_t[31];
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    pair_base[nlist] = s_run_e;
+    tpre[nlist] = (int32_t)s_run_t;
+    totals[0] = s_run_e;
+    totals[1] = s_run_t;
+  }
+}
+
 // first probed list of each query inside this shard's id range (ids ascend per query)
 __global__ void first_probe_kernel(const int64_t* __restrict__ probe_ids, int64_t nq, int nprobe, int64_t list_lo,
                                    int64_t list_hi, int32_t* __restrict__ first) {
@@ -961,12 +1252,14 @@ __global__ void merge_topk_kernel(const int64_t* __restrict__ ids, const double*
 }
 
 template <int MODE, bool REFINE, bool NIB>
-int launch_t(const Args& a, cudaStream_t s) {
+int launch_t(const Args& a, int ipb, cudaStream_t s) {
   const bool bigk = a.k > 32;
   const size_t sm = smem_bytes(a, MODE, REFINE, bigk);
   const bool qb4 = MODE == IVRQ_IP_BITWISE && a.qbits == 4;  // the SearchParams default
   auto kern = bigk ? (qb4 ? scan_kernel_bigk<MODE, REFINE, NIB, 4> : scan_kernel_bigk<MODE, REFINE, NIB, 0>)
-                   : (qb4 ? scan_kernel<MODE, REFINE, NIB, 4> : scan_kernel<MODE, REFINE, NIB, 0>);
+              : ipb == 2 ? scan_kernel<MODE, REFINE, NIB, 0, 2>
+              : ipb == 4 ? scan_kernel<MODE, REFINE, NIB, 0, 4>
+                         : (qb4 ? scan_kernel<MODE, REFINE, NIB, 4, 0> : scan_kernel<MODE, REFINE, NIB, 0, 0>);
   if (sm > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return fail(IVRQ_EUNSUP, "ivrq_search_scan: shared memory request too large");
@@ -976,9 +1269,9 @@ int launch_t(const Args& a, cudaStream_t s) {
 }
 
 template <int MODE>
-int launch_mode(const Args& a, bool refine, bool nib, cudaStream_t s) {
-  if (!refine) return launch_t<MODE, false, false>(a, s);
-  return nib ? launch_t<MODE, true, true>(a, s) : launch_t<MODE, true, false>(a, s);
+int launch_mode(const Args& a, bool refine, bool nib, int ipb, cudaStream_t s) {
+  if (!refine) return launch_t<MODE, false, false>(a, ipb, s);
+  return nib ? launch_t<MODE, true, true>(a, ipb, s) : launch_t<MODE, true, false>(a, ipb, s);
 }
 
 }  // namespace scan
@@ -1042,6 +1335,7 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
   a.stats = stats;
   const bool nib = rcode_nibbles(index->bits);
   cudaStream_t s = as_stream(stream);
+  retain_async_pool(s);
   // Schedule queries grouped by their first (lowest-id) probed list: that list
   // is refined in full (the threshold is still +inf), so neighbours in the
   // grid share it through L2.  Results do not depend on the order.
@@ -1109,8 +1403,82 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
       a.skip_first = 1;
     }
   }
-  const int rc = params->ip_mode == IVRQ_IP_BITWISE ? scan::launch_mode<IVRQ_IP_BITWISE>(a, refine, nib, s)
-                                                    : scan::launch_mode<IVRQ_IP_LUT>(a, refine, nib, s);
+  // list-major stage-1 inner products on the int8 tensor cores (bitwise mode, k <= 32)
+  int ipb = 0;
+  int32_t *pkeys = nullptr, *pslot = nullptr, *tpre = nullptr;
+  int64_t *pcnt = nullptr, *poff = nullptr, *porder = nullptr, *pbase = nullptr, *ptot = nullptr;
+  void* ipbuf = nullptr;
+  const char* tc_env = getenv("IVRQ_TC_STAGE1");
+  const int64_t ipmax = (int64_t)words_per_vector(index->dims) * 32 << (params->query_bits - 1);
+  if (params->ip_mode == IVRQ_IP_BITWISE && a.k <= 32 && (tc_env ? atoi(tc_env) != 0 : true) && nl >= 1) {
+    ipb = ipmax <= 32768 ? 2 : 4;
+    const int64_t npairs = nq * a.nprobe;
+    if (cudaMallocAsync(reinterpret_cast<void**>(&pkeys), npairs * sizeof(int32_t), s) != cudaSuccess ||
+        cudaMallocAsync(reinterpret_cast<void**>(&pslot), npairs * sizeof(int32_t), s) != cudaSuccess ||
+        cudaMallocAsync(reinterpret_cast<void**>(&porder), npairs * sizeof(int64_t), s) != cudaSuccess ||
+        cudaMallocAsync(reinterpret_cast<void**>(&pcnt), (nl + 1) * sizeof(int64_t), s) != cudaSuccess ||
+        cudaMallocAsync(reinterpret_cast<void**>(&poff), (nl + 2) * sizeof(int64_t), s) != cudaSuccess ||
+        cudaMallocAsync(reinterpret_cast<void**>(&pbase), (nl + 1) * sizeof(int64_t), s) != cudaSuccess ||
+        cudaMallocAsync(reinterpret_cast<void**>(&tpre), (nl + 1) * sizeof(int32_t), s) != cudaSuccess ||
+        cudaMallocAsync(reinterpret_cast<void**>(&ptot), 2 * sizeof(int64_t), s) != cudaSuccess)
+      return fail(IVRQ_ENOMEM, "ivrq_search_scan: workspace allocation failed");
+    scan::pair_key_kernel<<<(unsigned)ceil_div(nq, 256), 256, 0, s>>>(probe_ids, nq, a.nprobe, list_lo, list_hi,
+                                                                      a.skip_first, pkeys);
+    IVRQ_TRY(check_launch("ivrq_search_scan(pair keys)"));
+    IVRQ_TRY(ivrq_counting_sort(pkeys, npairs, (int32_t)(nl + 1), pcnt, poff, porder, stream));
+    scan::pair_slot_kernel<<<(unsigned)ceil_div(npairs, 256), 256, 0, s>>>(porder, poff, pkeys, npairs,
+                                                                          (int32_t)nl, pslot);
+    scan::pair_plan_kernel<<<1, 1024, 0, s>>>(index->offsets, poff, (int)nl, pbase, tpre, ptot);
+    IVRQ_TRY(check_launch("ivrq_search_scan(pair plan)"));
+    // ip buffer: bounded by every pair owning a row of the largest list (no
+    // host round trip), or the exact total read back when the bound is unknown
+    int64_t tot[2] = {0, 0};
+    if (index->max_list > 0) {
+      tot[0] = npairs * scan::ip_row_stride(index->max_list);
+    } else if (cudaMemcpyAsync(tot, ptot, sizeof(tot), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+               cudaStreamSynchronize(s) != cudaSuccess) {
+      return fail(IVRQ_ECUDA, "ivrq_search_scan: pair plan readback failed");
+    }
+    if (tot[0] > 0) {
+      if (cudaMallocAsync(&ipbuf, (size_t)tot[0] * ipb, s) != cudaSuccess)
+        return fail(IVRQ_ENOMEM, "ivrq_search_scan: inner-product buffer allocation failed");
+      scan::IpArgs ia{};
+      ia.ix = *index;
+      ia.planes = planes;
+      ia.qbits = a.qbits;
+      ia.g = a.g;
+      ia.nprobe = a.nprobe;
+      ia.nlist = (int)nl;
+      ia.porder = porder;
+      ia.poff = poff;
+      ia.pair_base = pbase;
+      ia.tpre = tpre;
+      ia.ipbuf = ipbuf;
+      const size_t ism = (size_t)scan::TQ * (32 * a.g + scan::TQ_PAD);
+      auto ik = ipb == 2 ? scan::ip_tile_kernel<int16_t> : scan::ip_tile_kernel<int32_t>;
+      if (ism > 48 * 1024 &&
+          cudaFuncSetAttribute(ik, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ism) != cudaSuccess)
+        return fail(IVRQ_EUNSUP, "ivrq_search_scan: dims too large for the tensor-core stage 1");
+      ik<<<(unsigned)(2 * sm_count_of_current_device()), scan::THREADS, ism, s>>>(ia);
+      IVRQ_TRY(check_launch("ivrq_search_scan(stage-1 tiles)"));
+    }
+    a.ipbuf = ipbuf;
+    a.pslot = pslot;
+    a.pair_base = pbase;
+  }
+  const int rc = params->ip_mode == IVRQ_IP_BITWISE ? scan::launch_mode<IVRQ_IP_BITWISE>(a, refine, nib, ipb, s)
+                                                    : scan::launch_mode<IVRQ_IP_LUT>(a, refine, nib, 0, s);
+  if (pkeys) {
+    cudaFreeAsync(pkeys, s);
+    cudaFreeAsync(pslot, s);
+    cudaFreeAsync(porder, s);
+    cudaFreeAsync(pcnt, s);
+    cudaFreeAsync(poff, s);
+    cudaFreeAsync(pbase, s);
+    cudaFreeAsync(tpre, s);
+    cudaFreeAsync(ptot, s);
+    if (ipbuf) cudaFreeAsync(ipbuf, s);
+  }
   if (first) {
     cudaFreeAsync(first, s);
     cudaFreeAsync(cnt, s);

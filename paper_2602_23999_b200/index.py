@@ -221,7 +221,7 @@ class IvfRabitqIndex:
                 dims=self.dims,
                 bits=self.bits,
                 n_clusters=self.n_clusters,
-                reserved0=0,
+                max_list=int(torch.diff(t["offsets"]).max().item()) if self.n_clusters else 0,
                 size=self.size,
                 eps_bound=self.eps_bound,
                 offsets=dev.ptr(t["offsets"]),

@@ -213,11 +213,126 @@ def search_device(
     return DeviceResult(ids=out_ids, dists=out_d, counts=counts, stats=stats)
 
 
+def _rows_to_lists(ids: np.ndarray, dists: np.ndarray, counts: np.ndarray) -> list[tuple[np.ndarray, np.ndarray]]:
+    """One (ids, dists) pair per row, trimmed to the row's count.
+
+    The pairs are row views of ``ids`` / ``dists``, which must be fresh arrays
+    owned by the caller (rows are disjoint, so the views are independent).
+    """
+    k = ids.shape[1]
+    if counts.size and int(counts.min()) == k:
+        return list(zip(ids, dists))
+    return [(ids[i, :n], dists[i, :n]) for i, n in enumerate(counts.tolist())]
+
+
 def results_to_lists(res: DeviceResult) -> list[tuple[np.ndarray, np.ndarray]]:
-    ids = dev.to_host(res.ids)
-    dists = dev.to_host(res.dists)
-    counts = dev.to_host(res.counts)
-    return [(ids[i, : counts[i]].copy(), dists[i, : counts[i]].copy()) for i in range(ids.shape[0])]
+    return _rows_to_lists(dev.to_host(res.ids), dev.to_host(res.dists), dev.to_host(res.counts))
+
+
+# ------------------------------------------------------------------ host pipeline
+_PINNED: dict[tuple[int, str], torch.Tensor] = {}
+
+
+def _pinned(device: torch.device, name: str, nbytes: int) -> torch.Tensor:
+    """A page-locked staging buffer (uint8), grown on demand and kept per device."""
+    key = (device.index or 0, name)
+    buf = _PINNED.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, pin_memory=True)
+        _PINNED[key] = buf
+    return buf
+
+
+_STAGE_THREADS = 4
+_POOL = None
+
+
+def _stage_pool():
+    """Threads for the pinned-memory staging copies (np.copyto drops the GIL)."""
+    global _POOL
+    if _POOL is None:
+        from concurrent.futures import ThreadPoolExecutor
+
+        _POOL = ThreadPoolExecutor(_STAGE_THREADS, thread_name_prefix="ivrq-stage")
+    return _POOL
+
+
+def _chunk_bounds(nq: int) -> list[int]:
+    """Query chunks of the host pipeline: big enough that each keeps the GPU busy
+    (the first-list phase shares list passes between queries of one chunk),
+    small enough that host work on one chunk hides behind the next chunk's kernels."""
+    import os
+
+    env = os.environ.get("IVRQ_E2E_CHUNKS")
+    n = int(env) if env else (1 if nq < 4096 else 2)
+    n = max(1, min(n, nq))
+    return [nq * i // n for i in range(n + 1)]
+
+
+def _search_pipelined(q: np.ndarray, index: IvfRabitqIndex, params: SearchParams):
+    """search_batch for host queries, pipelined over query chunks on one stream.
+
+    Per chunk: host memcpy into a pinned buffer, async H2D, the four search
+    launches, async D2H of (ids, dists, counts) into pinned memory, an event.
+    While the GPU runs chunk i the host stages chunk i+1's queries and turns
+    chunk i-1's results into the per-query lists.
+    """
+    device = dev.require_cuda()
+    nq, d = q.shape
+    k = params.k
+    bounds = _chunk_bounds(nq)
+    stream = torch.cuda.current_stream(device)
+    tdt = torch.float32 if q.dtype == np.float32 else torch.float64
+    pin_q_t = _pinned(device, "q", q.nbytes)[: q.nbytes].view(tdt).view(nq, d)
+    pin_q_np = pin_q_t.numpy()
+    nk = nq * k
+    pin_o = _pinned(device, "out", nk * 16 + nq * 4)
+    ids_t = pin_o[: nk * 8].view(torch.int64).view(nq, k)
+    dists_t = pin_o[nk * 8 : nk * 16].view(torch.float64).view(nq, k)
+    counts_t = pin_o[nk * 16 : nk * 16 + nq * 4].view(torch.int32)
+    ids_h, dists_h, counts_h = ids_t.numpy(), dists_t.numpy(), counts_t.numpy()
+    qd = torch.empty((nq, d), dtype=pin_q_t.dtype, device=device)
+    # the previous call's D2H into the same pinned buffers has been consumed
+    # (search_batch returns only after its last event), so no wait is needed here
+    ids_out = np.empty((nq, k), dtype=np.int64)
+    dists_out = np.empty((nq, k), dtype=np.float64)
+    counts_out = np.empty(nq, dtype=np.int32)
+    done: list[tuple[int, int, torch.cuda.Event]] = []
+    results: list[tuple[np.ndarray, np.ndarray]] = []
+
+    def finish(a: int, b: int, ev: torch.cuda.Event) -> None:
+        ev.synchronize()
+        np.copyto(ids_out[a:b], ids_h[a:b])
+        np.copyto(dists_out[a:b], dists_h[a:b])
+        np.copyto(counts_out[a:b], counts_h[a:b])
+        results.extend(_rows_to_lists(ids_out[a:b], dists_out[a:b], counts_out[a:b]))
+
+    def stage(i: int) -> list:
+        # host copy of chunk i into pinned memory, split over the staging threads
+        a, b = bounds[i], bounds[i + 1]
+        parts = np.linspace(a, b, _STAGE_THREADS + 1).astype(np.int64)
+        pool = _stage_pool()
+        return [pool.submit(np.copyto, pin_q_np[x:y], q[x:y]) for x, y in zip(parts[:-1], parts[1:]) if y > x]
+
+    with torch.cuda.stream(stream):
+        pending = stage(0)
+        for i in range(len(bounds) - 1):
+            a, b = bounds[i], bounds[i + 1]
+            for f in pending:
+                f.result()
+            qd[a:b].copy_(pin_q_t[a:b], non_blocking=True)
+            res = search_device(qd[a:b], index, params)
+            ids_t[a:b].copy_(res.ids, non_blocking=True)
+            dists_t[a:b].copy_(res.dists, non_blocking=True)
+            counts_t[a:b].copy_(res.counts, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(stream)
+            done.append((a, b, ev))
+            pending = stage(i + 1) if i + 2 < len(bounds) else []
+            if i > 0:
+                finish(*done[i - 1])
+        finish(*done[-1])
+    return results
 
 
 def _validate(q: np.ndarray, index: IvfRabitqIndex, params: SearchParams) -> None:
@@ -247,5 +362,4 @@ def search_batch(
         default_workers()
     if q.shape[0] == 0:
         return []
-    qd = dev.to_device(q)
-    return results_to_lists(search_device(qd, index, params))
+    return _search_pipelined(q, index, params)

@@ -296,3 +296,54 @@ def test_sharded_scan_chain_and_merge_on_one_gpu(case, si):
         mi, md, mc = _merge_gpu(stacked, 2, k)
         np.testing.assert_array_equal(dev.to_host(mi), g[f"s{si}_ids"])
         np.testing.assert_array_equal(dev.to_host(mc), g[f"s{si}_counts"])
+
+
+def _synthetic_index(n, d, nlist, bits, seed):
+    rng = np.random.default_rng(seed)
+    centers = rng.standard_normal((16, d)) * 3.0
+    x = (centers[rng.integers(0, 16, n)] + rng.standard_normal((n, d))).astype(np.float32)
+    q = (centers[rng.integers(0, 16, 700)] + rng.standard_normal((700, d))).astype(np.float32)
+    params = iv.BuildParams(n_clusters=nlist, quant=iv.QuantizationParams(bits=bits), kmeans_iters=3, seed=seed)
+    return iv.build_index(x, params), q
+
+
+@pytest.mark.parametrize(
+    "n,d,nlist,bits,qbits,nprobe,k",
+    [
+        (20000, 96, 64, 4, 4, 8, 10),  # int16 inner products, first-list phase
+        (12000, 300, 32, 8, 8, 6, 10),  # int32 inner products (300 * 128 > 2^15)
+        (15000, 128, 48, 1, 4, 7, 10),  # 1-bit index: every probe on the tensor-core stage 1
+        (15000, 70, 40, 3, 2, 40, 32),  # every list probed, ragged dims, k = 32
+        (8000, 64, 16, 5, 4, 4, 1),
+    ],
+)
+def test_tensor_core_stage1_matches_popcount_path(monkeypatch, n, d, nlist, bits, qbits, nprobe, k):
+    """List-major int8 MMA stage 1 == per-query AND+POPC stage 1: ids, dists, counts and survivor stats."""
+    ix, q = _synthetic_index(n, d, nlist, bits, seed=d)
+    sp = iv.SearchParams(k=k, n_probe=nprobe, ip_mode="bitwise", query_bits=qbits)
+    qd = dev.to_device(q)
+    out = {}
+    for tc in ("0", "1"):
+        monkeypatch.setenv("IVRQ_TC_STAGE1", tc)
+        r = search_device(qd, ix, sp, with_stats=True)
+        out[tc] = [dev.to_host(t) for t in (r.ids, r.dists, r.counts, r.stats)]
+    for a, b in zip(out["0"], out["1"]):
+        np.testing.assert_array_equal(a, b)
+
+
+def test_search_batch_pipeline_chunks_identical(monkeypatch):
+    """The chunked host pipeline of search_batch returns exactly the single-batch results."""
+    ix, q = _synthetic_index(20000, 64, 40, 4, seed=3)
+    q = np.concatenate([q] * 7)  # 4900 queries: two chunks by default
+    sp = iv.SearchParams(k=10, n_probe=5, ip_mode="bitwise")
+    r = search_device(dev.to_device(q), ix, sp)
+    ids, dists, counts = dev.to_host(r.ids), dev.to_host(r.dists), dev.to_host(r.counts)
+    for chunks in ("1", "2", "3", "5"):
+        monkeypatch.setenv("IVRQ_E2E_CHUNKS", chunks)
+        res = iv.search_batch(q, ix, sp)
+        assert len(res) == len(q)
+        for i in (0, 1, 2449, 2450, 4899):
+            np.testing.assert_array_equal(res[i][0], ids[i, : counts[i]])
+            np.testing.assert_array_equal(res[i][1], dists[i, : counts[i]])
+        got = np.stack([a for a, _ in res])
+        np.testing.assert_array_equal(got, ids)

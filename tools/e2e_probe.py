@@ -1,0 +1,79 @@
+"""Break the public search_batch() call into its host/device parts (C3 by default).
+
+    python tools/e2e_probe.py --config c3 --nprobe 8
+"""
+
+from __future__ import annotations
+
+import argparse
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import paper_2602_23999_b200 as iv  # noqa: E402
+from paper_2602_23999_b200 import _device as dev  # noqa: E402
+from paper_2602_23999_b200 import search as S  # noqa: E402
+from paper_2602_23999_b200.index import build_index_device  # noqa: E402
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="c3")
+    ap.add_argument("--nprobe", type=int, default=8)
+    ap.add_argument("--reps", type=int, default=5)
+    args = ap.parse_args()
+    cfg = bench.CONFIGS[args.config]
+    d0 = torch.device("cuda", 0)
+    x, q = bench.make_dataset_gpu(cfg["n"], bench.NQ, cfg["d"], d0)
+    params = iv.BuildParams(
+        n_clusters=cfg["nlist"], quant=iv.QuantizationParams(bits=cfg["bits"]), kmeans_iters=25,
+        train_fraction=bench.train_fraction(cfg["n"], cfg["nlist"]), seed=0,
+    )
+    ix = build_index_device(x, params)
+    q_host = q.cpu().numpy()
+    sp = iv.SearchParams(k=bench.K, n_probe=args.nprobe, ip_mode="bitwise")
+    for _ in range(args.reps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        qd = dev.to_device(q_host)
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        res = S.search_device(qd, ix, sp)
+        torch.cuda.synchronize()
+        t2 = time.perf_counter()
+        ids, dists, counts = dev.to_host(res.ids), dev.to_host(res.dists), dev.to_host(res.counts)
+        t3 = time.perf_counter()
+        out = S.results_to_lists(res)
+        t4 = time.perf_counter()
+        out2 = iv.search_batch(q_host, ix, sp)
+        torch.cuda.synchronize()
+        t5 = time.perf_counter()
+        print(
+            f"h2d {1e3*(t1-t0):.2f} ms  device {1e3*(t2-t1):.2f}  d2h {1e3*(t3-t2):.2f}  "
+            f"lists(+d2h) {1e3*(t4-t3):.2f}  search_batch {1e3*(t5-t4):.2f}",
+            file=sys.stderr,
+        )
+    assert len(out) == len(out2)
+    import os
+
+    for chunks in (1, 2, 3, 4, 5, 8):
+        os.environ["IVRQ_E2E_CHUNKS"] = str(chunks)
+        ts = []
+        for _ in range(args.reps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            out3 = iv.search_batch(q_host, ix, sp)
+            ts.append(time.perf_counter() - t0)
+        same = all(np.array_equal(a[0], b[0]) for a, b in zip(out3, out2))
+        print(f"chunks {chunks}: search_batch {1e3*np.median(ts):.2f} ms  identical={same}", file=sys.stderr)
+
+
+if __name__ == "__main__":
+    main()
