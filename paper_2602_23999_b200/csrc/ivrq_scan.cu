@@ -29,7 +29,7 @@ constexpr int SLICES = 8;              // base-128 digits of the query (refine)
 constexpr int SPAD = 16;               // slice row padding (bank spread)
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int64_t NO_ID = 0x7fffffffffffffffLL;
-// list-major stage-1 tiles (ip_tile_kernel)
+// list-major stage-1 inner products (ip_list_kernel)
 constexpr int TQ = 64;   // queries per tile: 4 m16 tiles, every warp
 constexpr int TV = 256;  // vectors per tile: 8 warps x 4 n8 tiles
 constexpr int TQ_PAD = 16;
@@ -59,7 +59,7 @@ struct Args {
   double* out_dists;
   int32_t* out_counts;
   int64_t* stats;
-  // stage-1 inner products precomputed list-major (ip_tile_kernel), or null
+  // stage-1 inner products precomputed list-major (ip_list_kernel), or null
   const void* ipbuf;
   const int32_t* pslot;      // [nq * nprobe] slot of (q, p) in its list's bucket
   const int64_t* pair_base;  // [nlist + 1]
@@ -83,7 +83,7 @@ __device__ __forceinline__ void stage1_chunk(const Args& a, const QueryCtx& qc, 
   const int tid = threadIdx.x, lane = tid & 31;
   const int g = a.g;
   double ipb[VPT];
-  if (IPB) {  // integer inner products from ip_tile_kernel (same integer as the popcount sum below)
+  if (IPB) {  // integer inner products from ip_list_kernel (same integer as the popcount sum below)
     using IPT = typename std::conditional<IPB == 2, int16_t, int32_t>::type;
     const IPT* r = reinterpret_cast<const IPT*>(iprow) + c0;
 #pragma unroll
@@ -566,6 +566,293 @@ __global__ void __launch_bounds__(THREADS, 4) scan_kernel(Args a) {
   }
 }
 
+// ------------------------------------------------------------ warp-per-query kernel (precomputed inner products)
+// With the stage-1 inner products already in HBM (ip_list_kernel) a query's
+// remaining work is a light stream (2-byte ip + 8-byte factors per vector)
+// plus the refine of its survivors, so one warp owns one query and nothing
+// synchronises beyond the warp: survivors queue in a per-warp ring in shared
+// memory, every 16 of them go through one m16n8k32 refine group, and the
+// warp's register top-32 queue IS the query's pool.  Same prune test, refine
+// arithmetic and (dist, id) order as scan_kernel, so results are identical.
+constexpr int WQ = 4;      // queries (warps) per CTA
+constexpr int SUB = 4;     // 32-vector sub-chunks loaded together (memory-level parallelism)
+constexpr int RING = 256;  // survivor ring per warp (holds < 32 + 32 * SUB)
+
+size_t warp_smem_bytes(int kpad, bool refine) {
+  const size_t per = (refine ? (size_t)SLICES * (kpad + SPAD) : 0) + RING * sizeof(int32_t);
+  return WQ * ((per + 15) & ~size_t(15));
+}
+
+__device__ __forceinline__ void load_a_frag(const uint8_t* row0, const uint8_t* row1, int p, int t4, bool nib,
+                                            uint32_t (&s0)[4], uint32_t (&s1)[4]) {
+  if (nib) {
+    const uint2 x0 = __ldg(reinterpret_cast<const uint2*>(row0 + 8 * (4 * p + t4)));
+    const uint2 x1 = __ldg(reinterpret_cast<const uint2*>(row1 + 8 * (4 * p + t4)));
+    s0[0] = x0.x & 0x0F0F0F0Fu;
+    s0[2] = (x0.x >> 4) & 0x0F0F0F0Fu;
+    s1[0] = x0.y & 0x0F0F0F0Fu;
+    s1[2] = (x0.y >> 4) & 0x0F0F0F0Fu;
+    s0[1] = x1.x & 0x0F0F0F0Fu;
+    s0[3] = (x1.x >> 4) & 0x0F0F0F0Fu;
+    s1[1] = x1.y & 0x0F0F0F0Fu;
+    s1[3] = (x1.y >> 4) & 0x0F0F0F0Fu;
+  } else {
+    const uint4 x0 = __ldg(reinterpret_cast<const uint4*>(row0 + 16 * (4 * p + t4)));
+    const uint4 x1 = __ldg(reinterpret_cast<const uint4*>(row1 + 16 * (4 * p + t4)));
+    s0[0] = x0.x;
+    s0[2] = x0.y;
+    s1[0] = x0.z;
+    s1[2] = x0.w;
+    s0[1] = x1.x;
+    s0[3] = x1.y;
+    s1[1] = x1.z;
+    s1[3] = x1.w;
+  }
+}
+
+// Refined distances of up to 32 candidates: entries head..head+m-1 of the
+// ring rv (mod RING), or rows head..head+m-1 directly when rv is null.  Two
+// m16 tiles share the query's B fragments; lane L < m receives candidate L.
+template <bool NIB>
+__device__ __forceinline__ void warp_refine32(const Args& a, const QueryCtx& qc, int64_t lo, double d_qc2,
+                                              const int8_t* sl_base, const int32_t* rv, int head, int m,
+                                              double& dist, int& vrow) {
+  const int lane = threadIdx.x & 31, gid = lane >> 2, t4 = lane & 3;
+  const int kp = a.kpad;
+  const int64_t rb = a.ix.rcode_bytes;
+  int vr[4];
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {  // rows gid, gid+8, gid+16, gid+24
+    const int e = min(gid + 8 * t, m - 1);
+    vr[t] = rv ? rv[(head + e) & (RING - 1)] : head + e;
+  }
+  const uint8_t* ra0 = a.ix.rcodes + (lo + vr[0]) * rb;
+  const uint8_t* ra1 = a.ix.rcodes + (lo + vr[1]) * rb;
+  const uint8_t* rb0 = a.ix.rcodes + (lo + vr[2]) * rb;
+  const uint8_t* rb1 = a.ix.rcodes + (lo + vr[3]) * rb;
+  const int8_t* sl = sl_base + gid * (kp + SPAD) + 4 * t4;
+  const bool two = m > 16;  // warp-uniform
+  int ca[4] = {0, 0, 0, 0}, cb[4] = {0, 0, 0, 0};
+#pragma unroll 3
+  for (int p = 0; p < kp / 64; ++p) {
+    uint32_t as0[4], as1[4], bs0[4], bs1[4];
+    load_a_frag(ra0, ra1, p, t4, NIB, as0, as1);
+    if (two) load_a_frag(rb0, rb1, p, t4, NIB, bs0, bs1);
+    const uint32_t b00 = *reinterpret_cast<const uint32_t*>(sl + 64 * p);
+    const uint32_t b10 = *reinterpret_cast<const uint32_t*>(sl + 64 * p + 16);
+    const uint32_t b01 = *reinterpret_cast<const uint32_t*>(sl + 64 * p + 32);
+    const uint32_t b11 = *reinterpret_cast<const uint32_t*>(sl + 64 * p + 48);
+    mma_u8s8(ca, as0[0], as0[1], as0[2], as0[3], b00, b10);
+    if (two) mma_u8s8(cb, bs0[0], bs0[1], bs0[2], bs0[3], b00, b10);
+    mma_u8s8(ca, as1[0], as1[1], as1[2], as1[3], b01, b11);
+    if (two) mma_u8s8(cb, bs1[0], bs1[1], bs1[2], bs1[3], b01, b11);
+  }
+  const long long w0 = (t4 & 1) ? 128LL : 2097152LL;
+  const long long w1 = (t4 & 1) ? 1LL : 16384LL;
+  // tile of this lane's candidate: lanes 0-15 <- tile a, 16-31 <- tile b
+  long long p0a = (long long)ca[0] * w0 + (long long)ca[1] * w1, p1a = (long long)ca[2] * w0 + (long long)ca[3] * w1;
+  long long p0b = (long long)cb[0] * w0 + (long long)cb[1] * w1, p1b = (long long)cb[2] * w0 + (long long)cb[3] * w1;
+  p0a += __shfl_xor_sync(FULL, p0a, 1);
+  p1a += __shfl_xor_sync(FULL, p1a, 1);
+  p0b += __shfl_xor_sync(FULL, p0b, 1);
+  p1b += __shfl_xor_sync(FULL, p1b, 1);
+  const long long l0a = __shfl_xor_sync(FULL, p0a, 2), l1a = __shfl_xor_sync(FULL, p1a, 2);
+  const long long l0b = __shfl_xor_sync(FULL, p0b, 2), l1b = __shfl_xor_sync(FULL, p1b, 2);
+  const int L = lane & 15, src = (L & 7) * 4;  // lane t4 == 0 of group (L & 7) holds the sums
+  const bool hi8 = L >= 8, tb = lane >= 16;
+  // each lane fetches its candidate's (hi, lo) halves from the owning group lane
+  // (the source lane supplies both row halves; the receiver picks)
+  const long long h0a = __shfl_sync(FULL, p0a, src), h1a = __shfl_sync(FULL, p1a, src);
+  const long long g0a = __shfl_sync(FULL, l0a, src), g1a = __shfl_sync(FULL, l1a, src);
+  const long long h0b = __shfl_sync(FULL, p0b, src), h1b = __shfl_sync(FULL, p1b, src);
+  const long long g0b = __shfl_sync(FULL, l0b, src), g1b = __shfl_sync(FULL, l1b, src);
+  const long long hA = hi8 ? h1a : h0a, lA = hi8 ? g1a : g0a;
+  const long long hB = hi8 ? h1b : h0b, lB = hi8 ? g1b : g0b;
+  dist = dinf();
+  vrow = -1;
+  if (lane < m) {
+    vrow = rv ? rv[(head + lane) & (RING - 1)] : head + lane;
+    const long long hi = tb ? hB : hA, lw = tb ? lB : lA;
+    const double hi_s = ldexp(1.0, qc.sexp - 26), lo_s = ldexp(1.0, qc.sexp - 54);
+    const double ip = dadd(dmul((double)hi, hi_s), dmul((double)lw, lo_s));
+    const float2 lf = __ldg(reinterpret_cast<const float2*>(a.ix.long_factors) + lo + vrow);
+    dist = dmax(dsub(dadd((double)lf.x, d_qc2), dmul((double)lf.y, dsub(ip, qc.kb_sum))), 0.0);
+  }
+}
+
+// offer (d, row) on each lane to the warp queue (pid loaded only when it can enter)
+__device__ __forceinline__ void warp_offer(const Args& a, double& qd, int64_t& qi, double d, int vrow, int64_t lo,
+                                           int k) {
+  const double kd = __shfl_sync(FULL, qd, k - 1);
+  const int64_t ki = __shfl_sync(FULL, qi, k - 1);
+  const bool maybe = vrow >= 0 && d <= kd;
+  if (!__any_sync(FULL, maybe)) return;
+  const int64_t id = maybe ? (int64_t)__ldg(a.ix.pids + lo + vrow) : NO_ID;
+  const bool pass = maybe && key_less(d, id, kd, ki);
+  if (!__any_sync(FULL, pass)) return;
+  warp_fold(qd, qi, d, id, pass, k);
+}
+
+template <bool REFINE, bool NIB, int IPB>
+__global__ void __launch_bounds__(WQ * 32) scan_warp_kernel(Args a) {
+  using IPT = typename std::conditional<IPB == 2, int16_t, int32_t>::type;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t slot_q = (int64_t)blockIdx.x * WQ + wid;
+  if (slot_q >= a.nq) return;  // whole warps only: nothing below synchronises the block
+  const int64_t q = a.qorder ? a.qorder[slot_q] : slot_q;
+  const int k = a.k, kp = a.kpad;
+  const size_t per = ((REFINE ? (size_t)SLICES * (kp + SPAD) : 0) + RING * sizeof(int32_t) + 15) & ~size_t(15);
+  unsigned char* wbase = smem + wid * per;
+  int8_t* s_sl = reinterpret_cast<int8_t*>(wbase);
+  int32_t* r_v = reinterpret_cast<int32_t*>(wbase + (REFINE ? (size_t)SLICES * (kp + SPAD) : 0));
+  if (REFINE) {
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(a.qslices + q * SLICES * (int64_t)kp);
+    for (int i = lane; i < SLICES * kp / 4; i += 32) {
+      const int sidx = (4 * i) / kp, kk = (4 * i) % kp;
+      *reinterpret_cast<uint32_t*>(s_sl + sidx * (kp + SPAD) + kk) = src[i];
+    }
+  }
+  const double* sc = a.scalars + q * IVRQ_QS_COUNT;
+  QueryCtx qc;
+  qc.delta = sc[IVRQ_QS_DELTA];
+  qc.half_code = sc[IVRQ_QS_HALF_CODE];
+  qc.ipm = sc[IVRQ_QS_IP_MARGIN];
+  qc.kb_sum = sc[IVRQ_QS_KB_SUM];
+  qc.sexp = REFINE ? (int)sc[IVRQ_QS_SLICE_EXP] : 0;
+  const int init_n = a.init_counts ? a.init_counts[q] : 0;
+  double qd = lane < init_n ? a.init_dists[q * k + lane] : dinf();
+  int64_t qi = lane < init_n ? a.init_ids[q * k + lane] : NO_ID;
+  double T = init_n >= k ? __shfl_sync(FULL, qd, k - 1) : dinf();
+  long long probed = (a.skip_first && a.stats) ? a.stats[2 * q] : 0;
+  long long surv = (a.skip_first && a.stats) ? a.stats[2 * q + 1] : 0;
+  __syncwarp();
+  const int64_t* pid_list = a.probe_ids + q * a.nprobe;
+  const double* pd2_list = a.probe_d2 + q * a.nprobe;
+  bool first_pending = a.skip_first != 0;
+  for (int p = 0; p < a.nprobe; ++p) {  // ascending cluster id (search.py:429)
+    const int64_t cg = pid_list[p];
+    if (cg < a.list_lo || cg >= a.list_hi) continue;
+    if (first_pending) {
+      first_pending = false;
+      continue;
+    }
+    const int64_t c = cg - a.list_lo;
+    const double d_qc2 = pd2_list[p];
+    const int64_t lo = a.ix.offsets[c], n_c = a.ix.offsets[c + 1] - lo;
+    if (n_c == 0) continue;
+    const double T_list = a.prune ? T : dinf();
+    probed += n_c;
+    if (REFINE && T_list == dinf()) {  // nothing can be pruned (lb2 <= +inf): refine the whole list
+      surv += n_c;
+      for (int64_t c0 = 0; c0 < n_c; c0 += 32) {
+        double d;
+        int vr;
+        warp_refine32<NIB>(a, qc, lo, d_qc2, s_sl, nullptr, (int)c0, (int)min((int64_t)32, n_c - c0), d, vr);
+        warp_offer(a, qd, qi, d, vr, lo, k);
+      }
+      const int cnt = __popc(__ballot_sync(FULL, lane < k && qi != NO_ID));
+      if (cnt >= k) T = __shfl_sync(FULL, qd, k - 1);
+      continue;
+    }
+    const double sq = dsqrt(d_qc2);
+    const IPT* iprow =
+        reinterpret_cast<const IPT*>(a.ipbuf) + a.pair_base[c] + a.pslot[q * a.nprobe + p] * ip_row_stride(n_c);
+    int head = 0, nb = 0;  // ring of pending survivors (warp-uniform)
+    for (int64_t c0 = 0; c0 < n_c; c0 += 32 * SUB) {
+      // loads of SUB sub-chunks first (ip, add, scale, err), then the tests
+      int ipv[SUB];
+      float fa[SUB], fs[SUB], fe[SUB];
+#pragma unroll
+      for (int u = 0; u < SUB; ++u) {
+        const int64_t vi = c0 + u * 32 + lane;
+        const bool in = vi < n_c;
+        ipv[u] = in ? (int)__ldg(iprow + vi) : 0;
+        fa[u] = in ? __ldg(a.ix.short_add + lo + vi) : 0.f;
+        fs[u] = in ? __ldg(a.ix.short_scale + lo + vi) : 0.f;
+        fe[u] = in ? __ldg(a.ix.short_err + lo + vi) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < SUB; ++u) {
+        const int64_t vi = c0 + u * 32 + lane;
+        if (c0 + u * 32 >= n_c) break;  // warp-uniform
+        bool keep = false;
+        double est2 = 0.0;
+        if (vi < n_c) {
+          const double ipb = dmul(qc.delta, (double)ipv[u]);
+          const double add = (double)fa[u];
+          const double scale = (double)fs[u];
+          const double ip_signed = dsub(ipb, qc.half_code);
+          est2 = dmax(dsub(dadd(add, d_qc2), dmul(scale, ip_signed)), 0.0);
+          if (est2 <= T_list) {
+            keep = true;  // lb2 <= est2 <= T
+          } else {
+            double margin = dmul((double)fe[u], sq);
+            if (qc.ipm != 0.0) {
+              // same decision as stage1_chunk: squares when unambiguous, else the reference expression
+              const double sm = dmul(scale, qc.ipm);
+              const double S = dadd(dmul(margin, margin), dmul(sm, sm));
+              const double gap = dsub(est2, T_list);
+              const double g2 = dmul(gap, gap);
+              if (S >= g2 * (1.0 + 0x1p-38)) {
+                keep = true;
+              } else if (S <= g2 * (1.0 - 0x1p-38) && gap > T_list * 0x1p-12) {
+                keep = false;
+              } else {
+                keep = dmax(dsub(est2, dsqrt(S)), 0.0) <= T_list;
+              }
+            } else {
+              keep = dmax(dsub(est2, margin), 0.0) <= T_list;
+            }
+          }
+        }
+        const unsigned kb = __ballot_sync(FULL, keep);
+        if (!kb) continue;
+        surv += __popc(kb);
+        if (!REFINE) {  // 1-bit index: the stage-1 estimate is the distance (search.py:362-366)
+          warp_offer(a, qd, qi, keep ? est2 : dinf(), keep ? (int)vi : -1, lo, k);
+          continue;
+        }
+        if (keep) r_v[(head + nb + __popc(kb & ((1u << lane) - 1u))) & (RING - 1)] = (int)vi;
+        nb += __popc(kb);
+      }
+      if (REFINE) {
+        __syncwarp();
+        while (nb >= 32) {
+          double d;
+          int vr;
+          warp_refine32<NIB>(a, qc, lo, d_qc2, s_sl, r_v, head, 32, d, vr);
+          warp_offer(a, qd, qi, d, vr, lo, k);
+          head = (head + 32) & (RING - 1);
+          nb -= 32;
+        }
+        __syncwarp();  // consumed ring slots may be rewritten
+      }
+    }
+    if (REFINE && nb > 0) {
+      double d;
+      int vr;
+      warp_refine32<NIB>(a, qc, lo, d_qc2, s_sl, r_v, head, nb, d, vr);
+      warp_offer(a, qd, qi, d, vr, lo, k);
+    }
+    __syncwarp();
+    const int cnt = __popc(__ballot_sync(FULL, lane < k && qi != NO_ID));
+    if (cnt >= k) T = __shfl_sync(FULL, qd, k - 1);  // search.py:444-447
+  }
+  const int pn = __popc(__ballot_sync(FULL, lane < k && qi != NO_ID));
+  if (lane < k) {
+    a.out_ids[q * k + lane] = lane < pn ? qi : -1;
+    a.out_dists[q * k + lane] = lane < pn ? qd : dinf();
+  }
+  if (lane == 0) {
+    a.out_counts[q] = pn;
+    if (a.stats) {
+      a.stats[2 * q] = probed;
+      a.stats[2 * q + 1] = surv;
+    }
+  }
+}
+
 // ------------------------------------------------------------ kernel, k > 32
 // block-wide bitonic sort (ascending (key, id)) of n (power of two) entries
 __device__ void bitonic_sort(double* key, int64_t* id, int n) {
@@ -934,7 +1221,7 @@ __global__ void __launch_bounds__(THREADS) first_list_kernel(FArgs a) {
 // w_j the two's-complement weights of the query_bits planes, i.e. exactly the
 // integer dot product sum_d bit[v,d] * qhat[q,d] of the 1-bit code with the
 // quantized query.  For every (list, query probing it) pair that the
-// per-query pass will scan, ip_tile_kernel computes that dot for every vector
+// per-query pass will scan, ip_list_kernel computes that dot for every vector
 // of the list as an int8 GEMM on mma.sync m16n8k32 (u8 0/1 codes x s8 qhat,
 // int32 accumulate: exact), reading each list's codes once per 64 queries
 // instead of once per query.  The per-query pass then reads 2 bytes per
@@ -946,14 +1233,16 @@ __global__ void __launch_bounds__(THREADS) first_list_kernel(FArgs a) {
 
 struct IpArgs {
   ivrq_index_view ix;
-  const uint32_t* planes;
-  int qbits, g, nprobe, nlist;
+  const int8_t* qhat;       // [nq][32 g] quantized queries (qhat_kernel)
+  int g, nprobe, nlist;
   const int64_t* porder;    // pair indices (q * nprobe + p) sorted by list
   const int64_t* poff;      // [nlist + 2] bucket starts in porder
   const int64_t* pair_base; // [nlist + 1] element offset of each list's rows
-  const int32_t* tpre;      // [nlist + 1] prefix of tiles per list
+  const int32_t* tpre;      // [nlist + 1] prefix of query groups (TQ pairs) per list
   void* ipbuf;              // int16 or int32 elements
 };
+
+constexpr int KCH = 8;  // 32-dim groups of code words per staged chunk
 
 __device__ __forceinline__ void mma_s8u8(int (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
   asm volatile(
@@ -967,145 +1256,183 @@ __device__ __forceinline__ uint32_t nib_bytes(uint32_t w, int shift) {
   return (((w >> shift) & 0xFu) * 0x00204081u) & 0x01010101u;
 }
 
-template <typename IPT>
-__device__ __forceinline__ void ip_tile(const IpArgs& a, int b, int8_t* sq);
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(sa), "l"(gmem), "r"(valid ? 4 : 0));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-// persistent: the CTAs stride over the tiles (their count is only known on device)
-template <typename IPT>
-__global__ void __launch_bounds__(THREADS, 2) ip_tile_kernel(IpArgs a) {
-  extern __shared__ __align__(16) unsigned char ism[];
-  const int total = a.tpre[a.nlist];
-  for (int b = blockIdx.x; b < total; b += gridDim.x) {
-    ip_tile<IPT>(a, b, reinterpret_cast<int8_t*>(ism));
-    __syncthreads();  // qhat tile is rewritten by the next tile
+// qhat[q][32 gi + i] = sum_j w_j bit_i(plane_j[gi]) (two's complement of query_bits bits)
+__global__ void qhat_kernel(const uint32_t* __restrict__ planes, int64_t nq, int g, int qb, int8_t* __restrict__ qhat) {
+  const int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (it >= nq * g) return;
+  const int64_t q = it / g;
+  const int gi = (int)(it % g);
+  uint32_t pl[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) pl[j] = j < qb ? planes[(q * qb + j) * g + gi] : 0u;
+  uint32_t out[8];
+#pragma unroll
+  for (int w4 = 0; w4 < 8; ++w4) {
+    uint32_t packed = 0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int i = 4 * w4 + e;
+      int v = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v |= (int)((pl[j] >> i) & 1u) << j;
+      v = (v << (32 - qb)) >> (32 - qb);
+      packed |= ((uint32_t)v & 0xFFu) << (8 * e);
+    }
+    out[w4] = packed;
   }
+  uint4* dst = reinterpret_cast<uint4*>(qhat + q * 32 * (int64_t)g + 32 * gi);
+  dst[0] = make_uint4(out[0], out[1], out[2], out[3]);
+  dst[1] = make_uint4(out[4], out[5], out[6], out[7]);
 }
 
+// One CTA per (list, group of <= TQ queries probing it), persistent over the
+// groups.  The group's qhat rows sit in shared memory; the list's code words
+// stream through a cp.async double buffer in (256 vectors x KCH groups)
+// stages; each warp owns 32 vectors x all queries of the group.
 template <typename IPT>
-__device__ __forceinline__ void ip_tile(const IpArgs& a, int b, int8_t* sq) {
-  int lo_c = 0, hi_c = a.nlist;  // tpre[lo_c] <= b < tpre[hi_c]
-  while (hi_c - lo_c > 1) {
-    const int mid = (lo_c + hi_c) >> 1;
-    if (a.tpre[mid] <= b) lo_c = mid; else hi_c = mid;
-  }
-  const int c = lo_c;
-  const int64_t lo = a.ix.offsets[c], n_c = a.ix.offsets[c + 1] - lo;
-  const int64_t nv_t = ceil_div(n_c, TV);
-  const int local = b - a.tpre[c];
-  const int qt = (int)(local / nv_t);
-  const int64_t v0 = (local % nv_t) * TV;
-  const int64_t pb = a.poff[c] + (int64_t)qt * TQ;
-  const int nqt = (int)min((int64_t)TQ, a.poff[c + 1] - pb);
-  const int g = a.g, qb = a.qbits;
+__global__ void __launch_bounds__(THREADS, 2) ip_list_kernel(IpArgs a) {
+  extern __shared__ __align__(16) unsigned char ism[];
+  const int g = a.g;
   const int ldq = 32 * g + TQ_PAD;  // bytes per query row of qhat
+  int8_t* sq = reinterpret_cast<int8_t*>(ism);
+  uint32_t* sw = reinterpret_cast<uint32_t*>(ism + (size_t)TQ * ldq);  // [2][KCH][TV]
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  // qhat[q][32*gi + i] = sum_j w_j * bit_i(plane_j[gi]), rows >= nqt zero
-  for (int it = tid; it < TQ * g; it += THREADS) {
-    const int r = it / g, gi = it % g;
-    uint32_t pl[8];
-    const int64_t q = r < nqt ? a.porder[pb + r] / a.nprobe : -1;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) pl[j] = (q >= 0 && j < qb) ? __ldg(a.planes + (q * qb + j) * g + gi) : 0u;
-    uint32_t* dst = reinterpret_cast<uint32_t*>(sq + r * ldq + 32 * gi);
-#pragma unroll
-    for (int w4 = 0; w4 < 8; ++w4) {
-      uint32_t packed = 0;
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int i = 4 * w4 + e;
-        int v = 0;
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-          if (j < qb) v |= (int)((pl[j] >> i) & 1u) << j;
-        v = (v << (32 - qb)) >> (32 - qb);  // two's complement of qb bits
-        packed |= ((uint32_t)v & 0xFFu) << (8 * e);
-      }
-      dst[w4] = packed;
-    }
-  }
-  __syncthreads();
   const int gid = lane >> 2, t4 = lane & 3;
-  const int nmt = (nqt + 15) >> 4;  // warp-uniform
-  const uint32_t* words = a.ix.packed_msb + (int64_t)g * lo;
-  int acc[4][4][4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = acc[i][j][2] = acc[i][j][3] = 0;
-  const int64_t vw = v0 + wid * 32;  // this warp's 32 vectors
-  if (vw < n_c) {
-    int64_t vrow[4];
-#pragma unroll
-    for (int nt = 0; nt < 4; ++nt) vrow[nt] = vw + nt * 8 + gid;
-    uint32_t wnext[4];
-#pragma unroll
-    for (int nt = 0; nt < 4; ++nt) wnext[nt] = vrow[nt] < n_c ? __ldg(words + vrow[nt]) : 0u;
-    for (int gi = 0; gi < g; ++gi) {
-      uint32_t wcur[4];
-#pragma unroll
-      for (int nt = 0; nt < 4; ++nt) {
-        wcur[nt] = wnext[nt];
-        wnext[nt] = (gi + 1 < g && vrow[nt] < n_c) ? __ldg(words + (int64_t)(gi + 1) * n_c + vrow[nt]) : 0u;
-      }
-      uint32_t bf[4][2];
-#pragma unroll
-      for (int nt = 0; nt < 4; ++nt) {
-        bf[nt][0] = nib_bytes(wcur[nt], 4 * t4);
-        bf[nt][1] = nib_bytes(wcur[nt], 16 + 4 * t4);
-      }
-#pragma unroll
-      for (int mt = 0; mt < 4; ++mt) {
-        if (mt < nmt) {
-          const int8_t* r0 = sq + (mt * 16 + gid) * ldq + 32 * gi + 4 * t4;
-          const int8_t* r1 = r0 + 8 * ldq;
-          uint32_t af[4];
-          af[0] = *reinterpret_cast<const uint32_t*>(r0);
-          af[1] = *reinterpret_cast<const uint32_t*>(r1);
-          af[2] = *reinterpret_cast<const uint32_t*>(r0 + 16);
-          af[3] = *reinterpret_cast<const uint32_t*>(r1 + 16);
-#pragma unroll
-          for (int nt = 0; nt < 4; ++nt) mma_s8u8(acc[mt][nt], af, bf[nt][0], bf[nt][1]);
-        }
-      }
+  const int total = a.tpre[a.nlist];
+  const int nks = (g + KCH - 1) / KCH;
+  for (int b = blockIdx.x; b < total; b += gridDim.x) {
+    int lo_c = 0, hi_c = a.nlist;  // tpre[lo_c] <= b < tpre[hi_c]
+    while (hi_c - lo_c > 1) {
+      const int mid = (lo_c + hi_c) >> 1;
+      if (a.tpre[mid] <= b) lo_c = mid; else hi_c = mid;
     }
-    const int64_t rs = ip_row_stride(n_c);
-    IPT* base = reinterpret_cast<IPT*>(a.ipbuf) + a.pair_base[c] + (int64_t)qt * TQ * rs;
+    const int c = lo_c;
+    const int64_t lo = a.ix.offsets[c], n_c = a.ix.offsets[c + 1] - lo;
+    const int qt = b - a.tpre[c];
+    const int64_t pb = a.poff[c] + (int64_t)qt * TQ;
+    const int nqt = (int)min((int64_t)TQ, a.poff[c + 1] - pb);
+    const int nmt = (nqt + 15) >> 4;  // warp-uniform
+    const uint32_t* words = a.ix.packed_msb + (int64_t)g * lo;
+    const int64_t nvt = ceil_div(n_c, TV);
+    const int nst = (int)(nvt * nks);
+    auto issue = [&](int st) {
+      const int64_t v0 = (st / nks) * (int64_t)TV;
+      const int k0 = (st % nks) * KCH;
+      uint32_t* dst = sw + (st & 1) * KCH * TV;
+      for (int i = tid; i < KCH * TV; i += THREADS) {
+        const int jj = i / TV, vv = i % TV;
+        const int64_t v = v0 + vv;
+        const bool ok = k0 + jj < g && v < n_c;
+        cp_async4(dst + i, ok ? words + (int64_t)(k0 + jj) * n_c + v : words, ok);
+      }
+      cp_async_commit();
+    };
+    __syncthreads();  // the previous group is done with sq / sw
+    issue(0);
+    for (int i = tid; i < TQ * (8 * g); i += THREADS) {  // qhat rows, 4 bytes at a time
+      const int r = i / (8 * g), w = i % (8 * g);
+      uint32_t v = 0;
+      if (r < nqt) v = __ldg(reinterpret_cast<const uint32_t*>(a.qhat + (a.porder[pb + r] / a.nprobe) * 32 * (int64_t)g) + w);
+      *reinterpret_cast<uint32_t*>(sq + r * ldq + 4 * w) = v;
+    }
+    int acc[4][4][4];
+    for (int st = 0; st < nst; ++st) {
+      const int kc = st % nks;
+      const int64_t v0 = (st / nks) * (int64_t)TV;
+      if (kc == 0) {
 #pragma unroll
-    for (int mt = 0; mt < 4; ++mt) {
-      if (mt >= nmt) continue;
+        for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int r = mt * 16 + gid + 8 * h;
-        if (r >= nqt) continue;
+          for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = acc[i][j][2] = acc[i][j][3] = 0;
+      }
+      if (st + 1 < nst) {
+        issue(st + 1);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncthreads();
+      const uint32_t* w0 = sw + (st & 1) * KCH * TV + wid * 32 + gid;
+      const int k0 = kc * KCH;
+      const int kn = min(KCH, g - k0);
+      for (int jj = 0; jj < kn; ++jj) {
+        const int gi = k0 + jj;
+        uint32_t bf[4][2];
 #pragma unroll
         for (int nt = 0; nt < 4; ++nt) {
-          const int64_t v = vw + nt * 8 + 2 * t4;  // even; v + 1 stays inside the padded row
-          if (v >= n_c) continue;
-          IPT* dst = base + (int64_t)r * rs + v;
-          const int x0 = acc[mt][nt][2 * h], x1 = acc[mt][nt][2 * h + 1];
-          if constexpr (sizeof(IPT) == 2) {
-            *reinterpret_cast<uint32_t*>(dst) = ((uint32_t)x0 & 0xFFFFu) | ((uint32_t)x1 << 16);
-          } else {
-            *reinterpret_cast<int2*>(dst) = make_int2(x0, x1);
+          const uint32_t w = w0[jj * TV + nt * 8];
+          bf[nt][0] = nib_bytes(w, 4 * t4);
+          bf[nt][1] = nib_bytes(w, 16 + 4 * t4);
+        }
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) {
+          if (mt < nmt) {
+            const int8_t* r0 = sq + (mt * 16 + gid) * ldq + 32 * gi + 4 * t4;
+            const int8_t* r1 = r0 + 8 * ldq;
+            uint32_t af[4];
+            af[0] = *reinterpret_cast<const uint32_t*>(r0);
+            af[1] = *reinterpret_cast<const uint32_t*>(r1);
+            af[2] = *reinterpret_cast<const uint32_t*>(r0 + 16);
+            af[3] = *reinterpret_cast<const uint32_t*>(r1 + 16);
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt) mma_s8u8(acc[mt][nt], af, bf[nt][0], bf[nt][1]);
           }
         }
       }
+      if (kc == nks - 1) {  // epilogue of this vector tile
+        const int64_t rs = ip_row_stride(n_c);
+        IPT* base = reinterpret_cast<IPT*>(a.ipbuf) + a.pair_base[c] + (int64_t)qt * TQ * rs;
+        const int64_t vw = v0 + wid * 32;
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) {
+          if (mt >= nmt) continue;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int r = mt * 16 + gid + 8 * h;
+            if (r >= nqt) continue;
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt) {
+              const int64_t v = vw + nt * 8 + 2 * t4;  // even; v + 1 stays inside the padded row
+              if (v >= n_c) continue;
+              IPT* dst = base + (int64_t)r * rs + v;
+              const int x0 = acc[mt][nt][2 * h], x1 = acc[mt][nt][2 * h + 1];
+              if constexpr (sizeof(IPT) == 2) {
+                *reinterpret_cast<uint32_t*>(dst) = ((uint32_t)x0 & 0xFFFFu) | ((uint32_t)x1 << 16);
+              } else {
+                *reinterpret_cast<int2*>(dst) = make_int2(x0, x1);
+              }
+            }
+          }
+        }
+      }
+      __syncthreads();  // buffer (st & 1) is refilled by issue(st + 2)
     }
   }
 }
 
 // pair keys: list of every in-range probe the per-query pass scans (the first
 // in-range probe is excluded when the first-list phase handles it)
+// excl: 0 every in-range probe, 1 all but the first in-range probe (scanned
+// with the threshold still +inf, where the inner products are not needed),
+// 2 none (prune off with refine on: no list needs them)
 __global__ void pair_key_kernel(const int64_t* __restrict__ probe_ids, int64_t nq, int nprobe, int64_t list_lo,
-                                int64_t list_hi, int skip_first, int32_t* __restrict__ keys) {
+                                int64_t list_hi, int excl, int32_t* __restrict__ keys) {
   const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= nq) return;
   const int32_t none = (int32_t)(list_hi - list_lo);
-  bool first = skip_first != 0;
+  bool first = excl == 1;
   for (int p = 0; p < nprobe; ++p) {
     const int64_t cg = probe_ids[q * nprobe + p];
     int32_t key = none;
-    if (cg >= list_lo && cg < list_hi) {
+    if (cg >= list_lo && cg < list_hi && excl != 2) {
       if (first) first = false;
       else key = (int32_t)(cg - list_lo);
     }
@@ -1144,7 +1471,7 @@ __global__ void __launch_bounds__(1024) pair_plan_kernel(const int64_t* __restri
     if (c < nlist) {
       const int64_t n_c = offsets[c + 1] - offsets[c], cnt = poff[c + 1] - poff[c];
       e = cnt * ip_row_stride(n_c);
-      t = (n_c > 0 && cnt > 0) ? ceil_div(cnt, TQ) * ceil_div(n_c, TV) : 0;
+      t = (n_c > 0 && cnt > 0) ? ceil_div(cnt, TQ) : 0;
     }
     int64_t ie = e, it = t;  // inclusive warp scans
 #pragma unroll
@@ -1251,9 +1578,20 @@ __global__ void merge_topk_kernel(const int64_t* __restrict__ ids, const double*
   out_counts[q] = n;
 }
 
+template <bool REFINE, bool NIB>
+int launch_warp(const Args& a, int ipb, cudaStream_t s) {
+  const size_t sm = warp_smem_bytes(a.kpad, REFINE);
+  auto kern = ipb == 2 ? scan_warp_kernel<REFINE, NIB, 2> : scan_warp_kernel<REFINE, NIB, 4>;
+  if (sm > 48 * 1024 && cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess)
+    return fail(IVRQ_EUNSUP, "ivrq_search_scan: shared memory request too large");
+  kern<<<(unsigned)ceil_div(a.nq, WQ), WQ * 32, sm, s>>>(a);
+  return check_launch("ivrq_search_scan");
+}
+
 template <int MODE, bool REFINE, bool NIB>
 int launch_t(const Args& a, int ipb, cudaStream_t s) {
   const bool bigk = a.k > 32;
+  if (ipb < 0) return launch_warp<REFINE, NIB>(a, -ipb, s);  // warp-per-query path
   const size_t sm = smem_bytes(a, MODE, REFINE, bigk);
   const bool qb4 = MODE == IVRQ_IP_BITWISE && a.qbits == 4;  // the SearchParams default
   auto kern = bigk ? (qb4 ? scan_kernel_bigk<MODE, REFINE, NIB, 4> : scan_kernel_bigk<MODE, REFINE, NIB, 0>)
@@ -1349,7 +1687,14 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
   double* pool_d = nullptr;
   int32_t* pool_n = nullptr;
   const char* fl_env = getenv("IVRQ_FIRST_LIST");
-  const bool first_phase = grouped && refine && a.k <= 32 && !init_counts && (fl_env ? atoi(fl_env) != 0 : true);
+  const char* tc_env = getenv("IVRQ_TC_STAGE1");
+  const char* wenv = getenv("IVRQ_WARP_SCAN");
+  // bitwise mode, k <= 32: stage-1 inner products list-major on the tensor
+  // cores, then one warp per query (first lists included)
+  const bool tc_path = params->ip_mode == IVRQ_IP_BITWISE && a.k <= 32 && (tc_env ? atoi(tc_env) != 0 : true) && nl >= 1;
+  const bool warp_path = tc_path && (wenv ? atoi(wenv) != 0 : true);
+  const bool first_phase = grouped && refine && a.k <= 32 && !init_counts &&
+                           (fl_env ? atoi(fl_env) != 0 : !warp_path);
   if (grouped && nq > 1 && nl >= 1) {
     if (cudaMallocAsync(reinterpret_cast<void**>(&first), nq * sizeof(int32_t), s) != cudaSuccess ||
         cudaMallocAsync(reinterpret_cast<void**>(&cnt), (nl + 1) * sizeof(int64_t), s) != cudaSuccess ||
@@ -1408,11 +1753,11 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
   int32_t *pkeys = nullptr, *pslot = nullptr, *tpre = nullptr;
   int64_t *pcnt = nullptr, *poff = nullptr, *porder = nullptr, *pbase = nullptr, *ptot = nullptr;
   void* ipbuf = nullptr;
-  const char* tc_env = getenv("IVRQ_TC_STAGE1");
   const int64_t ipmax = (int64_t)words_per_vector(index->dims) * 32 << (params->query_bits - 1);
-  if (params->ip_mode == IVRQ_IP_BITWISE && a.k <= 32 && (tc_env ? atoi(tc_env) != 0 : true) && nl >= 1) {
+  if (tc_path) {
     ipb = ipmax <= 32768 ? 2 : 4;
     const int64_t npairs = nq * a.nprobe;
+    const int excl = warp_path ? (refine && !a.prune ? 2 : (refine && !init_counts ? 1 : 0)) : (a.skip_first ? 1 : 0);
     if (cudaMallocAsync(reinterpret_cast<void**>(&pkeys), npairs * sizeof(int32_t), s) != cudaSuccess ||
         cudaMallocAsync(reinterpret_cast<void**>(&pslot), npairs * sizeof(int32_t), s) != cudaSuccess ||
         cudaMallocAsync(reinterpret_cast<void**>(&porder), npairs * sizeof(int64_t), s) != cudaSuccess ||
@@ -1423,7 +1768,7 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
         cudaMallocAsync(reinterpret_cast<void**>(&ptot), 2 * sizeof(int64_t), s) != cudaSuccess)
       return fail(IVRQ_ENOMEM, "ivrq_search_scan: workspace allocation failed");
     scan::pair_key_kernel<<<(unsigned)ceil_div(nq, 256), 256, 0, s>>>(probe_ids, nq, a.nprobe, list_lo, list_hi,
-                                                                      a.skip_first, pkeys);
+                                                                      excl, pkeys);
     IVRQ_TRY(check_launch("ivrq_search_scan(pair keys)"));
     IVRQ_TRY(ivrq_counting_sort(pkeys, npairs, (int32_t)(nl + 1), pcnt, poff, porder, stream));
     scan::pair_slot_kernel<<<(unsigned)ceil_div(npairs, 256), 256, 0, s>>>(porder, poff, pkeys, npairs,
@@ -1433,7 +1778,9 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
     // ip buffer: bounded by every pair owning a row of the largest list (no
     // host round trip), or the exact total read back when the bound is unknown
     int64_t tot[2] = {0, 0};
-    if (index->max_list > 0) {
+    if (excl == 2) {
+      tot[0] = 0;
+    } else if (index->max_list > 0) {
       tot[0] = npairs * scan::ip_row_stride(index->max_list);
     } else if (cudaMemcpyAsync(tot, ptot, sizeof(tot), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
                cudaStreamSynchronize(s) != cudaSuccess) {
@@ -1442,10 +1789,13 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
     if (tot[0] > 0) {
       if (cudaMallocAsync(&ipbuf, (size_t)tot[0] * ipb, s) != cudaSuccess)
         return fail(IVRQ_ENOMEM, "ivrq_search_scan: inner-product buffer allocation failed");
+      int8_t* qhat = nullptr;
+      if (cudaMallocAsync(reinterpret_cast<void**>(&qhat), (size_t)nq * 32 * a.g, s) != cudaSuccess)
+        return fail(IVRQ_ENOMEM, "ivrq_search_scan: workspace allocation failed");
+      scan::qhat_kernel<<<(unsigned)ceil_div(nq * a.g, 256), 256, 0, s>>>(planes, nq, a.g, a.qbits, qhat);
       scan::IpArgs ia{};
       ia.ix = *index;
-      ia.planes = planes;
-      ia.qbits = a.qbits;
+      ia.qhat = qhat;
       ia.g = a.g;
       ia.nprobe = a.nprobe;
       ia.nlist = (int)nl;
@@ -1454,19 +1804,21 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
       ia.pair_base = pbase;
       ia.tpre = tpre;
       ia.ipbuf = ipbuf;
-      const size_t ism = (size_t)scan::TQ * (32 * a.g + scan::TQ_PAD);
-      auto ik = ipb == 2 ? scan::ip_tile_kernel<int16_t> : scan::ip_tile_kernel<int32_t>;
+      const size_t ism = (size_t)scan::TQ * (32 * a.g + scan::TQ_PAD) + 2 * sizeof(uint32_t) * scan::KCH * scan::TV;
+      auto ik = ipb == 2 ? scan::ip_list_kernel<int16_t> : scan::ip_list_kernel<int32_t>;
       if (ism > 48 * 1024 &&
           cudaFuncSetAttribute(ik, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ism) != cudaSuccess)
         return fail(IVRQ_EUNSUP, "ivrq_search_scan: dims too large for the tensor-core stage 1");
       ik<<<(unsigned)(2 * sm_count_of_current_device()), scan::THREADS, ism, s>>>(ia);
       IVRQ_TRY(check_launch("ivrq_search_scan(stage-1 tiles)"));
+      cudaFreeAsync(qhat, s);
     }
     a.ipbuf = ipbuf;
     a.pslot = pslot;
     a.pair_base = pbase;
   }
-  const int rc = params->ip_mode == IVRQ_IP_BITWISE ? scan::launch_mode<IVRQ_IP_BITWISE>(a, refine, nib, ipb, s)
+  const int rc = params->ip_mode == IVRQ_IP_BITWISE
+                     ? scan::launch_mode<IVRQ_IP_BITWISE>(a, refine, nib, warp_path ? -ipb : ipb, s)
                                                     : scan::launch_mode<IVRQ_IP_LUT>(a, refine, nib, 0, s);
   if (pkeys) {
     cudaFreeAsync(pkeys, s);
