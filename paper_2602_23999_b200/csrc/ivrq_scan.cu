@@ -63,6 +63,11 @@ struct Args {
   const void* ipbuf;
   const int32_t* pslot;      // [nq * nprobe] slot of (q, p) in its list's bucket
   const int64_t* pair_base;  // [nlist + 1]
+  // refined distances of every vector of each query's first list (first_dist_kernel), or null:
+  // row of qorder slot i (bucket c) at fdist + fbase[c] + (i - qoff[c]) * ip_row_stride(n_c)
+  const double* fdist;
+  const int64_t* fbase;
+  const int64_t* qoff;
 };
 
 __device__ __forceinline__ double dinf() { return __longlong_as_double(0x7ff0000000000000LL); }
@@ -729,14 +734,12 @@ __global__ void __launch_bounds__(WQ * 32) scan_warp_kernel(Args a) {
   __syncwarp();
   const int64_t* pid_list = a.probe_ids + q * a.nprobe;
   const double* pd2_list = a.probe_d2 + q * a.nprobe;
-  bool first_pending = a.skip_first != 0;
+  bool first_pending = true;  // the first in-range probe is still ahead
   for (int p = 0; p < a.nprobe; ++p) {  // ascending cluster id (search.py:429)
     const int64_t cg = pid_list[p];
     if (cg < a.list_lo || cg >= a.list_hi) continue;
-    if (first_pending) {
-      first_pending = false;
-      continue;
-    }
+    const bool is_first = first_pending;
+    first_pending = false;
     const int64_t c = cg - a.list_lo;
     const double d_qc2 = pd2_list[p];
     const int64_t lo = a.ix.offsets[c], n_c = a.ix.offsets[c + 1] - lo;
@@ -745,6 +748,16 @@ __global__ void __launch_bounds__(WQ * 32) scan_warp_kernel(Args a) {
     probed += n_c;
     if (REFINE && T_list == dinf()) {  // nothing can be pruned (lb2 <= +inf): refine the whole list
       surv += n_c;
+      if (a.fdist && is_first) {  // the query's first list: refined on the tensor cores list-major
+        const double* frow = a.fdist + a.fbase[c] + (slot_q - a.qoff[c]) * ip_row_stride(n_c);
+        for (int64_t c0 = 0; c0 < n_c; c0 += 32) {
+          const int64_t vi = c0 + lane;
+          warp_offer(a, qd, qi, vi < n_c ? __ldg(frow + vi) : dinf(), vi < n_c ? (int)vi : -1, lo, k);
+        }
+        const int cnt = __popc(__ballot_sync(FULL, lane < k && qi != NO_ID));
+        if (cnt >= k) T = __shfl_sync(FULL, qd, k - 1);
+        continue;
+      }
       for (int64_t c0 = 0; c0 < n_c; c0 += 32) {
         double d;
         int vr;
@@ -1454,7 +1467,7 @@ __global__ void pair_slot_kernel(const int64_t* __restrict__ porder, const int64
 // pair_base (elements) and tile prefix over the lists; one block.
 // totals[0] = ip elements, totals[1] = tiles.
 __global__ void __launch_bounds__(1024) pair_plan_kernel(const int64_t* __restrict__ offsets,
-                                                         const int64_t* __restrict__ poff, int nlist,
+                                                         const int64_t* __restrict__ poff, int nlist, int grp,
                                                          int64_t* __restrict__ pair_base, int32_t* __restrict__ tpre,
                                                          int64_t* __restrict__ totals) {
   __shared__ int64_t s_e[32], s_t[32];
@@ -1471,7 +1484,7 @@ __global__ void __launch_bounds__(1024) pair_plan_kernel(const int64_t* __restri
     if (c < nlist) {
       const int64_t n_c = offsets[c + 1] - offsets[c], cnt = poff[c + 1] - poff[c];
       e = cnt * ip_row_stride(n_c);
-      t = (n_c > 0 && cnt > 0) ? ceil_div(cnt, TQ) : 0;
+      t = (n_c > 0 && cnt > 0) ? ceil_div(cnt, grp) : 0;
     }
     int64_t ie = e, it = t;  // inclusive warp scans
 #pragma unroll
@@ -1519,6 +1532,196 @@ __global__ void __launch_bounds__(1024) pair_plan_kernel(const int64_t* __restri
     tpre[nlist] = (int32_t)s_run_t;
     totals[0] = s_run_e;
     totals[1] = s_run_t;
+  }
+}
+
+// ------------------------------------------------------------ first lists, list-major refine
+// Each query's first in-range list is scanned with the threshold at +inf
+// (search.py:435 before any merge), so every vector is refined.  Queries that
+// share a first list share its rcodes: one CTA takes a list and FQ of those
+// queries, streams the list's rcode rows through shared memory (cp.async, 128
+// rows x one 64-dim step per stage) and runs the int8 MMAs against all FQ
+// queries' digit slices, writing the refined distance of every (query,
+// vector) (refine_chunk's exact arithmetic) for the warp kernel to merge.
+constexpr int FQ = 8;     // queries per group (n8 tiles of 8 digit slices)
+constexpr int FROWS = 128;  // rcode rows per tile: 8 warps x 16
+
+struct FdArgs {
+  ivrq_index_view ix;
+  int64_t list_lo;
+  const int64_t* probe_ids;
+  const double* probe_d2;
+  int nprobe, nlist, kpad;
+  const double* scalars;
+  const int8_t* qslices;
+  const int64_t* qorder;
+  const int64_t* qoff;    // [nlist + 2] first-list buckets in qorder
+  const int64_t* fbase;   // [nlist + 1]
+  const int32_t* gpre;    // [nlist + 1] prefix of ceil(bucket / FQ)
+  double* fdist;
+};
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(valid ? 16 : 0));
+}
+
+template <bool NIB>
+__global__ void __launch_bounds__(THREADS, 2) first_dist_kernel(FdArgs a) {
+  extern __shared__ __align__(16) unsigned char fsm2[];
+  __shared__ double s_dq[FQ], s_kb[FQ], s_hs[FQ], s_ls[FQ];
+  __shared__ int64_t s_row[FQ];
+  constexpr int CB = NIB ? 32 : 64;  // rcode bytes per row per 64-dim step
+  const int kp = a.kpad, ss = kp + SPAD;
+  int8_t* s_sl = reinterpret_cast<int8_t*>(fsm2);  // [FQ][SLICES][ss]
+  uint8_t* s_a = reinterpret_cast<uint8_t*>(fsm2 + (size_t)FQ * SLICES * ss);  // [2][FROWS][CB]
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int gid = lane >> 2, t4 = lane & 3;
+  const int np = kp / 64;
+  const int total = a.gpre[a.nlist];
+  const int64_t rb = a.ix.rcode_bytes;
+  for (int b = blockIdx.x; b < total; b += gridDim.x) {
+    int lo_c = 0, hi_c = a.nlist;
+    while (hi_c - lo_c > 1) {
+      const int mid = (lo_c + hi_c) >> 1;
+      if (a.gpre[mid] <= b) lo_c = mid; else hi_c = mid;
+    }
+    const int c = lo_c;
+    const int64_t lo = a.ix.offsets[c], n_c = a.ix.offsets[c + 1] - lo;
+    const int64_t qs = a.qoff[c] + (int64_t)(b - a.gpre[c]) * FQ;
+    const int nqg = (int)min((int64_t)FQ, a.qoff[c + 1] - qs);
+    const int64_t rs = ip_row_stride(n_c);
+    const uint8_t* rows = a.ix.rcodes + lo * rb;
+    const int nst = (int)ceil_div(n_c, FROWS) * np;
+    auto issue = [&](int st) {
+      const int64_t v0 = (int64_t)(st / np) * FROWS;
+      const int p = st % np;
+      uint8_t* dst = s_a + (st & 1) * FROWS * CB;
+      for (int i = tid; i < FROWS * CB / 16; i += THREADS) {
+        const int r = i / (CB / 16), part = i % (CB / 16);
+        const bool ok = v0 + r < n_c;
+        cp_async16(dst + r * CB + 16 * part, ok ? rows + (v0 + r) * rb + p * CB + 16 * part : rows, ok);
+      }
+      cp_async_commit();
+    };
+    __syncthreads();  // previous group done with shared memory
+    if (nst > 0) issue(0);
+    if (tid < FQ) {
+      double dq = 0.0, kb = 0.0;
+      int e = 0;
+      int64_t row = -1;
+      if (tid < nqg) {
+        const int64_t q = a.qorder[qs + tid];
+        for (int p = 0; p < a.nprobe; ++p) {  // the first in-range probe is list c
+          if (a.probe_ids[q * a.nprobe + p] == c + a.list_lo) {
+            dq = a.probe_d2[q * a.nprobe + p];
+            break;
+          }
+        }
+        kb = a.scalars[q * IVRQ_QS_COUNT + IVRQ_QS_KB_SUM];
+        e = (int)a.scalars[q * IVRQ_QS_COUNT + IVRQ_QS_SLICE_EXP];
+        row = a.fbase[c] + (qs + tid - a.qoff[c]) * rs;
+      }
+      s_dq[tid] = dq;
+      s_kb[tid] = kb;
+      s_hs[tid] = ldexp(1.0, e - 26);
+      s_ls[tid] = ldexp(1.0, e - 54);
+      s_row[tid] = row;
+    }
+    for (int i = tid; i < FQ * SLICES * kp / 4; i += THREADS) {
+      const int j = (4 * i) / (SLICES * kp), rem = (4 * i) % (SLICES * kp);
+      const int sidx = rem / kp, kk = rem % kp;
+      uint32_t v = 0;
+      if (j < nqg)
+        v = __ldg(reinterpret_cast<const uint32_t*>(a.qslices + a.qorder[qs + j] * SLICES * (int64_t)kp) + rem / 4);
+      *reinterpret_cast<uint32_t*>(s_sl + (j * SLICES + sidx) * ss + kk) = v;
+    }
+    int acc[FQ][4];
+    for (int st = 0; st < nst; ++st) {
+      const int p = st % np;
+      const int64_t v0 = (int64_t)(st / np) * FROWS;
+      if (p == 0) {
+#pragma unroll
+        for (int j = 0; j < FQ; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0;
+      }
+      if (st + 1 < nst) {
+        issue(st + 1);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncthreads();
+      const uint8_t* ta = s_a + (st & 1) * FROWS * CB + (wid * 16 + gid) * CB;
+      uint32_t as0[4], as1[4];
+      if (NIB) {
+        const uint2 x0 = *reinterpret_cast<const uint2*>(ta + 8 * t4);
+        const uint2 x1 = *reinterpret_cast<const uint2*>(ta + 8 * CB + 8 * t4);
+        as0[0] = x0.x & 0x0F0F0F0Fu;
+        as0[2] = (x0.x >> 4) & 0x0F0F0F0Fu;
+        as1[0] = x0.y & 0x0F0F0F0Fu;
+        as1[2] = (x0.y >> 4) & 0x0F0F0F0Fu;
+        as0[1] = x1.x & 0x0F0F0F0Fu;
+        as0[3] = (x1.x >> 4) & 0x0F0F0F0Fu;
+        as1[1] = x1.y & 0x0F0F0F0Fu;
+        as1[3] = (x1.y >> 4) & 0x0F0F0F0Fu;
+      } else {
+        const uint4 x0 = *reinterpret_cast<const uint4*>(ta + 16 * t4);
+        const uint4 x1 = *reinterpret_cast<const uint4*>(ta + 8 * CB + 16 * t4);
+        as0[0] = x0.x;
+        as0[2] = x0.y;
+        as1[0] = x0.z;
+        as1[2] = x0.w;
+        as0[1] = x1.x;
+        as0[3] = x1.y;
+        as1[1] = x1.z;
+        as1[3] = x1.w;
+      }
+#pragma unroll
+      for (int j = 0; j < FQ; ++j) {
+        if (j < nqg) {
+          const int8_t* sl = s_sl + (j * SLICES + gid) * ss + 4 * t4 + 64 * p;
+          const uint32_t b00 = *reinterpret_cast<const uint32_t*>(sl);
+          const uint32_t b10 = *reinterpret_cast<const uint32_t*>(sl + 16);
+          const uint32_t b01 = *reinterpret_cast<const uint32_t*>(sl + 32);
+          const uint32_t b11 = *reinterpret_cast<const uint32_t*>(sl + 48);
+          mma_u8s8(acc[j], as0[0], as0[1], as0[2], as0[3], b00, b10);
+          mma_u8s8(acc[j], as1[0], as1[1], as1[2], as1[3], b01, b11);
+        }
+      }
+      if (p == np - 1) {  // epilogue of this row tile (refine_chunk's arithmetic)
+        const long long w0 = (t4 & 1) ? 128LL : 2097152LL;
+        const long long w1 = (t4 & 1) ? 1LL : 16384LL;
+        const int64_t r0 = v0 + wid * 16 + gid;
+        float2 lf0 = make_float2(0.f, 0.f), lf1 = make_float2(0.f, 0.f);
+        if (t4 == 0) {
+          if (r0 < n_c) lf0 = __ldg(reinterpret_cast<const float2*>(a.ix.long_factors) + lo + r0);
+          if (r0 + 8 < n_c) lf1 = __ldg(reinterpret_cast<const float2*>(a.ix.long_factors) + lo + r0 + 8);
+        }
+#pragma unroll
+        for (int j = 0; j < FQ; ++j) {
+          if (j >= nqg) break;
+          long long p0 = (long long)acc[j][0] * w0 + (long long)acc[j][1] * w1;
+          long long p1 = (long long)acc[j][2] * w0 + (long long)acc[j][3] * w1;
+          p0 += __shfl_xor_sync(FULL, p0, 1);
+          p1 += __shfl_xor_sync(FULL, p1, 1);
+          const long long l0 = __shfl_xor_sync(FULL, p0, 2);
+          const long long l1 = __shfl_xor_sync(FULL, p1, 2);
+          if (t4 == 0) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int64_t r = r0 + 8 * h;
+              if (r >= n_c) continue;
+              const long long hi = h ? p1 : p0, lw = h ? l1 : l0;
+              const float2 lf = h ? lf1 : lf0;
+              const double ip = dadd(dmul((double)hi, s_hs[j]), dmul((double)lw, s_ls[j]));
+              a.fdist[s_row[j] + r] =
+                  dmax(dsub(dadd((double)lf.x, s_dq[j]), dmul((double)lf.y, dsub(ip, s_kb[j]))), 0.0);
+            }
+          }
+        }
+      }
+      __syncthreads();  // buffer (st & 1) is refilled by issue(st + 2)
+    }
   }
 }
 
@@ -1748,6 +1951,56 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
       a.skip_first = 1;
     }
   }
+  // first lists refined list-major for the warp-per-query kernel
+  int64_t *fbase = nullptr, *ftot = nullptr;
+  int32_t* fgpre = nullptr;
+  double* fdist = nullptr;
+  const char* fd_env = getenv("IVRQ_FIRST_DIST");
+  if (warp_path && refine && a.qorder && !init_counts && (fd_env ? atoi(fd_env) != 0 : true)) {
+    if (cudaMallocAsync(reinterpret_cast<void**>(&fbase), (nl + 1) * sizeof(int64_t), s) != cudaSuccess ||
+        cudaMallocAsync(reinterpret_cast<void**>(&fgpre), (nl + 1) * sizeof(int32_t), s) != cudaSuccess ||
+        cudaMallocAsync(reinterpret_cast<void**>(&ftot), 2 * sizeof(int64_t), s) != cudaSuccess)
+      return fail(IVRQ_ENOMEM, "ivrq_search_scan: workspace allocation failed");
+    scan::pair_plan_kernel<<<1, 1024, 0, s>>>(index->offsets, off, (int)nl, scan::FQ, fbase, fgpre, ftot);
+    IVRQ_TRY(check_launch("ivrq_search_scan(first-list plan)"));
+    int64_t tot[2] = {0, 0};
+    if (index->max_list > 0) {
+      tot[0] = nq * scan::ip_row_stride(index->max_list);  // one first-list row per query at most
+    } else if (cudaMemcpyAsync(tot, ftot, sizeof(tot), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+               cudaStreamSynchronize(s) != cudaSuccess) {
+      return fail(IVRQ_ECUDA, "ivrq_search_scan: first-list plan readback failed");
+    }
+    if (tot[0] > 0) {
+      if (cudaMallocAsync(reinterpret_cast<void**>(&fdist), (size_t)tot[0] * sizeof(double), s) != cudaSuccess)
+        return fail(IVRQ_ENOMEM, "ivrq_search_scan: first-list distance buffer allocation failed");
+      scan::FdArgs fa{};
+      fa.ix = *index;
+      fa.list_lo = list_lo;
+      fa.probe_ids = probe_ids;
+      fa.probe_d2 = probe_d2;
+      fa.nprobe = a.nprobe;
+      fa.nlist = (int)nl;
+      fa.kpad = a.kpad;
+      fa.scalars = scalars;
+      fa.qslices = qslices;
+      fa.qorder = a.qorder;
+      fa.qoff = off;
+      fa.fbase = fbase;
+      fa.gpre = fgpre;
+      fa.fdist = fdist;
+      const size_t fsm = (size_t)scan::FQ * scan::SLICES * (a.kpad + scan::SPAD) +
+                         2 * (size_t)scan::FROWS * (nib ? 32 : 64);
+      auto fk = nib ? scan::first_dist_kernel<true> : scan::first_dist_kernel<false>;
+      if (fsm > 48 * 1024 &&
+          cudaFuncSetAttribute(fk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm) != cudaSuccess)
+        return fail(IVRQ_EUNSUP, "ivrq_search_scan: dims too large for the first-list refine");
+      fk<<<(unsigned)(2 * sm_count_of_current_device()), scan::THREADS, fsm, s>>>(fa);
+      IVRQ_TRY(check_launch("ivrq_search_scan(first-list refine)"));
+      a.fdist = fdist;
+      a.fbase = fbase;
+      a.qoff = off;
+    }
+  }
   // list-major stage-1 inner products on the int8 tensor cores (bitwise mode, k <= 32)
   int ipb = 0;
   int32_t *pkeys = nullptr, *pslot = nullptr, *tpre = nullptr;
@@ -1773,7 +2026,7 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
     IVRQ_TRY(ivrq_counting_sort(pkeys, npairs, (int32_t)(nl + 1), pcnt, poff, porder, stream));
     scan::pair_slot_kernel<<<(unsigned)ceil_div(npairs, 256), 256, 0, s>>>(porder, poff, pkeys, npairs,
                                                                           (int32_t)nl, pslot);
-    scan::pair_plan_kernel<<<1, 1024, 0, s>>>(index->offsets, poff, (int)nl, pbase, tpre, ptot);
+    scan::pair_plan_kernel<<<1, 1024, 0, s>>>(index->offsets, poff, (int)nl, scan::TQ, pbase, tpre, ptot);
     IVRQ_TRY(check_launch("ivrq_search_scan(pair plan)"));
     // ip buffer: bounded by every pair owning a row of the largest list (no
     // host round trip), or the exact total read back when the bound is unknown
@@ -1820,6 +2073,12 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
   const int rc = params->ip_mode == IVRQ_IP_BITWISE
                      ? scan::launch_mode<IVRQ_IP_BITWISE>(a, refine, nib, warp_path ? -ipb : ipb, s)
                                                     : scan::launch_mode<IVRQ_IP_LUT>(a, refine, nib, 0, s);
+  if (fbase) {
+    cudaFreeAsync(fbase, s);
+    cudaFreeAsync(fgpre, s);
+    cudaFreeAsync(ftot, s);
+    if (fdist) cudaFreeAsync(fdist, s);
+  }
   if (pkeys) {
     cudaFreeAsync(pkeys, s);
     cudaFreeAsync(pslot, s);
