@@ -68,6 +68,7 @@ struct Args {
   const double* fdist;
   const int64_t* fbase;
   const int64_t* qoff;
+  int l2_prefetch;  // warp kernel: L2 prefetch of survivor rcode rows
 };
 
 __device__ __forceinline__ double dinf() { return __longlong_as_double(0x7ff0000000000000LL); }
@@ -579,7 +580,8 @@ __global__ void __launch_bounds__(THREADS, 4) scan_kernel(Args a) {
 // memory, every 16 of them go through one m16n8k32 refine group, and the
 // warp's register top-32 queue IS the query's pool.  Same prune test, refine
 // arithmetic and (dist, id) order as scan_kernel, so results are identical.
-constexpr int WQ = 4;      // queries (warps) per CTA
+constexpr int WQ = 2;      // queries (warps) per CTA
+constexpr int WQ_MINB = 12; // resident CTAs per SM the register budget is sized for
 constexpr int SUB = 4;     // 32-vector sub-chunks loaded together (memory-level parallelism)
 constexpr int RING = 256;  // survivor ring per warp (holds < 32 + 32 * SUB)
 
@@ -698,8 +700,8 @@ __device__ __forceinline__ void warp_offer(const Args& a, double& qd, int64_t& q
   warp_fold(qd, qi, d, id, pass, k);
 }
 
-template <bool REFINE, bool NIB, int IPB>
-__global__ void __launch_bounds__(WQ * 32) scan_warp_kernel(Args a) {
+template <bool REFINE, bool NIB, int IPB, int MINB>
+__global__ void __launch_bounds__(WQ * 32, MINB) scan_warp_kernel(Args a) {
   using IPT = typename std::conditional<IPB == 2, int16_t, int32_t>::type;
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -826,7 +828,13 @@ __global__ void __launch_bounds__(WQ * 32) scan_warp_kernel(Args a) {
           warp_offer(a, qd, qi, keep ? est2 : dinf(), keep ? (int)vi : -1, lo, k);
           continue;
         }
-        if (keep) r_v[(head + nb + __popc(kb & ((1u << lane) - 1u))) & (RING - 1)] = (int)vi;
+        if (keep) {
+          r_v[(head + nb + __popc(kb & ((1u << lane) - 1u))) & (RING - 1)] = (int)vi;
+          if (a.l2_prefetch) {  // the survivor's rcode row is read by a refine group a few batches later
+            const uint8_t* row = a.ix.rcodes + (lo + vi) * a.ix.rcode_bytes;
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(row), "r"((unsigned)a.ix.rcode_bytes));
+          }
+        }
         nb += __popc(kb);
       }
       if (REFINE) {
@@ -1784,7 +1792,10 @@ __global__ void merge_topk_kernel(const int64_t* __restrict__ ids, const double*
 template <bool REFINE, bool NIB>
 int launch_warp(const Args& a, int ipb, cudaStream_t s) {
   const size_t sm = warp_smem_bytes(a.kpad, REFINE);
-  auto kern = ipb == 2 ? scan_warp_kernel<REFINE, NIB, 2> : scan_warp_kernel<REFINE, NIB, 4>;
+  static const int minb = getenv("IVRQ_WARP_MINB") ? atoi(getenv("IVRQ_WARP_MINB")) : WQ_MINB;
+  auto kern = minb == 16  ? (ipb == 2 ? scan_warp_kernel<REFINE, NIB, 2, 16> : scan_warp_kernel<REFINE, NIB, 4, 16>)
+              : minb == 8 ? (ipb == 2 ? scan_warp_kernel<REFINE, NIB, 2, 8> : scan_warp_kernel<REFINE, NIB, 4, 8>)
+                          : (ipb == 2 ? scan_warp_kernel<REFINE, NIB, 2, WQ_MINB> : scan_warp_kernel<REFINE, NIB, 4, WQ_MINB>);
   if (sm > 48 * 1024 && cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess)
     return fail(IVRQ_EUNSUP, "ivrq_search_scan: shared memory request too large");
   kern<<<(unsigned)ceil_div(a.nq, WQ), WQ * 32, sm, s>>>(a);
@@ -1875,6 +1886,8 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
   a.out_counts = out_counts;
   a.stats = stats;
   const bool nib = rcode_nibbles(index->bits);
+  const char* pf_env = getenv("IVRQ_L2_PREFETCH");
+  a.l2_prefetch = pf_env ? atoi(pf_env) : 0;
   cudaStream_t s = as_stream(stream);
   retain_async_pool(s);
   // Schedule queries grouped by their first (lowest-id) probed list: that list
