@@ -32,6 +32,8 @@ int check_launch(const char* what);
 // per-call workspaces of the search do not re-map pages every call.
 void retain_async_pool(cudaStream_t s);
 int sm_count_of_current_device();
+// A non-blocking stream per device (and host thread) for intra-call fork/join.
+cudaStream_t side_stream();
 
 #define IVRQ_TRY(expr)              \
   do {                              \

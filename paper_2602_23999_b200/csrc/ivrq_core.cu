@@ -33,6 +33,16 @@ void retain_async_pool(cudaStream_t) {
   done_mask |= 1 << dev;
 }
 
+cudaStream_t side_stream() {
+  static thread_local cudaStream_t streams[32] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev >= 32) return nullptr;
+  if (!streams[dev] && cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking) != cudaSuccess) {
+    streams[dev] = nullptr;
+  }
+  return streams[dev];
+}
+
 int sm_count_of_current_device() {
   int dev = 0, v = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return 148;

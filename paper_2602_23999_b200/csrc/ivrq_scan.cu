@@ -14,6 +14,7 @@
 // reference's.  k <= 32 keeps per-warp top-32 queues in registers (bitonic
 // shuffle networks); larger k falls back to a block-wide bitonic sort.
 #include <cstdlib>
+#include <functional>
 #include <type_traits>
 
 #include "ivrq_common.cuh"
@@ -1964,7 +1965,9 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
       a.skip_first = 1;
     }
   }
-  // first lists refined list-major for the warp-per-query kernel
+  // first lists refined list-major for the warp-per-query kernel (launched
+  // below, concurrently with the stage-1 inner products on a side stream)
+  std::function<int()> fd_launch;
   int64_t *fbase = nullptr, *ftot = nullptr;
   int32_t* fgpre = nullptr;
   double* fdist = nullptr;
@@ -2007,8 +2010,10 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
       if (fsm > 48 * 1024 &&
           cudaFuncSetAttribute(fk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm) != cudaSuccess)
         return fail(IVRQ_EUNSUP, "ivrq_search_scan: dims too large for the first-list refine");
-      fk<<<(unsigned)(2 * sm_count_of_current_device()), scan::THREADS, fsm, s>>>(fa);
-      IVRQ_TRY(check_launch("ivrq_search_scan(first-list refine)"));
+      fd_launch = [fk, fa, fsm, s]() {
+        fk<<<(unsigned)(2 * sm_count_of_current_device()), scan::THREADS, fsm, s>>>(fa);
+        return check_launch("ivrq_search_scan(first-list refine)");
+      };
       a.fdist = fdist;
       a.fbase = fbase;
       a.qoff = off;
@@ -2058,7 +2063,6 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
       int8_t* qhat = nullptr;
       if (cudaMallocAsync(reinterpret_cast<void**>(&qhat), (size_t)nq * 32 * a.g, s) != cudaSuccess)
         return fail(IVRQ_ENOMEM, "ivrq_search_scan: workspace allocation failed");
-      scan::qhat_kernel<<<(unsigned)ceil_div(nq * a.g, 256), 256, 0, s>>>(planes, nq, a.g, a.qbits, qhat);
       scan::IpArgs ia{};
       ia.ix = *index;
       ia.qhat = qhat;
@@ -2075,14 +2079,37 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
       if (ism > 48 * 1024 &&
           cudaFuncSetAttribute(ik, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ism) != cudaSuccess)
         return fail(IVRQ_EUNSUP, "ivrq_search_scan: dims too large for the tensor-core stage 1");
-      ik<<<(unsigned)(2 * sm_count_of_current_device()), scan::THREADS, ism, s>>>(ia);
+      // fork: the stage-1 inner products on the side stream, the first-list
+      // refine on s; both only read the index and the prepared queries
+      cudaStream_t s2 = side_stream();
+      cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+      if (fd_launch && s2) {
+        cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming);
+        cudaEventRecord(ev_fork, s);
+        cudaStreamWaitEvent(s2, ev_fork, 0);
+      }
+      cudaStream_t si = (fd_launch && s2) ? s2 : s;
+      scan::qhat_kernel<<<(unsigned)ceil_div(nq * a.g, 256), 256, 0, si>>>(planes, nq, a.g, a.qbits, qhat);
+      ik<<<(unsigned)(2 * sm_count_of_current_device()), scan::THREADS, ism, si>>>(ia);
       IVRQ_TRY(check_launch("ivrq_search_scan(stage-1 tiles)"));
+      if (fd_launch) {
+        IVRQ_TRY(fd_launch());
+        fd_launch = nullptr;
+      }
+      if (ev_join) {
+        cudaEventRecord(ev_join, s2);
+        cudaStreamWaitEvent(s, ev_join, 0);
+        cudaEventDestroy(ev_fork);
+        cudaEventDestroy(ev_join);
+      }
       cudaFreeAsync(qhat, s);
     }
     a.ipbuf = ipbuf;
     a.pslot = pslot;
     a.pair_base = pbase;
   }
+  if (fd_launch) IVRQ_TRY(fd_launch());
   const int rc = params->ip_mode == IVRQ_IP_BITWISE
                      ? scan::launch_mode<IVRQ_IP_BITWISE>(a, refine, nib, warp_path ? -ipb : ipb, s)
                                                     : scan::launch_mode<IVRQ_IP_LUT>(a, refine, nib, 0, s);
