@@ -18,6 +18,7 @@
 #include <type_traits>
 
 #include "ivrq_common.cuh"
+#include "ivrq_tc.cuh"
 
 namespace ivrq {
 namespace scan {
@@ -70,6 +71,7 @@ struct Args {
   const int64_t* fbase;
   const int64_t* qoff;
   int l2_prefetch;  // warp kernel: L2 prefetch of survivor rcode rows
+  const double* rdist;  // refined distance of every probed (pair, vector) (tc_refine_kernel), or null
 };
 
 __device__ __forceinline__ double dinf() { return __longlong_as_double(0x7ff0000000000000LL); }
@@ -657,30 +659,31 @@ __device__ __forceinline__ void warp_refine32(const Args& a, const QueryCtx& qc,
   }
   const long long w0 = (t4 & 1) ? 128LL : 2097152LL;
   const long long w1 = (t4 & 1) ? 1LL : 16384LL;
-  // tile of this lane's candidate: lanes 0-15 <- tile a, 16-31 <- tile b
-  long long p0a = (long long)ca[0] * w0 + (long long)ca[1] * w1, p1a = (long long)ca[2] * w0 + (long long)ca[3] * w1;
-  long long p0b = (long long)cb[0] * w0 + (long long)cb[1] * w1, p1b = (long long)cb[2] * w0 + (long long)cb[3] * w1;
-  p0a += __shfl_xor_sync(FULL, p0a, 1);
-  p1a += __shfl_xor_sync(FULL, p1a, 1);
-  p0b += __shfl_xor_sync(FULL, p0b, 1);
-  p1b += __shfl_xor_sync(FULL, p1b, 1);
-  const long long l0a = __shfl_xor_sync(FULL, p0a, 2), l1a = __shfl_xor_sync(FULL, p1a, 2);
-  const long long l0b = __shfl_xor_sync(FULL, p0b, 2), l1b = __shfl_xor_sync(FULL, p1b, 2);
   const int L = lane & 15, src = (L & 7) * 4;  // lane t4 == 0 of group (L & 7) holds the sums
   const bool hi8 = L >= 8, tb = lane >= 16;
-  // each lane fetches its candidate's (hi, lo) halves from the owning group lane
-  // (the source lane supplies both row halves; the receiver picks)
-  const long long h0a = __shfl_sync(FULL, p0a, src), h1a = __shfl_sync(FULL, p1a, src);
-  const long long g0a = __shfl_sync(FULL, l0a, src), g1a = __shfl_sync(FULL, l1a, src);
-  const long long h0b = __shfl_sync(FULL, p0b, src), h1b = __shfl_sync(FULL, p1b, src);
-  const long long g0b = __shfl_sync(FULL, l0b, src), g1b = __shfl_sync(FULL, l1b, src);
-  const long long hA = hi8 ? h1a : h0a, lA = hi8 ? g1a : g0a;
-  const long long hB = hi8 ? h1b : h0b, lB = hi8 ? g1b : g0b;
+  // one tile at a time (register pressure): lanes 0-15 take tile a's rows, 16-31 tile b's
+  long long hsel = 0, lsel = 0;
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    const int* cc = t ? cb : ca;
+    long long p0 = (long long)cc[0] * w0 + (long long)cc[1] * w1;
+    long long p1 = (long long)cc[2] * w0 + (long long)cc[3] * w1;
+    p0 += __shfl_xor_sync(FULL, p0, 1);
+    p1 += __shfl_xor_sync(FULL, p1, 1);
+    const long long l0 = __shfl_xor_sync(FULL, p0, 2), l1 = __shfl_xor_sync(FULL, p1, 2);
+    // the source lane supplies both row halves; the receiver picks
+    const long long h0 = __shfl_sync(FULL, p0, src), h1 = __shfl_sync(FULL, p1, src);
+    const long long g0 = __shfl_sync(FULL, l0, src), g1 = __shfl_sync(FULL, l1, src);
+    if (tb == (t == 1)) {
+      hsel = hi8 ? h1 : h0;
+      lsel = hi8 ? g1 : g0;
+    }
+  }
   dist = dinf();
   vrow = -1;
   if (lane < m) {
     vrow = rv ? rv[(head + lane) & (RING - 1)] : head + lane;
-    const long long hi = tb ? hB : hA, lw = tb ? lB : lA;
+    const long long hi = hsel, lw = lsel;
     const double hi_s = ldexp(1.0, qc.sexp - 26), lo_s = ldexp(1.0, qc.sexp - 54);
     const double ip = dadd(dmul((double)hi, hi_s), dmul((double)lw, lo_s));
     const float2 lf = __ldg(reinterpret_cast<const float2*>(a.ix.long_factors) + lo + vrow);
@@ -858,6 +861,132 @@ __global__ void __launch_bounds__(WQ * 32, MINB) scan_warp_kernel(Args a) {
       warp_offer(a, qd, qi, d, vr, lo, k);
     }
     __syncwarp();
+    const int cnt = __popc(__ballot_sync(FULL, lane < k && qi != NO_ID));
+    if (cnt >= k) T = __shfl_sync(FULL, qd, k - 1);  // search.py:444-447
+  }
+  const int pn = __popc(__ballot_sync(FULL, lane < k && qi != NO_ID));
+  if (lane < k) {
+    a.out_ids[q * k + lane] = lane < pn ? qi : -1;
+    a.out_dists[q * k + lane] = lane < pn ? qd : dinf();
+  }
+  if (lane == 0) {
+    a.out_counts[q] = pn;
+    if (a.stats) {
+      a.stats[2 * q] = probed;
+      a.stats[2 * q + 1] = surv;
+    }
+  }
+}
+
+// ------------------------------------------------------------ per-query pass over precomputed distances
+// With the refined distance of every probed (pair, vector) in rdist
+// (tc_refine_kernel) and the stage-1 inner products in ipbuf, a query's pass
+// is a stream: per list in ascending id, the stage-1 estimate and prune
+// (same test as stage1_chunk), then its survivors' refined distances offered
+// to the warp's register queue (the pool).  No shared memory, few registers.
+constexpr int RDW = 4;    // queries (warps) per CTA
+constexpr int RSUB = 4;   // 32-vector sub-chunks per batch
+
+template <bool REFINE, int IPB>
+__global__ void __launch_bounds__(RDW * 32) scan_rd_kernel(Args a) {
+  using IPT = typename std::conditional<IPB == 2, int16_t, int32_t>::type;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t slot_q = (int64_t)blockIdx.x * RDW + wid;
+  if (slot_q >= a.nq) return;  // whole warps only
+  const int64_t q = a.qorder ? a.qorder[slot_q] : slot_q;
+  const int k = a.k;
+  const double* sc = a.scalars + q * IVRQ_QS_COUNT;
+  const double delta = sc[IVRQ_QS_DELTA], half_code = sc[IVRQ_QS_HALF_CODE], ipm = sc[IVRQ_QS_IP_MARGIN];
+  const int init_n = a.init_counts ? a.init_counts[q] : 0;
+  double qd = lane < init_n ? a.init_dists[q * k + lane] : dinf();
+  int64_t qi = lane < init_n ? a.init_ids[q * k + lane] : NO_ID;
+  double T = init_n >= k ? __shfl_sync(FULL, qd, k - 1) : dinf();
+  long long probed = 0, surv = 0;
+  const int64_t* pid_list = a.probe_ids + q * a.nprobe;
+  const double* pd2_list = a.probe_d2 + q * a.nprobe;
+  for (int p = 0; p < a.nprobe; ++p) {  // ascending cluster id (search.py:429)
+    const int64_t cg = pid_list[p];
+    if (cg < a.list_lo || cg >= a.list_hi) continue;
+    const int64_t c = cg - a.list_lo;
+    const int64_t lo = a.ix.offsets[c], n_c = a.ix.offsets[c + 1] - lo;
+    if (n_c == 0) continue;
+    const double d_qc2 = pd2_list[p];
+    const double T_list = a.prune ? T : dinf();
+    probed += n_c;
+    const int64_t rowbase = a.pair_base[c] + (int64_t)a.pslot[q * a.nprobe + p] * ip_row_stride(n_c);
+    const double* rrow = REFINE ? a.rdist + rowbase : nullptr;
+    if (REFINE && T_list == dinf()) {  // nothing can be pruned (lb2 <= +inf): every vector's refined distance
+      surv += n_c;
+      for (int64_t c0 = 0; c0 < n_c; c0 += 32) {
+        const int64_t vi = c0 + lane;
+        warp_offer(a, qd, qi, vi < n_c ? __ldg(rrow + vi) : dinf(), vi < n_c ? (int)vi : -1, lo, k);
+      }
+    } else {
+      const IPT* iprow = reinterpret_cast<const IPT*>(a.ipbuf) + rowbase;
+      const double sq = dsqrt(d_qc2);
+      for (int64_t c0 = 0; c0 < n_c; c0 += 32 * RSUB) {
+        int ipv[RSUB];
+        float fa[RSUB], fs[RSUB], fe[RSUB];
+#pragma unroll
+        for (int u = 0; u < RSUB; ++u) {
+          const int64_t vi = c0 + u * 32 + lane;
+          const bool in = vi < n_c;
+          ipv[u] = in ? (int)__ldg(iprow + vi) : 0;
+          fa[u] = in ? __ldg(a.ix.short_add + lo + vi) : 0.f;
+          fs[u] = in ? __ldg(a.ix.short_scale + lo + vi) : 0.f;
+          fe[u] = in ? __ldg(a.ix.short_err + lo + vi) : 0.f;
+        }
+        bool keep[RSUB];
+        double est[RSUB];
+#pragma unroll
+        for (int u = 0; u < RSUB; ++u) {
+          const int64_t vi = c0 + u * 32 + lane;
+          keep[u] = false;
+          est[u] = 0.0;
+          if (vi < n_c) {
+            const double ipb = dmul(delta, (double)ipv[u]);
+            const double scale = (double)fs[u];
+            const double est2 = dmax(dsub(dadd((double)fa[u], d_qc2), dmul(scale, dsub(ipb, half_code))), 0.0);
+            est[u] = est2;
+            bool kp;
+            if (est2 <= T_list) {
+              kp = true;  // lb2 <= est2 <= T
+            } else {
+              const double margin = dmul((double)fe[u], sq);
+              if (ipm != 0.0) {  // same decision as stage1_chunk
+                const double sm = dmul(scale, ipm);
+                const double S = dadd(dmul(margin, margin), dmul(sm, sm));
+                const double gap = dsub(est2, T_list);
+                const double g2 = dmul(gap, gap);
+                if (S >= g2 * (1.0 + 0x1p-38)) {
+                  kp = true;
+                } else if (S <= g2 * (1.0 - 0x1p-38) && gap > T_list * 0x1p-12) {
+                  kp = false;
+                } else {
+                  kp = dmax(dsub(est2, dsqrt(S)), 0.0) <= T_list;
+                }
+              } else {
+                kp = dmax(dsub(est2, margin), 0.0) <= T_list;
+              }
+            }
+            keep[u] = kp;
+          }
+        }
+        double dv[RSUB];
+#pragma unroll
+        for (int u = 0; u < RSUB; ++u) {  // survivors' refined distances, loads in flight together
+          const int64_t vi = c0 + u * 32 + lane;
+          dv[u] = keep[u] ? (REFINE ? __ldg(rrow + vi) : est[u]) : dinf();
+        }
+#pragma unroll
+        for (int u = 0; u < RSUB; ++u) {
+          const unsigned kb = __ballot_sync(FULL, keep[u]);
+          if (!kb) continue;
+          surv += __popc(kb);
+          warp_offer(a, qd, qi, dv[u], keep[u] ? (int)(c0 + u * 32 + lane) : -1, lo, k);
+        }
+      }
+    }
     const int cnt = __popc(__ballot_sync(FULL, lane < k && qi != NO_ID));
     if (cnt >= k) T = __shfl_sync(FULL, qd, k - 1);  // search.py:444-447
   }
@@ -1734,6 +1863,232 @@ __global__ void __launch_bounds__(THREADS, 2) first_dist_kernel(FdArgs a) {
   }
 }
 
+// ------------------------------------------------------------ refine of every probed pair on tcgen05
+// The refined distance (search.py:313-323) of every vector of every probed
+// (list, query) pair, list-major on the 5th-generation tensor cores: for a
+// list c and a group of G queries probing it, D[v][(j, s)] = <u_v, digit_s of
+// q_j> is one int8 GEMM (M = 128 vectors per TMEM tile, N = 8 G digit slices,
+// K = kpad) with the accumulator in TMEM.  Warp roles per CTA:
+//   warps 0-3  stage rcode tiles (128 rows x 128 B per stage) into a ring,
+//   warp 4     issues tcgen05.mma (one elected lane) and commits,
+//   warps 5-8  read the accumulator (tcgen05.ld), assemble each query's 8
+//              digit dots exactly in int64, round once to float64 and write
+//              the refined distance with refine_chunk's arithmetic.
+// The per-query pass (scan_warp_kernel) then only streams stage-1 inputs and
+// reads the refined distance of its survivors.
+constexpr int TCM = 128;     // vectors per tile = TMEM lanes
+constexpr int TCKC = 128;    // K bytes per A stage (4 MMAs of K = 32)
+constexpr int TCST = 4;      // A stages
+constexpr int TC_PROD = 4;  // producer warps
+constexpr int TC_THREADS = 32 * (TC_PROD + 1 + 4);
+
+struct TcArgs {
+  ivrq_index_view ix;
+  const int8_t* qslices;
+  int kpad, G, nib;
+  const double* scalars;
+  const double* probe_d2;
+  int nprobe, nlist;
+  const int64_t* porder;    // pair indices sorted by list
+  const int64_t* poff;      // [nlist + 2]
+  const int64_t* pair_base; // [nlist + 1]
+  const int32_t* gpre;      // [nlist + 1] prefix of ceil(bucket / G)
+  double* rdist;
+};
+
+__host__ __device__ inline uint32_t tmem_cols(int n) {  // power of two >= 32 (<= 512)
+  return n <= 32 ? 32u : n <= 64 ? 64u : n <= 128 ? 128u : n <= 256 ? 256u : 512u;
+}
+
+size_t tc_smem_bytes(int kpad, int G) {
+  return (size_t)8 * G * kpad + (size_t)TCST * TCM * TCKC + 64 * G + 256;
+}
+
+__global__ void __launch_bounds__(TC_THREADS, 1) tc_refine_kernel(TcArgs a) {
+  extern __shared__ __align__(1024) unsigned char tsm[];
+  const int G = a.G, N = 8 * G, kp = a.kpad;
+  int8_t* sB = reinterpret_cast<int8_t*>(tsm);                                  // [N rows x kpad], core-matrix layout
+  uint8_t* sA = reinterpret_cast<uint8_t*>(tsm + (size_t)N * kp);               // [TCST][128 x 128 B]
+  double* s_dq = reinterpret_cast<double*>(sA + TCST * TCM * TCKC);             // [G]
+  double* s_kb = s_dq + G;
+  double* s_hs = s_kb + G;
+  double* s_ls = s_hs + G;
+  int64_t* s_row = reinterpret_cast<int64_t*>(s_ls + G);                        // [G] rdist row of query j
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_row + G);                      // full[4] empty[4] accf[2] acce[2]
+  uint32_t* s_taddr = reinterpret_cast<uint32_t*>(bars + 2 * TCST + 4);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + TCST;
+  uint64_t* accf = bars + 2 * TCST;
+  uint64_t* acce = bars + 2 * TCST + 2;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid == 0) {
+    for (int i = 0; i < TCST; ++i) {
+      tc::mbar_init(&full[i], 32 * TC_PROD);
+      tc::mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&accf[i], 1);
+      tc::mbar_init(&acce[i], 128);
+    }
+    tc::fence_mbar_init();
+  }
+  if (wid == TC_PROD) tc::tmem_alloc(s_taddr, tmem_cols(2 * N));
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tbase = *s_taddr;
+  const int np = kp / TCKC;                 // stages per tile (kpad is a multiple of 64; TCKC 128 -> see kc loop)
+  const int nkc = (kp + TCKC - 1) / TCKC;   // K chunks per tile
+  (void)np;
+  const int64_t rb = a.ix.rcode_bytes;
+  const uint32_t idesc = tc::idesc_i8(TCM, N, false, true);
+  uint32_t it_prod = 0, it_mma = 0;  // stage counters (per role, identical sequences)
+  uint32_t tile_mma = 0, tile_epi = 0;
+  const int total = a.gpre[a.nlist];
+  for (int b = blockIdx.x; b < total; b += gridDim.x) {
+    int lo_c = 0, hi_c = a.nlist;
+    while (hi_c - lo_c > 1) {
+      const int mid = (lo_c + hi_c) >> 1;
+      if (a.gpre[mid] <= b) lo_c = mid; else hi_c = mid;
+    }
+    const int c = lo_c;
+    const int64_t lo = a.ix.offsets[c], n_c = a.ix.offsets[c + 1] - lo;
+    const int64_t ps = a.poff[c] + (int64_t)(b - a.gpre[c]) * G;
+    const int nqg = (int)min((int64_t)G, a.poff[c + 1] - ps);
+    const int64_t rs = ip_row_stride(n_c);
+    const int ntile = (int)ceil_div(n_c, TCM);
+    // ---- group operands: digit slices of the G queries (K order = rcode byte order)
+    __syncthreads();  // previous group's MMAs completed (epilogue waited on them) and its scalars consumed
+    for (int i = tid; i < N * (kp / 16); i += TC_THREADS) {
+      const int n = i / (kp / 16), P0 = 16 * (i % (kp / 16));
+      const int j = n >> 3, sl = n & 7;
+      uint4 v = make_uint4(0u, 0u, 0u, 0u);
+      if (j < nqg) {
+        const int64_t q = a.porder[ps + j] / a.nprobe;
+        const int p64 = P0 >> 6, t4 = (P0 >> 4) & 3;
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(a.qslices + (q * SLICES + sl) * (int64_t)kp + 64 * p64 + 4 * t4);
+        v = make_uint4(__ldg(src), __ldg(src + 4), __ldg(src + 8), __ldg(src + 12));  // h = 0..3 at +16 h bytes
+      }
+      *reinterpret_cast<uint4*>(sB + tc::kmajor_offset(n, P0, N)) = v;
+    }
+    if (tid < G) {
+      double dq = 0.0, kb = 0.0;
+      int e = 0;
+      int64_t row = 0;
+      if (tid < nqg) {
+        const int64_t pr = a.porder[ps + tid];
+        const int64_t q = pr / a.nprobe;
+        dq = a.probe_d2[pr];
+        kb = a.scalars[q * IVRQ_QS_COUNT + IVRQ_QS_KB_SUM];
+        e = (int)a.scalars[q * IVRQ_QS_COUNT + IVRQ_QS_SLICE_EXP];
+        row = a.pair_base[c] + (ps + tid - a.poff[c]) * rs;
+      }
+      s_dq[tid] = dq;
+      s_kb[tid] = kb;
+      s_hs[tid] = ldexp(1.0, e - 26);
+      s_ls[tid] = ldexp(1.0, e - 54);
+      s_row[tid] = row;
+    }
+    tc::fence_smem_async();
+    __syncthreads();
+    if (wid < TC_PROD) {
+      // ---- producers: rcode rows -> A ring (each warp a quarter of every stage)
+      const int pl = wid * 32 + lane;
+      const uint8_t* rows = a.ix.rcodes + lo * rb;
+      for (int t = 0; t < ntile; ++t) {
+        for (int kc = 0; kc < nkc; ++kc, ++it_prod) {
+          const int st = it_prod % TCST;
+          tc::mbar_wait(&empty[st], ((it_prod / TCST) & 1) ^ 1);
+          uint8_t* dst = sA + st * TCM * TCKC;
+          const int kb0 = kc * TCKC;
+          if (!a.nib) {
+            for (int i = pl; i < TCM * (TCKC / 16); i += 32 * TC_PROD) {
+              const int r = i / (TCKC / 16), pc = 16 * (i % (TCKC / 16));
+              const int64_t v = (int64_t)t * TCM + r;
+              const bool ok = v < n_c && kb0 + pc < kp;
+              cp_async16(dst + tc::kmajor_offset(r, pc, TCM), ok ? rows + v * rb + kb0 + pc : rows, ok);
+            }
+            asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(
+                             (uint32_t)__cvta_generic_to_shared(&full[st]))
+                         : "memory");
+          } else {
+            // two dims per byte: 8 bytes -> 16 elements [lo(0..3) hi(0..3) lo(4..7) hi(4..7)]
+            for (int i = pl; i < TCM * (TCKC / 16); i += 32 * TC_PROD) {
+              const int r = i / (TCKC / 16), pc = 16 * (i % (TCKC / 16));
+              const int64_t v = (int64_t)t * TCM + r;
+              uint4 o = make_uint4(0u, 0u, 0u, 0u);
+              if (v < n_c && kb0 + pc < kp) {
+                const uint2 x = __ldg(reinterpret_cast<const uint2*>(rows + v * rb + (kb0 + pc) / 2));
+                o = make_uint4(x.x & 0x0F0F0F0Fu, (x.x >> 4) & 0x0F0F0F0Fu, x.y & 0x0F0F0F0Fu, (x.y >> 4) & 0x0F0F0F0Fu);
+              }
+              *reinterpret_cast<uint4*>(dst + tc::kmajor_offset(r, pc, TCM)) = o;
+            }
+            tc::fence_smem_async();
+            tc::mbar_arrive(&full[st]);
+          }
+        }
+      }
+    } else if (wid == TC_PROD) {
+      // ---- MMA issuer
+      for (int t = 0; t < ntile; ++t, ++tile_mma) {
+        const int ab = tile_mma & 1;
+        tc::mbar_wait(&acce[ab], ((tile_mma >> 1) & 1) ^ 1);
+        tc::fence_after_sync();
+        for (int kc = 0; kc < nkc; ++kc, ++it_mma) {
+          const int st = it_mma % TCST;
+          tc::mbar_wait(&full[st], (it_mma / TCST) & 1);
+          tc::fence_after_sync();
+          if (lane == 0) {
+            const int ks = min(TCKC, kp - kc * TCKC) / 32;
+            for (int s = 0; s < ks; ++s) {
+              const uint64_t ad = tc::smem_desc(sA + st * TCM * TCKC + 2 * s * TCM * 16, TCM * 16, 128);
+              const int kk = kc * TCKC + 32 * s;
+              const uint64_t bd = tc::smem_desc(sB + (kk / 16) * N * 16, N * 16, 128);
+              tc::mma_i8(tbase + ab * N, ad, bd, idesc, kc > 0 || s > 0);
+            }
+            tc::commit(&empty[st]);
+            if (kc == nkc - 1) tc::commit(&accf[ab]);
+          }
+          __syncwarp();
+        }
+      }
+    } else {
+      // ---- epilogue: row r of the tile is TMEM lane r
+      const int quarter = wid & 3;
+      const int r = quarter * 32 + lane;
+      for (int t = 0; t < ntile; ++t, ++tile_epi) {
+        const int ab = tile_epi & 1;
+        tc::mbar_wait(&accf[ab], (tile_epi >> 1) & 1);
+        tc::fence_after_sync();
+        const int64_t v = (int64_t)t * TCM + r;
+        float2 lf = make_float2(0.f, 0.f);
+        if (v < n_c) lf = __ldg(reinterpret_cast<const float2*>(a.ix.long_factors) + lo + v);
+        for (int j0 = 0; j0 < G; j0 += 4) {
+          uint32_t d[32];
+          tc::tmem_ld32(tbase + ((uint32_t)(quarter * 32) << 16) + ab * N + 8 * j0, d);
+          tc::tmem_ld_wait();
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) {
+            const int j = j0 + jj;
+            if (j < nqg && v < n_c) {
+              const int* D = reinterpret_cast<const int*>(d + 8 * jj);
+              const long long hi = (long long)D[0] * 2097152LL + (long long)D[1] * 16384LL + (long long)D[2] * 128LL + D[3];
+              const long long lw = (long long)D[4] * 2097152LL + (long long)D[5] * 16384LL + (long long)D[6] * 128LL + D[7];
+              const double ip = dadd(dmul((double)hi, s_hs[j]), dmul((double)lw, s_ls[j]));
+              a.rdist[s_row[j] + v] = dmax(dsub(dadd((double)lf.x, s_dq[j]), dmul((double)lf.y, dsub(ip, s_kb[j]))), 0.0);
+            }
+          }
+        }
+        tc::fence_before_sync();
+        tc::mbar_arrive(&acce[ab]);
+      }
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (wid == TC_PROD) tc::tmem_dealloc(tbase, tmem_cols(2 * N));
+}
+
 // first probed list of each query inside this shard's id range (ids ascend per query)
 __global__ void first_probe_kernel(const int64_t* __restrict__ probe_ids, int64_t nq, int nprobe, int64_t list_lo,
                                    int64_t list_hi, int32_t* __restrict__ first) {
@@ -1788,6 +2143,13 @@ __global__ void merge_topk_kernel(const int64_t* __restrict__ ids, const double*
     out_dists[q * k + i] = dinf();
   }
   out_counts[q] = n;
+}
+
+inline int launch_rd(const Args& a, bool refine, int ipb, cudaStream_t s) {
+  auto kern = refine ? (ipb == 2 ? scan_rd_kernel<true, 2> : scan_rd_kernel<true, 4>)
+                     : (ipb == 2 ? scan_rd_kernel<false, 2> : scan_rd_kernel<false, 4>);
+  kern<<<(unsigned)ceil_div(a.nq, RDW), RDW * 32, 0, s>>>(a);
+  return check_launch("ivrq_search_scan");
 }
 
 template <bool REFINE, bool NIB>
@@ -1910,6 +2272,9 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
   // cores, then one warp per query (first lists included)
   const bool tc_path = params->ip_mode == IVRQ_IP_BITWISE && a.k <= 32 && (tc_env ? atoi(tc_env) != 0 : true) && nl >= 1;
   const bool warp_path = tc_path && (wenv ? atoi(wenv) != 0 : true);
+  // ... with every probed pair refined list-major on tcgen05 and a streaming per-query pass
+  const char* tr_env = getenv("IVRQ_TC_REFINE");
+  const bool rd_path = warp_path && (tr_env ? atoi(tr_env) != 0 : true) && (!refine || index->rcodes);
   const bool first_phase = grouped && refine && a.k <= 32 && !init_counts &&
                            (fl_env ? atoi(fl_env) != 0 : !warp_path);
   if (grouped && nq > 1 && nl >= 1) {
@@ -1972,7 +2337,7 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
   int32_t* fgpre = nullptr;
   double* fdist = nullptr;
   const char* fd_env = getenv("IVRQ_FIRST_DIST");
-  if (warp_path && refine && a.qorder && !init_counts && (fd_env ? atoi(fd_env) != 0 : true)) {
+  if (warp_path && !rd_path && refine && a.qorder && !init_counts && (fd_env ? atoi(fd_env) != 0 : true)) {
     if (cudaMallocAsync(reinterpret_cast<void**>(&fbase), (nl + 1) * sizeof(int64_t), s) != cudaSuccess ||
         cudaMallocAsync(reinterpret_cast<void**>(&fgpre), (nl + 1) * sizeof(int32_t), s) != cudaSuccess ||
         cudaMallocAsync(reinterpret_cast<void**>(&ftot), 2 * sizeof(int64_t), s) != cudaSuccess)
@@ -2021,6 +2386,9 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
   }
   // list-major stage-1 inner products on the int8 tensor cores (bitwise mode, k <= 32)
   int ipb = 0;
+  double* rdist = nullptr;
+  int32_t* rgpre = nullptr;
+  int64_t* rscratch = nullptr;
   int32_t *pkeys = nullptr, *pslot = nullptr, *tpre = nullptr;
   int64_t *pcnt = nullptr, *poff = nullptr, *porder = nullptr, *pbase = nullptr, *ptot = nullptr;
   void* ipbuf = nullptr;
@@ -2028,7 +2396,9 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
   if (tc_path) {
     ipb = ipmax <= 32768 ? 2 : 4;
     const int64_t npairs = nq * a.nprobe;
-    const int excl = warp_path ? (refine && !a.prune ? 2 : (refine && !init_counts ? 1 : 0)) : (a.skip_first ? 1 : 0);
+    const int excl = rd_path     ? 0
+                     : warp_path ? (refine && !a.prune ? 2 : (refine && !init_counts ? 1 : 0))
+                                 : (a.skip_first ? 1 : 0);
     if (cudaMallocAsync(reinterpret_cast<void**>(&pkeys), npairs * sizeof(int32_t), s) != cudaSuccess ||
         cudaMallocAsync(reinterpret_cast<void**>(&pslot), npairs * sizeof(int32_t), s) != cudaSuccess ||
         cudaMallocAsync(reinterpret_cast<void**>(&porder), npairs * sizeof(int64_t), s) != cudaSuccess ||
@@ -2051,7 +2421,7 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
     int64_t tot[2] = {0, 0};
     if (excl == 2) {
       tot[0] = 0;
-    } else if (index->max_list > 0) {
+    } else if (index->max_list > 0 && npairs * scan::ip_row_stride(index->max_list) <= (int64_t(1) << 28)) {
       tot[0] = npairs * scan::ip_row_stride(index->max_list);
     } else if (cudaMemcpyAsync(tot, ptot, sizeof(tot), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
                cudaStreamSynchronize(s) != cudaSuccess) {
@@ -2079,6 +2449,41 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
       if (ism > 48 * 1024 &&
           cudaFuncSetAttribute(ik, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ism) != cudaSuccess)
         return fail(IVRQ_EUNSUP, "ivrq_search_scan: dims too large for the tensor-core stage 1");
+      if (rd_path && refine) {
+        // refined distance of every probed pair on tcgen05 (concurrent with the inner products)
+        int G = 32;
+        while (G > 4 && ((size_t)8 * G * a.kpad > 100 * 1024)) G >>= 1;
+        if (cudaMallocAsync(reinterpret_cast<void**>(&rdist), (size_t)tot[0] * sizeof(double), s) != cudaSuccess ||
+            cudaMallocAsync(reinterpret_cast<void**>(&rgpre), (nl + 1) * sizeof(int32_t), s) != cudaSuccess ||
+            cudaMallocAsync(reinterpret_cast<void**>(&rscratch), (nl + 3) * sizeof(int64_t), s) != cudaSuccess)
+          return fail(IVRQ_ENOMEM, "ivrq_search_scan: refined-distance buffer allocation failed");
+        scan::pair_plan_kernel<<<1, 1024, 0, s>>>(index->offsets, poff, (int)nl, G, rscratch, rgpre, rscratch + nl + 1);
+        IVRQ_TRY(check_launch("ivrq_search_scan(refine plan)"));
+        scan::TcArgs ta{};
+        ta.ix = *index;
+        ta.qslices = qslices;
+        ta.kpad = a.kpad;
+        ta.G = G;
+        ta.nib = nib ? 1 : 0;
+        ta.scalars = scalars;
+        ta.probe_d2 = probe_d2;
+        ta.nprobe = a.nprobe;
+        ta.nlist = (int)nl;
+        ta.porder = porder;
+        ta.poff = poff;
+        ta.pair_base = pbase;
+        ta.gpre = rgpre;
+        ta.rdist = rdist;
+        const size_t tsm = scan::tc_smem_bytes(a.kpad, G);
+        if (cudaFuncSetAttribute(scan::tc_refine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm) !=
+            cudaSuccess)
+          return fail(IVRQ_EUNSUP, "ivrq_search_scan: dims too large for the tensor-core refine");
+        fd_launch = [ta, tsm, s]() {
+          scan::tc_refine_kernel<<<(unsigned)sm_count_of_current_device(), scan::TC_THREADS, tsm, s>>>(ta);
+          return check_launch("ivrq_search_scan(tensor-core refine)");
+        };
+        a.rdist = rdist;
+      }
       // fork: the stage-1 inner products on the side stream, the first-list
       // refine on s; both only read the index and the prepared queries
       cudaStream_t s2 = side_stream();
@@ -2111,8 +2516,14 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
   }
   if (fd_launch) IVRQ_TRY(fd_launch());
   const int rc = params->ip_mode == IVRQ_IP_BITWISE
-                     ? scan::launch_mode<IVRQ_IP_BITWISE>(a, refine, nib, warp_path ? -ipb : ipb, s)
+                     ? (rd_path && a.ipbuf ? scan::launch_rd(a, refine, ipb, s)
+                                           : scan::launch_mode<IVRQ_IP_BITWISE>(a, refine, nib, warp_path ? -ipb : ipb, s))
                                                     : scan::launch_mode<IVRQ_IP_LUT>(a, refine, nib, 0, s);
+  if (rdist) {
+    cudaFreeAsync(rdist, s);
+    cudaFreeAsync(rgpre, s);
+    cudaFreeAsync(rscratch, s);
+  }
   if (fbase) {
     cudaFreeAsync(fbase, s);
     cudaFreeAsync(fgpre, s);

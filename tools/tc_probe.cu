@@ -1,0 +1,107 @@
+// Stand-alone check of the tcgen05 kind::i8 primitives in ivrq_tc.cuh:
+// D[128 x N] = A[128 x K] (u8) * B[N x K]^T (s8), int32, against the CPU.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o /tmp/tcp tools/tc_probe.cu && /tmp/tcp
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "../paper_2602_23999_b200/csrc/ivrq_tc.cuh"
+
+using namespace ivrq;
+
+constexpr int M = 128;
+
+template <int N, int K>
+__global__ void __launch_bounds__(128) probe(const uint8_t* A, const int8_t* B, int* D) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  uint8_t* sa = sm;
+  int8_t* sb = reinterpret_cast<int8_t*>(sm + M * K);
+  __shared__ uint64_t bar;
+  __shared__ uint32_t taddr_s;
+  const int tid = threadIdx.x, wid = tid >> 5;
+  for (int i = tid; i < M * K; i += 128) sa[tc::kmajor_offset(i / K, i % K, M)] = A[i];
+  for (int i = tid; i < N * K; i += 128) sb[tc::kmajor_offset(i / K, i % K, N)] = B[i];
+  if (wid == 0) tc::tmem_alloc(&taddr_s, N < 32 ? 32 : N);
+  if (tid == 0) {
+    tc::mbar_init(&bar, 1);
+    tc::fence_mbar_init();
+  }
+  tc::fence_smem_async();
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t taddr = taddr_s;
+  if (tid == 0) {
+    constexpr uint32_t idesc = tc::idesc_i8(M, N, false, true);
+    for (int s = 0; s < K / 32; ++s) {
+      const uint64_t ad = tc::smem_desc(sa + 2 * s * M * 16, M * 16, 128);
+      const uint64_t bd = tc::smem_desc(sb + 2 * s * N * 16, N * 16, 128);
+      tc::mma_i8(taddr, ad, bd, idesc, s > 0);
+    }
+    tc::commit(&bar);
+  }
+  tc::mbar_wait(&bar, 0);
+  tc::fence_after_sync();
+  for (int c0 = 0; c0 < N; c0 += 32) {
+    uint32_t v[32];
+    tc::tmem_ld32(taddr + ((uint32_t)(wid * 32) << 16) + c0, v);
+    tc::tmem_ld_wait();
+    for (int j = 0; j < 32; ++j) D[(wid * 32 + (tid & 31)) * N + c0 + j] = (int)v[j];
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (wid == 0) tc::tmem_dealloc(taddr, N < 32 ? 32 : N);
+}
+
+template <int N, int K>
+int run() {
+  std::vector<uint8_t> A(M * K);
+  std::vector<int8_t> B(N * K);
+  srand(1);
+  for (auto& x : A) x = rand() & 255;
+  for (auto& x : B) x = (int8_t)(rand() & 255);
+  uint8_t* dA;
+  int8_t* dB;
+  int* dD;
+  cudaMalloc(&dA, A.size());
+  cudaMalloc(&dB, B.size());
+  cudaMalloc(&dD, M * N * 4);
+  cudaMemcpy(dA, A.data(), A.size(), cudaMemcpyHostToDevice);
+  cudaMemcpy(dB, B.data(), B.size(), cudaMemcpyHostToDevice);
+  cudaMemset(dD, 0, M * N * 4);
+  const int smem = M * K + N * K;
+  cudaFuncSetAttribute(probe<N, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  probe<N, K><<<1, 128, smem>>>(dA, dB, dD);
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    printf("N=%d K=%d: CUDA error %s\n", N, K, cudaGetErrorString(e));
+    return 1;
+  }
+  std::vector<int> D(M * N);
+  cudaMemcpy(D.data(), dD, D.size() * 4, cudaMemcpyDeviceToHost);
+  int bad = 0;
+  for (int i = 0; i < M; ++i)
+    for (int j = 0; j < N; ++j) {
+      long long s = 0;
+      for (int k = 0; k < K; ++k) s += (long long)A[i * K + k] * B[j * K + k];
+      if (s != D[i * N + j]) {
+        if (bad < 5) printf("  mismatch (%d,%d): gpu %d cpu %lld\n", i, j, D[i * N + j], s);
+        ++bad;
+      }
+    }
+  printf("N=%d K=%d: %d mismatches of %d\n", N, K, bad, M * N);
+  cudaFree(dA);
+  cudaFree(dB);
+  cudaFree(dD);
+  return bad != 0;
+}
+
+int main() {
+  int rc = 0;
+  rc |= run<32, 64>();
+  rc |= run<128, 256>();
+  rc |= run<256, 128>();
+  return rc;
+}
