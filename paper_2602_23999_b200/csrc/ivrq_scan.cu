@@ -1878,13 +1878,14 @@ __global__ void __launch_bounds__(THREADS, 2) first_dist_kernel(FdArgs a) {
 // reads the refined distance of its survivors.
 constexpr int TCM = 128;     // vectors per tile = TMEM lanes
 constexpr int TCKC = 128;    // K bytes per A stage (4 MMAs of K = 32)
-constexpr int TCST = 4;      // A stages
+constexpr int TCST = 6;      // A stages
 constexpr int TC_PROD = 4;  // producer warps
 constexpr int TC_THREADS = 32 * (TC_PROD + 1 + 4);
 
 struct TcArgs {
+  CUtensorMap map_a;        // rcodes [N rows x rcode_bytes] (8-bit codes), box 128 B x 128 rows, 128B swizzle
+  CUtensorMap map_b;        // tc-ordered slices [nq * 8 rows x kpad], box 128 B x 8 rows
   ivrq_index_view ix;
-  const int8_t* qslices;
   int kpad, G, nib;
   const double* scalars;
   const double* probe_d2;
@@ -1896,40 +1897,63 @@ struct TcArgs {
   double* rdist;
 };
 
+// digit slices in rcode byte order: out[q][s][P] = qslices[q][s][perm(P)] with
+// perm(64p + 16t + 4h + j) = 64p + 16h + 4t + j (the mma.sync fragment order transposed)
+__global__ void tc_slices_kernel(const int8_t* __restrict__ qslices, int64_t nq, int kp, int8_t* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // one 16-byte chunk
+  const int64_t nchunk = nq * SLICES * (kp / 16);
+  if (i >= nchunk) return;
+  const int64_t row = i / (kp / 16);
+  const int P0 = 16 * (int)(i % (kp / 16));
+  const int p64 = P0 >> 6, t4 = (P0 >> 4) & 3;
+  const uint32_t* src = reinterpret_cast<const uint32_t*>(qslices + row * kp + 64 * p64 + 4 * t4);
+  *reinterpret_cast<uint4*>(out + row * kp + P0) = make_uint4(src[0], src[4], src[8], src[12]);
+}
+
 __host__ __device__ inline uint32_t tmem_cols(int n) {  // power of two >= 32 (<= 512)
   return n <= 32 ? 32u : n <= 64 ? 64u : n <= 128 ? 128u : n <= 256 ? 256u : 512u;
 }
 
 size_t tc_smem_bytes(int kpad, int G) {
-  return (size_t)8 * G * kpad + (size_t)TCST * TCM * TCKC + 64 * G + 256;
+  const int nkc = (kpad + TCKC - 1) / TCKC;
+  return 1024 + (size_t)nkc * 8 * G * TCKC + (size_t)TCST * TCM * TCKC + 64 * G + 256;
 }
 
-__global__ void __launch_bounds__(TC_THREADS, 1) tc_refine_kernel(TcArgs a) {
-  extern __shared__ __align__(1024) unsigned char tsm[];
+// byte offset of (row R, byte k < 128) in a 128B-swizzled K-major tile (8-row atoms of 1024 B)
+__device__ __forceinline__ uint32_t sw128_offset(int R, int k) {
+  return (uint32_t)((R >> 3) * 1024 + (R & 7) * 128 + ((((k >> 4) ^ (R & 7)) & 7) << 4) + (k & 15));
+}
+
+__global__ void __launch_bounds__(TC_THREADS, 1) tc_refine_kernel(const __grid_constant__ TcArgs a) {
+  extern __shared__ __align__(1024) unsigned char tsm_raw[];
+  unsigned char* tsm = reinterpret_cast<unsigned char*>(((uintptr_t)tsm_raw + 1023) & ~(uintptr_t)1023);
   const int G = a.G, N = 8 * G, kp = a.kpad;
-  int8_t* sB = reinterpret_cast<int8_t*>(tsm);                                  // [N rows x kpad], core-matrix layout
-  uint8_t* sA = reinterpret_cast<uint8_t*>(tsm + (size_t)N * kp);               // [TCST][128 x 128 B]
-  double* s_dq = reinterpret_cast<double*>(sA + TCST * TCM * TCKC);             // [G]
+  const int nkc = (kp + TCKC - 1) / TCKC;  // 128-byte K chunks
+  int8_t* sB = reinterpret_cast<int8_t*>(tsm);                                   // [nkc][N rows x 128 B] swizzled
+  uint8_t* sA = reinterpret_cast<uint8_t*>(tsm + (size_t)nkc * N * TCKC);        // [TCST][128 rows x 128 B] swizzled
+  double* s_dq = reinterpret_cast<double*>(sA + TCST * TCM * TCKC);              // [G]
   double* s_kb = s_dq + G;
   double* s_hs = s_kb + G;
   double* s_ls = s_hs + G;
-  int64_t* s_row = reinterpret_cast<int64_t*>(s_ls + G);                        // [G] rdist row of query j
-  uint64_t* bars = reinterpret_cast<uint64_t*>(s_row + G);                      // full[4] empty[4] accf[2] acce[2]
-  uint32_t* s_taddr = reinterpret_cast<uint32_t*>(bars + 2 * TCST + 4);
-  uint64_t* full = bars;
-  uint64_t* empty = bars + TCST;
-  uint64_t* accf = bars + 2 * TCST;
-  uint64_t* acce = bars + 2 * TCST + 2;
+  int64_t* s_row = reinterpret_cast<int64_t*>(s_ls + G);                         // [G] rdist row of query j
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_row + G);
+  uint64_t* full = bars;                      // [TCST]
+  uint64_t* empty = bars + TCST;              // [TCST]
+  uint64_t* accf = bars + 2 * TCST;           // [2]
+  uint64_t* acce = bars + 2 * TCST + 2;       // [2]
+  uint64_t* bfull = bars + 2 * TCST + 4;      // [1]
+  uint32_t* s_taddr = reinterpret_cast<uint32_t*>(bars + 2 * TCST + 5);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   if (tid == 0) {
     for (int i = 0; i < TCST; ++i) {
-      tc::mbar_init(&full[i], 32 * TC_PROD);
+      tc::mbar_init(&full[i], a.nib ? 32 * TC_PROD : 1);
       tc::mbar_init(&empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       tc::mbar_init(&accf[i], 1);
       tc::mbar_init(&acce[i], 128);
     }
+    tc::mbar_init(bfull, 1);
     tc::fence_mbar_init();
   }
   if (wid == TC_PROD) tc::tmem_alloc(s_taddr, tmem_cols(2 * N));
@@ -1937,15 +1961,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_refine_kernel(TcArgs a) {
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tbase = *s_taddr;
-  const int np = kp / TCKC;                 // stages per tile (kpad is a multiple of 64; TCKC 128 -> see kc loop)
-  const int nkc = (kp + TCKC - 1) / TCKC;   // K chunks per tile
-  (void)np;
   const int64_t rb = a.ix.rcode_bytes;
   const uint32_t idesc = tc::idesc_i8(TCM, N, false, true);
-  uint32_t it_prod = 0, it_mma = 0;  // stage counters (per role, identical sequences)
-  uint32_t tile_mma = 0, tile_epi = 0;
+  uint32_t it_prod = 0, it_mma = 0, tile_mma = 0, tile_epi = 0, grp = 0;
   const int total = a.gpre[a.nlist];
-  for (int b = blockIdx.x; b < total; b += gridDim.x) {
+  for (int b = blockIdx.x; b < total; b += gridDim.x, ++grp) {
     int lo_c = 0, hi_c = a.nlist;
     while (hi_c - lo_c > 1) {
       const int mid = (lo_c + hi_c) >> 1;
@@ -1957,19 +1977,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_refine_kernel(TcArgs a) {
     const int nqg = (int)min((int64_t)G, a.poff[c + 1] - ps);
     const int64_t rs = ip_row_stride(n_c);
     const int ntile = (int)ceil_div(n_c, TCM);
-    // ---- group operands: digit slices of the G queries (K order = rcode byte order)
-    __syncthreads();  // previous group's MMAs completed (epilogue waited on them) and its scalars consumed
-    for (int i = tid; i < N * (kp / 16); i += TC_THREADS) {
-      const int n = i / (kp / 16), P0 = 16 * (i % (kp / 16));
-      const int j = n >> 3, sl = n & 7;
-      uint4 v = make_uint4(0u, 0u, 0u, 0u);
-      if (j < nqg) {
-        const int64_t q = a.porder[ps + j] / a.nprobe;
-        const int p64 = P0 >> 6, t4 = (P0 >> 4) & 3;
-        const uint32_t* src = reinterpret_cast<const uint32_t*>(a.qslices + (q * SLICES + sl) * (int64_t)kp + 64 * p64 + 4 * t4);
-        v = make_uint4(__ldg(src), __ldg(src + 4), __ldg(src + 8), __ldg(src + 12));  // h = 0..3 at +16 h bytes
+    __syncthreads();  // previous group's MMAs completed (its epilogue waited on them), scalars consumed
+    if (tid == 0) {   // group operand: the G queries' digit slices, 8 rows per query, by TMA
+      tc::mbar_expect_tx(bfull, (uint32_t)(nqg * nkc * 8 * TCKC));
+      for (int j = 0; j < nqg; ++j) {
+        const int q8 = (int)((a.porder[ps + j] / a.nprobe) * SLICES);
+        for (int kc = 0; kc < nkc; ++kc) tc::tma_load_2d(sB + kc * N * TCKC + j * 8 * TCKC, &a.map_b, kc * TCKC, q8, bfull);
       }
-      *reinterpret_cast<uint4*>(sB + tc::kmajor_offset(n, P0, N)) = v;
     }
     if (tid < G) {
       double dq = 0.0, kb = 0.0;
@@ -1989,30 +2003,29 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_refine_kernel(TcArgs a) {
       s_ls[tid] = ldexp(1.0, e - 54);
       s_row[tid] = row;
     }
-    tc::fence_smem_async();
     __syncthreads();
     if (wid < TC_PROD) {
-      // ---- producers: rcode rows -> A ring (each warp a quarter of every stage)
-      const int pl = wid * 32 + lane;
-      const uint8_t* rows = a.ix.rcodes + lo * rb;
-      for (int t = 0; t < ntile; ++t) {
-        for (int kc = 0; kc < nkc; ++kc, ++it_prod) {
-          const int st = it_prod % TCST;
-          tc::mbar_wait(&empty[st], ((it_prod / TCST) & 1) ^ 1);
-          uint8_t* dst = sA + st * TCM * TCKC;
-          const int kb0 = kc * TCKC;
-          if (!a.nib) {
-            for (int i = pl; i < TCM * (TCKC / 16); i += 32 * TC_PROD) {
-              const int r = i / (TCKC / 16), pc = 16 * (i % (TCKC / 16));
-              const int64_t v = (int64_t)t * TCM + r;
-              const bool ok = v < n_c && kb0 + pc < kp;
-              cp_async16(dst + tc::kmajor_offset(r, pc, TCM), ok ? rows + v * rb + kb0 + pc : rows, ok);
+      // ---- producers: rcode tiles -> A ring
+      if (!a.nib) {
+        if (tid == 0) {
+          for (int t = 0; t < ntile; ++t)
+            for (int kc = 0; kc < nkc; ++kc, ++it_prod) {
+              const int st = it_prod % TCST;
+              tc::mbar_wait(&empty[st], ((it_prod / TCST) & 1) ^ 1);
+              tc::mbar_expect_tx(&full[st], TCM * TCKC);
+              tc::tma_load_2d(sA + st * TCM * TCKC, &a.map_a, kc * TCKC, (int)(lo + (int64_t)t * TCM), &full[st]);
             }
-            asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(
-                             (uint32_t)__cvta_generic_to_shared(&full[st]))
-                         : "memory");
-          } else {
-            // two dims per byte: 8 bytes -> 16 elements [lo(0..3) hi(0..3) lo(4..7) hi(4..7)]
+        }
+      } else {
+        // two dims per byte: 8 bytes -> 16 elements [lo(0..3) hi(0..3) lo(4..7) hi(4..7)], swizzled stores
+        const int pl = wid * 32 + lane;
+        const uint8_t* rows = a.ix.rcodes + lo * rb;
+        for (int t = 0; t < ntile; ++t)
+          for (int kc = 0; kc < nkc; ++kc, ++it_prod) {
+            const int st = it_prod % TCST;
+            tc::mbar_wait(&empty[st], ((it_prod / TCST) & 1) ^ 1);
+            uint8_t* dst = sA + st * TCM * TCKC;
+            const int kb0 = kc * TCKC;
             for (int i = pl; i < TCM * (TCKC / 16); i += 32 * TC_PROD) {
               const int r = i / (TCKC / 16), pc = 16 * (i % (TCKC / 16));
               const int64_t v = (int64_t)t * TCM + r;
@@ -2021,15 +2034,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_refine_kernel(TcArgs a) {
                 const uint2 x = __ldg(reinterpret_cast<const uint2*>(rows + v * rb + (kb0 + pc) / 2));
                 o = make_uint4(x.x & 0x0F0F0F0Fu, (x.x >> 4) & 0x0F0F0F0Fu, x.y & 0x0F0F0F0Fu, (x.y >> 4) & 0x0F0F0F0Fu);
               }
-              *reinterpret_cast<uint4*>(dst + tc::kmajor_offset(r, pc, TCM)) = o;
+              *reinterpret_cast<uint4*>(dst + sw128_offset(r, pc)) = o;
             }
             tc::fence_smem_async();
             tc::mbar_arrive(&full[st]);
           }
-        }
       }
     } else if (wid == TC_PROD) {
       // ---- MMA issuer
+      tc::mbar_wait(bfull, grp & 1);
       for (int t = 0; t < ntile; ++t, ++tile_mma) {
         const int ab = tile_mma & 1;
         tc::mbar_wait(&acce[ab], ((tile_mma >> 1) & 1) ^ 1);
@@ -2040,11 +2053,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_refine_kernel(TcArgs a) {
           tc::fence_after_sync();
           if (lane == 0) {
             const int ks = min(TCKC, kp - kc * TCKC) / 32;
-            for (int s = 0; s < ks; ++s) {
-              const uint64_t ad = tc::smem_desc(sA + st * TCM * TCKC + 2 * s * TCM * 16, TCM * 16, 128);
-              const int kk = kc * TCKC + 32 * s;
-              const uint64_t bd = tc::smem_desc(sB + (kk / 16) * N * 16, N * 16, 128);
-              tc::mma_i8(tbase + ab * N, ad, bd, idesc, kc > 0 || s > 0);
+            for (int s2 = 0; s2 < ks; ++s2) {
+              const uint64_t ad = tc::smem_desc_sw128(sA + st * TCM * TCKC + 32 * s2);
+              const uint64_t bd = tc::smem_desc_sw128(sB + kc * N * TCKC + 32 * s2);
+              tc::mma_i8(tbase + ab * N, ad, bd, idesc, kc > 0 || s2 > 0);
             }
             tc::commit(&empty[st]);
             if (kc == nkc - 1) tc::commit(&accf[ab]);
@@ -2058,11 +2070,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_refine_kernel(TcArgs a) {
       const int r = quarter * 32 + lane;
       for (int t = 0; t < ntile; ++t, ++tile_epi) {
         const int ab = tile_epi & 1;
-        tc::mbar_wait(&accf[ab], (tile_epi >> 1) & 1);
-        tc::fence_after_sync();
         const int64_t v = (int64_t)t * TCM + r;
         float2 lf = make_float2(0.f, 0.f);
         if (v < n_c) lf = __ldg(reinterpret_cast<const float2*>(a.ix.long_factors) + lo + v);
+        tc::mbar_wait(&accf[ab], (tile_epi >> 1) & 1);
+        tc::fence_after_sync();
         for (int j0 = 0; j0 < G; j0 += 4) {
           uint32_t d[32];
           tc::tmem_ld32(tbase + ((uint32_t)(quarter * 32) << 16) + ab * N + 8 * j0, d);
@@ -2387,6 +2399,7 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
   // list-major stage-1 inner products on the int8 tensor cores (bitwise mode, k <= 32)
   int ipb = 0;
   double* rdist = nullptr;
+  int8_t* tcsl = nullptr;
   int32_t* rgpre = nullptr;
   int64_t* rscratch = nullptr;
   int32_t *pkeys = nullptr, *pslot = nullptr, *tpre = nullptr;
@@ -2459,9 +2472,19 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
           return fail(IVRQ_ENOMEM, "ivrq_search_scan: refined-distance buffer allocation failed");
         scan::pair_plan_kernel<<<1, 1024, 0, s>>>(index->offsets, poff, (int)nl, G, rscratch, rgpre, rscratch + nl + 1);
         IVRQ_TRY(check_launch("ivrq_search_scan(refine plan)"));
+        if (cudaMallocAsync(reinterpret_cast<void**>(&tcsl), (size_t)nq * scan::SLICES * a.kpad, s) != cudaSuccess)
+          return fail(IVRQ_ENOMEM, "ivrq_search_scan: workspace allocation failed");
+        scan::tc_slices_kernel<<<(unsigned)ceil_div(nq * scan::SLICES * (a.kpad / 16), 256), 256, 0, s>>>(
+            qslices, nq, a.kpad, tcsl);
         scan::TcArgs ta{};
+        // A: the rcode rows (8-bit codes; 4-bit indexes are unpacked by the producer warps instead)
+        if ((!nib && !tc::make_tmap_u8_sw128(&ta.map_a, index->rcodes, (uint64_t)index->rcode_bytes,
+                                             (uint64_t)index->size, (uint64_t)index->rcode_bytes, scan::TCKC,
+                                             scan::TCM)) ||
+            !tc::make_tmap_u8_sw128(&ta.map_b, tcsl, (uint64_t)a.kpad, (uint64_t)nq * scan::SLICES, (uint64_t)a.kpad,
+                                    scan::TCKC, 8))
+          return fail(IVRQ_ECUDA, "ivrq_search_scan: TMA tensor map encoding failed");
         ta.ix = *index;
-        ta.qslices = qslices;
         ta.kpad = a.kpad;
         ta.G = G;
         ta.nib = nib ? 1 : 0;
@@ -2519,6 +2542,7 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
                      ? (rd_path && a.ipbuf ? scan::launch_rd(a, refine, ipb, s)
                                            : scan::launch_mode<IVRQ_IP_BITWISE>(a, refine, nib, warp_path ? -ipb : ipb, s))
                                                     : scan::launch_mode<IVRQ_IP_LUT>(a, refine, nib, 0, s);
+  if (tcsl) cudaFreeAsync(tcsl, s);
   if (rdist) {
     cudaFreeAsync(rdist, s);
     cudaFreeAsync(rgpre, s);

@@ -10,6 +10,7 @@
 // (two chunks); the descriptor for K step s starts at base + 2 s LBO.
 #pragma once
 
+#include <cuda.h>
 #include <stdint.h>
 
 namespace ivrq {
@@ -29,6 +30,20 @@ __device__ __forceinline__ uint64_t smem_desc(const void* smem_ptr, uint32_t lbo
   d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFF) << 32;
   d |= (uint64_t)1 << 46;  // version
   // base offset 0, lbo mode 0, layout type 0 (SWIZZLE_NONE)
+  return d;
+}
+
+// descriptor of a K-major tile written by TMA with 128-byte swizzle: rows of
+// 128 bytes, 8-row atoms of 1024 bytes (1024-byte aligned).  K steps inside
+// the 128-byte row advance the start address by the step's byte offset.
+__device__ __forceinline__ uint64_t smem_desc_sw128(const void* smem_ptr) {
+  const uint32_t addr = (uint32_t)__cvta_generic_to_shared(smem_ptr);
+  uint64_t d = 0;
+  d |= (uint64_t)((addr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;                     // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;           // SBO: 8-row atom stride
+  d |= (uint64_t)1 << 46;                     // version
+  d |= (uint64_t)2 << 61;                     // SWIZZLE_128B
   return d;
 }
 
@@ -81,6 +96,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t parity) {
       : "memory");
 }
 
+// arrive on the mbarrier and add `bytes` to its expected transaction count
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* mbar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(mbar)),
+               "r"(bytes)
+               : "memory");
+}
+
+// 2-D TMA tile load (box of the tensor map at element coords (x inner, y outer)) completing on mbar
+__device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* map, int x, int y, uint64_t* mbar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          (uint32_t)__cvta_generic_to_shared(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"((uint32_t)__cvta_generic_to_shared(mbar))
+      : "memory");
+}
+
 __device__ __forceinline__ void fence_before_sync() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_after_sync() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 // generic-proxy shared-memory writes -> visible to the tensor core (async proxy)
@@ -114,5 +146,15 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
 
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
+}  // namespace tc
+}  // namespace ivrq
+
+namespace ivrq {
+namespace tc {
+// Host: 2-D uint8 tensor map (inner extent `inner` bytes, `outer` rows of
+// `row_stride` bytes) with a box of box_inner x box_outer and 128-byte swizzle.
+// Returns false if the driver entry point is unavailable or encoding fails.
+bool make_tmap_u8_sw128(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t row_stride,
+                        uint32_t box_inner, uint32_t box_outer);
 }  // namespace tc
 }  // namespace ivrq

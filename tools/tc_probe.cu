@@ -7,7 +7,28 @@
 #include <cstdlib>
 #include <vector>
 
+#include <cudaTypedefs.h>
+
 #include "../paper_2602_23999_b200/csrc/ivrq_tc.cuh"
+
+namespace ivrq {
+namespace tc {
+bool make_tmap_u8_sw128(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t row_stride,
+                        uint32_t box_inner, uint32_t box_outer) {
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn) return false;
+  auto encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  const cuuint64_t dims[2] = {inner, outer};
+  const cuuint64_t strides[1] = {row_stride};
+  const cuuint32_t box[2] = {box_inner, box_outer};
+  const cuuint32_t estr[2] = {1, 1};
+  return encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+}  // namespace tc
+}  // namespace ivrq
 
 using namespace ivrq;
 
@@ -53,6 +74,103 @@ __global__ void __launch_bounds__(128) probe(const uint8_t* A, const int8_t* B, 
   tc::fence_before_sync();
   __syncthreads();
   if (wid == 0) tc::tmem_dealloc(taddr, N < 32 ? 32 : N);
+}
+
+// TMA (128B swizzle) + SW128 descriptors: A [128 x K] u8, B [N x K] s8 row-major in global
+template <int N, int K>
+__global__ void __launch_bounds__(128) probe_tma(const __grid_constant__ CUtensorMap ma,
+                                                  const __grid_constant__ CUtensorMap mb, int* D) {
+  extern __shared__ __align__(1024) unsigned char sm_raw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>(((uintptr_t)sm_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sa = sm;                                        // [K/128][128 rows x 128 B]
+  int8_t* sb = reinterpret_cast<int8_t*>(sm + (K / 128) * M * 128);  // [K/128][N rows x 128 B]
+  __shared__ uint64_t bar, mbar;
+  __shared__ uint32_t taddr_s;
+  const int tid = threadIdx.x, wid = tid >> 5;
+  if (wid == 0) tc::tmem_alloc(&taddr_s, N < 32 ? 32 : N);
+  if (tid == 0) {
+    tc::mbar_init(&bar, 1);
+    tc::mbar_init(&mbar, 1);
+    tc::fence_mbar_init();
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  if (tid == 0) {
+    tc::mbar_expect_tx(&bar, (K / 128) * (M + N) * 128);
+    for (int c = 0; c < K / 128; ++c) {
+      tc::tma_load_2d(sa + c * M * 128, &ma, c * 128, 0, &bar);
+      for (int r0 = 0; r0 < N; r0 += 128) tc::tma_load_2d(sb + c * N * 128 + r0 * 128, &mb, c * 128, r0, &bar);
+    }
+  }
+  tc::mbar_wait(&bar, 0);
+  tc::fence_after_sync();
+  const uint32_t taddr = taddr_s;
+  if (tid == 0) {
+    constexpr uint32_t idesc = tc::idesc_i8(M, N, false, true);
+    for (int s = 0; s < K / 32; ++s) {
+      const int c = s / 4, off = (s % 4) * 32;
+      const uint64_t ad = tc::smem_desc_sw128(sa + c * M * 128 + off);
+      const uint64_t bd = tc::smem_desc_sw128(sb + c * N * 128 + off);
+      tc::mma_i8(taddr, ad, bd, idesc, s > 0);
+    }
+    tc::commit(&mbar);
+  }
+  tc::mbar_wait(&mbar, 0);
+  tc::fence_after_sync();
+  for (int c0 = 0; c0 < N; c0 += 32) {
+    uint32_t v[32];
+    tc::tmem_ld32(taddr + ((uint32_t)(wid * 32) << 16) + c0, v);
+    tc::tmem_ld_wait();
+    for (int j = 0; j < 32; ++j) D[(wid * 32 + (tid & 31)) * N + c0 + j] = (int)v[j];
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (wid == 0) tc::tmem_dealloc(taddr, N < 32 ? 32 : N);
+}
+
+template <int N, int K>
+int run_tma() {
+  std::vector<uint8_t> A(M * K);
+  std::vector<int8_t> B(N * K);
+  srand(7);
+  for (auto& x : A) x = rand() & 255;
+  for (auto& x : B) x = (int8_t)(rand() & 255);
+  uint8_t* dA;
+  int8_t* dB;
+  int* dD;
+  cudaMalloc(&dA, A.size());
+  cudaMalloc(&dB, B.size());
+  cudaMalloc(&dD, M * N * 4);
+  cudaMemcpy(dA, A.data(), A.size(), cudaMemcpyHostToDevice);
+  cudaMemcpy(dB, B.data(), B.size(), cudaMemcpyHostToDevice);
+  CUtensorMap ma, mb;
+  if (!tc::make_tmap_u8_sw128(&ma, dA, K, M, K, 128, 128) || !tc::make_tmap_u8_sw128(&mb, dB, K, N, K, 128, N < 128 ? N : 128)) {
+    printf("tensor map encode failed\n");
+    return 1;
+  }
+  const int smem = (K / 128) * (M + N) * 128 + 1024;
+  cudaFuncSetAttribute(probe_tma<N, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  probe_tma<N, K><<<1, 128, smem>>>(ma, mb, dD);
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    printf("TMA N=%d K=%d: CUDA error %s\n", N, K, cudaGetErrorString(e));
+    return 1;
+  }
+  std::vector<int> D(M * N);
+  cudaMemcpy(D.data(), dD, D.size() * 4, cudaMemcpyDeviceToHost);
+  int bad = 0;
+  for (int i = 0; i < M; ++i)
+    for (int j = 0; j < N; ++j) {
+      long long s = 0;
+      for (int k = 0; k < K; ++k) s += (long long)A[i * K + k] * B[j * K + k];
+      if (s != D[i * N + j]) {
+        if (bad < 5) printf("  mismatch (%d,%d): gpu %d cpu %lld\n", i, j, D[i * N + j], s);
+        ++bad;
+      }
+    }
+  printf("TMA/SW128 N=%d K=%d: %d mismatches of %d\n", N, K, bad, M * N);
+  return bad != 0;
 }
 
 template <int N, int K>
@@ -103,5 +221,8 @@ int main() {
   rc |= run<32, 64>();
   rc |= run<128, 256>();
   rc |= run<256, 128>();
+  rc |= run_tma<128, 256>();
+  rc |= run_tma<64, 384>();
+  rc |= run_tma<256, 128>();
   return rc;
 }
