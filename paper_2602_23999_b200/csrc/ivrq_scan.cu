@@ -72,6 +72,7 @@ struct Args {
   const int64_t* qoff;
   int l2_prefetch;  // warp kernel: L2 prefetch of survivor rcode rows
   const double* rdist;  // refined distance of every probed (pair, vector) (tc_refine_kernel), or null
+  int rd_prefetch;      // scan_rd_kernel: read every vector's refined distance with its stage-1 inputs
 };
 
 __device__ __forceinline__ double dinf() { return __longlong_as_double(0x7ff0000000000000LL); }
@@ -885,9 +886,8 @@ __global__ void __launch_bounds__(WQ * 32, MINB) scan_warp_kernel(Args a) {
 // (same test as stage1_chunk), then its survivors' refined distances offered
 // to the warp's register queue (the pool).  No shared memory, few registers.
 constexpr int RDW = 4;    // queries (warps) per CTA
-constexpr int RSUB = 4;   // 32-vector sub-chunks per batch
 
-template <bool REFINE, int IPB>
+template <bool REFINE, int IPB, int RSUB>
 __global__ void __launch_bounds__(RDW * 32) scan_rd_kernel(Args a) {
   using IPT = typename std::conditional<IPB == 2, int16_t, int32_t>::type;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -917,9 +917,19 @@ __global__ void __launch_bounds__(RDW * 32) scan_rd_kernel(Args a) {
     const double* rrow = REFINE ? a.rdist + rowbase : nullptr;
     if (REFINE && T_list == dinf()) {  // nothing can be pruned (lb2 <= +inf): every vector's refined distance
       surv += n_c;
-      for (int64_t c0 = 0; c0 < n_c; c0 += 32) {
-        const int64_t vi = c0 + lane;
-        warp_offer(a, qd, qi, vi < n_c ? __ldg(rrow + vi) : dinf(), vi < n_c ? (int)vi : -1, lo, k);
+      for (int64_t c0 = 0; c0 < n_c; c0 += 32 * RSUB) {
+        double dv[RSUB];
+#pragma unroll
+        for (int u = 0; u < RSUB; ++u) {
+          const int64_t vi = c0 + u * 32 + lane;
+          dv[u] = vi < n_c ? __ldg(rrow + vi) : dinf();
+        }
+#pragma unroll
+        for (int u = 0; u < RSUB; ++u) {
+          const int64_t vi = c0 + u * 32 + lane;
+          if (c0 + u * 32 >= n_c) break;  // warp-uniform
+          warp_offer(a, qd, qi, dv[u], vi < n_c ? (int)vi : -1, lo, k);
+        }
       }
     } else {
       const IPT* iprow = reinterpret_cast<const IPT*>(a.ipbuf) + rowbase;
@@ -927,10 +937,12 @@ __global__ void __launch_bounds__(RDW * 32) scan_rd_kernel(Args a) {
       for (int64_t c0 = 0; c0 < n_c; c0 += 32 * RSUB) {
         int ipv[RSUB];
         float fa[RSUB], fs[RSUB], fe[RSUB];
+        double pre[RSUB];  // refined distances fetched with the stage-1 inputs (one round trip per batch)
 #pragma unroll
         for (int u = 0; u < RSUB; ++u) {
           const int64_t vi = c0 + u * 32 + lane;
           const bool in = vi < n_c;
+          pre[u] = (REFINE && a.rd_prefetch && in) ? __ldg(rrow + vi) : 0.0;
           ipv[u] = in ? (int)__ldg(iprow + vi) : 0;
           fa[u] = in ? __ldg(a.ix.short_add + lo + vi) : 0.f;
           fs[u] = in ? __ldg(a.ix.short_scale + lo + vi) : 0.f;
@@ -976,7 +988,7 @@ __global__ void __launch_bounds__(RDW * 32) scan_rd_kernel(Args a) {
 #pragma unroll
         for (int u = 0; u < RSUB; ++u) {  // survivors' refined distances, loads in flight together
           const int64_t vi = c0 + u * 32 + lane;
-          dv[u] = keep[u] ? (REFINE ? __ldg(rrow + vi) : est[u]) : dinf();
+          dv[u] = keep[u] ? (REFINE ? (a.rd_prefetch ? pre[u] : __ldg(rrow + vi)) : est[u]) : dinf();
         }
 #pragma unroll
         for (int u = 0; u < RSUB; ++u) {
@@ -1978,11 +1990,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_refine_kernel(const __grid_c
     const int64_t rs = ip_row_stride(n_c);
     const int ntile = (int)ceil_div(n_c, TCM);
     __syncthreads();  // previous group's MMAs completed (its epilogue waited on them), scalars consumed
-    if (tid == 0) {   // group operand: the G queries' digit slices, 8 rows per query, by TMA
-      tc::mbar_expect_tx(bfull, (uint32_t)(nqg * nkc * 8 * TCKC));
-      for (int j = 0; j < nqg; ++j) {
-        const int q8 = (int)((a.porder[ps + j] / a.nprobe) * SLICES);
-        for (int kc = 0; kc < nkc; ++kc) tc::tma_load_2d(sB + kc * N * TCKC + j * 8 * TCKC, &a.map_b, kc * TCKC, q8, bfull);
+    if (wid == 0) {   // group operand: the G queries' digit slices, 8 rows per query, by TMA (one lane per query)
+      if (lane == 0) tc::mbar_expect_tx(bfull, (uint32_t)(nqg * nkc * 8 * TCKC));
+      __syncwarp();
+      if (lane < nqg) {
+        const int q8 = (int)((a.porder[ps + lane] / a.nprobe) * SLICES);
+        for (int kc = 0; kc < nkc; ++kc)
+          tc::tma_load_2d(sB + kc * N * TCKC + lane * 8 * TCKC, &a.map_b, kc * TCKC, q8, bfull);
       }
     }
     if (tid < G) {
@@ -2157,9 +2171,15 @@ __global__ void merge_topk_kernel(const int64_t* __restrict__ ids, const double*
   out_counts[q] = n;
 }
 
+template <int RS>
+inline auto rd_kernel_for(bool refine, int ipb) {
+  return refine ? (ipb == 2 ? scan_rd_kernel<true, 2, RS> : scan_rd_kernel<true, 4, RS>)
+                : (ipb == 2 ? scan_rd_kernel<false, 2, RS> : scan_rd_kernel<false, 4, RS>);
+}
+
 inline int launch_rd(const Args& a, bool refine, int ipb, cudaStream_t s) {
-  auto kern = refine ? (ipb == 2 ? scan_rd_kernel<true, 2> : scan_rd_kernel<true, 4>)
-                     : (ipb == 2 ? scan_rd_kernel<false, 2> : scan_rd_kernel<false, 4>);
+  static const int rsub = getenv("IVRQ_RD_SUB") ? atoi(getenv("IVRQ_RD_SUB")) : 4;  // 32-vector sub-chunks per batch
+  auto kern = rsub == 8 ? rd_kernel_for<8>(refine, ipb) : rsub == 2 ? rd_kernel_for<2>(refine, ipb) : rd_kernel_for<4>(refine, ipb);
   kern<<<(unsigned)ceil_div(a.nq, RDW), RDW * 32, 0, s>>>(a);
   return check_launch("ivrq_search_scan");
 }
@@ -2263,6 +2283,8 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
   const bool nib = rcode_nibbles(index->bits);
   const char* pf_env = getenv("IVRQ_L2_PREFETCH");
   a.l2_prefetch = pf_env ? atoi(pf_env) : 0;
+  const char* rp_env = getenv("IVRQ_RD_PREFETCH");
+  a.rd_prefetch = rp_env ? atoi(rp_env) : 1;
   cudaStream_t s = as_stream(stream);
   retain_async_pool(s);
   // Schedule queries grouped by their first (lowest-id) probed list: that list
