@@ -2115,6 +2115,213 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_refine_kernel(const __grid_c
   if (wid == TC_PROD) tc::tmem_dealloc(tbase, tmem_cols(2 * N));
 }
 
+// ------------------------------------------------------------ stage-1 inner products on tcgen05
+// The binary inner products ip = <bit_v, qhat_q> of every probed (list,
+// query) pair (ip_list_kernel's integer, search.py:163-183), list-major on
+// the 5th-generation tensor cores: A = the list's 1-bit codes expanded to
+// 0/1 bytes by the producer warps (128 vectors x 128 dims per stage, written
+// in the 128B-swizzled K-major layout), B = the group's quantized queries in
+// pair order (one TMA box of up to 256 rows per 128-dim chunk), accumulator
+// 128 x N int32 in TMEM, epilogue writes the int16/int32 inner products.
+constexpr int IPQ_MAX = 256;  // queries per group (N <= 256), fewer when the group's qhat rows exceed ~120 KB
+
+inline int ip_group_size(int g) {
+  int q = (120 * 1024) / (32 * g);
+  q = q > IPQ_MAX ? IPQ_MAX : q;
+  return q < 16 ? 16 : q & ~15;
+}
+
+struct TcIpArgs {
+  CUtensorMap map_b;        // qhat in pair order [npairs rows x 32 g], box 128 B x IPQ rows
+  ivrq_index_view ix;
+  int g, nlist, ip32, ipq;
+  const int64_t* poff;      // [nlist + 2]
+  const int64_t* pair_base; // [nlist + 1]
+  const int32_t* gpre;      // [nlist + 1] prefix of ceil(bucket / ipq)
+  void* ipbuf;
+};
+
+size_t tc_ip_smem_bytes(int g) {
+  const int nkc = (32 * g + TCKC - 1) / TCKC;
+  return 1024 + (size_t)nkc * ip_group_size(g) * TCKC + (size_t)TCST * TCM * TCKC + 256;
+}
+
+// qhat rows gathered into pair order: out[i] = qhat[porder[i] / nprobe] (the first total pairs)
+__global__ void qhat_pairs_kernel(const int8_t* __restrict__ qhat, const int64_t* __restrict__ porder,
+                                  const int64_t* __restrict__ poff, int nlist, int nprobe, int rowb,
+                                  int8_t* __restrict__ out) {
+  const int64_t npairs = poff[nlist];
+  const int per = rowb / 16;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < npairs * per; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / per;
+    const int c16 = (int)(i % per);
+    const int64_t q = porder[r] / nprobe;
+    reinterpret_cast<uint4*>(out + r * rowb)[c16] = reinterpret_cast<const uint4*>(qhat + q * rowb)[c16];
+  }
+}
+
+__global__ void __launch_bounds__(TC_THREADS, 1) tc_ip_kernel(const __grid_constant__ TcIpArgs a) {
+  extern __shared__ __align__(1024) unsigned char ism_raw[];
+  unsigned char* ism = reinterpret_cast<unsigned char*>(((uintptr_t)ism_raw + 1023) & ~(uintptr_t)1023);
+  const int g = a.g, kb_total = 32 * g, IPQ = a.ipq;
+  const int nkc = (kb_total + TCKC - 1) / TCKC;
+  int8_t* sB = reinterpret_cast<int8_t*>(ism);                                   // [nkc][IPQ rows x 128 B]
+  uint8_t* sA = reinterpret_cast<uint8_t*>(ism + (size_t)nkc * IPQ * TCKC);      // [TCST][128 rows x 128 B]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sA + TCST * TCM * TCKC);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + TCST;
+  uint64_t* accf = bars + 2 * TCST;
+  uint64_t* acce = bars + 2 * TCST + 2;
+  uint64_t* bfull = bars + 2 * TCST + 4;
+  uint32_t* s_taddr = reinterpret_cast<uint32_t*>(bars + 2 * TCST + 5);
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid == 0) {
+    for (int i = 0; i < TCST; ++i) {
+      tc::mbar_init(&full[i], 32 * TC_PROD);
+      tc::mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&accf[i], 1);
+      tc::mbar_init(&acce[i], 128);
+    }
+    tc::mbar_init(bfull, 1);
+    tc::fence_mbar_init();
+  }
+  if (wid == TC_PROD) tc::tmem_alloc(s_taddr, 512);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tbase = *s_taddr;
+  uint32_t it_prod = 0, it_mma = 0, tile_mma = 0, tile_epi = 0, grp = 0;
+  const int total = a.gpre[a.nlist];
+  for (int b = blockIdx.x; b < total; b += gridDim.x, ++grp) {
+    int lo_c = 0, hi_c = a.nlist;
+    while (hi_c - lo_c > 1) {
+      const int mid = (lo_c + hi_c) >> 1;
+      if (a.gpre[mid] <= b) lo_c = mid; else hi_c = mid;
+    }
+    const int c = lo_c;
+    const int64_t lo = a.ix.offsets[c], n_c = a.ix.offsets[c + 1] - lo;
+    const int64_t ps = a.poff[c] + (int64_t)(b - a.gpre[c]) * IPQ;
+    const int nqg = (int)min((int64_t)IPQ, a.poff[c + 1] - ps);
+    const int N = (nqg + 15) & ~15;
+    const int64_t rs = ip_row_stride(n_c);
+    const int ntile = (int)ceil_div(n_c, TCM);
+    __syncthreads();  // previous group's MMAs completed (its epilogue waited on them)
+    if (tid == 0) {   // B: the group's qhat rows (contiguous in pair order)
+      tc::mbar_expect_tx(bfull, (uint32_t)(nkc * IPQ * TCKC));
+      for (int kc = 0; kc < nkc; ++kc) tc::tma_load_2d(sB + kc * IPQ * TCKC, &a.map_b, kc * TCKC, (int)ps, bfull);
+    }
+    if (wid < TC_PROD) {
+      // ---- producers: code words -> 0/1 bytes, swizzled (each thread: row r, one word = 32 dims = 2 x 16 B)
+      const int pl = wid * 32 + lane;
+      const uint32_t* words = a.ix.packed_msb + (int64_t)g * lo;
+      constexpr int PER = TCM * (TCKC / 32) / (32 * TC_PROD);  // words per producer thread per stage
+      // consecutive lanes -> consecutive vectors (coalesced); the next stage's words are loaded
+      // before this stage's slot is awaited, so the load latency overlaps the pipeline
+      auto load_stage = [&](int sidx, uint32_t (&w)[PER]) {
+        const int t = sidx / nkc, kc = sidx % nkc;
+#pragma unroll
+        for (int e = 0; e < PER; ++e) {
+          const int i = pl + e * 32 * TC_PROD;
+          const int r = i % TCM, jw = i / TCM;
+          const int gi = kc * (TCKC / 32) + jw;
+          const int64_t v = (int64_t)t * TCM + r;
+          w[e] = (v < n_c && gi < g) ? __ldg(words + (int64_t)gi * n_c + v) : 0u;
+        }
+      };
+      const int nst = ntile * nkc;
+      uint32_t wn[PER];
+      if (nst > 0) load_stage(0, wn);
+      for (int sidx = 0; sidx < nst; ++sidx, ++it_prod) {
+        uint32_t wc[PER];
+#pragma unroll
+        for (int e = 0; e < PER; ++e) wc[e] = wn[e];
+        if (sidx + 1 < nst) load_stage(sidx + 1, wn);
+        {
+          const int st = it_prod % TCST;
+          tc::mbar_wait(&empty[st], ((it_prod / TCST) & 1) ^ 1);
+          uint8_t* dst = sA + st * TCM * TCKC;
+#pragma unroll
+          for (int e = 0; e < PER; ++e) {
+            const int i = pl + e * 32 * TC_PROD;
+            const int r = i % TCM, jw = i / TCM;
+            const uint32_t w = wc[e];
+            uint4 o0, o1;
+            o0.x = nib_bytes(w, 0);
+            o0.y = nib_bytes(w, 4);
+            o0.z = nib_bytes(w, 8);
+            o0.w = nib_bytes(w, 12);
+            o1.x = nib_bytes(w, 16);
+            o1.y = nib_bytes(w, 20);
+            o1.z = nib_bytes(w, 24);
+            o1.w = nib_bytes(w, 28);
+            *reinterpret_cast<uint4*>(dst + sw128_offset(r, 32 * jw)) = o0;
+            *reinterpret_cast<uint4*>(dst + sw128_offset(r, 32 * jw + 16)) = o1;
+          }
+          tc::fence_smem_async();
+          tc::mbar_arrive(&full[st]);
+        }
+      }
+    } else if (wid == TC_PROD) {
+      // ---- MMA issuer
+      const uint32_t idesc = tc::idesc_i8(TCM, N, false, true);
+      tc::mbar_wait(bfull, grp & 1);
+      for (int t = 0; t < ntile; ++t, ++tile_mma) {
+        const int ab = tile_mma & 1;
+        tc::mbar_wait(&acce[ab], ((tile_mma >> 1) & 1) ^ 1);
+        tc::fence_after_sync();
+        for (int kc = 0; kc < nkc; ++kc, ++it_mma) {
+          const int st = it_mma % TCST;
+          tc::mbar_wait(&full[st], (it_mma / TCST) & 1);
+          tc::fence_after_sync();
+          if (lane == 0) {
+            const int ks = min(TCKC, kb_total - kc * TCKC) / 32;
+            for (int s2 = 0; s2 < ks; ++s2) {
+              const uint64_t ad = tc::smem_desc_sw128(sA + st * TCM * TCKC + 32 * s2);
+              const uint64_t bd = tc::smem_desc_sw128(sB + kc * IPQ * TCKC + 32 * s2);
+              tc::mma_i8(tbase + ab * IPQ, ad, bd, idesc, kc > 0 || s2 > 0);
+            }
+            tc::commit(&empty[st]);
+            if (kc == nkc - 1) tc::commit(&accf[ab]);
+          }
+          __syncwarp();
+        }
+      }
+    } else {
+      // ---- epilogue: TMEM lane r = vector, column j = query slot
+      const int quarter = wid & 3;
+      const int r = quarter * 32 + lane;
+      for (int t = 0; t < ntile; ++t, ++tile_epi) {
+        const int ab = tile_epi & 1;
+        const int64_t v = (int64_t)t * TCM + r;
+        tc::mbar_wait(&accf[ab], (tile_epi >> 1) & 1);
+        tc::fence_after_sync();
+        for (int j0 = 0; j0 < nqg; j0 += 32) {
+          uint32_t d[32];
+          tc::tmem_ld32(tbase + ((uint32_t)(quarter * 32) << 16) + ab * IPQ + j0, d);
+          tc::tmem_ld_wait();
+          if (v < n_c) {
+            const int jn = min(32, nqg - j0);
+            if (a.ip32) {
+              int32_t* base = reinterpret_cast<int32_t*>(a.ipbuf) + a.pair_base[c] + (ps - a.poff[c] + j0) * rs + v;
+              for (int jj = 0; jj < jn; ++jj) base[jj * rs] = (int32_t)d[jj];
+            } else {
+              int16_t* base = reinterpret_cast<int16_t*>(a.ipbuf) + a.pair_base[c] + (ps - a.poff[c] + j0) * rs + v;
+              for (int jj = 0; jj < jn; ++jj) base[jj * rs] = (int16_t)(int32_t)d[jj];
+            }
+          }
+        }
+        tc::fence_before_sync();
+        tc::mbar_arrive(&acce[ab]);
+      }
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (wid == TC_PROD) tc::tmem_dealloc(tbase, 512);
+}
+
 // first probed list of each query inside this shard's id range (ids ascend per query)
 __global__ void first_probe_kernel(const int64_t* __restrict__ probe_ids, int64_t nq, int nprobe, int64_t list_lo,
                                    int64_t list_hi, int32_t* __restrict__ first) {
@@ -2308,7 +2515,11 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
   const bool warp_path = tc_path && (wenv ? atoi(wenv) != 0 : true);
   // ... with every probed pair refined list-major on tcgen05 and a streaming per-query pass
   const char* tr_env = getenv("IVRQ_TC_REFINE");
-  const bool rd_path = warp_path && (tr_env ? atoi(tr_env) != 0 : true) && (!refine || index->rcodes);
+  // Dense refine costs (probed vectors) x kpad MACs against (survivors) x kpad gathered for the
+  // in-warp refine: at D <= 768 the tensor cores win, at D = 1536 (5x more probed than surviving
+  // vectors) the survivor-only path does.  IVRQ_TC_REFINE=0/1 forces either.
+  const bool rd_path = warp_path && (!refine || index->rcodes) &&
+                       (tr_env ? atoi(tr_env) != 0 : (!refine || kpad64(index->dims) <= 768));
   const bool first_phase = grouped && refine && a.k <= 32 && !init_counts &&
                            (fl_env ? atoi(fl_env) != 0 : !warp_path);
   if (grouped && nq > 1 && nl >= 1) {
@@ -2422,6 +2633,9 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
   int ipb = 0;
   double* rdist = nullptr;
   int8_t* tcsl = nullptr;
+  int8_t* qpairs = nullptr;
+  int32_t* igpre = nullptr;
+  int64_t* iscratch = nullptr;
   int32_t* rgpre = nullptr;
   int64_t* rscratch = nullptr;
   int32_t *pkeys = nullptr, *pslot = nullptr, *tpre = nullptr;
@@ -2541,7 +2755,40 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
       }
       cudaStream_t si = (fd_launch && s2) ? s2 : s;
       scan::qhat_kernel<<<(unsigned)ceil_div(nq * a.g, 256), 256, 0, si>>>(planes, nq, a.g, a.qbits, qhat);
-      ik<<<(unsigned)(2 * sm_count_of_current_device()), scan::THREADS, ism, si>>>(ia);
+      const char* ti_env = getenv("IVRQ_TC_IP");
+      if (ti_env ? atoi(ti_env) != 0 : true) {
+        // stage-1 inner products on tcgen05: qhat rows gathered into pair order, then list-major GEMM tiles
+        const int rowb = 32 * a.g;
+        if (cudaMallocAsync(reinterpret_cast<void**>(&qpairs), (size_t)npairs * rowb, si) != cudaSuccess ||
+            cudaMallocAsync(reinterpret_cast<void**>(&igpre), (nl + 1) * sizeof(int32_t), si) != cudaSuccess ||
+            cudaMallocAsync(reinterpret_cast<void**>(&iscratch), (nl + 3) * sizeof(int64_t), si) != cudaSuccess)
+          return fail(IVRQ_ENOMEM, "ivrq_search_scan: workspace allocation failed");
+        const int ipq = scan::ip_group_size(a.g);
+        scan::pair_plan_kernel<<<1, 1024, 0, si>>>(index->offsets, poff, (int)nl, ipq, iscratch, igpre,
+                                                    iscratch + nl + 1);
+        scan::qhat_pairs_kernel<<<(unsigned)(4 * sm_count_of_current_device()), 256, 0, si>>>(
+            qhat, porder, poff, (int)nl, a.nprobe, rowb, qpairs);
+        scan::TcIpArgs ta{};
+        if (!tc::make_tmap_u8_sw128(&ta.map_b, qpairs, (uint64_t)rowb, (uint64_t)npairs, (uint64_t)rowb, scan::TCKC,
+                                    ipq))
+          return fail(IVRQ_ECUDA, "ivrq_search_scan: TMA tensor map encoding failed");
+        ta.ix = *index;
+        ta.g = a.g;
+        ta.nlist = (int)nl;
+        ta.ip32 = ipb == 4 ? 1 : 0;
+        ta.ipq = ipq;
+        ta.poff = poff;
+        ta.pair_base = pbase;
+        ta.gpre = igpre;
+        ta.ipbuf = ipbuf;
+        const size_t tsm = scan::tc_ip_smem_bytes(a.g);
+        if (cudaFuncSetAttribute(scan::tc_ip_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm) !=
+            cudaSuccess)
+          return fail(IVRQ_EUNSUP, "ivrq_search_scan: dims too large for the tensor-core stage 1");
+        scan::tc_ip_kernel<<<(unsigned)sm_count_of_current_device(), scan::TC_THREADS, tsm, si>>>(ta);
+      } else {
+        ik<<<(unsigned)(2 * sm_count_of_current_device()), scan::THREADS, ism, si>>>(ia);
+      }
       IVRQ_TRY(check_launch("ivrq_search_scan(stage-1 tiles)"));
       if (fd_launch) {
         IVRQ_TRY(fd_launch());
@@ -2565,6 +2812,11 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
                                            : scan::launch_mode<IVRQ_IP_BITWISE>(a, refine, nib, warp_path ? -ipb : ipb, s))
                                                     : scan::launch_mode<IVRQ_IP_LUT>(a, refine, nib, 0, s);
   if (tcsl) cudaFreeAsync(tcsl, s);
+  if (qpairs) {
+    cudaFreeAsync(qpairs, s);
+    cudaFreeAsync(igpre, s);
+    cudaFreeAsync(iscratch, s);
+  }
   if (rdist) {
     cudaFreeAsync(rdist, s);
     cudaFreeAsync(rgpre, s);
