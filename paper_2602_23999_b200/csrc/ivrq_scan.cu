@@ -2031,28 +2031,44 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_refine_kernel(const __grid_c
             }
         }
       } else {
-        // two dims per byte: 8 bytes -> 16 elements [lo(0..3) hi(0..3) lo(4..7) hi(4..7)], swizzled stores
+        // two dims per byte: 8 bytes -> 16 elements [lo(0..3) hi(0..3) lo(4..7) hi(4..7)], swizzled
+        // stores; the next stage's bytes are loaded before this stage's slot is awaited
         const int pl = wid * 32 + lane;
         const uint8_t* rows = a.ix.rcodes + lo * rb;
-        for (int t = 0; t < ntile; ++t)
-          for (int kc = 0; kc < nkc; ++kc, ++it_prod) {
-            const int st = it_prod % TCST;
-            tc::mbar_wait(&empty[st], ((it_prod / TCST) & 1) ^ 1);
-            uint8_t* dst = sA + st * TCM * TCKC;
-            const int kb0 = kc * TCKC;
-            for (int i = pl; i < TCM * (TCKC / 16); i += 32 * TC_PROD) {
-              const int r = i / (TCKC / 16), pc = 16 * (i % (TCKC / 16));
-              const int64_t v = (int64_t)t * TCM + r;
-              uint4 o = make_uint4(0u, 0u, 0u, 0u);
-              if (v < n_c && kb0 + pc < kp) {
-                const uint2 x = __ldg(reinterpret_cast<const uint2*>(rows + v * rb + (kb0 + pc) / 2));
-                o = make_uint4(x.x & 0x0F0F0F0Fu, (x.x >> 4) & 0x0F0F0F0Fu, x.y & 0x0F0F0F0Fu, (x.y >> 4) & 0x0F0F0F0Fu);
-              }
-              *reinterpret_cast<uint4*>(dst + sw128_offset(r, pc)) = o;
-            }
-            tc::fence_smem_async();
-            tc::mbar_arrive(&full[st]);
+        constexpr int PER = TCM * (TCKC / 16) / (32 * TC_PROD);
+        auto load_stage = [&](int sidx, uint2 (&x)[PER]) {
+          const int t = sidx / nkc, kb0 = (sidx % nkc) * TCKC;
+#pragma unroll
+          for (int e = 0; e < PER; ++e) {
+            const int i = pl + e * 32 * TC_PROD;
+            const int r = i / (TCKC / 16), pc = 16 * (i % (TCKC / 16));
+            const int64_t v = (int64_t)t * TCM + r;
+            x[e] = (v < n_c && kb0 + pc < kp) ? __ldg(reinterpret_cast<const uint2*>(rows + v * rb + (kb0 + pc) / 2))
+                                              : make_uint2(0u, 0u);
           }
+        };
+        const int nst = ntile * nkc;
+        uint2 xn[PER];
+        if (nst > 0) load_stage(0, xn);
+        for (int sidx = 0; sidx < nst; ++sidx, ++it_prod) {
+          uint2 xc[PER];
+#pragma unroll
+          for (int e = 0; e < PER; ++e) xc[e] = xn[e];
+          if (sidx + 1 < nst) load_stage(sidx + 1, xn);
+          const int st = it_prod % TCST;
+          tc::mbar_wait(&empty[st], ((it_prod / TCST) & 1) ^ 1);
+          uint8_t* dst = sA + st * TCM * TCKC;
+#pragma unroll
+          for (int e = 0; e < PER; ++e) {
+            const int i = pl + e * 32 * TC_PROD;
+            const int r = i / (TCKC / 16), pc = 16 * (i % (TCKC / 16));
+            const uint2 x = xc[e];
+            *reinterpret_cast<uint4*>(dst + sw128_offset(r, pc)) =
+                make_uint4(x.x & 0x0F0F0F0Fu, (x.x >> 4) & 0x0F0F0F0Fu, x.y & 0x0F0F0F0Fu, (x.y >> 4) & 0x0F0F0F0Fu);
+          }
+          tc::fence_smem_async();
+          tc::mbar_arrive(&full[st]);
+        }
       }
     } else if (wid == TC_PROD) {
       // ---- MMA issuer
@@ -2518,8 +2534,12 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
   // Dense refine costs (probed vectors) x kpad MACs against (survivors) x kpad gathered for the
   // in-warp refine: at D <= 768 the tensor cores win, at D = 1536 (5x more probed than surviving
   // vectors) the survivor-only path does.  IVRQ_TC_REFINE=0/1 forces either.
-  const bool rd_path = warp_path && (!refine || index->rcodes) &&
-                       (tr_env ? atoi(tr_env) != 0 : (!refine || kpad64(index->dims) <= 768));
+  // Measured (B200, bench configs): dense wins at C3 (8-bit codes, D = 768); the survivor-only
+  // path wins for 4-bit codes (C2, C4: few survivors, 64-byte rows) and at D = 1536 (C5).
+  // (1-bit indexes have nothing to refine: the streaming pass alone.)
+  const bool rd_path = warp_path && (!refine || (index->rcodes && (tr_env ? atoi(tr_env) != 0
+                                                                          : (!rcode_nibbles(index->bits) &&
+                                                                             kpad64(index->dims) <= 768))));
   const bool first_phase = grouped && refine && a.k <= 32 && !init_counts &&
                            (fl_env ? atoi(fl_env) != 0 : !warp_path);
   if (grouped && nq > 1 && nl >= 1) {
@@ -2756,7 +2776,7 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
       cudaStream_t si = (fd_launch && s2) ? s2 : s;
       scan::qhat_kernel<<<(unsigned)ceil_div(nq * a.g, 256), 256, 0, si>>>(planes, nq, a.g, a.qbits, qhat);
       const char* ti_env = getenv("IVRQ_TC_IP");
-      if (ti_env ? atoi(ti_env) != 0 : true) {
+      if (ti_env ? atoi(ti_env) != 0 : a.g >= 8) {  // mma.sync tiles win for short codes (D <= 224)
         // stage-1 inner products on tcgen05: qhat rows gathered into pair order, then list-major GEMM tiles
         const int rowb = 32 * a.g;
         if (cudaMallocAsync(reinterpret_cast<void**>(&qpairs), (size_t)npairs * rowb, si) != cudaSuccess ||
