@@ -180,6 +180,37 @@ def measured_peaks() -> dict:
     return {"hbm_gbs": 6650.0, "_fallback": True}
 
 
+def count_launches(step_fn) -> tuple[int, list[str]]:
+    """Kernels one search step launches, counted by CUPTI (torch.profiler), ours and library."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        step_fn()
+        torch.cuda.synchronize()
+    names: dict[str, int] = {}
+    for ev in prof.events():
+        if ev.device_type == torch.autograd.DeviceType.CUDA and not ev.name.startswith(("Memcpy", "Memset")):
+            names[ev.name] = names.get(ev.name, 0) + 1
+    ours = {k: v for k, v in names.items() if "ivrq" in k or "scan::" in k or "gemm::" in k or "enc::" in k}
+    short = sorted({k.split("(")[0].replace("void ", "")[:60] for k in ours})
+    return int(sum(ours.values())), short
+
+
+def ncu_traffic(cfg_name: str, nprobe: int):
+    """DRAM bytes (read + write) of the scan stage per search, from the committed ncu capture
+    (profiles/<round>/traffic_<cfg>.json, written by tools/ncu_traffic.py), or None."""
+    for p in sorted((ROOT / "profiles").glob(f"*/traffic_{cfg_name}.json"), reverse=True):
+        try:
+            t = json.loads(p.read_text())
+        except ValueError:
+            continue
+        if t.get("n_probe") == nprobe:
+            return {"dram_bytes": t["dram_bytes"], "source": str(p.relative_to(ROOT)), "kernels": t.get("kernels")}
+    return None
+
+
 def dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -310,6 +341,7 @@ def run_ours(args, cfg_name: str) -> dict:
         tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
         e2e_s = float(t.item())
     assert len(out) == NQ
+    launches_per_step, kernel_names = count_launches(lambda: search_device(queries, index, sp))
     scan_mean_ms = float(np.mean(scan_ms))
     peaks = measured_peaks()
     peak = float(peaks.get("hbm_gbs", 6650.0))
@@ -349,15 +381,17 @@ def run_ours(args, cfg_name: str) -> dict:
             "h2d_bytes_per_step": int(q_host.nbytes),
             "d2h_bytes_per_step": int(NQ * K * 16 + NQ * 4),
         },
-        "gpu_launches": args.steps * 6,
+        "gpu_launches": args.steps * launches_per_step,
+        "gpu_launches_per_step": launches_per_step,
+        "gpu_kernels": kernel_names,
         "roofline": {
             "bound": "hbm",
-            "kernel": "ivrq scan_kernel (fused stage-1 + refine + top-k)",
+            "kernel": "scan stage (stage-1 inner products, refine, per-query prune/top-k kernels; events around the stage)",
             "achieved": round(achieved, 1),
             "peak": peak,
             "unit": "GB/s",
             "frac": round(achieved / peak, 4),
-            "traffic": None,
+            "traffic": ncu_traffic(cfg_name, nprobe),
             "algorithmic_bytes_per_launch": int(alg_bytes),
             "bytes_formula": f"probed*(4*ceil(D/32)+12) + survivors*({surv_b})",
             "probed_per_query": round(probed / NQ, 1),
