@@ -315,20 +315,35 @@ def _synthetic_index(n, d, nlist, bits, seed):
         (15000, 128, 48, 1, 4, 7, 10),  # 1-bit index: every probe on the tensor-core stage 1
         (15000, 70, 40, 3, 2, 40, 32),  # every list probed, ragged dims, k = 32
         (8000, 64, 16, 5, 4, 4, 1),
+        (6000, 1000, 12, 4, 4, 5, 10),  # D = 1000: kpad 1024 (8 refine chunks), g = 32
     ],
 )
 def test_tensor_core_stage1_matches_popcount_path(monkeypatch, n, d, nlist, bits, qbits, nprobe, k):
-    """List-major int8 MMA stage 1 == per-query AND+POPC stage 1: ids, dists, counts and survivor stats."""
+    """Every list-major tensor-core path == the per-query AND+POPC scan: ids, dists, counts, survivor stats.
+
+    Variants: the default policy; tcgen05 stage 1 and tcgen05 dense refine forced on (4-bit codes
+    go through the producer-warp nibble unpack); mma.sync stage 1 with the in-warp survivor refine.
+    """
     ix, q = _synthetic_index(n, d, nlist, bits, seed=d)
     sp = iv.SearchParams(k=k, n_probe=nprobe, ip_mode="bitwise", query_bits=qbits)
     qd = dev.to_device(q)
+    variants = {
+        "popcount": {"IVRQ_TC_STAGE1": "0"},
+        "default": {},
+        "tcgen05": {"IVRQ_TC_IP": "1", "IVRQ_TC_REFINE": "1"},
+        "mma_sync": {"IVRQ_TC_IP": "0", "IVRQ_TC_REFINE": "0"},
+    }
     out = {}
-    for tc in ("0", "1"):
-        monkeypatch.setenv("IVRQ_TC_STAGE1", tc)
+    for name, env in variants.items():
+        for key in ("IVRQ_TC_STAGE1", "IVRQ_TC_IP", "IVRQ_TC_REFINE"):
+            monkeypatch.delenv(key, raising=False)
+        for key, val in env.items():
+            monkeypatch.setenv(key, val)
         r = search_device(qd, ix, sp, with_stats=True)
-        out[tc] = [dev.to_host(t) for t in (r.ids, r.dists, r.counts, r.stats)]
-    for a, b in zip(out["0"], out["1"]):
-        np.testing.assert_array_equal(a, b)
+        out[name] = [dev.to_host(t) for t in (r.ids, r.dists, r.counts, r.stats)]
+    for name in ("default", "tcgen05", "mma_sync"):
+        for a, b in zip(out["popcount"], out[name]):
+            np.testing.assert_array_equal(a, b, err_msg=name)
 
 
 def test_search_batch_pipeline_chunks_identical(monkeypatch):

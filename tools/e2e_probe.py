@@ -63,7 +63,23 @@ def main() -> None:
     assert len(out) == len(out2)
     import os
 
-    for chunks in (1, 2, 3, 4, 5, 8):
+    for nqs in (2500, 5000, 10000):
+        ts = []
+        for _ in range(args.reps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            S.search_device(q[:nqs], ix, sp)
+            torch.cuda.synchronize()
+            ts.append(time.perf_counter() - t0)
+        print(f"device search of {nqs} queries: {1e3*np.median(ts):.2f} ms", file=sys.stderr)
+    # host-side pieces of the pipeline
+    pin = torch.empty(q_host.nbytes, dtype=torch.uint8, pin_memory=True).numpy().view(np.float32).reshape(q_host.shape)
+    t0 = time.perf_counter(); np.copyto(pin, q_host); t1 = time.perf_counter()
+    print(f"host memcpy into pinned (1 thread): {1e3*(t1-t0):.2f} ms", file=sys.stderr)
+    ids_h, d_h, c_h = dev.to_host(res.ids), dev.to_host(res.dists), dev.to_host(res.counts)
+    t0 = time.perf_counter(); out4 = S._rows_to_lists(ids_h.copy(), d_h.copy(), c_h.copy()); t1 = time.perf_counter()
+    print(f"result lists: {1e3*(t1-t0):.2f} ms", file=sys.stderr)
+    for chunks in (1, 2, 3, 4):
         os.environ["IVRQ_E2E_CHUNKS"] = str(chunks)
         ts = []
         for _ in range(args.reps):
