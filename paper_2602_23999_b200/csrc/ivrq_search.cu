@@ -1,11 +1,16 @@
 // Search path: query rotation, coarse probe, query preparation and the fused
 // two-stage list scan.  Reference: search.py (search_batch 390-454).
 #include <algorithm>
+#include <cstdlib>
 
 #include "ivrq_common.cuh"
 #include "ivrq_gemm.cuh"
 
 namespace ivrq {
+
+int probe_tc(const double* q_rot, int64_t nq, int32_t dims, const float* centroids, const double* centroid_sqnorms,
+             int32_t n_clusters, int32_t n_probe, int32_t order_by_id, int64_t* ids, double* d2, const double* q_sq,
+             cudaStream_t s);
 
 // ============================================================ query rotation
 // q_rot[i][j] = sum_k q[i][k] * R[j][k]   (search.py:422: q @ rotation.T)
@@ -307,6 +312,11 @@ extern "C" int ivrq_select_clusters_ordered(const double* q_rot, int64_t nq, int
   double* dist = reinterpret_cast<double*>(workspace);
   double* q_sq = dist + rows * n_clusters;
   IVRQ_TRY(ivrq_row_sqnorms(q_rot, 1, nq, dims, q_sq, stream));
+  const char* tp_env = getenv("IVRQ_TC_PROBE");
+  if (tp_env ? atoi(tp_env) != 0 : true) {
+    retain_async_pool(s);
+    return probe_tc(q_rot, nq, dims, centroids, centroid_sqnorms, n_clusters, n_probe, order_by_id, ids, d2, q_sq, s);
+  }
   gemm::RowMajor<float> lb{centroids, n_clusters, dims};
   size_t sel_smem = order_by_id ? 0 : (size_t)n_probe * 16;
   if (sel_smem > 48 * 1024) {
