@@ -26,19 +26,20 @@
 namespace ivrq {
 namespace probe {
 
-constexpr int QT = 32;   // queries per tile  (A rows: 32 x 4 digits = 128 = TMEM lanes)
-constexpr int CT = 64;   // centroids per tile (B rows: 64 x 4 digits = N = 256)
+// NDIG digits per row: queries per tile 128 / NDIG (A rows = TMEM lanes), centroids 256 / NDIG (N = 256)
+template <int NDIG> constexpr int QT_ = 128 / NDIG;
+template <int NDIG> constexpr int CT_ = 256 / NDIG;
 constexpr int KC = 128;  // K bytes per stage
 constexpr int ST = 4;    // stages
 constexpr int EPW = 8;        // epilogue warps (2 per TMEM lane quarter)
 constexpr int THREADS = 32 * (2 + EPW);  // warp 0 TMA, warp 1 MMA, warps 2.. epilogue
-constexpr int NCOL = 4 * CT;  // 256 accumulator columns per tile
+constexpr int NCOL = 256;  // accumulator columns per tile
 
 // ---------------------------------------------------------------- digits
 // One warp per row.  out: digit s of row r at out[(s * rows + r) * kp + k] (queries,
 // slice_major) or out[(4 r + s) * kp + k] (centroids).  e_out: scale exponent e
 // (x = X 2^(e-27)), l1_out: |X|_1.
-template <typename T>
+template <typename T, int NDIG>
 __global__ void digits_kernel(const T* __restrict__ x, int64_t rows, int d, int kp, int slice_major,
                               int8_t* __restrict__ out, int32_t* __restrict__ e_out, double* __restrict__ l1_out) {
   const int lane = threadIdx.x & 31;
@@ -53,19 +54,19 @@ __global__ void digits_kernel(const T* __restrict__ x, int64_t rows, int d, int 
   if (mx > 0.0) frexp(mx, &e);  // mx < 2^e
   double l1 = 0.0;
   for (int k = lane; k < kp; k += 32) {
-    long long X = k < d ? llrint(ldexp((double)xr[k], 27 - e)) : 0;
+    long long X = k < d ? llrint(ldexp((double)xr[k], 7 * NDIG - 1 - e)) : 0;  // |X| <= 2^(7 NDIG - 1)
     l1 += (double)(X < 0 ? -X : X);
-    int8_t dg[4];
+    int8_t dg[NDIG];
 #pragma unroll
-    for (int s = 3; s >= 0; --s) {
+    for (int s = NDIG - 1; s >= 0; --s) {
       const long long rr = ((X + 64) & 127) - 64;
       dg[s] = (int8_t)rr;
       X = (X - rr) >> 7;
     }
-    dg[0] = (int8_t)(dg[0] + (int8_t)(X * 128));  // |X| <= 2^27: the top digit absorbs the remainder (|D_0| <= 65)
+    dg[0] = (int8_t)(dg[0] + (int8_t)(X * 128));  // the top digit absorbs the remainder (|D_0| <= 65)
 #pragma unroll
-    for (int s = 0; s < 4; ++s) {
-      const int64_t row = slice_major ? (int64_t)s * rows + r : 4 * r + s;
+    for (int s = 0; s < NDIG; ++s) {
+      const int64_t row = slice_major ? (int64_t)s * rows + r : NDIG * r + s;
       out[row * kp + k] = dg[s];
     }
   }
@@ -92,7 +93,9 @@ struct TpArgs {
   float* bnd;           // [nrows][2][nlist]: lower bounds L, then upper bounds U
 };
 
+template <int NDIG>
 __global__ void __launch_bounds__(THREADS, 1) tc_probe_kernel(const __grid_constant__ TpArgs a) {
+  constexpr int QT = QT_<NDIG>, CT = CT_<NDIG>;
   extern __shared__ __align__(1024) unsigned char psm_raw[];
   unsigned char* psm = reinterpret_cast<unsigned char*>(((uintptr_t)psm_raw + 1023) & ~(uintptr_t)1023);
   int8_t* sA = reinterpret_cast<int8_t*>(psm);                       // [ST][128 rows x 128 B]
@@ -135,7 +138,7 @@ __global__ void __launch_bounds__(THREADS, 1) tc_probe_kernel(const __grid_const
           tc::mbar_wait(&empty[st], ((it / ST) & 1) ^ 1);
           tc::mbar_expect_tx(&full[st], (128 + NCOL) * KC);
           // A rows 4 j + s: the tile's 32 queries x 4 digits, one box
-          tc::tma_load_2d(sA + st * 128 * KC, &a.map_q, kc * KC, (int)(4 * qrow), &full[st]);
+          tc::tma_load_2d(sA + st * 128 * KC, &a.map_q, kc * KC, (int)(NDIG * qrow), &full[st]);
           tc::tma_load_2d(sB + st * NCOL * KC, &a.map_c, kc * KC, ct * NCOL, &full[st]);
         }
       }
@@ -164,12 +167,13 @@ __global__ void __launch_bounds__(THREADS, 1) tc_probe_kernel(const __grid_const
       }
     }
   } else {
-    // epilogue: TMEM lane = A row = 4 j + s (query j of the tile, digit s); column 4 c + t (centroid c, digit t)
+    // epilogue: TMEM lane = A row = NDIG j + s (query j of the tile, digit s); column NDIG c + t
     const int quarter = wid & 3;
     const int half = (wid - 2) >> 2;  // which half of the tile's centroids this warp finishes
-    const int s = lane & 3;
-    const int jq = quarter * 8 + (lane >> 2);  // query within the tile
+    const int s = lane % NDIG;
+    const int jq = quarter * (32 / NDIG) + lane / NDIG;  // query within the tile
     const int b1 = (lane >> 1) & 1, b0 = lane & 1;
+    constexpr int CPC = 32 / NDIG;  // centroids per 32-column chunk
     uint32_t tcount = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tcount) {
       const int ab = tcount & 1;
@@ -184,8 +188,8 @@ __global__ void __launch_bounds__(THREADS, 1) tc_probe_kernel(const __grid_const
         qe = a.q_e[qg];
       }
       // the tile's centroid scalars, staged while the MMAs run (double-buffered by tile parity)
-      __shared__ double s_csq[2][CT], s_cl1[2][CT];
-      __shared__ int32_t s_ce[2][CT];
+      __shared__ double s_csq[2][128], s_cl1[2][128];
+      __shared__ int32_t s_ce[2][128];
       {
         const int et = tid - 64;  // 0..32*EPW-1
         if (et < CT) {
@@ -198,52 +202,72 @@ __global__ void __launch_bounds__(THREADS, 1) tc_probe_kernel(const __grid_const
       }
       tc::mbar_wait(&accf[ab], (tcount >> 1) & 1);
       tc::fence_after_sync();
-      for (int cc0 = half * (CT / 2); cc0 < (half + 1) * (CT / 2); cc0 += 8) {  // 8 centroids x 4 digits = 32 cols
+      auto emit = [&](int cl, double dot_scaled_hi, double dot_scaled_lo, int shift_hi) {
+        const int64_t c = (int64_t)ct * CT + cl;
+        if (qr < a.nrows && c < a.nlist) {
+          const int sc = qe + s_ce[ab][cl] - 2 * (7 * NDIG - 1);  // s_q s_c
+          const double csq = s_csq[ab][cl];
+          const double dot = dadd(ldexp(dot_scaled_hi, sc + shift_hi), ldexp(dot_scaled_lo, sc));
+          const double dist = dsub(dadd(qsq, csq), dmul(2.0, dot));
+          const double rep = ldexp(ql1 + s_cl1[ab][cl] + 0.5 * a.d, sc);  // 2 (s_q s_c / 2)(|Q|_1+|C|_1+K/2)
+          const double slack = (qsq + csq + 2.0 * fabs(dot)) * 0x1p-40;
+          const double E = rep * 1.0000001 + slack;
+          float* br = a.bnd + qr * 2 * (int64_t)a.nlist;
+          br[c] = __double2float_rd(fmax(dist - E, 0.0));
+          br[a.nlist + c] = __double2float_ru(fmax(dist + E, 0.0));
+        }
+      };
+      for (int cc0 = half * (CT / 2); cc0 < (half + 1) * (CT / 2); cc0 += CPC) {
         uint32_t v[32];
-        tc::tmem_ld32(tbase + ((uint32_t)(quarter * 32) << 16) + ab * NCOL + 4 * cc0, v);
+        tc::tmem_ld32(tbase + ((uint32_t)(quarter * 32) << 16) + ab * NCOL + NDIG * cc0, v);
         tc::tmem_ld_wait();
-        // this digit s of the query against digits t, weight 128^(6-s-t): hi collects s+t <= 2
-        // (weight 128^(2-s-t)), lo s+t >= 3 (weight 128^(6-s-t))
-        long long H[8], L[8];
+        if constexpr (NDIG == 4) {
+          // weight 128^(6-s-t): hi collects s+t <= 2 (weight 128^(2-s-t)), lo s+t >= 3 (128^(6-s-t))
+          long long H[8], L[8];
 #pragma unroll
-        for (int c8 = 0; c8 < 8; ++c8) {
-          long long h = 0, l = 0;
+          for (int c8 = 0; c8 < 8; ++c8) {
+            long long h = 0, l = 0;
 #pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            const long long x = (long long)(int)v[4 * c8 + t];
-            const int u = s + t;
-            if (u <= 2) h += x << (7 * (2 - u));
-            else l += x << (7 * (6 - u));
+            for (int t = 0; t < 4; ++t) {
+              const long long x = (long long)(int)v[4 * c8 + t];
+              const int u = s + t;
+              if (u <= 2) h += x << (7 * (2 - u));
+              else l += x << (7 * (6 - u));
+            }
+            H[c8] = h;
+            L[c8] = l;
           }
-          H[c8] = h;
-          L[c8] = l;
-        }
-        // sum over the query's 4 digit lanes, transposed: lane s ends with centroids 2s, 2s+1
-        long long H1[4], L1[4];
+          // sum over the query's 4 digit lanes, transposed: lane s ends with centroids 2s, 2s+1
+          long long H1[4], L1[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const long long sh = b1 ? H[i] : H[i + 4], sl = b1 ? L[i] : L[i + 4];
-          H1[i] = (b1 ? H[i + 4] : H[i]) + __shfl_xor_sync(0xffffffffu, sh, 2);
-          L1[i] = (b1 ? L[i + 4] : L[i]) + __shfl_xor_sync(0xffffffffu, sl, 2);
-        }
+          for (int i = 0; i < 4; ++i) {
+            const long long sh = b1 ? H[i] : H[i + 4], sl = b1 ? L[i] : L[i + 4];
+            H1[i] = (b1 ? H[i + 4] : H[i]) + __shfl_xor_sync(0xffffffffu, sh, 2);
+            L1[i] = (b1 ? L[i + 4] : L[i]) + __shfl_xor_sync(0xffffffffu, sl, 2);
+          }
 #pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          const long long sh = b0 ? H1[i] : H1[i + 2], sl = b0 ? L1[i] : L1[i + 2];
-          const long long Ht = (b0 ? H1[i + 2] : H1[i]) + __shfl_xor_sync(0xffffffffu, sh, 1);
-          const long long Lt = (b0 ? L1[i + 2] : L1[i]) + __shfl_xor_sync(0xffffffffu, sl, 1);
-          const int cl = cc0 + 2 * s + i;
-          const int64_t c = (int64_t)ct * CT + cl;
-          if (qr < a.nrows && c < a.nlist) {
-            const int sc = qe + s_ce[ab][cl] - 54;  // s_q s_c = 2^(qe-27) 2^(ce-27)
-            const double csq = s_csq[ab][cl];
-            const double dot = dadd(ldexp((double)Ht, sc + 28), ldexp((double)Lt, sc));
-            const double dist = dsub(dadd(qsq, csq), dmul(2.0, dot));
-            const double rep = ldexp(ql1 + s_cl1[ab][cl] + 0.5 * a.d, sc);  // 2 (s_q s_c / 2)(|Q|_1+|C|_1+K/2)
-            const double slack = (qsq + csq + 2.0 * fabs(dot)) * 0x1p-40;
-            const double E = rep * 1.0000001 + slack;
-            float* br = a.bnd + qr * 2 * (int64_t)a.nlist;
-            br[c] = __double2float_rd(fmax(dist - E, 0.0));
-            br[a.nlist + c] = __double2float_ru(fmax(dist + E, 0.0));
+          for (int i = 0; i < 2; ++i) {
+            const long long sh = b0 ? H1[i] : H1[i + 2], sl = b0 ? L1[i] : L1[i + 2];
+            const long long Ht = (b0 ? H1[i + 2] : H1[i]) + __shfl_xor_sync(0xffffffffu, sh, 1);
+            const long long Lt = (b0 ? L1[i + 2] : L1[i]) + __shfl_xor_sync(0xffffffffu, sl, 1);
+            emit(cc0 + 2 * s + i, (double)Ht, (double)Lt, 28);
+          }
+        } else {
+          // NDIG == 2: weight 128^(2-s-t), the whole sum fits an int64 (|.| < 2^38)
+          long long P[16];
+#pragma unroll
+          for (int c16 = 0; c16 < 16; ++c16) {
+            long long p = 0;
+#pragma unroll
+            for (int t = 0; t < 2; ++t) p += ((long long)(int)v[2 * c16 + t]) << (7 * (2 - s - t));
+            P[c16] = p;
+          }
+          // sum over the 2 digit lanes, transposed: lane s ends with centroids 8s .. 8s+7
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const long long sh = b0 ? P[i] : P[i + 8];
+            const long long Pt = (b0 ? P[i + 8] : P[i]) + __shfl_xor_sync(0xffffffffu, sh, 1);
+            emit(cc0 + 8 * s + i, 0.0, (double)Pt, 0);
           }
         }
       }
@@ -468,7 +492,7 @@ int probe_tc(const double* q_rot, int64_t nq, int32_t dims, const float* centroi
   int32_t *qe = nullptr, *ce = nullptr;
   double *ql1 = nullptr, *cl1 = nullptr;
   float* bounds = nullptr;
-  const int64_t rows = std::max<int64_t>(QT, std::min<int64_t>(nq, ((int64_t)256 << 20) / ((int64_t)n_clusters * 8)));
+  const int64_t rows = std::max<int64_t>(128, std::min<int64_t>(nq, ((int64_t)256 << 20) / ((int64_t)n_clusters * 8)));
   if (cudaMallocAsync(reinterpret_cast<void**>(&qd), (size_t)4 * nq * kp, s) != cudaSuccess ||
       cudaMallocAsync(reinterpret_cast<void**>(&cd), (size_t)4 * n_clusters * kp, s) != cudaSuccess ||
       cudaMallocAsync(reinterpret_cast<void**>(&qe), nq * sizeof(int32_t), s) != cudaSuccess ||
@@ -477,13 +501,16 @@ int probe_tc(const double* q_rot, int64_t nq, int32_t dims, const float* centroi
       cudaMallocAsync(reinterpret_cast<void**>(&cl1), n_clusters * sizeof(double), s) != cudaSuccess ||
       cudaMallocAsync(reinterpret_cast<void**>(&bounds), (size_t)rows * n_clusters * 2 * sizeof(float), s) != cudaSuccess)
     return fail(IVRQ_ENOMEM, "ivrq_select_clusters: workspace allocation failed");
-  digits_kernel<double><<<(unsigned)ceil_div(nq, 8), 256, 0, s>>>(q_rot, nq, dims, kp, 0, qd, qe, ql1);
-  digits_kernel<float><<<(unsigned)ceil_div(n_clusters, 8), 256, 0, s>>>(centroids, n_clusters, dims, kp, 0, cd, ce,
-                                                                          cl1);
+  static const int ndig = getenv("IVRQ_PROBE_DIGITS") ? atoi(getenv("IVRQ_PROBE_DIGITS")) : 2;
+  const int QT = ndig == 4 ? QT_<4> : QT_<2>, CT = ndig == 4 ? CT_<4> : CT_<2>;
+  auto dq = ndig == 4 ? digits_kernel<double, 4> : digits_kernel<double, 2>;
+  auto dc = ndig == 4 ? digits_kernel<float, 4> : digits_kernel<float, 2>;
+  dq<<<(unsigned)ceil_div(nq, 8), 256, 0, s>>>(q_rot, nq, dims, kp, 0, qd, qe, ql1);
+  dc<<<(unsigned)ceil_div(n_clusters, 8), 256, 0, s>>>(centroids, n_clusters, dims, kp, 0, cd, ce, cl1);
   IVRQ_TRY(check_launch("ivrq_select_clusters(digits)"));
   TpArgs ta{};
-  if (!tc::make_tmap_u8_sw128(&ta.map_q, qd, (uint64_t)kp, (uint64_t)4 * nq, (uint64_t)kp, KC, 4 * QT) ||
-      !tc::make_tmap_u8_sw128(&ta.map_c, cd, (uint64_t)kp, (uint64_t)4 * n_clusters, (uint64_t)kp, KC, NCOL))
+  if (!tc::make_tmap_u8_sw128(&ta.map_q, qd, (uint64_t)kp, (uint64_t)ndig * nq, (uint64_t)kp, KC, 128) ||
+      !tc::make_tmap_u8_sw128(&ta.map_c, cd, (uint64_t)kp, (uint64_t)ndig * n_clusters, (uint64_t)kp, KC, NCOL))
     return fail(IVRQ_ECUDA, "ivrq_select_clusters: TMA tensor map encoding failed");
   ta.nq = nq;
   ta.nlist = n_clusters;
@@ -497,7 +524,8 @@ int probe_tc(const double* q_rot, int64_t nq, int32_t dims, const float* centroi
   ta.c_l1 = cl1;
   ta.bnd = bounds;
   const size_t sm = tp_smem_bytes();
-  if (cudaFuncSetAttribute(tc_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess ||
+  auto tk = ndig == 4 ? tc_probe_kernel<4> : tc_probe_kernel<2>;
+  if (cudaFuncSetAttribute(tk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess ||
       cudaFuncSetAttribute(probe_rescore_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ROW * 4) !=
           cudaSuccess)
     return fail(IVRQ_EUNSUP, "ivrq_select_clusters: tensor-core probe shared memory");
@@ -507,7 +535,7 @@ int probe_tc(const double* q_rot, int64_t nq, int32_t dims, const float* centroi
     ta.nrows = rn;
     const int64_t tiles = ceil_div(rn, QT) * ceil_div(n_clusters, CT);
     const int grid = (int)std::min<int64_t>(tiles, sm_count_of_current_device());
-    tc_probe_kernel<<<grid, THREADS, sm, s>>>(ta);
+    tk<<<grid, THREADS, sm, s>>>(ta);
     IVRQ_TRY(check_launch("ivrq_select_clusters(tc bounds)"));
     const size_t rsm = n_clusters <= SMEM_ROW ? (size_t)n_clusters * sizeof(float) : 0;
     probe_rescore_kernel<<<(unsigned)rn, RS_THREADS, rsm, s>>>(bounds, r0, n_clusters, n_probe, order_by_id, q_rot,
