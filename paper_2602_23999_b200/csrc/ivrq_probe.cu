@@ -374,7 +374,8 @@ __global__ void __launch_bounds__(RS_THREADS) probe_rescore_kernel(float* __rest
                                                                    const double* __restrict__ q_sq,
                                                                    const double* __restrict__ c_sq,
                                                                    int64_t* __restrict__ ids_out,
-                                                                   double* __restrict__ d2_out) {
+                                                                   double* __restrict__ d2_out,
+                                                                   unsigned long long* __restrict__ stats) {
   extern __shared__ float s_up[];  // [nlist] when nlist <= SMEM_ROW
   __shared__ int32_t hist[256];
   __shared__ int32_t s_nc;
@@ -412,6 +413,10 @@ __global__ void __launch_bounds__(RS_THREADS) probe_rescore_kernel(float* __rest
   }
   __syncthreads();
   const int nc = s_nc;
+  if (stats && tid == 0) {
+    atomicAdd(stats, (unsigned long long)nc);
+    if (nc > MAX_CAND) atomicAdd(stats + 1, 1ull);
+  }
   if (nc > MAX_CAND) {
     // ---- fallback: every distance in float64, stored over the row's bounds (8 bytes per centroid)
     double* exact = reinterpret_cast<double*>(lrow);
@@ -493,6 +498,12 @@ int probe_tc(const double* q_rot, int64_t nq, int32_t dims, const float* centroi
   double *ql1 = nullptr, *cl1 = nullptr;
   float* bounds = nullptr;
   const int64_t rows = std::max<int64_t>(128, std::min<int64_t>(nq, ((int64_t)256 << 20) / ((int64_t)n_clusters * 8)));
+  static const bool want_stats = getenv("IVRQ_PROBE_STATS") != nullptr;
+  unsigned long long* pstats = nullptr;
+  if (want_stats) {
+    cudaMalloc(reinterpret_cast<void**>(&pstats), 16);
+    cudaMemset(pstats, 0, 16);
+  }
   if (cudaMallocAsync(reinterpret_cast<void**>(&qd), (size_t)4 * nq * kp, s) != cudaSuccess ||
       cudaMallocAsync(reinterpret_cast<void**>(&cd), (size_t)4 * n_clusters * kp, s) != cudaSuccess ||
       cudaMallocAsync(reinterpret_cast<void**>(&qe), nq * sizeof(int32_t), s) != cudaSuccess ||
@@ -539,7 +550,7 @@ int probe_tc(const double* q_rot, int64_t nq, int32_t dims, const float* centroi
     IVRQ_TRY(check_launch("ivrq_select_clusters(tc bounds)"));
     const size_t rsm = n_clusters <= SMEM_ROW ? (size_t)n_clusters * sizeof(float) : 0;
     probe_rescore_kernel<<<(unsigned)rn, RS_THREADS, rsm, s>>>(bounds, r0, n_clusters, n_probe, order_by_id, q_rot,
-                                                               centroids, dims, q_sq, centroid_sqnorms, ids, d2);
+                                                               centroids, dims, q_sq, centroid_sqnorms, ids, d2, pstats);
     IVRQ_TRY(check_launch("ivrq_select_clusters(rescore)"));
   }
   cudaFreeAsync(qd, s);
@@ -549,6 +560,13 @@ int probe_tc(const double* q_rot, int64_t nq, int32_t dims, const float* centroi
   cudaFreeAsync(ql1, s);
   cudaFreeAsync(cl1, s);
   cudaFreeAsync(bounds, s);
+  if (pstats) {  // debugging aid: mean candidates per query and overflows (synchronises)
+    unsigned long long h[2];
+    cudaMemcpy(h, pstats, 16, cudaMemcpyDeviceToHost);
+    fprintf(stderr, "[ivrq probe] nq=%lld nlist=%d nprobe=%d candidates/query=%.2f overflow=%llu\n", (long long)nq,
+            n_clusters, n_probe, (double)h[0] / (double)nq, h[1]);
+    cudaFree(pstats);
+  }
   return IVRQ_OK;
 }
 
