@@ -1907,6 +1907,7 @@ struct TcArgs {
   const int64_t* pair_base; // [nlist + 1]
   const int32_t* gpre;      // [nlist + 1] prefix of ceil(bucket / G)
   double* rdist;
+  unsigned long long* prof;  // optional wait-cycle counters (IVRQ_TC_PROF)
 };
 
 // digit slices in rcode byte order: out[q][s][P] = qslices[q][s][perm(P)] with
@@ -1974,8 +1975,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_refine_kernel(const __grid_c
   tc::fence_after_sync();
   const uint32_t tbase = *s_taddr;
   const int64_t rb = a.ix.rcode_bytes;
-  const uint32_t idesc = tc::idesc_i8(TCM, N, false, true);
   uint32_t it_prod = 0, it_mma = 0, tile_mma = 0, tile_epi = 0, grp = 0;
+  const long long t_start = a.prof ? clock64() : 0;
+  long long a_grp_end = 0;
   const int total = a.gpre[a.nlist];
   for (int b = blockIdx.x; b < total; b += gridDim.x, ++grp) {
     int lo_c = 0, hi_c = a.nlist;
@@ -1990,6 +1992,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_refine_kernel(const __grid_c
     const int64_t rs = ip_row_stride(n_c);
     const int ntile = (int)ceil_div(n_c, TCM);
     __syncthreads();  // previous group's MMAs completed (its epilogue waited on them), scalars consumed
+    if (a.prof && wid == TC_PROD && lane == 0 && a_grp_end) atomicAdd(a.prof + 5, (unsigned long long)(clock64() - a_grp_end));
     if (wid == 0) {   // group operand: the G queries' digit slices, 8 rows per query, by TMA (one lane per query)
       if (lane == 0) tc::mbar_expect_tx(bfull, (uint32_t)(nqg * nkc * 8 * TCKC));
       __syncwarp();
@@ -2071,17 +2074,28 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_refine_kernel(const __grid_c
         }
       }
     } else if (wid == TC_PROD) {
-      // ---- MMA issuer
+      // ---- MMA issuer (optionally timing its waits: a.prof[0..3] = B, accumulator, A, total cycles)
+      // N of this group's MMAs: its queries' 8 digit rows, rounded to 16 (lists probed by few queries
+      // do not pay for a full group)
+      const uint32_t idesc = tc::idesc_i8(TCM, 8 * ((nqg + 1) & ~1), false, true);
+      long long t0 = a.prof ? clock64() : 0;
       tc::mbar_wait(bfull, grp & 1);
+      long long t1 = a.prof ? clock64() : 0;
+      if (a.prof && lane == 0) atomicAdd(a.prof + 0, (unsigned long long)(t1 - t0));
       for (int t = 0; t < ntile; ++t, ++tile_mma) {
         const int ab = tile_mma & 1;
+        t0 = a.prof ? clock64() : 0;
         tc::mbar_wait(&acce[ab], ((tile_mma >> 1) & 1) ^ 1);
+        if (a.prof && lane == 0) atomicAdd(a.prof + 1, (unsigned long long)(clock64() - t0));
         tc::fence_after_sync();
         for (int kc = 0; kc < nkc; ++kc, ++it_mma) {
           const int st = it_mma % TCST;
+          t0 = a.prof ? clock64() : 0;
           tc::mbar_wait(&full[st], (it_mma / TCST) & 1);
+          if (a.prof && lane == 0) atomicAdd(a.prof + 2, (unsigned long long)(clock64() - t0));
           tc::fence_after_sync();
           if (lane == 0) {
+            const long long ti = a.prof ? clock64() : 0;
             const int ks = min(TCKC, kp - kc * TCKC) / 32;
             for (int s2 = 0; s2 < ks; ++s2) {
               const uint64_t ad = tc::smem_desc_sw128(sA + st * TCM * TCKC + 32 * s2);
@@ -2090,10 +2104,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_refine_kernel(const __grid_c
             }
             tc::commit(&empty[st]);
             if (kc == nkc - 1) tc::commit(&accf[ab]);
+            if (a.prof) atomicAdd(a.prof + 4, (unsigned long long)(clock64() - ti));
           }
           __syncwarp();
         }
       }
+      if (a.prof && lane == 0) a_grp_end = clock64();
     } else {
       // ---- epilogue: row r of the tile is TMEM lane r
       const int quarter = wid & 3;
@@ -2128,6 +2144,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_refine_kernel(const __grid_c
   }
   tc::fence_before_sync();
   __syncthreads();
+  if (a.prof && tid == 0) atomicAdd(a.prof + 3, (unsigned long long)(clock64() - t_start));
   if (wid == TC_PROD) tc::tmem_dealloc(tbase, tmem_cols(2 * N));
 }
 
@@ -2690,7 +2707,10 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
     int64_t tot[2] = {0, 0};
     if (excl == 2) {
       tot[0] = 0;
-    } else if (index->max_list > 0 && npairs * scan::ip_row_stride(index->max_list) <= (int64_t(1) << 28)) {
+    } else if (index->max_list > 0 &&
+               npairs * scan::ip_row_stride(index->max_list) * (ipb + (rd_path && refine ? 8 : 0)) <=
+                   (int64_t(8) << 30)) {
+      // bound without a host round trip while the buffers stay within 8 GiB of the 180 GB of HBM
       tot[0] = npairs * scan::ip_row_stride(index->max_list);
     } else if (cudaMemcpyAsync(tot, ptot, sizeof(tot), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
                cudaStreamSynchronize(s) != cudaSuccess) {
@@ -2757,9 +2777,25 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
         if (cudaFuncSetAttribute(scan::tc_refine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm) !=
             cudaSuccess)
           return fail(IVRQ_EUNSUP, "ivrq_search_scan: dims too large for the tensor-core refine");
+        static const bool tprof = getenv("IVRQ_TC_PROF") != nullptr;
+        if (tprof) {
+          cudaMalloc(reinterpret_cast<void**>(&ta.prof), 8 * sizeof(unsigned long long));
+          cudaMemset(ta.prof, 0, 8 * sizeof(unsigned long long));
+        }
         fd_launch = [ta, tsm, s]() {
           scan::tc_refine_kernel<<<(unsigned)sm_count_of_current_device(), scan::TC_THREADS, tsm, s>>>(ta);
-          return check_launch("ivrq_search_scan(tensor-core refine)");
+          const int rc = check_launch("ivrq_search_scan(tensor-core refine)");
+          if (ta.prof) {  // debugging aid (synchronises): where the MMA lane waited
+            unsigned long long h[8];
+            cudaMemcpy(h, ta.prof, sizeof(h), cudaMemcpyDeviceToHost);
+            const double tot = (double)h[3];
+            fprintf(stderr,
+                    "[ivrq tc_refine] MMA lane (share of CTA cycles): wait B %.3f, wait accumulator %.3f, wait A %.3f, "
+                    "issue %.3f, group switch %.3f\n",
+                    h[0] / tot, h[1] / tot, h[2] / tot, h[4] / tot, h[5] / tot);
+            cudaFree(ta.prof);
+          }
+          return rc;
         };
         a.rdist = rdist;
       }

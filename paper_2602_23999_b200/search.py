@@ -221,7 +221,7 @@ def _rows_to_lists(ids: np.ndarray, dists: np.ndarray, counts: np.ndarray) -> li
     """
     k = ids.shape[1]
     if counts.size and int(counts.min()) == k:
-        return list(zip(ids, dists))
+        return list(zip(list(ids), list(dists)))
     return [(ids[i, :n], dists[i, :n]) for i, n in enumerate(counts.tolist())]
 
 

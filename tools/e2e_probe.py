@@ -63,7 +63,7 @@ def main() -> None:
     assert len(out) == len(out2)
     import os
 
-    for nqs in (2500, 5000, 10000):
+    for nqs in (2000, 3000, 5000, 7000, 10000):
         ts = []
         for _ in range(args.reps):
             torch.cuda.synchronize()
@@ -72,6 +72,37 @@ def main() -> None:
             torch.cuda.synchronize()
             ts.append(time.perf_counter() - t0)
         print(f"device search of {nqs} queries: {1e3*np.median(ts):.2f} ms", file=sys.stderr)
+    # host enqueue time of one search (no sync) vs its device time
+    for _ in range(3):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        S.search_device(q, ix, sp)
+        t1 = time.perf_counter()
+        torch.cuda.synchronize()
+        t2 = time.perf_counter()
+        print(f"enqueue {1e3*(t1-t0):.2f} ms, until done {1e3*(t2-t0):.2f} ms", file=sys.stderr)
+    # per C-ABI call host time within one search (enqueue only)
+    from paper_2602_23999_b200 import _lib
+    orig = _lib.call
+    acc = {}
+
+    def timed(name, *a):
+        t0 = time.perf_counter()
+        orig(name, *a)
+        acc[name] = acc.get(name, 0.0) + time.perf_counter() - t0
+
+    _lib.call = timed
+    S._lib.call = timed
+    for _ in range(3):
+        torch.cuda.synchronize()
+        acc.clear()
+        t0 = time.perf_counter()
+        S.search_device(q, ix, sp)
+        tot = time.perf_counter() - t0
+        torch.cuda.synchronize()
+    _lib.call = orig
+    S._lib.call = orig
+    print("enqueue split (ms): " + ", ".join(f"{k} {1e3*v:.3f}" for k, v in acc.items()) + f", python rest {1e3*(tot-sum(acc.values())):.3f}", file=sys.stderr)
     # host-side pieces of the pipeline
     pin = torch.empty(q_host.nbytes, dtype=torch.uint8, pin_memory=True).numpy().view(np.float32).reshape(q_host.shape)
     t0 = time.perf_counter(); np.copyto(pin, q_host); t1 = time.perf_counter()
@@ -79,7 +110,7 @@ def main() -> None:
     ids_h, d_h, c_h = dev.to_host(res.ids), dev.to_host(res.dists), dev.to_host(res.counts)
     t0 = time.perf_counter(); out4 = S._rows_to_lists(ids_h.copy(), d_h.copy(), c_h.copy()); t1 = time.perf_counter()
     print(f"result lists: {1e3*(t1-t0):.2f} ms", file=sys.stderr)
-    for chunks in (1, 2, 3, 4):
+    for chunks in (1, 2, 3):
         os.environ["IVRQ_E2E_CHUNKS"] = str(chunks)
         ts = []
         for _ in range(args.reps):

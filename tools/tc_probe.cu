@@ -173,6 +173,60 @@ int run_tma() {
   return bad != 0;
 }
 
+// throughput: every SM issues REPS x (K/32) MMAs (M=128, N, K=32) from smem into one accumulator
+template <int N>
+__global__ void __launch_bounds__(128) mma_rate(long long* out, int reps) {
+  extern __shared__ __align__(1024) unsigned char sm_raw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>(((uintptr_t)sm_raw + 1023) & ~(uintptr_t)1023);
+  __shared__ uint64_t bar;
+  __shared__ uint32_t taddr_s;
+  const int tid = threadIdx.x, wid = tid >> 5;
+  for (int i = tid; i < (128 + N) * 128; i += 128) sm[i] = (unsigned char)(i * 7);
+  if (wid == 0) tc::tmem_alloc(&taddr_s, N < 32 ? 32 : N);
+  if (tid == 0) {
+    tc::mbar_init(&bar, 1);
+    tc::fence_mbar_init();
+  }
+  tc::fence_smem_async();
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  if (tid == 0) {
+    const uint32_t idesc = tc::idesc_i8(M, N, false, true);
+    const long long t0 = clock64();
+    for (int r = 0; r < reps; ++r)
+      for (int s2 = 0; s2 < 4; ++s2)
+        tc::mma_i8(taddr_s, tc::smem_desc_sw128(sm + 32 * s2), tc::smem_desc_sw128(sm + 128 * 128 + 32 * s2), idesc,
+                   r | s2);
+    const long long t1 = clock64();
+    tc::commit(&bar);
+    tc::mbar_wait(&bar, 0);
+    const long long t2 = clock64();
+    out[2 * blockIdx.x] = t1 - t0;
+    out[2 * blockIdx.x + 1] = t2 - t0;
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (wid == 0) tc::tmem_dealloc(taddr_s, N < 32 ? 32 : N);
+}
+
+template <int N>
+void rate() {
+  const int reps = 2000, blocks = 148;
+  long long* d;
+  cudaMalloc(&d, blocks * 16);
+  const int smem = (128 + N) * 128 + 1024;
+  cudaFuncSetAttribute(mma_rate<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  mma_rate<N><<<blocks, 128, smem>>>(d, reps);
+  cudaDeviceSynchronize();
+  std::vector<long long> h(2 * blocks);
+  cudaMemcpy(h.data(), d, h.size() * 8, cudaMemcpyDeviceToHost);
+  const double n_mma = 4.0 * reps;
+  printf("int8 MMA M=128 N=%d K=32: issue %.1f clk/MMA, complete %.1f clk/MMA -> %.0f MAC/clk/SM\n", N,
+         h[0] / n_mma, h[1] / n_mma, 128.0 * N * 32 / (h[1] / n_mma));
+  cudaFree(d);
+}
+
 template <int N, int K>
 int run() {
   std::vector<uint8_t> A(M * K);
@@ -224,5 +278,8 @@ int main() {
   rc |= run_tma<128, 256>();
   rc |= run_tma<64, 384>();
   rc |= run_tma<256, 128>();
+  rate<64>();
+  rate<128>();
+  rate<256>();
   return rc;
 }
