@@ -130,9 +130,9 @@ class DeviceResult:
     stats: torch.Tensor | None  # (nq, 2) int64: vectors probed, stage-1 survivors
 
 
-def rotate_queries_device(q: torch.Tensor, index: IvfRabitqIndex) -> torch.Tensor:
+def rotate_queries_device(q: torch.Tensor, index: IvfRabitqIndex, out: torch.Tensor | None = None) -> torch.Tensor:
     nq, d = q.shape
-    q_rot = torch.empty((nq, d), dtype=torch.float64, device=q.device)
+    q_rot = torch.empty((nq, d), dtype=torch.float64, device=q.device) if out is None else out
     if nq:
         _lib.call(
             "ivrq_rotate_queries",
@@ -244,6 +244,7 @@ def _pinned(device: torch.device, name: str, nbytes: int) -> torch.Tensor:
 
 
 _STAGE_THREADS = 4
+_STAGE_PIECES = 4  # host->device pieces of a single-batch search (copy / transfer / rotation overlap)
 _POOL = None
 
 
@@ -263,8 +264,12 @@ def _chunk_bounds(nq: int) -> list[int]:
     small enough that host work on one chunk hides behind the next chunk's kernels."""
     import os
 
+    split = os.environ.get("IVRQ_E2E_SPLIT")  # e.g. "0.7": two chunks, the first 70% of the queries
+    if split and nq >= 4096:
+        a = int(nq * float(split))
+        return [0, a, nq] if 0 < a < nq else [0, nq]
     env = os.environ.get("IVRQ_E2E_CHUNKS")
-    n = int(env) if env else (1 if nq < 4096 else 2)
+    n = int(env) if env else 1  # each chunk re-streams the index (list-major kernels): one batch
     n = max(1, min(n, nq))
     return [nq * i // n for i in range(n + 1)]
 
@@ -313,6 +318,45 @@ def _search_pipelined(q: np.ndarray, index: IvfRabitqIndex, params: SearchParams
         parts = np.linspace(a, b, _STAGE_THREADS + 1).astype(np.int64)
         pool = _stage_pool()
         return [pool.submit(np.copyto, pin_q_np[x:y], q[x:y]) for x, y in zip(parts[:-1], parts[1:]) if y > x]
+
+    def stage_rotate(a: int, b: int, q_rot: torch.Tensor) -> None:
+        # pieces: host copy of piece p+1 runs while piece p is transferred and rotated
+        pieces = np.linspace(a, b, _STAGE_PIECES + 1).astype(np.int64)
+        pool = _stage_pool()
+        futs = [pool.submit(np.copyto, pin_q_np[x:y], q[x:y]) for x, y in zip(pieces[:-1], pieces[1:])]
+        for (x, y), f in zip(zip(pieces[:-1], pieces[1:]), futs):
+            f.result()
+            if y > x:
+                qd[x:y].copy_(pin_q_t[x:y], non_blocking=True)
+                rotate_queries_device(qd[x:y], index, out=q_rot[x - a : y - a])
+
+    if len(bounds) == 2:  # one batch: staging, transfer and rotation overlap piecewise
+        import os
+        import time
+
+        trace = os.environ.get("IVRQ_E2E_TRACE")
+        t0 = time.perf_counter()
+        with torch.cuda.stream(stream):
+            q_rot = torch.empty((nq, d), dtype=torch.float64, device=device)
+            stage_rotate(0, nq, q_rot)
+            t1 = time.perf_counter()
+            res = search_device(None, index, params, q_rot=q_rot)
+            ids_t.copy_(res.ids, non_blocking=True)
+            dists_t.copy_(res.dists, non_blocking=True)
+            counts_t.copy_(res.counts, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(stream)
+            t2 = time.perf_counter()
+            ev.synchronize()
+            t3 = time.perf_counter()
+            finish(0, nq, ev)
+            t4 = time.perf_counter()
+        if trace:
+            import sys
+
+            print(f"[e2e] staged+rotate-enqueued {1e3*(t1-t0):.2f} enqueue {1e3*(t2-t1):.2f} "
+                  f"gpu-wait {1e3*(t3-t2):.2f} lists {1e3*(t4-t3):.2f} ms", file=sys.stderr)
+        return results
 
     with torch.cuda.stream(stream):
         pending = stage(0)

@@ -110,6 +110,37 @@ def main() -> None:
     ids_h, d_h, c_h = dev.to_host(res.ids), dev.to_host(res.dists), dev.to_host(res.counts)
     t0 = time.perf_counter(); out4 = S._rows_to_lists(ids_h.copy(), d_h.copy(), c_h.copy()); t1 = time.perf_counter()
     print(f"result lists: {1e3*(t1-t0):.2f} ms", file=sys.stderr)
+    import cProfile
+    import pstats
+
+    pr = cProfile.Profile()
+    pr.enable()
+    for _ in range(3):
+        iv.search_batch(q_host, ix, sp)
+    pr.disable()
+    pstats.Stats(pr, stream=sys.stderr).sort_stats("tottime").print_stats(12)
+    for thr in (4, 8, 16):
+        S._STAGE_THREADS = thr
+        S._POOL = None
+        ts = []
+        for _ in range(args.reps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            iv.search_batch(q_host, ix, sp)
+            ts.append(time.perf_counter() - t0)
+        print(f"stage threads {thr}: search_batch {1e3*np.median(ts):.2f} ms", file=sys.stderr)
+    S._STAGE_THREADS = 4
+    S._POOL = None
+    for split in ():
+        os.environ["IVRQ_E2E_SPLIT"] = split
+        ts = []
+        for _ in range(args.reps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            out3 = iv.search_batch(q_host, ix, sp)
+            ts.append(time.perf_counter() - t0)
+        print(f"split {split}: search_batch {1e3*np.median(ts):.2f} ms", file=sys.stderr)
+    os.environ.pop("IVRQ_E2E_SPLIT", None)
     for chunks in (1, 2, 3):
         os.environ["IVRQ_E2E_CHUNKS"] = str(chunks)
         ts = []
@@ -122,5 +153,37 @@ def main() -> None:
         print(f"chunks {chunks}: search_batch {1e3*np.median(ts):.2f} ms  identical={same}", file=sys.stderr)
 
 
+
+
+def host_register_probe():
+    """cudaHostRegister of a 30 MB numpy buffer vs staging copies (run standalone)."""
+    import ctypes
+
+    q = np.random.rand(10000, 768).astype(np.float32)
+    cud = ctypes.CDLL("libcudart.so") if False else None
+    rt = torch.cuda.cudart()
+    dst = torch.empty(q.shape, dtype=torch.float32, device="cuda")
+    for _ in range(3):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        rt.cudaHostRegister(q.ctypes.data, q.nbytes, 0)
+        t1 = time.perf_counter()
+        dst.copy_(torch.from_numpy(q), non_blocking=True)
+        torch.cuda.synchronize()
+        t2 = time.perf_counter()
+        rt.cudaHostUnregister(q.ctypes.data)
+        t3 = time.perf_counter()
+        print(f"register {1e3*(t1-t0):.2f} ms, dma {1e3*(t2-t1):.2f} ms, unregister {1e3*(t3-t2):.2f} ms", file=sys.stderr)
+    for _ in range(2):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        dst.copy_(torch.from_numpy(q))
+        torch.cuda.synchronize()
+        print(f"pageable copy {1e3*(time.perf_counter()-t0):.2f} ms", file=sys.stderr)
+
+
 if __name__ == "__main__":
-    main()
+    if "--register" in sys.argv:
+        host_register_probe()
+    else:
+        main()
