@@ -887,8 +887,8 @@ __global__ void __launch_bounds__(WQ * 32, MINB) scan_warp_kernel(Args a) {
 // to the warp's register queue (the pool).  No shared memory, few registers.
 constexpr int RDW = 4;    // queries (warps) per CTA
 
-template <bool REFINE, int IPB, int RSUB>
-__global__ void __launch_bounds__(RDW * 32) scan_rd_kernel(Args a) {
+template <bool REFINE, int IPB, int RSUB, int MINB = 1>
+__global__ void __launch_bounds__(RDW * 32, MINB) scan_rd_kernel(Args a) {
   using IPT = typename std::conditional<IPB == 2, int16_t, int32_t>::type;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t slot_q = (int64_t)blockIdx.x * RDW + wid;
@@ -2411,15 +2411,20 @@ __global__ void merge_topk_kernel(const int64_t* __restrict__ ids, const double*
   out_counts[q] = n;
 }
 
-template <int RS>
+template <int RS, int MB = 1>
 inline auto rd_kernel_for(bool refine, int ipb) {
-  return refine ? (ipb == 2 ? scan_rd_kernel<true, 2, RS> : scan_rd_kernel<true, 4, RS>)
-                : (ipb == 2 ? scan_rd_kernel<false, 2, RS> : scan_rd_kernel<false, 4, RS>);
+  return refine ? (ipb == 2 ? scan_rd_kernel<true, 2, RS, MB> : scan_rd_kernel<true, 4, RS, MB>)
+                : (ipb == 2 ? scan_rd_kernel<false, 2, RS, MB> : scan_rd_kernel<false, 4, RS, MB>);
 }
 
 inline int launch_rd(const Args& a, bool refine, int ipb, cudaStream_t s) {
   static const int rsub = getenv("IVRQ_RD_SUB") ? atoi(getenv("IVRQ_RD_SUB")) : 4;  // 32-vector sub-chunks per batch
-  auto kern = rsub == 8 ? rd_kernel_for<8>(refine, ipb) : rsub == 2 ? rd_kernel_for<2>(refine, ipb) : rd_kernel_for<4>(refine, ipb);
+  static const int rminb = getenv("IVRQ_RD_MINB") ? atoi(getenv("IVRQ_RD_MINB")) : 6;  // B200 A/B: 1, 6, 8
+  auto kern = rsub == 8 ? rd_kernel_for<8>(refine, ipb)
+              : rsub == 2 ? (rminb == 8 ? rd_kernel_for<2, 8>(refine, ipb) : rd_kernel_for<2>(refine, ipb))
+              : rminb == 8 ? rd_kernel_for<4, 8>(refine, ipb)
+              : rminb == 6 ? rd_kernel_for<4, 6>(refine, ipb)
+                           : rd_kernel_for<4>(refine, ipb);
   kern<<<(unsigned)ceil_div(a.nq, RDW), RDW * 32, 0, s>>>(a);
   return check_launch("ivrq_search_scan");
 }
