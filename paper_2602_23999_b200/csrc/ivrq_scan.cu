@@ -71,6 +71,11 @@ struct Args {
   const int64_t* fbase;
   const int64_t* qoff;
   int l2_prefetch;  // warp kernel: L2 prefetch of survivor rcode rows
+  // per (query, probe) list metadata (probe_meta_kernel), so the warp kernels prefetch the next
+  // list's CSR bounds and row base one list ahead instead of chaining dependent loads per list
+  const int64_t* m_lo;      // [nq * nprobe] first row of the probed list
+  const int32_t* m_nc;      // [nq * nprobe] its size, -1 = another shard's list
+  const int64_t* m_base;    // [nq * nprobe] (list, query) pair row base in ipbuf / rdist
   const double* rdist;  // refined distance of every probed (pair, vector) (tc_refine_kernel), or null
   int rd_prefetch;      // scan_rd_kernel: read every vector's refined distance with its stage-1 inputs
 };
@@ -576,6 +581,40 @@ __global__ void __launch_bounds__(THREADS, 4) scan_kernel(Args a) {
   }
 }
 
+// ------------------------------------------------------------ per-probe metadata
+__global__ void probe_meta_kernel(Args a, int64_t* __restrict__ m_lo, int32_t* __restrict__ m_nc,
+                                  int64_t* __restrict__ m_base) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.nq * a.nprobe) return;
+  const int64_t cg = a.probe_ids[i];
+  if (cg < a.list_lo || cg >= a.list_hi) {
+    m_nc[i] = -1;
+    m_lo[i] = 0;
+    m_base[i] = 0;
+    return;
+  }
+  const int64_t c = cg - a.list_lo;
+  const int64_t lo = a.ix.offsets[c], n_c = a.ix.offsets[c + 1] - lo;
+  m_lo[i] = lo;
+  m_nc[i] = (int32_t)n_c;
+  m_base[i] = a.pslot ? a.pair_base[c] + (int64_t)a.pslot[i] * ip_row_stride(n_c) : 0;
+}
+
+struct ListMeta {
+  int64_t lo, base;
+  int32_t nc;
+  double d2;
+};
+
+__device__ __forceinline__ ListMeta list_meta(const Args& a, int64_t qp) {
+  ListMeta m;
+  m.lo = __ldg(a.m_lo + qp);
+  m.nc = __ldg(a.m_nc + qp);
+  m.base = __ldg(a.m_base + qp);
+  m.d2 = __ldg(a.probe_d2 + qp);
+  return m;
+}
+
 // ------------------------------------------------------------ warp-per-query kernel (precomputed inner products)
 // With the stage-1 inner products already in HBM (ip_list_kernel) a query's
 // remaining work is a light stream (2-byte ip + 8-byte factors per vector)
@@ -739,17 +778,17 @@ __global__ void __launch_bounds__(WQ * 32, MINB) scan_warp_kernel(Args a) {
   long long probed = (a.skip_first && a.stats) ? a.stats[2 * q] : 0;
   long long surv = (a.skip_first && a.stats) ? a.stats[2 * q + 1] : 0;
   __syncwarp();
-  const int64_t* pid_list = a.probe_ids + q * a.nprobe;
-  const double* pd2_list = a.probe_d2 + q * a.nprobe;
   bool first_pending = true;  // the first in-range probe is still ahead
+  ListMeta nxt = list_meta(a, q * a.nprobe);
   for (int p = 0; p < a.nprobe; ++p) {  // ascending cluster id (search.py:429)
-    const int64_t cg = pid_list[p];
-    if (cg < a.list_lo || cg >= a.list_hi) continue;
+    const ListMeta cur = nxt;
+    if (p + 1 < a.nprobe) nxt = list_meta(a, q * a.nprobe + p + 1);  // prefetched one list ahead
+    if (cur.nc < 0) continue;  // another shard's list
     const bool is_first = first_pending;
     first_pending = false;
-    const int64_t c = cg - a.list_lo;
-    const double d_qc2 = pd2_list[p];
-    const int64_t lo = a.ix.offsets[c], n_c = a.ix.offsets[c + 1] - lo;
+    const int64_t c = a.probe_ids[q * a.nprobe + p] - a.list_lo;
+    const double d_qc2 = cur.d2;
+    const int64_t lo = cur.lo, n_c = cur.nc;
     if (n_c == 0) continue;
     const double T_list = a.prune ? T : dinf();
     probed += n_c;
@@ -776,8 +815,7 @@ __global__ void __launch_bounds__(WQ * 32, MINB) scan_warp_kernel(Args a) {
       continue;
     }
     const double sq = dsqrt(d_qc2);
-    const IPT* iprow =
-        reinterpret_cast<const IPT*>(a.ipbuf) + a.pair_base[c] + a.pslot[q * a.nprobe + p] * ip_row_stride(n_c);
+    const IPT* iprow = reinterpret_cast<const IPT*>(a.ipbuf) + cur.base;
     int head = 0, nb = 0;  // ring of pending survivors (warp-uniform)
     for (int64_t c0 = 0; c0 < n_c; c0 += 32 * SUB) {
       // loads of SUB sub-chunks first (ip, add, scale, err), then the tests
@@ -902,18 +940,16 @@ __global__ void __launch_bounds__(RDW * 32, MINB) scan_rd_kernel(Args a) {
   int64_t qi = lane < init_n ? a.init_ids[q * k + lane] : NO_ID;
   double T = init_n >= k ? __shfl_sync(FULL, qd, k - 1) : dinf();
   long long probed = 0, surv = 0;
-  const int64_t* pid_list = a.probe_ids + q * a.nprobe;
-  const double* pd2_list = a.probe_d2 + q * a.nprobe;
+  ListMeta nxt = list_meta(a, q * a.nprobe);
   for (int p = 0; p < a.nprobe; ++p) {  // ascending cluster id (search.py:429)
-    const int64_t cg = pid_list[p];
-    if (cg < a.list_lo || cg >= a.list_hi) continue;
-    const int64_t c = cg - a.list_lo;
-    const int64_t lo = a.ix.offsets[c], n_c = a.ix.offsets[c + 1] - lo;
-    if (n_c == 0) continue;
-    const double d_qc2 = pd2_list[p];
+    const ListMeta cur = nxt;
+    if (p + 1 < a.nprobe) nxt = list_meta(a, q * a.nprobe + p + 1);  // prefetched one list ahead
+    if (cur.nc <= 0) continue;  // another shard's list, or empty
+    const int64_t lo = cur.lo, n_c = cur.nc;
+    const double d_qc2 = cur.d2;
     const double T_list = a.prune ? T : dinf();
     probed += n_c;
-    const int64_t rowbase = a.pair_base[c] + (int64_t)a.pslot[q * a.nprobe + p] * ip_row_stride(n_c);
+    const int64_t rowbase = cur.base;
     const double* rrow = REFINE ? a.rdist + rowbase : nullptr;
     if (REFINE && T_list == dinf()) {  // nothing can be pruned (lb2 <= +inf): every vector's refined distance
       surv += n_c;
@@ -2868,10 +2904,29 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
     a.pair_base = pbase;
   }
   if (fd_launch) IVRQ_TRY(fd_launch());
+  int64_t *m_lo = nullptr, *m_base = nullptr;
+  int32_t* m_nc = nullptr;
+  if (warp_path) {  // both warp kernels walk the per-probe metadata
+    const int64_t np = nq * a.nprobe;
+    if (cudaMallocAsync(reinterpret_cast<void**>(&m_lo), np * sizeof(int64_t), s) != cudaSuccess ||
+        cudaMallocAsync(reinterpret_cast<void**>(&m_base), np * sizeof(int64_t), s) != cudaSuccess ||
+        cudaMallocAsync(reinterpret_cast<void**>(&m_nc), np * sizeof(int32_t), s) != cudaSuccess)
+      return fail(IVRQ_ENOMEM, "ivrq_search_scan: workspace allocation failed");
+    scan::probe_meta_kernel<<<(unsigned)ceil_div(np, 256), 256, 0, s>>>(a, m_lo, m_nc, m_base);
+    IVRQ_TRY(check_launch("ivrq_search_scan(probe metadata)"));
+    a.m_lo = m_lo;
+    a.m_nc = m_nc;
+    a.m_base = m_base;
+  }
   const int rc = params->ip_mode == IVRQ_IP_BITWISE
                      ? (rd_path && a.ipbuf ? scan::launch_rd(a, refine, ipb, s)
                                            : scan::launch_mode<IVRQ_IP_BITWISE>(a, refine, nib, warp_path ? -ipb : ipb, s))
                                                     : scan::launch_mode<IVRQ_IP_LUT>(a, refine, nib, 0, s);
+  if (m_lo) {
+    cudaFreeAsync(m_lo, s);
+    cudaFreeAsync(m_base, s);
+    cudaFreeAsync(m_nc, s);
+  }
   if (tcsl) cudaFreeAsync(tcsl, s);
   if (qpairs) {
     cudaFreeAsync(qpairs, s);
