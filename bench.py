@@ -422,9 +422,15 @@ def cpu_baseline(index, q_host, gt, sp, budget_s=20.0) -> dict:
     """The oracle (NumPy restatement of the reference) on a bounded query sample, 1 host thread."""
     from oracle import ivrq_oracle as orc
 
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    from threadpoolctl import threadpool_limits
+
     ix = _host_index_arrays(index)
     codes = orc.decode_codes(ix) if ix["bits"] > 1 else None
+    with threadpool_limits(1):  # 1 host thread, BLAS included (the reference default, IVRQ_THREADS=1)
+        return _cpu_baseline_timed(orc, ix, codes, q_host, gt, sp, budget_s)
+
+
+def _cpu_baseline_timed(orc, ix, codes, q_host, gt, sp, budget_s) -> dict:
     t = time.perf_counter()
     orc.search(q_host[:4], ix, sp.k, sp.n_probe, ip_mode=sp.ip_mode, query_bits=sp.query_bits, codes=codes)
     per_q = max((time.perf_counter() - t) / 4, 1e-4)
@@ -448,13 +454,19 @@ def cpu_baseline(index, q_host, gt, sp, budget_s=20.0) -> dict:
 # ---------------------------------------------------------------- reference arm
 
 
+_REF_INDEX: dict = {}  # set before the worker pool forks: the index is inherited, never pickled per task
+
+
 def _ref_worker(payload):
     from oracle import ivrq_oracle as orc
 
-    ix, codes, qs, k, nprobe, mode, qbits = payload
-    t = time.perf_counter()
-    orc.search(qs, ix, k, nprobe, ip_mode=mode, query_bits=qbits, codes=codes)
-    return len(qs), time.perf_counter() - t
+    from threadpoolctl import threadpool_limits
+
+    qs, k, nprobe, mode, qbits = payload
+    with threadpool_limits(1):  # one BLAS thread per process (the reference's fastest setting)
+        t = time.perf_counter()
+        orc.search(qs, _REF_INDEX["ix"], k, nprobe, ip_mode=mode, query_bits=qbits, codes=_REF_INDEX["codes"])
+        return len(qs), time.perf_counter() - t
 
 
 def run_reference(args, cfg_name: str) -> dict:
@@ -491,13 +503,14 @@ def run_reference(args, cfg_name: str) -> dict:
     per_step = max(cores, int(args.ref_queries_per_step))
     ctx = mp.get_context("fork")
     step_qps = []
+    _REF_INDEX["ix"], _REF_INDEX["codes"] = ix, codes
     with ctx.Pool(cores) as pool:
         for step in range(args.warmup + args.steps):
             lo = (step * per_step) % NQ
             qs = q_host[lo : lo + per_step]
             chunks = np.array_split(qs, cores)
             t = time.perf_counter()
-            pool.map(_ref_worker, [(ix, codes, c, K, nprobe, args.mode, 4) for c in chunks if len(c)])
+            pool.map(_ref_worker, [(c, K, nprobe, args.mode, 4) for c in chunks if len(c)])
             dt = time.perf_counter() - t
             if step >= args.warmup:
                 step_qps.append(len(qs) / dt)
@@ -534,7 +547,7 @@ def main() -> None:
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-nprobe", type=int, default=8)
-    ap.add_argument("--ref-queries-per-step", type=int, default=64)
+    ap.add_argument("--ref-queries-per-step", type=int, default=1024)
     ap.add_argument("--gt-queries", type=int, default=0, help="queries with exact ground truth (0 = all)")
     ap.add_argument("--build-breakdown", action="store_true", help="rebuild once with per-stage timings")
     args = ap.parse_args()
