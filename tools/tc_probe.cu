@@ -173,6 +173,106 @@ int run_tma() {
   return bad != 0;
 }
 
+// TS form: A (128 x K, u8) TMA-loaded (SW128) then tcgen05.cp'd into TMEM, B (N x K, s8) from smem
+template <int N, int K>
+__global__ void __launch_bounds__(128) probe_ts(const __grid_constant__ CUtensorMap ma,
+                                                 const __grid_constant__ CUtensorMap mb, int* D) {
+  extern __shared__ __align__(1024) unsigned char sm_raw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>(((uintptr_t)sm_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sa = sm;
+  int8_t* sb = reinterpret_cast<int8_t*>(sm + (K / 128) * M * 128);
+  __shared__ uint64_t bar, mbar;
+  __shared__ uint32_t taddr_s;
+  const int tid = threadIdx.x, wid = tid >> 5;
+  constexpr int ACOLS = K / 4;  // A in TMEM: K bytes per lane
+  constexpr int NC = (ACOLS + N) <= 32 ? 32 : (ACOLS + N) <= 64 ? 64 : (ACOLS + N) <= 128 ? 128 : (ACOLS + N) <= 256 ? 256 : 512;
+  if (wid == 0) tc::tmem_alloc(&taddr_s, NC);
+  if (tid == 0) {
+    tc::mbar_init(&bar, 1);
+    tc::mbar_init(&mbar, 1);
+    tc::fence_mbar_init();
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  if (tid == 0) {
+    tc::mbar_expect_tx(&bar, (K / 128) * (M + N) * 128);
+    for (int c = 0; c < K / 128; ++c) {
+      tc::tma_load_2d(sa + c * M * 128, &ma, c * 128, 0, &bar);
+      for (int r0 = 0; r0 < N; r0 += 128) tc::tma_load_2d(sb + c * N * 128 + r0 * 128, &mb, c * 128, r0, &bar);
+    }
+  }
+  tc::mbar_wait(&bar, 0);
+  tc::fence_after_sync();
+  const uint32_t taddr = taddr_s;
+  const uint32_t ta = taddr + N;  // A columns after the accumulator
+  if (tid == 0) {
+    for (int s = 0; s < K / 32; ++s) {
+      const int c = s / 4, off = (s % 4) * 32;
+      tc::tmem_cp_128x256b(ta + 8 * s, tc::smem_desc_sw128(sa + c * M * 128 + off));
+    }
+    constexpr uint32_t idesc = tc::idesc_i8(M, N, false, true);
+    for (int s = 0; s < K / 32; ++s) {
+      const int c = s / 4, off = (s % 4) * 32;
+      tc::mma_i8_ts(taddr, ta + 8 * s, tc::smem_desc_sw128(sb + c * N * 128 + off), idesc, s > 0);
+    }
+    tc::commit(&mbar);
+  }
+  tc::mbar_wait(&mbar, 0);
+  tc::fence_after_sync();
+  for (int c0 = 0; c0 < N; c0 += 32) {
+    uint32_t v[32];
+    tc::tmem_ld32(taddr + ((uint32_t)(wid * 32) << 16) + c0, v);
+    tc::tmem_ld_wait();
+    for (int j = 0; j < 32; ++j) D[(wid * 32 + (tid & 31)) * N + c0 + j] = (int)v[j];
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (wid == 0) tc::tmem_dealloc(taddr, NC);
+}
+
+template <int N, int K>
+int run_ts() {
+  std::vector<uint8_t> A(M * K);
+  std::vector<int8_t> B(N * K);
+  srand(11);
+  for (auto& x : A) x = rand() & 255;
+  for (auto& x : B) x = (int8_t)(rand() & 255);
+  uint8_t* dA;
+  int8_t* dB;
+  int* dD;
+  cudaMalloc(&dA, A.size());
+  cudaMalloc(&dB, B.size());
+  cudaMalloc(&dD, M * N * 4);
+  cudaMemcpy(dA, A.data(), A.size(), cudaMemcpyHostToDevice);
+  cudaMemcpy(dB, B.data(), B.size(), cudaMemcpyHostToDevice);
+  CUtensorMap ma, mb;
+  tc::make_tmap_u8_sw128(&ma, dA, K, M, K, 128, 128);
+  tc::make_tmap_u8_sw128(&mb, dB, K, N, K, 128, N < 128 ? N : 128);
+  const int smem = (K / 128) * (M + N) * 128 + 1024;
+  cudaFuncSetAttribute(probe_ts<N, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  probe_ts<N, K><<<1, 128, smem>>>(ma, mb, dD);
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    printf("TS N=%d K=%d: CUDA error %s\n", N, K, cudaGetErrorString(e));
+    return 1;
+  }
+  std::vector<int> Dh(M * N);
+  cudaMemcpy(Dh.data(), dD, Dh.size() * 4, cudaMemcpyDeviceToHost);
+  int bad = 0;
+  for (int i = 0; i < M; ++i)
+    for (int j = 0; j < N; ++j) {
+      long long sacc = 0;
+      for (int k = 0; k < K; ++k) sacc += (long long)A[i * K + k] * B[j * K + k];
+      if (sacc != Dh[i * N + j]) {
+        if (bad < 5) printf("  mismatch (%d,%d): gpu %d cpu %lld\n", i, j, Dh[i * N + j], sacc);
+        ++bad;
+      }
+    }
+  printf("TS (A in TMEM via tcgen05.cp) N=%d K=%d: %d mismatches of %d\n", N, K, bad, M * N);
+  return bad != 0;
+}
+
 // throughput: every SM issues REPS x (K/32) MMAs (M=128, N, K=32) from smem into one accumulator
 template <int N>
 __global__ void __launch_bounds__(128) mma_rate(long long* out, int reps) {
@@ -278,6 +378,8 @@ int main() {
   rc |= run_tma<128, 256>();
   rc |= run_tma<64, 384>();
   rc |= run_tma<256, 128>();
+  rc |= run_ts<128, 256>();
+  rc |= run_ts<64, 128>();
   rate<64>();
   rate<128>();
   rate<256>();
