@@ -2184,6 +2184,249 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_refine_kernel(const __grid_c
   if (wid == TC_PROD) tc::tmem_dealloc(tbase, tmem_cols(2 * N));
 }
 
+// ------------------------------------------------------------ refine, A operand in TMEM (TS form)
+// Same result as tc_refine_kernel with the roles swapped so the tensor core reads
+// only one operand from shared memory: the group's digit slices (M = 128 rows =
+// 16 queries x 8 digits) are staged once per group by TMA and copied into TMEM
+// (tcgen05.cp); every rcode tile (N = 128 vectors, TMA ring) then meets them in a
+// TS-form MMA.  Per MMA the SMEM traffic is the rcode tile only (written by TMA,
+// read once), which the int8 peak can sustain; the SS form also re-read the
+// resident slices.  The epilogue thread of TMEM lane 8 j + s holds digit s of
+// query j for 32 vectors at a time; the 8 digit lanes of a query are reduced by
+// a transposed shuffle tree (hi = digits 0-3, lo = digits 4-7, exact int64) and
+// each lane finishes 4 vectors with refine_chunk's float64 arithmetic.
+constexpr int TSG = 16;  // queries per group: M = 128 digit rows
+
+size_t tc_ts_smem_bytes(int kpad) {
+  const int nkc = (kpad + TCKC - 1) / TCKC;
+  return 1024 + (size_t)nkc * 128 * TCKC + (size_t)TCST * TCM * TCKC + 64 * TSG + 256 + 2 * TCM * 8;
+}
+
+__global__ void __launch_bounds__(TC_THREADS, 1) tc_refine_ts_kernel(const __grid_constant__ TcArgs a) {
+  extern __shared__ __align__(1024) unsigned char tsm_raw[];
+  unsigned char* tsm = reinterpret_cast<unsigned char*>(((uintptr_t)tsm_raw + 1023) & ~(uintptr_t)1023);
+  const int kp = a.kpad;
+  const int nkc = (kp + TCKC - 1) / TCKC;
+  int8_t* sB = reinterpret_cast<int8_t*>(tsm);                                   // [nkc][128 rows x 128 B] slices
+  uint8_t* sA = reinterpret_cast<uint8_t*>(tsm + (size_t)nkc * 128 * TCKC);      // [TCST][128 vectors x 128 B]
+  double* s_dq = reinterpret_cast<double*>(sA + TCST * TCM * TCKC);              // [TSG]
+  double* s_kb = s_dq + TSG;
+  double* s_hs = s_kb + TSG;
+  double* s_ls = s_hs + TSG;
+  int64_t* s_row = reinterpret_cast<int64_t*>(s_ls + TSG);
+  float2* s_lf = reinterpret_cast<float2*>(s_row + TSG);                         // [2][TCM] long factors of the tile
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_lf + 2 * TCM);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + TCST;
+  uint64_t* accf = bars + 2 * TCST;
+  uint64_t* acce = bars + 2 * TCST + 2;
+  uint64_t* bfull = bars + 2 * TCST + 4;
+  uint32_t* s_taddr = reinterpret_cast<uint32_t*>(bars + 2 * TCST + 5);
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid == 0) {
+    for (int i = 0; i < TCST; ++i) {
+      tc::mbar_init(&full[i], a.nib ? 32 * TC_PROD : 1);
+      tc::mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&accf[i], 1);
+      tc::mbar_init(&acce[i], 128);
+    }
+    tc::mbar_init(bfull, 1);
+    tc::fence_mbar_init();
+  }
+  if (wid == TC_PROD) tc::tmem_alloc(s_taddr, 512);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tbase = *s_taddr;      // accumulators: columns [0, 256)
+  const uint32_t tslices = tbase + 256; // the group's digit slices: kpad / 4 columns
+  const int64_t rb = a.ix.rcode_bytes;
+  const uint32_t idesc = tc::idesc_i8(128, TCM, true, false);  // A = slices (s8), B = rcodes (u8)
+  uint32_t it_prod = 0, it_mma = 0, tile_mma = 0, tile_epi = 0, grp = 0;
+  const int total = a.gpre[a.nlist];
+  for (int b = blockIdx.x; b < total; b += gridDim.x, ++grp) {
+    int lo_c = 0, hi_c = a.nlist;
+    while (hi_c - lo_c > 1) {
+      const int mid = (lo_c + hi_c) >> 1;
+      if (a.gpre[mid] <= b) lo_c = mid; else hi_c = mid;
+    }
+    const int c = lo_c;
+    const int64_t lo = a.ix.offsets[c], n_c = a.ix.offsets[c + 1] - lo;
+    const int64_t ps = a.poff[c] + (int64_t)(b - a.gpre[c]) * TSG;
+    const int nqg = (int)min((int64_t)TSG, a.poff[c + 1] - ps);
+    const int64_t rs = ip_row_stride(n_c);
+    const int ntile = (int)ceil_div(n_c, TCM);
+    __syncthreads();  // previous group's MMAs (and slice copies) completed, scalars consumed
+    if (wid == 0) {   // the group's digit slices: 8 rows per query, by TMA (one lane per query)
+      if (lane == 0) tc::mbar_expect_tx(bfull, (uint32_t)(nqg * nkc * 8 * TCKC));
+      __syncwarp();
+      if (lane < nqg) {
+        const int q8 = (int)((a.porder[ps + lane] / a.nprobe) * SLICES);
+        for (int kc = 0; kc < nkc; ++kc)
+          tc::tma_load_2d(sB + kc * 128 * TCKC + lane * 8 * TCKC, &a.map_b, kc * TCKC, q8, bfull);
+      }
+    }
+    if (tid < TSG) {
+      double dq = 0.0, kb = 0.0;
+      int e = 0;
+      int64_t row = 0;
+      if (tid < nqg) {
+        const int64_t pr = a.porder[ps + tid];
+        const int64_t q = pr / a.nprobe;
+        dq = a.probe_d2[pr];
+        kb = a.scalars[q * IVRQ_QS_COUNT + IVRQ_QS_KB_SUM];
+        e = (int)a.scalars[q * IVRQ_QS_COUNT + IVRQ_QS_SLICE_EXP];
+        row = a.pair_base[c] + (ps + tid - a.poff[c]) * rs;
+      }
+      s_dq[tid] = dq;
+      s_kb[tid] = kb;
+      s_hs[tid] = ldexp(1.0, e - 26);
+      s_ls[tid] = ldexp(1.0, e - 54);
+      s_row[tid] = row;
+    }
+    __syncthreads();
+    if (wid < TC_PROD) {
+      if (!a.nib) {
+        if (tid == 0) {
+          for (int t = 0; t < ntile; ++t)
+            for (int kc = 0; kc < nkc; ++kc, ++it_prod) {
+              const int st = it_prod % TCST;
+              tc::mbar_wait(&empty[st], ((it_prod / TCST) & 1) ^ 1);
+              tc::mbar_expect_tx(&full[st], TCM * TCKC);
+              tc::tma_load_2d(sA + st * TCM * TCKC, &a.map_a, kc * TCKC, (int)(lo + (int64_t)t * TCM), &full[st]);
+            }
+        }
+      } else {
+        const int pl = wid * 32 + lane;
+        const uint8_t* rows = a.ix.rcodes + lo * rb;
+        constexpr int PER = TCM * (TCKC / 16) / (32 * TC_PROD);
+        auto load_stage = [&](int sidx, uint2 (&x)[PER]) {
+          const int t = sidx / nkc, kb0 = (sidx % nkc) * TCKC;
+#pragma unroll
+          for (int e = 0; e < PER; ++e) {
+            const int i = pl + e * 32 * TC_PROD;
+            const int r = i / (TCKC / 16), pc = 16 * (i % (TCKC / 16));
+            const int64_t v = (int64_t)t * TCM + r;
+            x[e] = (v < n_c && kb0 + pc < kp) ? __ldg(reinterpret_cast<const uint2*>(rows + v * rb + (kb0 + pc) / 2))
+                                              : make_uint2(0u, 0u);
+          }
+        };
+        const int nst = ntile * nkc;
+        uint2 xn[PER];
+        if (nst > 0) load_stage(0, xn);
+        for (int sidx = 0; sidx < nst; ++sidx, ++it_prod) {
+          uint2 xc[PER];
+#pragma unroll
+          for (int e = 0; e < PER; ++e) xc[e] = xn[e];
+          if (sidx + 1 < nst) load_stage(sidx + 1, xn);
+          const int st = it_prod % TCST;
+          tc::mbar_wait(&empty[st], ((it_prod / TCST) & 1) ^ 1);
+          uint8_t* dst = sA + st * TCM * TCKC;
+#pragma unroll
+          for (int e = 0; e < PER; ++e) {
+            const int i = pl + e * 32 * TC_PROD;
+            const int r = i / (TCKC / 16), pc = 16 * (i % (TCKC / 16));
+            const uint2 x = xc[e];
+            *reinterpret_cast<uint4*>(dst + sw128_offset(r, pc)) =
+                make_uint4(x.x & 0x0F0F0F0Fu, (x.x >> 4) & 0x0F0F0F0Fu, x.y & 0x0F0F0F0Fu, (x.y >> 4) & 0x0F0F0F0Fu);
+          }
+          tc::fence_smem_async();
+          tc::mbar_arrive(&full[st]);
+        }
+      }
+    } else if (wid == TC_PROD) {
+      // ---- MMA issuer: slices -> TMEM once per group, then a TS MMA per 32 dims of every rcode tile
+      tc::mbar_wait(bfull, grp & 1);
+      tc::fence_after_sync();
+      if (lane == 0)
+        for (int s2 = 0; s2 < kp / 32; ++s2)
+          tc::tmem_cp_128x256b(tslices + 8 * s2, tc::smem_desc_sw128(sB + (s2 / 4) * 128 * TCKC + 32 * (s2 % 4)));
+      __syncwarp();
+      for (int t = 0; t < ntile; ++t, ++tile_mma) {
+        const int ab = tile_mma & 1;
+        tc::mbar_wait(&acce[ab], ((tile_mma >> 1) & 1) ^ 1);
+        tc::fence_after_sync();
+        for (int kc = 0; kc < nkc; ++kc, ++it_mma) {
+          const int st = it_mma % TCST;
+          tc::mbar_wait(&full[st], (it_mma / TCST) & 1);
+          tc::fence_after_sync();
+          if (lane == 0) {
+            const int ks = min(TCKC, kp - kc * TCKC) / 32;
+            for (int s2 = 0; s2 < ks; ++s2) {
+              const uint64_t bd = tc::smem_desc_sw128(sA + st * TCM * TCKC + 32 * s2);
+              tc::mma_i8_ts(tbase + ab * TCM, tslices + 8 * (kc * 4 + s2), bd, idesc, kc > 0 || s2 > 0);
+            }
+            tc::commit(&empty[st]);
+            if (kc == nkc - 1) tc::commit(&accf[ab]);
+          }
+          __syncwarp();
+        }
+      }
+    } else {
+      // ---- epilogue: TMEM lane 8 j + s (query j, digit s), columns = the tile's 128 vectors
+      const int quarter = wid & 3;
+      const int row = quarter * 32 + lane;
+      const int j = row >> 3, s = row & 7;
+      const int b0 = s & 1, b1 = (s >> 1) & 1, b2 = s >> 2;
+      const int wsh = 7 * (3 - (s & 3));  // digit weight inside its half: 128^(3 - s mod 4)
+      for (int t = 0; t < ntile; ++t, ++tile_epi) {
+        const int ab = tile_epi & 1;
+        {  // the tile's long factors, staged while the MMAs run (double-buffered by tile parity)
+          const int et = tid - 32 * (TC_PROD + 1);  // 0..127
+          const int64_t v = (int64_t)t * TCM + et;
+          s_lf[ab * TCM + et] = v < n_c ? __ldg(reinterpret_cast<const float2*>(a.ix.long_factors) + lo + v)
+                                        : make_float2(0.f, 0.f);
+          asm volatile("bar.sync 1, 128;" ::: "memory");  // epilogue warps only
+        }
+        tc::mbar_wait(&accf[ab], (tile_epi >> 1) & 1);
+        tc::fence_after_sync();
+        for (int v0 = 0; v0 < TCM; v0 += 32) {
+          uint32_t d[32];
+          tc::tmem_ld32(tbase + ((uint32_t)(quarter * 32) << 16) + ab * TCM + v0, d);
+          tc::tmem_ld_wait();
+          long long X[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) X[i] = ((long long)(int)d[i]) << wsh;
+          // (register arrays indexed at compile time only; the lane's half is chosen by selects)
+          long long Y[16];
+#pragma unroll
+          for (int m = 0; m < 16; ++m) {
+            const long long keep = b0 ? X[16 + m] : X[m], give = b0 ? X[m] : X[16 + m];
+            Y[m] = keep + __shfl_xor_sync(0xffffffffu, give, 1);
+          }
+          long long Z[8];
+#pragma unroll
+          for (int m = 0; m < 8; ++m) {
+            const long long keep = b1 ? Y[8 + m] : Y[m], give = b1 ? Y[m] : Y[8 + m];
+            Z[m] = keep + __shfl_xor_sync(0xffffffffu, give, 2);
+          }
+          // lanes s and s^4 hold the hi (digits 0-3) and lo (4-7) sums of the same 8 vectors
+#pragma unroll
+          for (int m = 0; m < 4; ++m) {
+            const long long mine = b2 ? Z[4 + m] : Z[m];
+            const long long other = __shfl_xor_sync(0xffffffffu, b2 ? Z[m] : Z[4 + m], 4);
+            const long long hi = b2 ? other : mine, lw = b2 ? mine : other;
+            const int vl = v0 + 16 * b0 + 8 * b1 + 4 * b2 + m;
+            const int64_t v = (int64_t)t * TCM + vl;
+            if (j < nqg && v < n_c) {
+              const float2 lf = s_lf[ab * TCM + vl];
+              const double ip = dadd(dmul((double)hi, s_hs[j]), dmul((double)lw, s_ls[j]));
+              a.rdist[s_row[j] + v] =
+                  dmax(dsub(dadd((double)lf.x, s_dq[j]), dmul((double)lf.y, dsub(ip, s_kb[j]))), 0.0);
+            }
+          }
+        }
+        tc::fence_before_sync();
+        tc::mbar_arrive(&acce[ab]);
+      }
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (wid == TC_PROD) tc::tmem_dealloc(tbase, 512);
+}
+
 // ------------------------------------------------------------ stage-1 inner products on tcgen05
 // The binary inner products ip = <bit_v, qhat_q> of every probed (list,
 // query) pair (ip_list_kernel's integer, search.py:163-183), list-major on
@@ -2823,6 +3066,23 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
           cudaMalloc(reinterpret_cast<void**>(&ta.prof), 8 * sizeof(unsigned long long));
           cudaMemset(ta.prof, 0, 8 * sizeof(unsigned long long));
         }
+        const char* ts_env = getenv("IVRQ_TC_TS");
+        // TS form measured slower at C3 (1.96 vs 1.78 ms per search on the B200): opt-in only
+        const bool ts = (ts_env ? atoi(ts_env) != 0 : false) && a.kpad <= 768;
+        if (ts) {
+          // TS form: 16-query groups, slices staged as 128 rows per 128-dim chunk
+          ta.G = scan::TSG;
+          scan::pair_plan_kernel<<<1, 1024, 0, s>>>(index->offsets, poff, (int)nl, scan::TSG, rscratch, rgpre,
+                                                     rscratch + nl + 1);
+          const size_t tss = scan::tc_ts_smem_bytes(a.kpad);
+          if (cudaFuncSetAttribute(scan::tc_refine_ts_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)tss) != cudaSuccess)
+            return fail(IVRQ_EUNSUP, "ivrq_search_scan: dims too large for the tensor-core refine");
+          fd_launch = [ta, tss, s]() {
+            scan::tc_refine_ts_kernel<<<(unsigned)sm_count_of_current_device(), scan::TC_THREADS, tss, s>>>(ta);
+            return check_launch("ivrq_search_scan(tensor-core refine)");
+          };
+        } else
         fd_launch = [ta, tsm, s]() {
           scan::tc_refine_kernel<<<(unsigned)sm_count_of_current_device(), scan::TC_THREADS, tsm, s>>>(ta);
           const int rc = check_launch("ivrq_search_scan(tensor-core refine)");

@@ -331,17 +331,18 @@ def test_tensor_core_stage1_matches_popcount_path(monkeypatch, n, d, nlist, bits
         "popcount": {"IVRQ_TC_STAGE1": "0"},
         "default": {},
         "tcgen05": {"IVRQ_TC_IP": "1", "IVRQ_TC_REFINE": "1"},
+        "tcgen05_ts": {"IVRQ_TC_IP": "1", "IVRQ_TC_REFINE": "1", "IVRQ_TC_TS": "1"},
         "mma_sync": {"IVRQ_TC_IP": "0", "IVRQ_TC_REFINE": "0"},
     }
     out = {}
     for name, env in variants.items():
-        for key in ("IVRQ_TC_STAGE1", "IVRQ_TC_IP", "IVRQ_TC_REFINE"):
+        for key in ("IVRQ_TC_STAGE1", "IVRQ_TC_IP", "IVRQ_TC_REFINE", "IVRQ_TC_TS"):
             monkeypatch.delenv(key, raising=False)
         for key, val in env.items():
             monkeypatch.setenv(key, val)
         r = search_device(qd, ix, sp, with_stats=True)
         out[name] = [dev.to_host(t) for t in (r.ids, r.dists, r.counts, r.stats)]
-    for name in ("default", "tcgen05", "mma_sync"):
+    for name in ("default", "tcgen05", "tcgen05_ts", "mma_sync"):
         for a, b in zip(out["popcount"], out[name]):
             np.testing.assert_array_equal(a, b, err_msg=name)
 
