@@ -2064,7 +2064,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_refine_kernel(const __grid_c
           for (int t = 0; t < ntile; ++t)
             for (int kc = 0; kc < nkc; ++kc, ++it_prod) {
               const int st = it_prod % TCST;
+              const long long tw = a.prof ? clock64() : 0;
               tc::mbar_wait(&empty[st], ((it_prod / TCST) & 1) ^ 1);
+              if (a.prof) atomicAdd(a.prof + 6, (unsigned long long)(clock64() - tw));
               tc::mbar_expect_tx(&full[st], TCM * TCKC);
               tc::tma_load_2d(sA + st * TCM * TCKC, &a.map_a, kc * TCKC, (int)(lo + (int64_t)t * TCM), &full[st]);
             }
@@ -2155,7 +2157,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_refine_kernel(const __grid_c
         const int64_t v = (int64_t)t * TCM + r;
         float2 lf = make_float2(0.f, 0.f);
         if (v < n_c) lf = __ldg(reinterpret_cast<const float2*>(a.ix.long_factors) + lo + v);
+        const long long te = a.prof ? clock64() : 0;
         tc::mbar_wait(&accf[ab], (tile_epi >> 1) & 1);
+        if (a.prof && tid == 32 * (TC_PROD + 1)) atomicAdd(a.prof + 7, (unsigned long long)(clock64() - te));
         tc::fence_after_sync();
         for (int j0 = 0; j0 < G; j0 += 4) {
           uint32_t d[32];
@@ -3026,6 +3030,7 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
         // refined distance of every probed pair on tcgen05 (concurrent with the inner products)
         int G = 32;
         while (G > 4 && ((size_t)8 * G * a.kpad > 100 * 1024)) G >>= 1;
+        if (getenv("IVRQ_TC_G")) G = std::min(G, atoi(getenv("IVRQ_TC_G")));  // A/B: smaller groups
         if (cudaMallocAsync(reinterpret_cast<void**>(&rdist), (size_t)tot[0] * sizeof(double), s) != cudaSuccess ||
             cudaMallocAsync(reinterpret_cast<void**>(&rgpre), (nl + 1) * sizeof(int32_t), s) != cudaSuccess ||
             cudaMallocAsync(reinterpret_cast<void**>(&rscratch), (nl + 3) * sizeof(int64_t), s) != cudaSuccess)
@@ -3092,8 +3097,8 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
             const double tot = (double)h[3];
             fprintf(stderr,
                     "[ivrq tc_refine] MMA lane (share of CTA cycles): wait B %.3f, wait accumulator %.3f, wait A %.3f, "
-                    "issue %.3f, group switch %.3f\n",
-                    h[0] / tot, h[1] / tot, h[2] / tot, h[4] / tot, h[5] / tot);
+                    "issue %.3f, group switch %.3f; producer wait-empty %.3f; epilogue wait-accf %.3f\n",
+                    h[0] / tot, h[1] / tot, h[2] / tot, h[4] / tot, h[5] / tot, h[6] / tot, h[7] / tot);
             cudaFree(ta.prof);
           }
           return rc;

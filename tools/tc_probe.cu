@@ -310,6 +310,93 @@ __global__ void __launch_bounds__(128) mma_rate(long long* out, int reps) {
   if (wid == 0) tc::tmem_dealloc(taddr_s, N < 32 ? 32 : N);
 }
 
+// same, but A cycles through 6 distinct 16 KB stage tiles and B walks 6 distinct 128-byte K chunks
+// (the refine kernel's smem footprint), optionally with TMA refilling the A stages concurrently
+template <int N>
+__global__ void __launch_bounds__(128) mma_rate_stream(long long* out, int reps, const __grid_constant__ CUtensorMap ma,
+                                                       int with_tma) {
+  extern __shared__ __align__(1024) unsigned char sm_raw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>(((uintptr_t)sm_raw + 1023) & ~(uintptr_t)1023);
+  unsigned char* sa = sm;                 // 6 x 16 KB
+  unsigned char* sb = sm + 6 * 128 * 128; // 6 x N x 128
+  __shared__ uint64_t bar, tbar, cbar, tbar2;
+  __shared__ uint32_t taddr_s;
+  const int tid = threadIdx.x, wid = tid >> 5;
+  for (int i = tid; i < (6 * 128 + 6 * N) * 128; i += 128) sm[i] = (unsigned char)(i * 7);
+  if (wid == 0) tc::tmem_alloc(&taddr_s, 512);
+  if (tid == 0) {
+    tc::mbar_init(&bar, 1);
+    tc::mbar_init(&tbar, 1);
+    tc::mbar_init(&cbar, 1);
+    tc::mbar_init(&tbar2, 1);
+    tc::mbar_arrive(&tbar2);  // phase 0 completes
+    tc::fence_mbar_init();
+  }
+  tc::fence_smem_async();
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  if (tid == 0) {
+    const uint32_t idesc = tc::idesc_i8(M, N, false, true);
+    const long long t0 = clock64();
+    for (int r = 0; r < reps; ++r) {
+      const int st = r % 6;
+      if (with_tma & 8) tc::fence_after_sync();  // the refine kernel's per-stage fence
+      if (with_tma & 16) tc::mbar_wait(&tbar2, 0);  // a (satisfied) barrier wait per stage
+      for (int s2 = 0; s2 < 4; ++s2)
+        tc::mma_i8(taddr_s, tc::smem_desc_sw128(sa + st * 16384 + 32 * s2),
+                   tc::smem_desc_sw128(sb + st * N * 128 + 32 * s2), idesc, r | s2);
+      if (with_tma & 2) tc::commit(&cbar);  // a commit per stage, as in the refine kernel
+    }
+    const long long t1 = clock64();
+    tc::commit(&bar);
+    tc::mbar_wait(&bar, 0);
+    out[2 * blockIdx.x] = t1 - t0;
+    out[2 * blockIdx.x + 1] = clock64() - t0;
+  } else if (wid >= 2 && (with_tma & 4)) {
+    // concurrent TMEM reads of another accumulator region (the epilogue's tcgen05.ld)
+    const int q4 = wid & 3;
+    for (int r = 0; r < reps / 8; ++r) {
+      uint32_t v[32];
+      tc::tmem_ld32(taddr_s + ((uint32_t)(q4 * 32) << 16) + 256 + (r % 4) * 32, v);
+      tc::tmem_ld_wait();
+      if (v[0] == 0xdeadbeef) out[0] = v[1];
+    }
+  } else if (tid == 32 && (with_tma & 1)) {
+    // keep TMA writing 16 KB tiles into a stage (the data race with the MMA is irrelevant for timing)
+    for (int r = 0; r < reps / 4; ++r) {
+      tc::mbar_expect_tx(&tbar, 16384);
+      tc::tma_load_2d(sa + (r % 6) * 16384, &ma, 0, (r * 128) % 4096, &tbar);
+      tc::mbar_wait(&tbar, r & 1);
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (wid == 0) tc::tmem_dealloc(taddr_s, 512);
+}
+
+template <int N>
+void rate_stream(int with_tma) {
+  const int reps = 2000, blocks = 148;
+  long long* d;
+  cudaMalloc(&d, blocks * 16);
+  uint8_t* src;
+  cudaMalloc(&src, 4096 * 128);
+  cudaMemset(src, 1, 4096 * 128);
+  CUtensorMap ma;
+  tc::make_tmap_u8_sw128(&ma, src, 128, 4096, 128, 128, 128);
+  const int smem = (6 * 128 + 6 * N) * 128 + 1024;
+  cudaFuncSetAttribute(mma_rate_stream<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  mma_rate_stream<N><<<blocks, 128, smem>>>(d, reps, ma, with_tma);
+  cudaError_t e = cudaDeviceSynchronize();
+  std::vector<long long> h(2 * blocks);
+  cudaMemcpy(h.data(), d, h.size() * 8, cudaMemcpyDeviceToHost);
+  const double n_mma = 4.0 * reps;
+  printf("streamed operands N=%d tma=%d: %.1f clk/MMA (%s)\n", N, with_tma, h[1] / n_mma, cudaGetErrorString(e));
+  cudaFree(d);
+  cudaFree(src);
+}
+
 template <int N>
 void rate() {
   const int reps = 2000, blocks = 148;
@@ -380,6 +467,15 @@ int main() {
   rc |= run_tma<256, 128>();
   rc |= run_ts<128, 256>();
   rc |= run_ts<64, 128>();
+  rate_stream<128>(0);
+  rate_stream<128>(1);
+  rate_stream<128>(2);
+  rate_stream<128>(4);
+  rate_stream<128>(7);
+  rate_stream<128>(8);
+  rate_stream<128>(16);
+  rate_stream<128>(2 | 8 | 16);
+  rate_stream<64>(0);
   rate<64>();
   rate<128>();
   rate<256>();
