@@ -65,6 +65,125 @@ __global__ void kpp_leaf_kernel(const double* __restrict__ d2, const int64_t* __
   node_val[l] = pairwise_leaf(d2 + leaf_start[l], leaf_len[l]);
 }
 
+// ---- exact searchsorted(cumsum(d2), target) without the sequential walk (almost always)
+// NumPy's cumsum S_i rounds after every addition; with d2 >= 0 it is monotone and
+// |S_i - P_i| <= (i + 1) u S_i (u = 2^-53) against the exact prefix P_i.  The block
+// computes P_i in double-double (error ~2^-100 P), finds the first i with P_i >=
+// target, and accepts i when target lies outside the rounding band on both sides:
+// P_i - target > band and target - P_{i-1} > band imply S_i >= target > S_{i-1},
+// which is exactly NumPy's answer.  Otherwise (|target - P| within ~i 2^-52 P:
+// vanishingly rare) the caller walks the sequential chain.
+__device__ __forceinline__ void two_sum(double a, double b, double& s, double& e) {
+  s = __dadd_rn(a, b);
+  const double bb = __dsub_rn(s, a);
+  e = __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb));
+}
+struct DD {
+  double hi, lo;
+};
+__device__ __forceinline__ DD dd_add(DD a, DD b) {
+  double s, e;
+  two_sum(a.hi, b.hi, s, e);
+  e = __dadd_rn(e, __dadd_rn(a.lo, b.lo));
+  double s2, e2;
+  two_sum(s, e, s2, e2);
+  return DD{s2, e2};
+}
+__device__ __forceinline__ DD dd_add1(DD a, double b) {
+  double s, e;
+  two_sum(a.hi, b, s, e);
+  e = __dadd_rn(e, a.lo);
+  double s2, e2;
+  two_sum(s, e, s2, e2);
+  return DD{s2, e2};
+}
+// a - b as a double (a, b double-double, a ~ b): accurate to ~2^-100 |a|
+__device__ __forceinline__ double dd_diff(DD a, double b) { return __dadd_rn(__dsub_rn(a.hi, b), a.lo); }
+
+__device__ bool kpp_fast_exact(const double* __restrict__ d2, int64_t n, double target, int64_t* out_idx,
+                               double* s_hi /* shared, [2 * blockDim.x] */, const double* __restrict__ leaf_sum,
+                               const int64_t* __restrict__ leaf_start, const int32_t* __restrict__ leaf_len,
+                               int nleaf) {
+  // Prefix over the pairwise-tree leaves (<= 128 contiguous elements each, their float64 sums already
+  // computed by kpp_leaf_kernel, relative error <= 128 u), double-double accumulation, then the
+  // crossing leaf walked element by element in double-double.  The band adds the leaf-sum error.
+  double* s_lo = s_hi + blockDim.x;
+  __shared__ int s_seg;
+  __shared__ int s_ok;
+  __shared__ int64_t s_res;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int per = (nleaf + nt - 1) / nt;
+  const int l0 = tid * per, l1 = min(nleaf, l0 + per);
+  DD t{0.0, 0.0};
+  for (int l = l0; l < l1; ++l) t = dd_add1(t, leaf_sum[l]);
+  s_hi[tid] = t.hi;
+  s_lo[tid] = t.lo;
+  if (tid == 0) {
+    s_seg = nt;
+    s_ok = 0;
+    s_res = n - 1;
+  }
+  __syncthreads();
+  for (int o = 1; o < nt; o <<= 1) {  // inclusive scan (Hillis-Steele, double-double)
+    DD v{s_hi[tid], s_lo[tid]};
+    if (tid >= o) v = dd_add(v, DD{s_hi[tid - o], s_lo[tid - o]});
+    __syncthreads();
+    s_hi[tid] = v.hi;
+    s_lo[tid] = v.lo;
+    __syncthreads();
+  }
+  const DD incl{s_hi[tid], s_lo[tid]};
+  const DD excl = tid ? DD{s_hi[tid - 1], s_lo[tid - 1]} : DD{0.0, 0.0};
+  const double total_hi = s_hi[nt - 1];
+  const double leaf_err = 0x1p-44 * total_hi;  // >= 4 x 128 u x (sum of the leaves before the crossing)
+  if (l0 < l1 && dd_diff(incl, target) >= 0.0 && dd_diff(excl, target) < 0.0) atomicMin(&s_seg, tid);
+  __syncthreads();
+  if (tid == s_seg) {
+    DD run = excl;
+    int L = l1 - 1;
+    for (int l = l0; l < l1; ++l) {  // crossing leaf
+      const DD nx = dd_add1(run, leaf_sum[l]);
+      if (dd_diff(nx, target) >= 0.0) {
+        L = l;
+        break;
+      }
+      run = nx;
+    }
+    DD prev = run;
+    int64_t hit = -1;
+    const int64_t st = leaf_start[L];
+    const int len = leaf_len[L];
+    for (int i = 0; i < len; ++i) {
+      prev = run;
+      run = dd_add1(run, d2[st + i]);
+      if (dd_diff(run, target) >= 0.0) {
+        hit = st + i;
+        break;
+      }
+    }
+    if (hit >= 0) {
+      const double band = (double)(hit + 2) * 0x1p-51 * run.hi + leaf_err + 0x1p-90 * total_hi;
+      const double above = dd_diff(run, target), below = -dd_diff(prev, target);
+      if (above > band && (hit == 0 || below > band)) {
+        s_res = hit;
+        s_ok = 1;
+      }
+    }
+  } else if (tid == 0 && s_seg == nt) {
+    const DD all{s_hi[nt - 1], s_lo[nt - 1]};
+    const double band = (double)(n + 1) * 0x1p-51 * all.hi + leaf_err;
+    if (-dd_diff(all, target) > band) {  // past the end: the reference's index is clamped to n - 1
+      s_res = n - 1;
+      s_ok = 1;
+    }
+  }
+  __syncthreads();
+  const bool ok = s_ok != 0;
+  if (ok && tid == 0) *out_idx = s_res;
+  __syncthreads();
+  return ok;
+}
+
 // Combine the tree (internal nodes in increasing height order), compute
 // target = r * total and searchsorted(cumsum(d2), target) with the sequential
 // cumsum of NumPy (exact_scan) or a blocked scan for very large n; then copy
@@ -100,11 +219,13 @@ __global__ void __launch_bounds__(1024) kpp_select_kernel(
       return;
     }
     const double target = dmul(draws[j], total);
-    if (exact_scan) {
+    constexpr int SC = 2048;
+    __shared__ double sbuf[2][SC];  // sequential walk staging; also the fast path's scan buffer
+    if (exact_scan == 1 && kpp_fast_exact(d2, n, target, &s_idx, &sbuf[0][0], node_val, leaf_start, leaf_len, nleaf)) {
+      // decided without the sequential walk (see kpp_fast_exact)
+    } else if (exact_scan) {
       // NumPy's sequential cumsum, walked by one thread out of shared memory
       // while the rest of the block streams the next chunk in.
-      constexpr int SC = 2048;
-      __shared__ double sbuf[2][SC];
       __shared__ int s_found;
       if (tid == 0) {
         s_found = 0;
@@ -827,11 +948,15 @@ extern "C" int ivrq_kmeanspp(const float* x, int64_t n, int32_t d, int32_t n_clu
   }
   cudaMemcpyAsync(dlb, tree.level_begin.data(), (nlevels + 1) * sizeof(int32_t), cudaMemcpyHostToDevice, s);
   cudaMemsetAsync(halt, 0, sizeof(int), s);
-  // NumPy's sequential cumsum is replayed exactly up to 2^17 training rows
-  // (every test workload and C1-C3); beyond, a deterministic blocked scan.
+  // NumPy's sequential cumsum decisions are replayed exactly for any n: the
+  // double-double prefix with a rounding band decides almost every step in
+  // parallel (kpp_fast_exact); the sequential walk remains for the band cases.
+  // IVRQ_KPP_EXACT_MAX caps n for the exact replay (beyond: the blocked scan);
+  // IVRQ_KPP_SEQUENTIAL=1 forces the walk for every step (tests).
   const char* ex_env = getenv("IVRQ_KPP_EXACT_MAX");
-  const int64_t exact_max = ex_env ? atoll(ex_env) : ((int64_t)1 << 17);
-  const int exact = n <= exact_max ? 1 : 0;
+  const int64_t exact_max = ex_env ? atoll(ex_env) : ((int64_t)1 << 40);
+  const char* seq_env = getenv("IVRQ_KPP_SEQUENTIAL");
+  const int exact = n <= exact_max ? ((seq_env && atoi(seq_env)) ? 2 : 1) : 0;
   const unsigned ub = (unsigned)ceil_div(n, rowchain::ROWS);
   int j = j_begin;
   if (j == 0) {

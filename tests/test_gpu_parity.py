@@ -363,3 +363,18 @@ def test_search_batch_pipeline_chunks_identical(monkeypatch):
             np.testing.assert_array_equal(res[i][1], dists[i, : counts[i]])
         got = np.stack([a for a, _ in res])
         np.testing.assert_array_equal(got, ids)
+
+
+def test_kmeanspp_parallel_exact_matches_sequential_walk(monkeypatch):
+    """k-means++ sampling decided by the double-double prefix + rounding band equals
+    NumPy's sequential cumsum walk (searchsorted(cumsum(d2), r * total)) step for step."""
+    from paper_2602_23999_b200.clustering import _kmeanspp_device
+
+    rng = np.random.default_rng(12)
+    x = (rng.standard_normal((40000, 24)) * rng.uniform(0.1, 10.0, (40000, 1))).astype(np.float32)
+    xd = dev.to_device(x)
+    out = {}
+    for seq in ("0", "1"):
+        monkeypatch.setenv("IVRQ_KPP_SEQUENTIAL", seq)
+        out[seq] = dev.to_host(_kmeanspp_device(xd, 300, seed=5))
+    np.testing.assert_array_equal(out["0"], out["1"])
