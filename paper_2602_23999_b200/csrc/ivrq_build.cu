@@ -378,14 +378,39 @@ __global__ void cs_counts_kernel(const int32_t* __restrict__ tcount, int64_t nti
   counts[c] = s;
 }
 
-__global__ void cs_scan_kernel(const int64_t* __restrict__ counts, int k, int64_t* __restrict__ offsets) {
-  // single thread; k <= a few 10^4
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  int64_t s = 0;
-  offsets[0] = 0;
-  for (int c = 0; c < k; ++c) {
-    s += counts[c];
-    offsets[c + 1] = s;
+__global__ void __launch_bounds__(1024) cs_scan_kernel(const int64_t* __restrict__ counts, int k,
+                                                      int64_t* __restrict__ offsets) {
+  // exclusive prefix of the label counts: one block, each thread a contiguous
+  // run of labels, warp-shuffle scans of the run totals
+  __shared__ int64_t wsum[32];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int per = (k + blockDim.x - 1) / blockDim.x;
+  const int c0 = min(k, tid * per), c1 = min(k, c0 + per);
+  int64_t t = 0;
+  for (int c = c0; c < c1; ++c) t += counts[c];
+  int64_t incl = t;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) wsum[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    int64_t w = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t v = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += v;
+    }
+    wsum[lane] = w;  // inclusive over warps
+  }
+  __syncthreads();
+  int64_t run = incl - t + (wid ? wsum[wid - 1] : 0);
+  if (tid == 0) offsets[0] = 0;
+  for (int c = c0; c < c1; ++c) {
+    run += counts[c];
+    offsets[c + 1] = run;
   }
 }
 
@@ -1011,7 +1036,9 @@ extern "C" int ivrq_counting_sort(const int32_t* labels, int64_t n, int32_t k, i
   }
   if ((size_t)k * 4 > 200 * 1024) return fail(IVRQ_EUNSUP, "ivrq_counting_sort: too many clusters");
   int64_t tile = 2048;
-  while (ceil_div(n, tile) * (int64_t)k > ((int64_t)1 << 25)) tile *= 2;
+  // tiles x labels stays within max(n, 2^20) entries: the per-label passes over
+  // the tile counts (cs_counts, cs_base) are then no larger than the rows
+  while (ceil_div(n, tile) * (int64_t)k > std::max(n, (int64_t)1 << 20) && tile < (int64_t)1 << 16) tile *= 2;
   const int64_t ntiles = ceil_div(n, tile);
   int32_t *tcount, *rank;
   IVRQ_TRY(dalloc(&tcount, (size_t)(ntiles * k), s, "ivrq_counting_sort"));
@@ -1020,7 +1047,7 @@ extern "C" int ivrq_counting_sort(const int32_t* labels, int64_t n, int32_t k, i
   if (sm > 48 * 1024) cudaFuncSetAttribute(cs_local_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   cs_local_kernel<<<(unsigned)ntiles, 128, sm, s>>>(labels, n, k, tile, tcount, rank);
   cs_counts_kernel<<<(unsigned)ceil_div(k, 256), 256, 0, s>>>(tcount, ntiles, k, counts);
-  cs_scan_kernel<<<1, 32, 0, s>>>(counts, k, offsets);
+  cs_scan_kernel<<<1, 1024, 0, s>>>(counts, k, offsets);
   cs_base_kernel<<<(unsigned)ceil_div(k, 256), 256, 0, s>>>(tcount, ntiles, k, offsets);
   cs_scatter_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(labels, rank, n, k, tile, tcount, offsets, order);
   int rc = check_launch("ivrq_counting_sort");

@@ -93,6 +93,11 @@ struct TpArgs {
   float* bnd;           // [nrows][2][nlist]: lower bounds L, then upper bounds U
 };
 
+// 2^e as a float64 (exact multiplier for ldexp when 2^e is normal)
+__device__ __forceinline__ double pow2(int e) {
+  return (e >= -1022 && e <= 1023) ? __longlong_as_double((long long)(e + 1023) << 52) : ldexp(1.0, e);
+}
+
 template <int NDIG>
 __global__ void __launch_bounds__(THREADS, 1) tc_probe_kernel(const __grid_constant__ TpArgs a) {
   constexpr int QT = QT_<NDIG>, CT = CT_<NDIG>;
@@ -190,6 +195,7 @@ __global__ void __launch_bounds__(THREADS, 1) tc_probe_kernel(const __grid_const
       // the tile's centroid scalars, staged while the MMAs run (double-buffered by tile parity)
       __shared__ double s_csq[2][128], s_cl1[2][128];
       __shared__ int32_t s_ce[2][128];
+      __shared__ float s_stage[EPW * 2 * 16 * 16];  // per epilogue warp: 16 queries x 16 centroids, L and U
       {
         const int et = tid - 64;  // 0..32*EPW-1
         if (et < CT) {
@@ -202,21 +208,32 @@ __global__ void __launch_bounds__(THREADS, 1) tc_probe_kernel(const __grid_const
       }
       tc::mbar_wait(&accf[ab], (tcount >> 1) & 1);
       tc::fence_after_sync();
+      // bounds of (query jq, centroid cl): float64 with exact power-of-two scalings, rounded outwards
+      auto bounds = [&](int cl, double dot_scaled_hi, double dot_scaled_lo, int shift_hi, float& lo_b, float& up_b) {
+        const int sc = qe + s_ce[ab][cl] - 2 * (7 * NDIG - 1);  // s_q s_c
+        const double csq = s_csq[ab][cl];
+        const double p2 = pow2(sc);
+        const double dot = dadd(dmul(dot_scaled_hi, pow2(sc + shift_hi)), dmul(dot_scaled_lo, p2));
+        const double dist = dsub(dadd(qsq, csq), dmul(2.0, dot));
+        const double rep = dmul(ql1 + s_cl1[ab][cl] + 0.5 * a.d, p2);  // 2 (s_q s_c / 2)(|Q|_1+|C|_1+K/2)
+        const double slack = (qsq + csq + 2.0 * fabs(dot)) * 0x1p-40;
+        const double E = rep * 1.0000001 + slack;
+        lo_b = __double2float_rd(fmax(dist - E, 0.0));
+        up_b = __double2float_ru(fmax(dist + E, 0.0));
+      };
       auto emit = [&](int cl, double dot_scaled_hi, double dot_scaled_lo, int shift_hi) {
         const int64_t c = (int64_t)ct * CT + cl;
         if (qr < a.nrows && c < a.nlist) {
-          const int sc = qe + s_ce[ab][cl] - 2 * (7 * NDIG - 1);  // s_q s_c
-          const double csq = s_csq[ab][cl];
-          const double dot = dadd(ldexp(dot_scaled_hi, sc + shift_hi), ldexp(dot_scaled_lo, sc));
-          const double dist = dsub(dadd(qsq, csq), dmul(2.0, dot));
-          const double rep = ldexp(ql1 + s_cl1[ab][cl] + 0.5 * a.d, sc);  // 2 (s_q s_c / 2)(|Q|_1+|C|_1+K/2)
-          const double slack = (qsq + csq + 2.0 * fabs(dot)) * 0x1p-40;
-          const double E = rep * 1.0000001 + slack;
+          float lb, ub;
+          bounds(cl, dot_scaled_hi, dot_scaled_lo, shift_hi, lb, ub);
           float* br = a.bnd + qr * 2 * (int64_t)a.nlist;
-          br[c] = __double2float_rd(fmax(dist - E, 0.0));
-          br[a.nlist + c] = __double2float_ru(fmax(dist + E, 0.0));
+          br[c] = lb;
+          br[a.nlist + c] = ub;
         }
       };
+      // NDIG == 2 stages each 32-column chunk (16 queries x 16 centroids, L and U) in shared memory
+      // so that every query row is written as two 64-byte runs
+      float* stg = s_stage + (wid - 2) * (2 * 16 * 16);
       for (int cc0 = half * (CT / 2); cc0 < (half + 1) * (CT / 2); cc0 += CPC) {
         uint32_t v[32];
         tc::tmem_ld32(tbase + ((uint32_t)(quarter * 32) << 16) + ab * NCOL + NDIG * cc0, v);
@@ -263,12 +280,26 @@ __global__ void __launch_bounds__(THREADS, 1) tc_probe_kernel(const __grid_const
             P[c16] = p;
           }
           // sum over the 2 digit lanes, transposed: lane s ends with centroids 8s .. 8s+7
+          const int jl = lane >> 1;  // query within the warp's 16
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const long long sh = b0 ? P[i] : P[i + 8];
             const long long Pt = (b0 ? P[i + 8] : P[i]) + __shfl_xor_sync(0xffffffffu, sh, 1);
-            emit(cc0 + 8 * s + i, 0.0, (double)Pt, 0);
+            float lb, ub;
+            bounds(cc0 + 8 * s + i, 0.0, (double)Pt, 0, lb, ub);
+            stg[jl * 16 + 8 * s + i] = lb;
+            stg[256 + jl * 16 + 8 * s + i] = ub;
           }
+          __syncwarp();
+          const int ci = lane & 15, which = lane >> 4;  // lanes 0-15: L, 16-31: U
+          const int64_t c = (int64_t)ct * CT + cc0 + ci;
+#pragma unroll 4
+          for (int j = 0; j < 16; ++j) {
+            const int64_t qrow = (int64_t)qt * QT + quarter * 16 + j;
+            if (qrow < a.nrows && c < a.nlist)
+              a.bnd[qrow * 2 * (int64_t)a.nlist + (int64_t)which * a.nlist + c] = stg[which * 256 + j * 16 + ci];
+          }
+          __syncwarp();
         }
       }
       tc::fence_before_sync();
@@ -291,6 +322,7 @@ size_t tp_smem_bytes() { return 1024 + (size_t)ST * (128 + NCOL) * KC + 256; }
 // an exact radix select instead.
 constexpr int RS_THREADS = 256;
 constexpr int MAX_CAND = 1024;
+constexpr int RS_REG = 64;  // U values per thread held in registers (nlist <= 16384)
 
 __device__ __forceinline__ double exact_dist(const double* qv, const float* cv, int d, double qs, double cs) {
   const int lane = threadIdx.x & 31;
@@ -366,6 +398,10 @@ __device__ K radix_kth(int n, int k, int total_bits, int32_t* hist, Get get, int
 }
 
 constexpr int SMEM_ROW = 16384;  // upper bounds staged in shared memory up to this many centroids
+__host__ __device__ inline bool rs_fast_tau(int nlist, int nprobe) {
+  // short rows: the radix select over shared memory is already cheaper than the register pass
+  return nlist >= 4096 && nlist <= RS_REG * RS_THREADS && nprobe <= RS_THREADS;
+}
 
 __global__ void __launch_bounds__(RS_THREADS) probe_rescore_kernel(float* __restrict__ bnd, int64_t q0, int nlist,
                                                                    int nprobe, int order_by_id,
@@ -391,17 +427,85 @@ __global__ void __launch_bounds__(RS_THREADS) probe_rescore_kernel(float* __rest
   const double qs = q_sq[q];
   int64_t* out_i = ids_out + q * nprobe;
   double* out_d = d2_out + q * nprobe;
-  const bool staged = nlist <= SMEM_ROW;
-  if (staged) {
-    for (int i = tid; i < nlist; i += RS_THREADS) s_up[i] = urow[i];
+  // ---- tau: n_probe-th smallest U.  Fast path (nlist <= RS_REG * RS_THREADS, n_probe <= RS_THREADS):
+  // the row is held in registers; T0 = the n_probe-th smallest of the per-thread minima bounds
+  // tau from above (n_probe distinct elements are <= T0), the few U <= T0 are gathered and
+  // tau is their n_probe-th smallest by rank counting.  Otherwise, or when the gathered set
+  // is too large (heavy ties), an MSB-first radix select over the whole row.
+  __shared__ float s_sel[MAX_CAND];
+  __shared__ int32_t s_ns;
+  __shared__ float s_tau;
+  __shared__ int s_have;
+  if (tid == 0) {
+    s_ns = 0;
+    s_have = 0;
+  }
+  __syncthreads();
+  const bool fast_tau = rs_fast_tau(nlist, nprobe);
+  if (fast_tau) {
+    float u[RS_REG];
+    float m = __int_as_float(0x7f800000);  // +inf
+#pragma unroll
+    for (int j = 0; j < RS_REG; ++j) {
+      const int i = tid + j * RS_THREADS;
+      u[j] = i < nlist ? urow[i] : __int_as_float(0x7f800000);
+      m = fminf(m, u[j]);
+    }
+    s_sel[tid] = m;  // RS_THREADS <= MAX_CAND
+    __syncthreads();
+    {
+      int lt = 0, le = 0;
+      for (int f = 0; f < RS_THREADS; ++f) {
+        const float x = s_sel[f];
+        lt += x < m;
+        le += x <= m;
+      }
+      __syncthreads();
+      if (lt < nprobe && nprobe <= le) s_tau = m;  // every writer holds the same value
+      __syncthreads();
+    }
+    const float t0 = s_tau;
+#pragma unroll
+    for (int j = 0; j < RS_REG; ++j) {
+      if (u[j] <= t0) {
+        const int p = atomicAdd(&s_ns, 1);
+        if (p < MAX_CAND) s_sel[p] = u[j];
+      }
+    }
+    __syncthreads();
+    const int ns = s_ns;
+    if (ns <= MAX_CAND) {
+      for (int e = tid; e < ns; e += RS_THREADS) {
+        const float x = s_sel[e];
+        int lt = 0, le = 0;
+        for (int f = 0; f < ns; ++f) {
+          const float y = s_sel[f];
+          lt += y < x;
+          le += y <= x;
+        }
+        if (lt < nprobe && nprobe <= le) {
+          s_tau = x;
+          s_have = 1;
+        }
+      }
+    }
     __syncthreads();
   }
-  const float* up = staged ? s_up : urow;
-  // ---- tau: n_probe-th smallest U (non-negative floats order as uint32)
-  int unused;
-  const uint32_t tau_bits =
-      radix_kth<uint32_t>(nlist, nprobe, 32, hist, [&](int i) { return __float_as_uint(up[i]); }, unused);
-  const float tau = __uint_as_float(tau_bits);
+  float tau;
+  if (s_have) {
+    tau = s_tau;
+  } else {
+    const bool staged = nlist <= SMEM_ROW && !fast_tau;  // the fast path launches without the staging buffer
+    if (staged) {
+      for (int i = tid; i < nlist; i += RS_THREADS) s_up[i] = urow[i];
+      __syncthreads();
+    }
+    const float* up = staged ? s_up : urow;
+    int unused;
+    const uint32_t tau_bits =
+        radix_kth<uint32_t>(nlist, nprobe, 32, hist, [&](int i) { return __float_as_uint(up[i]); }, unused);
+    tau = __uint_as_float(tau_bits);
+  }
   // ---- candidates: L <= tau (a superset of the exact top n_probe)
   if (tid == 0) s_nc = 0;
   __syncthreads();
@@ -548,7 +652,8 @@ int probe_tc(const double* q_rot, int64_t nq, int32_t dims, const float* centroi
     const int grid = (int)std::min<int64_t>(tiles, sm_count_of_current_device());
     tk<<<grid, THREADS, sm, s>>>(ta);
     IVRQ_TRY(check_launch("ivrq_select_clusters(tc bounds)"));
-    const size_t rsm = n_clusters <= SMEM_ROW ? (size_t)n_clusters * sizeof(float) : 0;
+    const size_t rsm =
+        n_clusters <= SMEM_ROW && !rs_fast_tau(n_clusters, n_probe) ? (size_t)n_clusters * sizeof(float) : 0;
     probe_rescore_kernel<<<(unsigned)rn, RS_THREADS, rsm, s>>>(bounds, r0, n_clusters, n_probe, order_by_id, q_rot,
                                                                centroids, dims, q_sq, centroid_sqnorms, ids, d2, pstats);
     IVRQ_TRY(check_launch("ivrq_select_clusters(rescore)"));

@@ -378,3 +378,23 @@ def test_kmeanspp_parallel_exact_matches_sequential_walk(monkeypatch):
         monkeypatch.setenv("IVRQ_KPP_SEQUENTIAL", seq)
         out[seq] = dev.to_host(_kmeanspp_device(xd, 300, seed=5))
     np.testing.assert_array_equal(out["0"], out["1"])
+
+
+@pytest.mark.parametrize(
+    "nlist,nprobe,dup",
+    [(1024, 8, 1), (8192, 64, 1), (16384, 128, 1), (20000, 16, 1), (8192, 32, 128), (16384, 64, 2048)],
+)
+def test_tensor_core_probe_matches_gemm_probe(monkeypatch, nlist, nprobe, dup):
+    """The tcgen05 bounds probe (register or radix tau, candidate or full-row rescoring) selects the
+    same clusters as the float64 GEMM probe, ties included (dup copies of every centroid)."""
+    rng = np.random.default_rng(nlist + dup)
+    d = 96
+    q = rng.standard_normal((300, d))
+    uniq = rng.standard_normal((nlist // dup, d)).astype(np.float32)
+    cent = Centroids(np.repeat(uniq, dup, axis=0))
+    out = {}
+    for env in ("1", "0"):
+        monkeypatch.setenv("IVRQ_TC_PROBE", env)
+        out[env] = iv.select_clusters(q, cent, nprobe)
+    np.testing.assert_array_equal(out["1"][0], out["0"][0])
+    np.testing.assert_allclose(out["1"][1], out["0"][1], rtol=1e-12, atol=1e-12)

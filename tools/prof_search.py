@@ -1,6 +1,7 @@
 """Profiling driver: build one synthetic config and run the search a few times.
 
-    ncu --set full -k regex:scan_kernel -s 2 -c 1 -o gpurun_out/prof python tools/prof_search.py --config c3 --nprobe 8
+    ncu --profile-from-start off --set full -k regex:scan_kernel -c 1 -o gpurun_out/prof \
+        python tools/prof_search.py --config c3 --nprobe 8
 """
 
 from __future__ import annotations
@@ -41,6 +42,9 @@ def main() -> None:
     torch.cuda.synchronize()
     print(f"build {time.perf_counter() - t:.2f}s", file=sys.stderr)
     sp = iv.SearchParams(k=bench.K, n_probe=args.nprobe, ip_mode=args.mode)
+    search_device(q, ix, sp)  # warm-up (allocator pools, tensor maps) outside the profiled range
+    torch.cuda.synchronize()
+    torch.cuda.profiler.start()  # ncu --profile-from-start off: only the searches below are captured
     for _ in range(args.reps):
         ev: dict = {}
         search_device(q, ix, sp, events=ev)
@@ -56,6 +60,8 @@ def main() -> None:
             ),
             file=sys.stderr,
         )
+    torch.cuda.synchronize()
+    torch.cuda.profiler.stop()
 
 
 if __name__ == "__main__":
