@@ -278,6 +278,15 @@ IVRQ_API int ivrq_encode(const void* o_rot, int32_t o_is_f64, const double* dist
                 float* long_factors, uint8_t* codes, double* t_out, int32_t* bad_rows,
                 void* stream);
 
+/* Per-kernel timing for benchmarks (no reference counterpart).  While enabled,
+ * the search records CUDA events on the launching stream around its dominant
+ * kernels ("tc_refine_kernel", "scan_rd_kernel", "scan_warp_kernel",
+ * "tc_ip_kernel", "ip_list_kernel"); enabling starts a new window.
+ * ivrq_kernel_time waits for the recorded events of `name` and returns their
+ * summed duration and launch count. */
+IVRQ_API int ivrq_kernel_timing(int32_t enable);
+IVRQ_API int ivrq_kernel_time(const char* name, double* total_ms, int64_t* launches);
+
 #ifdef __cplusplus
 }
 #endif

@@ -68,6 +68,8 @@ P = c_void_p  # device pointers are passed as integers
 # name -> (restype, argtypes)
 _SIGNATURES: dict[str, tuple[object, list[object]]] = {
     "ivrq_abi_version": (c_int, []),
+    "ivrq_kernel_timing": (c_int, [ctypes.c_int32]),
+    "ivrq_kernel_time": (c_int, [ctypes.c_char_p, POINTER(ctypes.c_double), POINTER(ctypes.c_int64)]),
     "ivrq_last_error": (ctypes.c_char_p, []),
     "ivrq_device_sm_count": (c_int, [c_int, POINTER(c_int)]),
     "ivrq_row_sqnorms": (c_int, [P, c_int, c_int64, c_int32, P, P]),

@@ -35,6 +35,27 @@ int sm_count_of_current_device();
 // A non-blocking stream per device (and host thread) for intra-call fork/join.
 cudaStream_t side_stream();
 
+// Optional per-kernel timing (ivrq_kernel_timing / ivrq_kernel_time): while
+// enabled, a KernelTimer around a launch records CUDA events on the launching
+// stream; disabled (the default) it does nothing.
+bool kernel_timing_enabled();
+void kernel_timing_record(const char* name, cudaEvent_t begin, cudaEvent_t end);
+struct KernelTimer {
+  const char* name;
+  cudaStream_t stream;
+  cudaEvent_t begin = nullptr;
+  KernelTimer(const char* n, cudaStream_t s) : name(n), stream(s) {
+    if (kernel_timing_enabled() && cudaEventCreate(&begin) == cudaSuccess) cudaEventRecord(begin, stream);
+  }
+  ~KernelTimer() {
+    cudaEvent_t end = nullptr;
+    if (begin && cudaEventCreate(&end) == cudaSuccess) {
+      cudaEventRecord(end, stream);
+      kernel_timing_record(name, begin, end);
+    }
+  }
+};
+
 #define IVRQ_TRY(expr)              \
   do {                              \
     int _rc = (expr);               \

@@ -1,6 +1,11 @@
 // Error state, device queries and the einsum-order row norms.
 #include <cudaTypedefs.h>
 
+#include <atomic>
+#include <mutex>
+#include <string>
+#include <vector>
+
 #include "ivrq_common.cuh"
 #include "ivrq_rowchain.cuh"
 #include "ivrq_tc.cuh"
@@ -58,6 +63,23 @@ bool make_tmap_u8_sw128(CUtensorMap* map, const void* base, uint64_t inner, uint
 }
 }  // namespace tc
 
+namespace {
+struct TimedLaunch {
+  std::string name;
+  cudaEvent_t begin, end;
+};
+std::mutex g_kt_mu;
+std::vector<TimedLaunch> g_kt;
+std::atomic<int> g_kt_on{0};
+}  // namespace
+
+bool kernel_timing_enabled() { return g_kt_on.load(std::memory_order_relaxed) != 0; }
+
+void kernel_timing_record(const char* name, cudaEvent_t begin, cudaEvent_t end) {
+  std::lock_guard<std::mutex> lk(g_kt_mu);
+  g_kt.push_back({name, begin, end});
+}
+
 cudaStream_t side_stream() {
   static thread_local cudaStream_t streams[32] = {};
   int dev = 0;
@@ -106,6 +128,39 @@ __global__ void __launch_bounds__(rowchain::THREADS) row_sqnorm_kernel(const T* 
 using namespace ivrq;
 
 extern "C" int ivrq_abi_version(void) { return IVRQ_ABI_VERSION; }
+
+extern "C" int ivrq_kernel_timing(int32_t enable) {
+  std::lock_guard<std::mutex> lk(ivrq::g_kt_mu);
+  if (enable) {  // a new measurement window: drop what the previous one recorded
+    for (auto& t : ivrq::g_kt) {
+      cudaEventSynchronize(t.end);
+      cudaEventDestroy(t.begin);
+      cudaEventDestroy(t.end);
+    }
+    ivrq::g_kt.clear();
+  }
+  ivrq::g_kt_on.store(enable ? 1 : 0);
+  return IVRQ_OK;
+}
+
+extern "C" int ivrq_kernel_time(const char* name, double* total_ms, int64_t* launches) {
+  if (!name || !total_ms || !launches) return ivrq::fail(IVRQ_EINVAL, "ivrq_kernel_time: null argument");
+  std::lock_guard<std::mutex> lk(ivrq::g_kt_mu);
+  double tot = 0.0;
+  int64_t n = 0;
+  for (auto& t : ivrq::g_kt) {
+    if (t.name != name) continue;
+    if (cudaEventSynchronize(t.end) != cudaSuccess) return ivrq::fail(IVRQ_ECUDA, "ivrq_kernel_time: event wait failed");
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, t.begin, t.end) != cudaSuccess)
+      return ivrq::fail(IVRQ_ECUDA, "ivrq_kernel_time: elapsed time unavailable");
+    tot += ms;
+    ++n;
+  }
+  *total_ms = tot;
+  *launches = n;
+  return IVRQ_OK;
+}
 
 extern "C" const char* ivrq_last_error(void) { return g_last_error.c_str(); }
 

@@ -1944,6 +1944,8 @@ struct TcArgs {
   const int32_t* gpre;      // [nlist + 1] prefix of ceil(bucket / G)
   double* rdist;
   unsigned long long* prof;  // optional wait-cycle counters (IVRQ_TC_PROF)
+  int nst;                   // A stages
+  int dbg;                   // IVRQ_TC_DBG (diagnostics only, results invalid): 1 = no epilogue math/stores, 2 = no MMAs
 };
 
 // digit slices in rcode byte order: out[q][s][P] = qslices[q][s][perm(P)] with
@@ -1963,9 +1965,9 @@ __host__ __device__ inline uint32_t tmem_cols(int n) {  // power of two >= 32 (<
   return n <= 32 ? 32u : n <= 64 ? 64u : n <= 128 ? 128u : n <= 256 ? 256u : 512u;
 }
 
-size_t tc_smem_bytes(int kpad, int G) {
+size_t tc_smem_bytes(int kpad, int G, int nst) {
   const int nkc = (kpad + TCKC - 1) / TCKC;
-  return 1024 + (size_t)nkc * 8 * G * TCKC + (size_t)TCST * TCM * TCKC + 64 * G + 256;
+  return 1024 + (size_t)nkc * 8 * G * TCKC + (size_t)nst * TCM * TCKC + 64 * G + 256;
 }
 
 // byte offset of (row R, byte k < 128) in a 128B-swizzled K-major tile (8-row atoms of 1024 B)
@@ -1977,6 +1979,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_refine_kernel(const __grid_c
   extern __shared__ __align__(1024) unsigned char tsm_raw[];
   unsigned char* tsm = reinterpret_cast<unsigned char*>(((uintptr_t)tsm_raw + 1023) & ~(uintptr_t)1023);
   const int G = a.G, N = 8 * G, kp = a.kpad;
+  const int TCST = a.nst;  // A ring depth (runtime: traded against the group size for shared memory)
   const int nkc = (kp + TCKC - 1) / TCKC;  // 128-byte K chunks
   int8_t* sB = reinterpret_cast<int8_t*>(tsm);                                   // [nkc][N rows x 128 B] swizzled
   uint8_t* sA = reinterpret_cast<uint8_t*>(tsm + (size_t)nkc * N * TCKC);        // [TCST][128 rows x 128 B] swizzled
@@ -2135,7 +2138,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_refine_kernel(const __grid_c
           if (lane == 0) {
             const long long ti = a.prof ? clock64() : 0;
             const int ks = min(TCKC, kp - kc * TCKC) / 32;
-            for (int s2 = 0; s2 < ks; ++s2) {
+            for (int s2 = 0; s2 < ks && a.dbg != 2 && a.dbg != 3; ++s2) {
               const uint64_t ad = tc::smem_desc_sw128(sA + st * TCM * TCKC + 32 * s2);
               const uint64_t bd = tc::smem_desc_sw128(sB + kc * N * TCKC + 32 * s2);
               tc::mma_i8(tbase + ab * N, ad, bd, idesc, kc > 0 || s2 > 0);
@@ -2161,7 +2164,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_refine_kernel(const __grid_c
         tc::mbar_wait(&accf[ab], (tile_epi >> 1) & 1);
         if (a.prof && tid == 32 * (TC_PROD + 1)) atomicAdd(a.prof + 7, (unsigned long long)(clock64() - te));
         tc::fence_after_sync();
-        for (int j0 = 0; j0 < G; j0 += 4) {
+        for (int j0 = 0; j0 < G && a.dbg != 1 && a.dbg != 3; j0 += 4) {
           uint32_t d[32];
           tc::tmem_ld32(tbase + ((uint32_t)(quarter * 32) << 16) + ab * N + 8 * j0, d);
           tc::tmem_ld_wait();
@@ -2708,7 +2711,10 @@ inline int launch_rd(const Args& a, bool refine, int ipb, cudaStream_t s) {
               : rminb == 8 ? rd_kernel_for<4, 8>(refine, ipb)
               : rminb == 6 ? rd_kernel_for<4, 6>(refine, ipb)
                            : rd_kernel_for<4>(refine, ipb);
-  kern<<<(unsigned)ceil_div(a.nq, RDW), RDW * 32, 0, s>>>(a);
+  {
+    KernelTimer kt("scan_rd_kernel", s);
+    kern<<<(unsigned)ceil_div(a.nq, RDW), RDW * 32, 0, s>>>(a);
+  }
   return check_launch("ivrq_search_scan");
 }
 
@@ -2721,7 +2727,10 @@ int launch_warp(const Args& a, int ipb, cudaStream_t s) {
                           : (ipb == 2 ? scan_warp_kernel<REFINE, NIB, 2, WQ_MINB> : scan_warp_kernel<REFINE, NIB, 4, WQ_MINB>);
   if (sm > 48 * 1024 && cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess)
     return fail(IVRQ_EUNSUP, "ivrq_search_scan: shared memory request too large");
-  kern<<<(unsigned)ceil_div(a.nq, WQ), WQ * 32, sm, s>>>(a);
+  {
+    KernelTimer kt("scan_warp_kernel", s);
+    kern<<<(unsigned)ceil_div(a.nq, WQ), WQ * 32, sm, s>>>(a);
+  }
   return check_launch("ivrq_search_scan");
 }
 
@@ -3028,9 +3037,18 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
         return fail(IVRQ_EUNSUP, "ivrq_search_scan: dims too large for the tensor-core stage 1");
       if (rd_path && refine) {
         // refined distance of every probed pair on tcgen05 (concurrent with the inner products)
+        // group size: the rcode tiles of a list are streamed once per group, so the largest group whose
+        // digit slices fit next to a ring of >= 4 A stages (C3, D = 768: G = 24, 4 stages; measured
+        // 3.10 vs 3.40 ms per scan stage against G = 16 with 6 stages)
+        const size_t smem_cap = 227 * 1024;
         int G = 32;
-        while (G > 4 && ((size_t)8 * G * a.kpad > 100 * 1024)) G >>= 1;
-        if (getenv("IVRQ_TC_G")) G = std::min(G, atoi(getenv("IVRQ_TC_G")));  // A/B: smaller groups
+        while (G > 4 && scan::tc_smem_bytes(a.kpad, G, 4) > smem_cap) G -= 4;
+        int nst = scan::TCST;
+        while (nst > 2 && scan::tc_smem_bytes(a.kpad, G, nst) > smem_cap) --nst;
+        if (getenv("IVRQ_TC_G")) G = atoi(getenv("IVRQ_TC_G"));  // A/B: group size (multiple of 2) and A stages
+        if (getenv("IVRQ_TC_ST")) nst = atoi(getenv("IVRQ_TC_ST"));
+        if (G < 4 || G > 32 || (G & 3) || nst < 2 || nst > 8 || scan::tc_smem_bytes(a.kpad, G, nst) > smem_cap)
+          return fail(IVRQ_EINVAL, "ivrq_search_scan: tensor-core refine group/stage configuration does not fit");
         if (cudaMallocAsync(reinterpret_cast<void**>(&rdist), (size_t)tot[0] * sizeof(double), s) != cudaSuccess ||
             cudaMallocAsync(reinterpret_cast<void**>(&rgpre), (nl + 1) * sizeof(int32_t), s) != cudaSuccess ||
             cudaMallocAsync(reinterpret_cast<void**>(&rscratch), (nl + 3) * sizeof(int64_t), s) != cudaSuccess)
@@ -3062,7 +3080,9 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
         ta.pair_base = pbase;
         ta.gpre = rgpre;
         ta.rdist = rdist;
-        const size_t tsm = scan::tc_smem_bytes(a.kpad, G);
+        ta.dbg = getenv("IVRQ_TC_DBG") ? atoi(getenv("IVRQ_TC_DBG")) : 0;
+        ta.nst = nst;
+        const size_t tsm = scan::tc_smem_bytes(a.kpad, G, nst);
         if (cudaFuncSetAttribute(scan::tc_refine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm) !=
             cudaSuccess)
           return fail(IVRQ_EUNSUP, "ivrq_search_scan: dims too large for the tensor-core refine");
@@ -3089,7 +3109,10 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
           };
         } else
         fd_launch = [ta, tsm, s]() {
-          scan::tc_refine_kernel<<<(unsigned)sm_count_of_current_device(), scan::TC_THREADS, tsm, s>>>(ta);
+          {
+            KernelTimer kt("tc_refine_kernel", s);
+            scan::tc_refine_kernel<<<(unsigned)sm_count_of_current_device(), scan::TC_THREADS, tsm, s>>>(ta);
+          }
           const int rc = check_launch("ivrq_search_scan(tensor-core refine)");
           if (ta.prof) {  // debugging aid (synchronises): where the MMA lane waited
             unsigned long long h[8];
@@ -3147,8 +3170,10 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
         if (cudaFuncSetAttribute(scan::tc_ip_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm) !=
             cudaSuccess)
           return fail(IVRQ_EUNSUP, "ivrq_search_scan: dims too large for the tensor-core stage 1");
+        KernelTimer kt("tc_ip_kernel", si);
         scan::tc_ip_kernel<<<(unsigned)sm_count_of_current_device(), scan::TC_THREADS, tsm, si>>>(ta);
       } else {
+        KernelTimer kt("ip_list_kernel", si);
         ik<<<(unsigned)(2 * sm_count_of_current_device()), scan::THREADS, ism, si>>>(ia);
       }
       IVRQ_TRY(check_launch("ivrq_search_scan(stage-1 tiles)"));
