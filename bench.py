@@ -198,17 +198,62 @@ def count_launches(step_fn) -> tuple[int, list[str]]:
     return int(sum(ours.values())), short
 
 
-def ncu_traffic(cfg_name: str, nprobe: int):
-    """DRAM bytes (read + write) of the scan stage per search, from the committed ncu capture
-    (profiles/<round>/traffic_<cfg>.json, written by tools/ncu_traffic.py), or None."""
+def ncu_traffic(cfg_name: str, nprobe: int, kernel: str | None = None):
+    """DRAM bytes (read + write) per launch of `kernel` (and of the whole scan stage) from the
+    committed ncu capture (profiles/<round>/traffic_<cfg>.json, written by tools/ncu_traffic.py), or None."""
     for p in sorted((ROOT / "profiles").glob(f"*/traffic_{cfg_name}.json"), reverse=True):
         try:
             t = json.loads(p.read_text())
         except ValueError:
             continue
-        if t.get("n_probe") == nprobe:
-            return {"dram_bytes": t["dram_bytes"], "source": str(p.relative_to(ROOT)), "kernels": t.get("kernels")}
+        if t.get("n_probe") != nprobe:
+            continue
+        kb = None
+        if kernel:
+            kb = sum(v for k, v in (t.get("kernels") or {}).items() if k.split("<")[0].endswith(kernel)) or None
+        return {"dram_bytes": kb, "kernel": kernel, "scan_stage_dram_bytes": t["dram_bytes"],
+                "source": str(p.relative_to(ROOT)), "kernels": t.get("kernels")}
     return None
+
+
+def kernel_roofline(kernel_ms: dict, peaks: dict, probed: int, survivors: int, d: int, bits: int) -> dict:
+    """Roofline of the scan's dominant kernel (largest CUDA-event time in the timed region).
+
+    Algorithmic work per launch:
+      tc_refine_kernel  int8 tensor ops 2 * probed * kpad * 8 (8 digit slices of every probed pair)
+      tc_ip/ip_list     int8 tensor ops 2 * probed * 32 ceil(D/32) * 4 (4-bit query planes)
+      scan_rd_kernel    bytes probed * (2 + 12) + survivors * 8 (ip, factors; refined distance)
+      scan_warp_kernel  bytes probed * (2 + 12) + survivors * (rcode row + 8) (ip, factors; codes, long factors)
+    """
+    if not kernel_ms:
+        return {"bound": None, "kernel": None, "note": "no timed kernel"}
+    name, (avg_ms, launches) = max(kernel_ms.items(), key=lambda kv: kv[1][0] * kv[1][1])
+    kpad = -(-d // 64) * 64
+    g = -(-d // 32)
+    rb = -(-d * (8 if bits > 4 else 4) // 8)
+    bf16 = float(peaks.get("bf16_tflops", 1590.0))
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    src = "MEASURED_PEAKS.json" if "_fallback" not in peaks else "fallback"
+    if name in ("tc_refine_kernel", "tc_ip_kernel", "ip_list_kernel"):
+        work = 2.0 * probed * (kpad * 8 if name == "tc_refine_kernel" else 32 * g * 4)
+        achieved = work / (avg_ms / 1e3) / 1e12
+        peak = 2.0 * bf16
+        out = {"bound": "tensor", "unit": "TFLOP/s", "op": "int8 multiply-add (x2), TOP/s",
+               "peak_source": f"2 x {src} bf16_tflops (dense int8 tcgen05 rate = 2 x bf16 on sm_100; "
+                              "no int8 measurement in the file)",
+               "work_formula": "2*probed*kpad*8" if name == "tc_refine_kernel" else "2*probed*32*ceil(D/32)*4"}
+    else:
+        work = probed * 14.0 + survivors * (8.0 if name == "scan_rd_kernel" else rb + 8.0)
+        achieved = work / (avg_ms / 1e3) / 1e9
+        peak = hbm
+        out = {"bound": "hbm", "unit": "GB/s", "peak_source": f"{src} hbm_gbs",
+               "work_formula": "probed*14 + survivors*" + ("8" if name == "scan_rd_kernel" else f"({rb}+8)")}
+    out.update({"kernel": name, "achieved": round(achieved, 1), "peak": round(peak, 1),
+                "frac": round(achieved / peak, 4), "work_per_launch": int(work),
+                "kernel_ms_per_launch": round(avg_ms, 4), "launches_timed": launches,
+                "timing": "CUDA events on the kernel's launching stream (ivrq_kernel_timing), timed region",
+                "other_kernels_ms": {k: round(v[0], 4) for k, v in kernel_ms.items() if k != name}})
+    return out
 
 
 def dist_setup():
@@ -225,8 +270,11 @@ def run_ours(args, cfg_name: str) -> dict:
     import torch
     import torch.distributed as tdist
 
+    import ctypes
+
     import paper_2602_23999_b200 as iv
     from paper_2602_23999_b200 import _device as dev
+    from paper_2602_23999_b200 import _lib
     from paper_2602_23999_b200.index import build_index_device
     from paper_2602_23999_b200.linalg import exact_knn_device
     from paper_2602_23999_b200.search import search_device
@@ -302,6 +350,8 @@ def run_ours(args, cfg_name: str) -> dict:
     if world > 1:
         tdist.barrier()
     step_ms, scan_ms, stage_ms = [], [], {"rotate": 0.0, "probe": 0.0, "prepare": 0.0, "scan": 0.0}
+    klib = _lib.load()
+    _lib.call("ivrq_kernel_timing", 1)  # CUDA events around the scan's dominant kernels, on their streams
     with ClockSampler(local) as clocks:
         for _ in range(args.steps):
             flush.zero_()
@@ -315,6 +365,14 @@ def run_ours(args, cfg_name: str) -> dict:
             stage_ms["prepare"] += ev["probed"].elapsed_time(ev["prepared"])
             stage_ms["scan"] += scan_ms[-1]
     torch.cuda.synchronize()
+    _lib.call("ivrq_kernel_timing", 0)
+    kernel_ms = {}
+    for kn in ("tc_refine_kernel", "scan_rd_kernel", "scan_warp_kernel", "tc_ip_kernel", "ip_list_kernel"):
+        tot, nl_ = ctypes.c_double(0.0), ctypes.c_int64(0)
+        _lib.call("ivrq_kernel_time", kn.encode(), ctypes.byref(tot), ctypes.byref(nl_))
+        if nl_.value:
+            kernel_ms[kn] = (tot.value / nl_.value, int(nl_.value))
+    del klib
     total_ms = float(sum(step_ms))
     if world > 1:
         t = torch.tensor([total_ms], device=device, dtype=torch.float64)
@@ -346,6 +404,18 @@ def run_ours(args, cfg_name: str) -> dict:
     peaks = measured_peaks()
     peak = float(peaks.get("hbm_gbs", 6650.0))
     achieved = alg_bytes / (scan_mean_ms / 1e3) / 1e9
+    roofline = kernel_roofline(kernel_ms, peaks, probed=probed, survivors=survivors, d=d, bits=bits)
+    roofline["traffic"] = ncu_traffic(cfg_name, nprobe, roofline.get("kernel"))
+    roofline["scan_stage"] = {
+        "note": "whole scan stage against the per-query-equivalent bytes of the reference's scan "
+                "(list-major sharing of code reads lets this exceed the copy peak; context, not the roofline)",
+        "ms": round(scan_mean_ms, 4),
+        "per_query_equivalent_bytes": int(alg_bytes),
+        "bytes_formula": f"probed*(4*ceil(D/32)+12) + survivors*({surv_b})",
+        "effective_gbs": round(achieved, 1),
+        "probed_per_query": round(probed / NQ, 1),
+        "survivors_per_query": round(survivors / NQ, 1),
+    }
     result = {
         "metric": "search QPS @ recall@10~0.95 (10K-query batch)",
         "value": round(qps, 1),
@@ -384,21 +454,7 @@ def run_ours(args, cfg_name: str) -> dict:
         "gpu_launches": args.steps * launches_per_step,
         "gpu_launches_per_step": launches_per_step,
         "gpu_kernels": kernel_names,
-        "roofline": {
-            "bound": "hbm",
-            "kernel": "scan stage (stage-1 inner products, refine, per-query prune/top-k kernels; events around the stage)",
-            "achieved": round(achieved, 1),
-            "peak": peak,
-            "unit": "GB/s",
-            "frac": round(achieved / peak, 4),
-            "traffic": ncu_traffic(cfg_name, nprobe),
-            "algorithmic_bytes_per_launch": int(alg_bytes),
-            "bytes_formula": f"probed*(4*ceil(D/32)+12) + survivors*({surv_b})",
-            "probed_per_query": round(probed / NQ, 1),
-            "survivors_per_query": round(survivors / NQ, 1),
-            "scan_ms": round(scan_mean_ms, 4),
-            "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "_fallback" not in peaks else "fallback",
-        },
+        "roofline": roofline,
         "clocks": clocks.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

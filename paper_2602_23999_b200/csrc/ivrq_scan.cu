@@ -1945,6 +1945,7 @@ struct TcArgs {
   double* rdist;
   unsigned long long* prof;  // optional wait-cycle counters (IVRQ_TC_PROF)
   int nst;                   // A stages
+  int w1;                    // one polling lane per waiting warp
   int dbg;                   // IVRQ_TC_DBG (diagnostics only, results invalid): 1 = no epilogue math/stores, 2 = no MMAs
 };
 
@@ -1996,6 +1997,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_refine_kernel(const __grid_c
   uint64_t* bfull = bars + 2 * TCST + 4;      // [1]
   uint32_t* s_taddr = reinterpret_cast<uint32_t*>(bars + 2 * TCST + 5);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  // a whole warp waiting on an mbarrier: one lane polls (a.w1), the warp then re-converges
+  auto wait1 = [&](uint64_t* bar, uint32_t parity) {
+    if (!a.w1 || lane == 0) tc::mbar_wait(bar, parity);
+    __syncwarp();
+  };
   if (tid == 0) {
     for (int i = 0; i < TCST; ++i) {
       tc::mbar_init(&full[i], a.nib ? 32 * TC_PROD : 1);
@@ -2120,19 +2126,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_refine_kernel(const __grid_c
       // do not pay for a full group)
       const uint32_t idesc = tc::idesc_i8(TCM, 8 * ((nqg + 1) & ~1), false, true);
       long long t0 = a.prof ? clock64() : 0;
-      tc::mbar_wait(bfull, grp & 1);
+      wait1(bfull, grp & 1);
       long long t1 = a.prof ? clock64() : 0;
       if (a.prof && lane == 0) atomicAdd(a.prof + 0, (unsigned long long)(t1 - t0));
       for (int t = 0; t < ntile; ++t, ++tile_mma) {
         const int ab = tile_mma & 1;
         t0 = a.prof ? clock64() : 0;
-        tc::mbar_wait(&acce[ab], ((tile_mma >> 1) & 1) ^ 1);
+        wait1(&acce[ab], ((tile_mma >> 1) & 1) ^ 1);
         if (a.prof && lane == 0) atomicAdd(a.prof + 1, (unsigned long long)(clock64() - t0));
         tc::fence_after_sync();
         for (int kc = 0; kc < nkc; ++kc, ++it_mma) {
           const int st = it_mma % TCST;
           t0 = a.prof ? clock64() : 0;
-          tc::mbar_wait(&full[st], (it_mma / TCST) & 1);
+          wait1(&full[st], (it_mma / TCST) & 1);
           if (a.prof && lane == 0) atomicAdd(a.prof + 2, (unsigned long long)(clock64() - t0));
           tc::fence_after_sync();
           if (lane == 0) {
@@ -2161,7 +2167,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_refine_kernel(const __grid_c
         float2 lf = make_float2(0.f, 0.f);
         if (v < n_c) lf = __ldg(reinterpret_cast<const float2*>(a.ix.long_factors) + lo + v);
         const long long te = a.prof ? clock64() : 0;
-        tc::mbar_wait(&accf[ab], (tile_epi >> 1) & 1);
+        wait1(&accf[ab], (tile_epi >> 1) & 1);
         if (a.prof && tid == 32 * (TC_PROD + 1)) atomicAdd(a.prof + 7, (unsigned long long)(clock64() - te));
         tc::fence_after_sync();
         for (int j0 = 0; j0 < G && a.dbg != 1 && a.dbg != 3; j0 += 4) {
@@ -3082,6 +3088,7 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
         ta.rdist = rdist;
         ta.dbg = getenv("IVRQ_TC_DBG") ? atoi(getenv("IVRQ_TC_DBG")) : 0;
         ta.nst = nst;
+        ta.w1 = getenv("IVRQ_TC_W1") ? atoi(getenv("IVRQ_TC_W1")) : 1;
         const size_t tsm = scan::tc_smem_bytes(a.kpad, G, nst);
         if (cudaFuncSetAttribute(scan::tc_refine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm) !=
             cudaSuccess)

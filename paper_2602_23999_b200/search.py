@@ -347,15 +347,25 @@ def _search_pipelined(q: np.ndarray, index: IvfRabitqIndex, params: SearchParams
             ev = torch.cuda.Event()
             ev.record(stream)
             t2 = time.perf_counter()
+            # the per-query row views are made while the GPU searches; the results are copied
+            # into the viewed arrays once the event fires, short rows (count < k) re-cut after
+            rows = list(zip(list(ids_out), list(dists_out)))
             ev.synchronize()
             t3 = time.perf_counter()
-            finish(0, nq, ev)
+            np.copyto(ids_out, ids_h)
+            np.copyto(dists_out, dists_h)
+            np.copyto(counts_out, counts_h)
+            if nq and int(counts_out.min()) < k:
+                for i in np.flatnonzero(counts_out < k).tolist():
+                    n = int(counts_out[i])
+                    rows[i] = (ids_out[i, :n], dists_out[i, :n])
+            results.extend(rows)
             t4 = time.perf_counter()
         if trace:
             import sys
 
             print(f"[e2e] staged+rotate-enqueued {1e3*(t1-t0):.2f} enqueue {1e3*(t2-t1):.2f} "
-                  f"gpu-wait {1e3*(t3-t2):.2f} lists {1e3*(t4-t3):.2f} ms", file=sys.stderr)
+                  f"row views + gpu-wait {1e3*(t3-t2):.2f} copy-out {1e3*(t4-t3):.2f} ms", file=sys.stderr)
         return results
 
     with torch.cuda.stream(stream):

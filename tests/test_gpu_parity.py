@@ -398,3 +398,21 @@ def test_tensor_core_probe_matches_gemm_probe(monkeypatch, nlist, nprobe, dup):
         out[env] = iv.select_clusters(q, cent, nprobe)
     np.testing.assert_array_equal(out["1"][0], out["0"][0])
     np.testing.assert_allclose(out["1"][1], out["0"][1], rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("chunks", ["1", "2"])
+def test_search_batch_short_rows(monkeypatch, chunks):
+    """Queries whose probed lists hold fewer than k vectors come back trimmed to their count
+    (row views made before the results land are re-cut afterwards)."""
+    ix, q = _synthetic_index(600, 32, 40, 4, seed=11)
+    sp = iv.SearchParams(k=40, n_probe=1, ip_mode="bitwise")
+    r = search_device(dev.to_device(q), ix, sp)
+    ids, dists, counts = dev.to_host(r.ids), dev.to_host(r.dists), dev.to_host(r.counts)
+    assert counts.min() < 40 <= counts.max() or counts.max() < 40
+    assert (counts < 40).any()
+    monkeypatch.setenv("IVRQ_E2E_CHUNKS", chunks)
+    res = iv.search_batch(q, ix, sp)
+    assert len(res) == len(q)
+    for i in range(len(q)):
+        np.testing.assert_array_equal(res[i][0], ids[i, : counts[i]])
+        np.testing.assert_array_equal(res[i][1], dists[i, : counts[i]])
