@@ -615,6 +615,47 @@ __device__ __forceinline__ ListMeta list_meta(const Args& a, int64_t qp) {
   return m;
 }
 
+// ------------------------------------------------------------ float32 stage-1 decision
+// The prune test keeps a vector iff max(est2 - sqrt(S), 0) <= T (search.py:360-366 with the
+// stage1_chunk shortcuts), est2 = max((add + d_qc2) - scale (delta ip - half_code), 0) and
+// S = (err sqrt(d_qc2))^2 + (scale ip_margin)^2, all in float64.  Evaluated in float32, est2 is
+// within E = 2^-19 M of the float64 value (M = |add| + d_qc2 + |scale| (|delta ip| + |half_code|):
+// about ten float32 roundings of at most 2^-24 M each, input conversions included) and S within
+// 2^-19 relative.  Outside those bands the float32 answer is the float64 one; inside (about 1e-5 of
+// the vectors) the caller runs the float64 test.  Returns 1 keep, 0 prune, -1 undecided.
+struct Stage1F32 {
+  float delta, half, ahalf, dqc, sq, ipm, T_lo, T_hi;
+};
+
+__device__ __forceinline__ Stage1F32 stage1_f32(double delta, double half_code, double ipm, double d_qc2, double sq,
+                                                double T) {
+  Stage1F32 f;
+  f.delta = (float)delta;
+  f.half = (float)half_code;
+  f.ahalf = fabsf(f.half);
+  f.dqc = (float)d_qc2;
+  f.sq = (float)sq;
+  f.ipm = (float)ipm;
+  f.T_lo = __double2float_rd(T);
+  f.T_hi = __double2float_ru(T);
+  return f;
+}
+
+__device__ __forceinline__ int stage1_decide_f32(int ip, float add, float scale, float err, const Stage1F32& f) {
+  const float t1 = f.delta * (float)ip;
+  const float e = (add + f.dqc) - scale * (t1 - f.half);
+  const float M = fabsf(add) + f.dqc + fabsf(scale) * (fabsf(t1) + f.ahalf);
+  const float E = M * 0x1p-19f;
+  const float dk = (e + E) - f.T_lo;  // >= est2 - T
+  if (dk <= 0.f) return 1;
+  const float mg = err * f.sq, sm = scale * f.ipm;
+  const float S = mg * mg + sm * sm;
+  if (dk * dk < S * (1.f - 0x1p-19f)) return 1;
+  const float dr = (e - E) - f.T_hi;  // <= est2 - T
+  if (dr > 0.f && dr * dr > S * (1.f + 0x1p-19f)) return 0;
+  return -1;
+}
+
 // ------------------------------------------------------------ warp-per-query kernel (precomputed inner products)
 // With the stage-1 inner products already in HBM (ip_list_kernel) a query's
 // remaining work is a light stream (2-byte ip + 8-byte factors per vector)
@@ -836,6 +877,8 @@ __global__ void __launch_bounds__(WQ * 32, MINB) scan_warp_kernel(Args a) {
         if (c0 + u * 32 >= n_c) break;  // warp-uniform
         bool keep = false;
         double est2 = 0.0;
+        // (the float32 pre-decision of scan_rd_kernel measured no faster here: this kernel is
+        // latency-bound on its survivor refine, not on the float64 test)
         if (vi < n_c) {
           const double ipb = dmul(qc.delta, (double)ipv[u]);
           const double add = (double)fa[u];
@@ -970,6 +1013,7 @@ __global__ void __launch_bounds__(RDW * 32, MINB) scan_rd_kernel(Args a) {
     } else {
       const IPT* iprow = reinterpret_cast<const IPT*>(a.ipbuf) + rowbase;
       const double sq = dsqrt(d_qc2);
+      const Stage1F32 f32 = stage1_f32(delta, half_code, ipm, d_qc2, sq, T_list);
       for (int64_t c0 = 0; c0 < n_c; c0 += 32 * RSUB) {
         int ipv[RSUB];
         float fa[RSUB], fs[RSUB], fe[RSUB];
@@ -991,7 +1035,10 @@ __global__ void __launch_bounds__(RDW * 32, MINB) scan_rd_kernel(Args a) {
           const int64_t vi = c0 + u * 32 + lane;
           keep[u] = false;
           est[u] = 0.0;
-          if (vi < n_c) {
+          const int dec = (REFINE && vi < n_c) ? stage1_decide_f32(ipv[u], fa[u], fs[u], fe[u], f32) : -1;
+          if (dec >= 0) {
+            keep[u] = dec != 0;
+          } else if (vi < n_c) {
             const double ipb = dmul(delta, (double)ipv[u]);
             const double scale = (double)fs[u];
             const double est2 = dmax(dsub(dadd((double)fa[u], d_qc2), dmul(scale, dsub(ipb, half_code))), 0.0);
