@@ -2015,7 +2015,7 @@ __host__ __device__ inline uint32_t tmem_cols(int n) {  // power of two >= 32 (<
 
 size_t tc_smem_bytes(int kpad, int G, int nst) {
   const int nkc = (kpad + TCKC - 1) / TCKC;
-  return 1024 + (size_t)nkc * 8 * G * TCKC + (size_t)nst * TCM * TCKC + 64 * G + 256;
+  return 1024 + (size_t)nkc * 8 * G * TCKC + (size_t)nst * TCM * TCKC + 128 * G + 256;
 }
 
 // byte offset of (row R, byte k < 128) in a 128B-swizzled K-major tile (8-row atoms of 1024 B)
@@ -2031,18 +2031,26 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_refine_kernel(const __grid_c
   const int nkc = (kp + TCKC - 1) / TCKC;  // 128-byte K chunks
   int8_t* sB = reinterpret_cast<int8_t*>(tsm);                                   // [nkc][N rows x 128 B] swizzled
   uint8_t* sA = reinterpret_cast<uint8_t*>(tsm + (size_t)nkc * N * TCKC);        // [TCST][128 rows x 128 B] swizzled
-  double* s_dq = reinterpret_cast<double*>(sA + TCST * TCM * TCKC);              // [G]
-  double* s_kb = s_dq + G;
-  double* s_hs = s_kb + G;
-  double* s_ls = s_hs + G;
-  int64_t* s_row = reinterpret_cast<int64_t*>(s_ls + G);                         // [G] rdist row of query j
-  uint64_t* bars = reinterpret_cast<uint64_t*>(s_row + G);
+  // per-query scalars of a group, double-buffered by group parity: [2][G] each
+  double* s_dq = reinterpret_cast<double*>(sA + TCST * TCM * TCKC);
+  double* s_kb = s_dq + 2 * G;
+  double* s_hs = s_kb + 2 * G;
+  double* s_ls = s_hs + 2 * G;
+  int64_t* s_row = reinterpret_cast<int64_t*>(s_ls + 2 * G);                     // rdist row of query j
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_row + 2 * G);
   uint64_t* full = bars;                      // [TCST]
   uint64_t* empty = bars + TCST;              // [TCST]
   uint64_t* accf = bars + 2 * TCST;           // [2]
   uint64_t* acce = bars + 2 * TCST + 2;       // [2]
   uint64_t* bfull = bars + 2 * TCST + 4;      // [1]
-  uint32_t* s_taddr = reinterpret_cast<uint32_t*>(bars + 2 * TCST + 5);
+  uint64_t* bempty = bars + 2 * TCST + 5;     // [1] the group's MMAs are done with sB
+  uint64_t* scf = bars + 2 * TCST + 6;        // [2] scalars of buffer i written
+  uint64_t* sce = bars + 2 * TCST + 8;        // [2] scalars of buffer i consumed by the epilogue
+  uint32_t* s_taddr = reinterpret_cast<uint32_t*>(bars + 2 * TCST + 10);
+  // 8-bit codes: query groups hand over through mbarriers (B reloaded as soon as the previous
+  // group's MMAs retire, scalars double-buffered) instead of a CTA barrier that drains the
+  // pipeline at every group; the 4-bit path (all producer warps unpacking) keeps the barrier
+  const bool async_grp = !a.nib;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   // a whole warp waiting on an mbarrier: one lane polls (a.w1), the warp then re-converges
   auto wait1 = [&](uint64_t* bar, uint32_t parity) {
@@ -2059,6 +2067,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_refine_kernel(const __grid_c
       tc::mbar_init(&acce[i], 128);
     }
     tc::mbar_init(bfull, 1);
+    tc::mbar_init(bempty, 1);
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&scf[i], 1);
+      tc::mbar_init(&sce[i], 128);
+    }
     tc::fence_mbar_init();
   }
   if (wid == TC_PROD) tc::tmem_alloc(s_taddr, tmem_cols(2 * N));
@@ -2083,9 +2096,36 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_refine_kernel(const __grid_c
     const int nqg = (int)min((int64_t)G, a.poff[c + 1] - ps);
     const int64_t rs = ip_row_stride(n_c);
     const int ntile = (int)ceil_div(n_c, TCM);
-    __syncthreads();  // previous group's MMAs completed (its epilogue waited on them), scalars consumed
+    const int sb = (int)(grp & 1);  // scalar buffer of this group
+    if (!async_grp) __syncthreads();  // previous group's MMAs completed (its epilogue waited on them), scalars consumed
     if (a.prof && wid == TC_PROD && lane == 0 && a_grp_end) atomicAdd(a.prof + 5, (unsigned long long)(clock64() - a_grp_end));
-    if (wid == 0) {   // group operand: the G queries' digit slices, 8 rows per query, by TMA (one lane per query)
+    if (wid == (async_grp ? 1 : 0)) {
+      // group scalars (lane j: query j), then the group operand: the G queries' digit slices,
+      // 8 rows per query, by TMA (one lane per query)
+      if (async_grp) wait1(&sce[sb], ((grp >> 1) & 1) ^ 1);  // the epilogue is done with group grp - 2
+      if (lane < G) {
+        double dq = 0.0, kb = 0.0;
+        int e = 0;
+        int64_t row = 0;
+        if (lane < nqg) {
+          const int64_t pr = a.porder[ps + lane];
+          const int64_t q = pr / a.nprobe;
+          dq = a.probe_d2[pr];
+          kb = a.scalars[q * IVRQ_QS_COUNT + IVRQ_QS_KB_SUM];
+          e = (int)a.scalars[q * IVRQ_QS_COUNT + IVRQ_QS_SLICE_EXP];
+          row = a.pair_base[c] + (ps + lane - a.poff[c]) * rs;
+        }
+        s_dq[sb * G + lane] = dq;
+        s_kb[sb * G + lane] = kb;
+        s_hs[sb * G + lane] = ldexp(1.0, e - 26);
+        s_ls[sb * G + lane] = ldexp(1.0, e - 54);
+        s_row[sb * G + lane] = row;
+      }
+      __syncwarp();
+      if (async_grp) {
+        if (lane == 0) tc::mbar_arrive(&scf[sb]);
+        wait1(bempty, (grp & 1) ^ 1);  // the previous group's MMAs no longer read sB
+      }
       if (lane == 0) tc::mbar_expect_tx(bfull, (uint32_t)(nqg * nkc * 8 * TCKC));
       __syncwarp();
       if (lane < nqg) {
@@ -2094,25 +2134,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_refine_kernel(const __grid_c
           tc::tma_load_2d(sB + kc * N * TCKC + lane * 8 * TCKC, &a.map_b, kc * TCKC, q8, bfull);
       }
     }
-    if (tid < G) {
-      double dq = 0.0, kb = 0.0;
-      int e = 0;
-      int64_t row = 0;
-      if (tid < nqg) {
-        const int64_t pr = a.porder[ps + tid];
-        const int64_t q = pr / a.nprobe;
-        dq = a.probe_d2[pr];
-        kb = a.scalars[q * IVRQ_QS_COUNT + IVRQ_QS_KB_SUM];
-        e = (int)a.scalars[q * IVRQ_QS_COUNT + IVRQ_QS_SLICE_EXP];
-        row = a.pair_base[c] + (ps + tid - a.poff[c]) * rs;
-      }
-      s_dq[tid] = dq;
-      s_kb[tid] = kb;
-      s_hs[tid] = ldexp(1.0, e - 26);
-      s_ls[tid] = ldexp(1.0, e - 54);
-      s_row[tid] = row;
-    }
-    __syncthreads();
+    if (!async_grp) __syncthreads();
     if (wid < TC_PROD) {
       // ---- producers: rcode tiles -> A ring
       if (!a.nib) {
@@ -2203,11 +2225,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_refine_kernel(const __grid_c
           __syncwarp();
         }
       }
+      if (async_grp && lane == 0) tc::commit(bempty);  // sB free once this group's MMAs retire
+      __syncwarp();
       if (a.prof && lane == 0) a_grp_end = clock64();
     } else {
       // ---- epilogue: row r of the tile is TMEM lane r
       const int quarter = wid & 3;
       const int r = quarter * 32 + lane;
+      if (async_grp) wait1(&scf[sb], (grp >> 1) & 1);
       for (int t = 0; t < ntile; ++t, ++tile_epi) {
         const int ab = tile_epi & 1;
         const int64_t v = (int64_t)t * TCM + r;
@@ -2228,14 +2253,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_refine_kernel(const __grid_c
               const int* D = reinterpret_cast<const int*>(d + 8 * jj);
               const long long hi = (long long)D[0] * 2097152LL + (long long)D[1] * 16384LL + (long long)D[2] * 128LL + D[3];
               const long long lw = (long long)D[4] * 2097152LL + (long long)D[5] * 16384LL + (long long)D[6] * 128LL + D[7];
-              const double ip = dadd(dmul((double)hi, s_hs[j]), dmul((double)lw, s_ls[j]));
-              a.rdist[s_row[j] + v] = dmax(dsub(dadd((double)lf.x, s_dq[j]), dmul((double)lf.y, dsub(ip, s_kb[j]))), 0.0);
+              const int js = sb * G + j;
+              const double ip = dadd(dmul((double)hi, s_hs[js]), dmul((double)lw, s_ls[js]));
+              a.rdist[s_row[js] + v] =
+                  dmax(dsub(dadd((double)lf.x, s_dq[js]), dmul((double)lf.y, dsub(ip, s_kb[js]))), 0.0);
             }
           }
         }
         tc::fence_before_sync();
         tc::mbar_arrive(&acce[ab]);
       }
+      if (async_grp) tc::mbar_arrive(&sce[sb]);  // this group's scalars may be overwritten
     }
   }
   tc::fence_before_sync();
