@@ -2573,7 +2573,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_ip_kernel(const __grid_const
   uint64_t* accf = bars + 2 * TCST;
   uint64_t* acce = bars + 2 * TCST + 2;
   uint64_t* bfull = bars + 2 * TCST + 4;
-  uint32_t* s_taddr = reinterpret_cast<uint32_t*>(bars + 2 * TCST + 5);
+  uint64_t* bempty = bars + 2 * TCST + 5;  // the group's MMAs are done with sB
+  uint32_t* s_taddr = reinterpret_cast<uint32_t*>(bars + 2 * TCST + 6);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   if (tid == 0) {
     for (int i = 0; i < TCST; ++i) {
@@ -2585,6 +2586,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_ip_kernel(const __grid_const
       tc::mbar_init(&acce[i], 128);
     }
     tc::mbar_init(bfull, 1);
+    tc::mbar_init(bempty, 1);
     tc::fence_mbar_init();
   }
   if (wid == TC_PROD) tc::tmem_alloc(s_taddr, 512);
@@ -2607,11 +2609,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_ip_kernel(const __grid_const
     const int N = (nqg + 15) & ~15;
     const int64_t rs = ip_row_stride(n_c);
     const int ntile = (int)ceil_div(n_c, TCM);
-    __syncthreads();  // previous group's MMAs completed (its epilogue waited on them)
-    if (tid == 0) {   // B: the group's qhat rows (contiguous in pair order)
-      tc::mbar_expect_tx(bfull, (uint32_t)(nkc * IPQ * TCKC));
-      for (int kc = 0; kc < nkc; ++kc) tc::tma_load_2d(sB + kc * IPQ * TCKC, &a.map_b, kc * TCKC, (int)ps, bfull);
-    }
+    // no CTA barrier between groups: the MMA warp reloads B once the previous group's MMAs retire
+    // (bempty) while the producers keep filling the A ring and the epilogue drains the last tiles
     if (wid < TC_PROD) {
       // ---- producers: code words -> 0/1 bytes, swizzled (each thread: row r, one word = 32 dims = 2 x 16 B)
       const int pl = wid * 32 + lane;
@@ -2666,6 +2665,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_ip_kernel(const __grid_const
     } else if (wid == TC_PROD) {
       // ---- MMA issuer
       const uint32_t idesc = tc::idesc_i8(TCM, N, false, true);
+      tc::mbar_wait(bempty, (grp & 1) ^ 1);
+      if (lane == 0) {  // B: the group's qhat rows (contiguous in pair order)
+        tc::mbar_expect_tx(bfull, (uint32_t)(nkc * IPQ * TCKC));
+        for (int kc = 0; kc < nkc; ++kc) tc::tma_load_2d(sB + kc * IPQ * TCKC, &a.map_b, kc * TCKC, (int)ps, bfull);
+      }
+      __syncwarp();
       tc::mbar_wait(bfull, grp & 1);
       for (int t = 0; t < ntile; ++t, ++tile_mma) {
         const int ab = tile_mma & 1;
@@ -2688,6 +2693,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_ip_kernel(const __grid_const
           __syncwarp();
         }
       }
+      if (lane == 0) tc::commit(bempty);  // sB free once this group's MMAs retire
+      __syncwarp();
     } else {
       // ---- epilogue: TMEM lane r = vector, column j = query slot
       const int quarter = wid & 3;
@@ -3119,11 +3126,11 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
       if (rd_path && refine) {
         // refined distance of every probed pair on tcgen05 (concurrent with the inner products)
         // group size: the rcode tiles of a list are streamed once per group, so the largest group whose
-        // digit slices fit next to a ring of >= 4 A stages (C3, D = 768: G = 24, 4 stages; measured
-        // 3.10 vs 3.40 ms per scan stage against G = 16 with 6 stages)
+        // digit slices fit next to a ring of >= 3 A stages (C3, D = 768: G = 28, 3 stages; scan stage
+        // measured 2.72 ms against 2.78 (G = 24, 4 stages), 2.88 (20, 5), 3.19 (16, 6), 3.64 (12, 8))
         const size_t smem_cap = 227 * 1024;
         int G = 32;
-        while (G > 4 && scan::tc_smem_bytes(a.kpad, G, 4) > smem_cap) G -= 4;
+        while (G > 4 && scan::tc_smem_bytes(a.kpad, G, 3) > smem_cap) G -= 4;
         int nst = scan::TCST;
         while (nst > 2 && scan::tc_smem_bytes(a.kpad, G, nst) > smem_cap) --nst;
         if (getenv("IVRQ_TC_G")) G = atoi(getenv("IVRQ_TC_G"));  // A/B: group size (multiple of 2) and A stages
