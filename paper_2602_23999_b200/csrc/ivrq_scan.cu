@@ -665,7 +665,8 @@ __device__ __forceinline__ int stage1_decide_f32(int ip, float add, float scale,
 // warp's register top-32 queue IS the query's pool.  Same prune test, refine
 // arithmetic and (dist, id) order as scan_kernel, so results are identical.
 constexpr int WQ = 2;      // queries (warps) per CTA
-constexpr int WQ_MINB = 12; // resident CTAs per SM the register budget is sized for
+constexpr int WQ_MINB = 8;  // resident CTAs per SM the register budget is sized for (B200 A/B, scan ms:
+                            // C2 2.93 vs 3.01 at 12, C4 8.6 vs 9.06, C5 16.6 vs 18.3)
 constexpr int SUB = 4;     // 32-vector sub-chunks loaded together (memory-level parallelism)
 constexpr int RING = 256;  // survivor ring per warp (holds < 32 + 32 * SUB)
 
@@ -2809,9 +2810,13 @@ inline int launch_rd(const Args& a, bool refine, int ipb, cudaStream_t s) {
 template <bool REFINE, bool NIB>
 int launch_warp(const Args& a, int ipb, cudaStream_t s) {
   const size_t sm = warp_smem_bytes(a.kpad, REFINE);
-  static const int minb = getenv("IVRQ_WARP_MINB") ? atoi(getenv("IVRQ_WARP_MINB")) : WQ_MINB;
+  // wide rows (D >= 1024: the digit slices take ~12 KB of shared memory per warp) trade residency
+  // for registers: C5 (D = 1536) scan 15.4 ms at 6 vs 16.8 at 8; C4 (D = 96) 8.6 at 8 vs 10.0 at 6
+  static const int minb_env = getenv("IVRQ_WARP_MINB") ? atoi(getenv("IVRQ_WARP_MINB")) : 0;
+  const int minb = minb_env ? minb_env : (a.kpad >= 1024 ? 6 : WQ_MINB);
   auto kern = minb == 16  ? (ipb == 2 ? scan_warp_kernel<REFINE, NIB, 2, 16> : scan_warp_kernel<REFINE, NIB, 4, 16>)
-              : minb == 8 ? (ipb == 2 ? scan_warp_kernel<REFINE, NIB, 2, 8> : scan_warp_kernel<REFINE, NIB, 4, 8>)
+              : minb == 12 ? (ipb == 2 ? scan_warp_kernel<REFINE, NIB, 2, 12> : scan_warp_kernel<REFINE, NIB, 4, 12>)
+              : minb == 6 ? (ipb == 2 ? scan_warp_kernel<REFINE, NIB, 2, 6> : scan_warp_kernel<REFINE, NIB, 4, 6>)
                           : (ipb == 2 ? scan_warp_kernel<REFINE, NIB, 2, WQ_MINB> : scan_warp_kernel<REFINE, NIB, 4, WQ_MINB>);
   if (sm > 48 * 1024 && cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess)
     return fail(IVRQ_EUNSUP, "ivrq_search_scan: shared memory request too large");
