@@ -355,6 +355,9 @@ def run_ours(args, cfg_name: str) -> dict:
         tdist.barrier()
     step_ms, scan_ms, stage_ms = [], [], {"rotate": 0.0, "probe": 0.0, "prepare": 0.0, "scan": 0.0}
     klib = _lib.load()
+    prof_range = os.environ.get("BENCH_PROFILE_RANGE") == "1"  # ncu --profile-from-start off: timed steps only
+    if prof_range:
+        torch.cuda.profiler.start()
     _lib.call("ivrq_kernel_timing", 1)  # CUDA events around the scan's dominant kernels, on their streams
     with ClockSampler(local) as clocks:
         for _ in range(args.steps):
@@ -369,6 +372,8 @@ def run_ours(args, cfg_name: str) -> dict:
             stage_ms["prepare"] += ev["probed"].elapsed_time(ev["prepared"])
             stage_ms["scan"] += scan_ms[-1]
     torch.cuda.synchronize()
+    if prof_range:
+        torch.cuda.profiler.stop()
     _lib.call("ivrq_kernel_timing", 0)
     kernel_ms = {}
     for kn in ("tc_refine_kernel", "scan_rd_kernel", "scan_warp_kernel", "tc_ip_kernel", "ip_list_kernel"):

@@ -2631,13 +2631,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_ip_kernel(const __grid_const
         }
       };
       const int nst = ntile * nkc;
-      uint32_t wn[PER];
-      if (nst > 0) load_stage(0, wn);
-      for (int sidx = 0; sidx < nst; ++sidx, ++it_prod) {
+      // words of the next PF stages in flight (registers): one load round trip per PF stages
+      constexpr int PF = 4;
+      uint32_t wq[PF][PER];
+#pragma unroll
+      for (int j = 0; j < PF; ++j)
+        if (j < nst) load_stage(j, wq[j]);
+      for (int s0 = 0; s0 < nst; s0 += PF) {
+#pragma unroll
+      for (int j = 0; j < PF; ++j) {
+        const int sidx = s0 + j;
+        if (sidx >= nst) break;
         uint32_t wc[PER];
 #pragma unroll
-        for (int e = 0; e < PER; ++e) wc[e] = wn[e];
-        if (sidx + 1 < nst) load_stage(sidx + 1, wn);
+        for (int e = 0; e < PER; ++e) wc[e] = wq[j][e];
+        if (sidx + PF < nst) load_stage(sidx + PF, wq[j]);
         {
           const int st = it_prod % TCST;
           tc::mbar_wait(&empty[st], ((it_prod / TCST) & 1) ^ 1);
@@ -2662,6 +2670,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_ip_kernel(const __grid_const
           tc::fence_smem_async();
           tc::mbar_arrive(&full[st]);
         }
+        ++it_prod;
+      }
       }
     } else if (wid == TC_PROD) {
       // ---- MMA issuer
