@@ -1977,6 +1977,8 @@ constexpr int TCKC = 128;    // K bytes per A stage (4 MMAs of K = 32)
 constexpr int TCST = 6;      // A stages
 constexpr int TC_PROD = 4;  // producer warps
 constexpr int TC_THREADS = 32 * (TC_PROD + 1 + 4);
+constexpr int TCR_EPI = 8;  // tc_refine epilogue warps: 2 per TMEM lane quarter, each half of the group's queries
+constexpr int TCR_THREADS = 32 * (TC_PROD + 1 + TCR_EPI);
 
 struct TcArgs {
   CUtensorMap map_a;        // rcodes [N rows x rcode_bytes] (8-bit codes), box 128 B x 128 rows, 128B swizzle
@@ -2024,7 +2026,7 @@ __device__ __forceinline__ uint32_t sw128_offset(int R, int k) {
   return (uint32_t)((R >> 3) * 1024 + (R & 7) * 128 + ((((k >> 4) ^ (R & 7)) & 7) << 4) + (k & 15));
 }
 
-__global__ void __launch_bounds__(TC_THREADS, 1) tc_refine_kernel(const __grid_constant__ TcArgs a) {
+__global__ void __launch_bounds__(TCR_THREADS, 1) tc_refine_kernel(const __grid_constant__ TcArgs a) {
   extern __shared__ __align__(1024) unsigned char tsm_raw[];
   unsigned char* tsm = reinterpret_cast<unsigned char*>(((uintptr_t)tsm_raw + 1023) & ~(uintptr_t)1023);
   const int G = a.G, N = 8 * G, kp = a.kpad;
@@ -2065,13 +2067,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_refine_kernel(const __grid_c
     }
     for (int i = 0; i < 2; ++i) {
       tc::mbar_init(&accf[i], 1);
-      tc::mbar_init(&acce[i], 128);
+      tc::mbar_init(&acce[i], 32 * TCR_EPI);
     }
     tc::mbar_init(bfull, 1);
     tc::mbar_init(bempty, 1);
     for (int i = 0; i < 2; ++i) {
       tc::mbar_init(&scf[i], 1);
-      tc::mbar_init(&sce[i], 128);
+      tc::mbar_init(&sce[i], 32 * TCR_EPI);
     }
     tc::fence_mbar_init();
   }
@@ -2230,9 +2232,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_refine_kernel(const __grid_c
       __syncwarp();
       if (a.prof && lane == 0) a_grp_end = clock64();
     } else {
-      // ---- epilogue: row r of the tile is TMEM lane r
+      // ---- epilogue: row r of the tile is TMEM lane r (a warp reads lane quarter wid % 4); the two
+      // warps of a quarter split the group's queries
       const int quarter = wid & 3;
       const int r = quarter * 32 + lane;
+      const int jh = ((G >> 1) + 3) & ~3;
+      const int j_lo = ((wid - (TC_PROD + 1)) >> 2) * jh, j_hi = min(G, j_lo + jh);
       if (async_grp) wait1(&scf[sb], (grp >> 1) & 1);
       for (int t = 0; t < ntile; ++t, ++tile_epi) {
         const int ab = tile_epi & 1;
@@ -2243,7 +2248,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_refine_kernel(const __grid_c
         wait1(&accf[ab], (tile_epi >> 1) & 1);
         if (a.prof && tid == 32 * (TC_PROD + 1)) atomicAdd(a.prof + 7, (unsigned long long)(clock64() - te));
         tc::fence_after_sync();
-        for (int j0 = 0; j0 < G && a.dbg != 1 && a.dbg != 3; j0 += 4) {
+        for (int j0 = j_lo; j0 < j_hi && a.dbg != 1 && a.dbg != 3; j0 += 4) {
           uint32_t d[32];
           tc::tmem_ld32(tbase + ((uint32_t)(quarter * 32) << 16) + ab * N + 8 * j0, d);
           tc::tmem_ld_wait();
@@ -3215,7 +3220,7 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
         fd_launch = [ta, tsm, s]() {
           {
             KernelTimer kt("tc_refine_kernel", s);
-            scan::tc_refine_kernel<<<(unsigned)sm_count_of_current_device(), scan::TC_THREADS, tsm, s>>>(ta);
+            scan::tc_refine_kernel<<<(unsigned)sm_count_of_current_device(), scan::TCR_THREADS, tsm, s>>>(ta);
           }
           const int rc = check_launch("ivrq_search_scan(tensor-core refine)");
           if (ta.prof) {  // debugging aid (synchronises): where the MMA lane waited
