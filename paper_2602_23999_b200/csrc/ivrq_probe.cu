@@ -30,8 +30,8 @@ namespace probe {
 template <int NDIG> constexpr int QT_ = 128 / NDIG;
 template <int NDIG> constexpr int CT_ = 256 / NDIG;
 constexpr int KC = 128;  // K bytes per stage
-constexpr int ST = 4;    // stages
-constexpr int EPW = 8;        // epilogue warps (2 per TMEM lane quarter)
+constexpr int ST = 3;    // stages
+constexpr int EPW = 16;       // epilogue warps (4 per TMEM lane quarter: the epilogue, not the MMAs, bounds the tile)
 constexpr int THREADS = 32 * (2 + EPW);  // warp 0 TMA, warp 1 MMA, warps 2.. epilogue
 constexpr int NCOL = 256;  // accumulator columns per tile
 
@@ -174,7 +174,8 @@ __global__ void __launch_bounds__(THREADS, 1) tc_probe_kernel(const __grid_const
   } else {
     // epilogue: TMEM lane = A row = NDIG j + s (query j of the tile, digit s); column NDIG c + t
     const int quarter = wid & 3;
-    const int half = (wid - 2) >> 2;  // which half of the tile's centroids this warp finishes
+    constexpr int PARTS = EPW / 4;      // warps per TMEM lane quarter
+    const int part = (wid - 2) >> 2;  // which part of the tile's centroids this warp finishes
     const int s = lane % NDIG;
     const int jq = quarter * (32 / NDIG) + lane / NDIG;  // query within the tile
     const int b1 = (lane >> 1) & 1, b0 = lane & 1;
@@ -234,7 +235,7 @@ __global__ void __launch_bounds__(THREADS, 1) tc_probe_kernel(const __grid_const
       // NDIG == 2 stages each 32-column chunk (16 queries x 16 centroids, L and U) in shared memory
       // so that every query row is written as two 64-byte runs
       float* stg = s_stage + (wid - 2) * (2 * 16 * 16);
-      for (int cc0 = half * (CT / 2); cc0 < (half + 1) * (CT / 2); cc0 += CPC) {
+      for (int cc0 = part * (CT / PARTS); cc0 < (part + 1) * (CT / PARTS); cc0 += CPC) {
         uint32_t v[32];
         tc::tmem_ld32(tbase + ((uint32_t)(quarter * 32) << 16) + ab * NCOL + NDIG * cc0, v);
         tc::tmem_ld_wait();
