@@ -161,12 +161,22 @@ __global__ void __launch_bounds__(256) probe_select_kernel(const double* __restr
 // and build_luts (search.py:115-132).
 __global__ void prepare_kernel(const double* __restrict__ q_rot, int64_t nq, int d, int mode, int qbits,
                                int index_bits, double eps_bound, double* __restrict__ scalars,
-                               uint32_t* __restrict__ planes, float* __restrict__ luts, int8_t* __restrict__ qslices) {
+                               uint32_t* __restrict__ planes, float* __restrict__ luts, int8_t* __restrict__ qslices,
+                               int stage_rows) {
+  extern __shared__ double prep_rows[];  // [warps][d] when launched with shared memory, else unused
   const int lane = threadIdx.x & 31;
   const int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (q >= nq) return;
-  const double* x = q_rot + q * d;
+  const double* xg = q_rot + q * d;
   const int g = words_per_vector(d);
+  const double* x = xg;
+  if (stage_rows) {  // the row is read coalesced into shared memory once; the serial pairwise sum below
+                     // then walks shared memory instead of issuing dependent global loads
+    double* row = prep_rows + (size_t)(threadIdx.x >> 5) * d;
+    for (int i = lane; i < d; i += 32) row[i] = xg[i];
+    __syncwarp();
+    x = row;
+  }
   double sum_q = 0.0;
   if (lane == 0) sum_q = pairwise_sum_seq(x, d);
   sum_q = __shfl_sync(0xffffffffu, sum_q, 0);
@@ -346,10 +356,14 @@ extern "C" int ivrq_prepare_queries(const double* q_rot, int64_t nq, int32_t dim
   if (params->ip_mode == IVRQ_IP_LUT && !luts) return fail(IVRQ_EINVAL, "lut mode needs luts");
   if (params->refine && index_bits >= 2 && !qslices) return fail(IVRQ_EINVAL, "refine needs qslices");
   if (nq == 0) return IVRQ_OK;
-  const int wpb = 4;
-  prepare_kernel<<<(unsigned)ceil_div(nq, wpb), wpb * 32, 0, as_stream(stream)>>>(
+  // rows staged in shared memory (up to 48 KB per block: 4 warps at D <= 1536, fewer beyond)
+  int wpb = 4;
+  while (wpb > 1 && (size_t)wpb * dims * sizeof(double) > 48 * 1024) --wpb;
+  const size_t psm = (size_t)wpb * dims * sizeof(double);
+  const int stage = psm <= 48 * 1024 ? 1 : 0;
+  prepare_kernel<<<(unsigned)ceil_div(nq, wpb), wpb * 32, stage ? psm : 0, as_stream(stream)>>>(
       q_rot, nq, dims, params->ip_mode, params->query_bits, index_bits, eps_bound, scalars, planes, luts,
-      (params->refine && index_bits >= 2) ? qslices : nullptr);
+      (params->refine && index_bits >= 2) ? qslices : nullptr, stage);
   return check_launch("ivrq_prepare_queries");
 }
 
