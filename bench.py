@@ -18,6 +18,14 @@ float64 k-NN on the GPU.
 N > 1 GPUs: each rank holds a replica built from the same seed and searches
 its own 10,000-query batch (weak scaling, no data-path collective); the time
 is the max over ranks.
+
+Both arms print the same ``config`` (the workload: shape, nlist, bits, n_probe,
+k, query batch); measured quantities (recall, nprobe sweep, build seconds,
+stage times) are separate keys.  ``--impl reference`` never imports
+paper_2602_23999_b200: it builds the index on the host (the reference's own
+``build_index`` for the 100K-row config, the oracle port with a parallel
+per-list encoder otherwise) and times the unmodified reference ``search_batch``
+from baseline/_ref in one forked process per host core.
 """
 
 from __future__ import annotations
@@ -38,13 +46,16 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 CONFIGS = {
-    # name: (N, D, nlist, bits, nprobe (None -> smallest sweep value with recall >= target))
-    "c1": dict(n=100_000, d=128, nlist=256, bits=1, nprobe=16, desc="synthetic 100Kx128, nlist 256, 1-bit, nprobe 16"),
-    "c2": dict(n=1_000_000, d=128, nlist=1024, bits=4, nprobe=None, desc="synthetic 1Mx128, nlist 1024, 4-bit"),
-    "c3": dict(n=1_000_000, d=768, nlist=1024, bits=8, nprobe=None, desc="synthetic 1Mx768, nlist 1024, 8-bit"),
-    "c4": dict(n=10_000_000, d=96, nlist=16384, bits=4, nprobe=None, desc="synthetic 10Mx96, nlist 16384, 4-bit"),
-    "c5": dict(n=5_000_000, d=1536, nlist=8192, bits=4, nprobe=None, desc="synthetic 5Mx1536, nlist 8192, 4-bit"),
+    # n_probe: the smallest sweep value with recall@10 >= 0.95 (C3, C5), or where recall saturates
+    # below it (C2, C4: 4-bit codes), measured by this script's sweep (reported under "quality")
+    "c1": dict(n=100_000, d=128, nlist=256, bits=1, nprobe=16, desc="synthetic 100Kx128, nlist 256, 1-bit"),
+    "c2": dict(n=1_000_000, d=128, nlist=1024, bits=4, nprobe=16, desc="synthetic 1Mx128, nlist 1024, 4-bit"),
+    "c3": dict(n=1_000_000, d=768, nlist=1024, bits=8, nprobe=8, desc="synthetic 1Mx768, nlist 1024, 8-bit"),
+    "c4": dict(n=10_000_000, d=96, nlist=16384, bits=4, nprobe=64, desc="synthetic 10Mx96, nlist 16384, 4-bit"),
+    "c5": dict(n=5_000_000, d=1536, nlist=8192, bits=4, nprobe=32, desc="synthetic 5Mx1536, nlist 8192, 4-bit"),
 }
+METRIC = "search QPS @ recall@10~0.95 (10K-query batch)"
+DATA_NOTE = "synthetic Gaussian mixture (reference conftest recipe, torch RNG on cuda:0)"
 SWEEP = (1, 2, 4, 8, 16, 32, 64, 128)
 TARGET_RECALL = 0.95
 NQ = 10_000
@@ -170,6 +181,18 @@ def train_fraction(n, nlist):
     return min(n, max(math.ceil(n / 10), 10 * nlist)) / n
 
 
+def config_dict(cfg_name: str, mode: str) -> dict:
+    """The workload, identical for both arms (--impl ours / reference)."""
+    cfg = CONFIGS[cfg_name]
+    return {
+        "workload": cfg_name + ": " + cfg["desc"],
+        "n": cfg["n"], "dims": cfg["d"], "nlist": cfg["nlist"], "bits": cfg["bits"],
+        "n_probe": cfg["nprobe"], "k": K, "n_queries": NQ, "ip_mode": mode, "query_bits": 4,
+        "build_params": {"kmeans_iters": 25, "train_fraction": round(train_fraction(cfg["n"], cfg["nlist"]), 5),
+                         "seed": 0},
+    }
+
+
 def recall_at_k(ids: np.ndarray, gt: np.ndarray, k: int) -> float:
     hits = 0
     for a, b in zip(ids[:, :k], gt[:, :k]):
@@ -182,6 +205,18 @@ def measured_peaks() -> dict:
     if p.exists():
         return json.loads(p.read_text())
     return {"hbm_gbs": 6650.0, "_fallback": True}
+
+
+def int8_peak(peaks: dict) -> tuple[float, str]:
+    """Dense int8 tcgen05 peak: the committed tools/tc_probe.cu measurement, else 2 x bf16."""
+    for p in sorted((ROOT / "profiles").glob("*/int8_peak.json"), reverse=True):
+        try:
+            t = json.loads(p.read_text())
+            return float(t["tops"]), f"{p.relative_to(ROOT)} (tools/tc_probe.cu, measured on a B200)"
+        except (ValueError, KeyError):
+            continue
+    src = "MEASURED_PEAKS.json" if "_fallback" not in peaks else "fallback"
+    return 2.0 * float(peaks.get("bf16_tflops", 1590.0)), f"2 x {src} bf16_tflops (no int8 measurement committed)"
 
 
 def count_launches(step_fn) -> tuple[int, list[str]]:
@@ -235,16 +270,14 @@ def kernel_roofline(kernel_ms: dict, peaks: dict, probed: int, survivors: int, d
     kpad = -(-d // 64) * 64
     g = -(-d // 32)
     rb = -(-d * (8 if bits > 4 else 4) // 8)
-    bf16 = float(peaks.get("bf16_tflops", 1590.0))
     hbm = float(peaks.get("hbm_gbs", 6650.0))
     src = "MEASURED_PEAKS.json" if "_fallback" not in peaks else "fallback"
     if name in ("tc_refine_kernel", "tc_ip_kernel", "ip_list_kernel"):
         work = 2.0 * probed * (kpad * 8 if name == "tc_refine_kernel" else 32 * g * 4)
         achieved = work / (avg_ms / 1e3) / 1e12
-        peak = 2.0 * bf16
+        peak, psrc = int8_peak(peaks)
         out = {"bound": "tensor", "unit": "TFLOP/s", "op": "int8 multiply-add (x2), TOP/s",
-               "peak_source": f"2 x {src} bf16_tflops (dense int8 tcgen05 rate = 2 x bf16 on sm_100; "
-                              "no int8 measurement in the file)",
+               "peak_source": psrc,
                "work_formula": "2*probed*kpad*8" if name == "tc_refine_kernel" else "2*probed*32*ceil(D/32)*4"}
     else:
         work = probed * 14.0 + survivors * (8.0 if name == "scan_rd_kernel" else rb + 8.0)
@@ -271,13 +304,12 @@ def dist_setup():
 
 
 def run_ours(args, cfg_name: str) -> dict:
+    import ctypes
+
     import torch
     import torch.distributed as tdist
 
-    import ctypes
-
     import paper_2602_23999_b200 as iv
-    from paper_2602_23999_b200 import _device as dev
     from paper_2602_23999_b200 import _lib
     from paper_2602_23999_b200.index import build_index_device
     from paper_2602_23999_b200.linalg import exact_knn_device
@@ -311,40 +343,27 @@ def run_ours(args, cfg_name: str) -> dict:
         torch.cuda.empty_cache()
         index = build_index_device(x, params, timings=build_stages)
         log(f"[bench] build stages {build_stages}")
-    # ---- ground truth + nprobe choice
+    # ---- ground truth (exact float64 k-NN on the GPU) and the recall sweep around the config's n_probe
     tg = time.perf_counter()
     n_gt = NQ if args.gt_queries <= 0 else min(NQ, args.gt_queries)
     gt_ids, _ = exact_knn_device(x, queries[:n_gt].to(torch.float64), K)
     gt = gt_ids.cpu().numpy()
     log(f"[bench] ground truth ({n_gt} queries) {time.perf_counter() - tg:.1f}s")
-    sweep = []
     nprobe = cfg["nprobe"]
     mode = args.mode
-    if nprobe is None:
-        for p in SWEEP:
-            if p > nlist:
-                break
-            r = search_device(queries, index, iv.SearchParams(k=K, n_probe=p, ip_mode=mode))
-            rec = recall_at_k(r.ids.cpu().numpy()[:n_gt], gt, K)
-            sweep.append({"n_probe": p, "recall": round(rec, 4)})
-            if rec >= TARGET_RECALL:
-                nprobe = p
-                break
-            if len(sweep) >= 2 and rec - sweep[-2]["recall"] < 0.002:
-                nprobe = sweep[-2]["n_probe"]  # recall saturated below the target (code width bound)
-                break
-        if nprobe is None:
-            nprobe = sweep[-1]["n_probe"]
+    sweep = []
+    for p in SWEEP:
+        if p > nlist or p > 2 * nprobe:
+            break
+        r = search_device(queries[:n_gt], index, iv.SearchParams(k=K, n_probe=p, ip_mode=mode))
+        sweep.append({"n_probe": p, "recall": round(recall_at_k(r.ids.cpu().numpy(), gt, K), 4)})
     sp = iv.SearchParams(k=K, n_probe=nprobe, ip_mode=mode)
     res = search_device(queries, index, sp, with_stats=True)
-    recall = recall_at_k(res.ids.cpu().numpy()[:n_gt], gt, K)
+    res_ids = res.ids.cpu().numpy()
+    res_dists = res.dists.cpu().numpy()
+    recall = recall_at_k(res_ids[:n_gt], gt, K)
     stats = res.stats.cpu().numpy()
     probed, survivors = int(stats[:, 0].sum()), int(stats[:, 1].sum())
-    g = (d + 31) // 32
-    bpv = (d * (bits - 1) + 7) // 8
-    stage1_b = 4 * g + 12
-    surv_b = (bpv + 16) if bits > 1 else 8
-    alg_bytes = probed * stage1_b + survivors * surv_b
     log(f"[bench] nprobe={nprobe} recall={recall:.4f} probed/q={probed / NQ:.0f} surv/q={survivors / NQ:.0f}")
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)  # > 126 MB L2
@@ -354,7 +373,6 @@ def run_ours(args, cfg_name: str) -> dict:
     if world > 1:
         tdist.barrier()
     step_ms, scan_ms, stage_ms = [], [], {"rotate": 0.0, "probe": 0.0, "prepare": 0.0, "scan": 0.0}
-    klib = _lib.load()
     prof_range = os.environ.get("BENCH_PROFILE_RANGE") == "1"  # ncu --profile-from-start off: timed steps only
     if prof_range:
         torch.cuda.profiler.start()
@@ -381,7 +399,6 @@ def run_ours(args, cfg_name: str) -> dict:
         _lib.call("ivrq_kernel_time", kn.encode(), ctypes.byref(tot), ctypes.byref(nl_))
         if nl_.value:
             kernel_ms[kn] = (tot.value / nl_.value, int(nl_.value))
-    del klib
     total_ms = float(sum(step_ms))
     if world > 1:
         t = torch.tensor([total_ms], device=device, dtype=torch.float64)
@@ -408,25 +425,30 @@ def run_ours(args, cfg_name: str) -> dict:
         tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
         e2e_s = float(t.item())
     assert len(out) == NQ
+    assert all(np.array_equal(out[i][0], res_ids[i, : len(out[i][0])]) for i in range(0, NQ, 97))
     launches_per_step, kernel_names = count_launches(lambda: search_device(queries, index, sp))
     scan_mean_ms = float(np.mean(scan_ms))
     peaks = measured_peaks()
-    peak = float(peaks.get("hbm_gbs", 6650.0))
-    achieved = alg_bytes / (scan_mean_ms / 1e3) / 1e9
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
     roofline = kernel_roofline(kernel_ms, peaks, probed=probed, survivors=survivors, d=d, bits=bits)
-    roofline["traffic"] = ncu_traffic(cfg_name, nprobe, roofline.get("kernel"))
+    traffic = ncu_traffic(cfg_name, nprobe, roofline.get("kernel"))
+    roofline["traffic"] = traffic
+    g = (d + 31) // 32
+    surv_b = ((d * (bits - 1) + 7) // 8 + 16) if bits > 1 else 8
     roofline["scan_stage"] = {
-        "note": "whole scan stage against the per-query-equivalent bytes of the reference's scan "
-                "(list-major sharing of code reads lets this exceed the copy peak; context, not the roofline)",
         "ms": round(scan_mean_ms, 4),
-        "per_query_equivalent_bytes": int(alg_bytes),
-        "bytes_formula": f"probed*(4*ceil(D/32)+12) + survivors*({surv_b})",
-        "effective_gbs": round(achieved, 1),
         "probed_per_query": round(probed / NQ, 1),
         "survivors_per_query": round(survivors / NQ, 1),
+        "alg_bytes_formula": f"probed*(4*ceil(D/32)+12) + survivors*({surv_b})  (SURVEY 8(d), per query)",
+        "alg_bytes": int(probed * (4 * g + 12) + survivors * surv_b),
     }
+    if traffic and traffic.get("scan_stage_dram_bytes"):
+        dram = float(traffic["scan_stage_dram_bytes"])
+        roofline["scan_dram_frac"] = round(dram / (scan_mean_ms / 1e3) / 1e9 / hbm, 4)
+        roofline["scan_stage"]["dram_bytes"] = int(dram)
+        roofline["scan_stage"]["dram_gbs"] = round(dram / (scan_mean_ms / 1e3) / 1e9, 1)
     result = {
-        "metric": "search QPS @ recall@10~0.95 (10K-query batch)",
+        "metric": METRIC,
         "value": round(qps, 1),
         "unit": "queries/s",
         "n_gpus": world,
@@ -437,23 +459,12 @@ def run_ours(args, cfg_name: str) -> dict:
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "f64 estimator / int popcount / u8 codes",
-        "data": "synthetic Gaussian mixture (reference conftest recipe, torch RNG), L2 flushed between steps",
-        "config": {
-            "workload": cfg_name + ": " + cfg["desc"],
-            "n_probe": nprobe,
-            "k": K,
-            "n_queries": NQ,
-            "ip_mode": mode,
-            "query_bits": 4,
-            "recall_at_10": round(recall, 4),
-            "recall_queries": n_gt,
-            "nprobe_sweep": sweep,
-            "build_seconds": round(build_s, 3),
-            "build_stage_seconds": {k2: round(v, 3) for k2, v in build_stages.items()},
-            "build_params": {"kmeans_iters": 25, "train_fraction": round(params.train_fraction, 5), "seed": 0},
-            "stage_ms_per_step": {k2: round(v / args.steps, 4) for k2, v in stage_ms.items()},
-            "l2": "flushed (256 MB write) between timed steps",
-        },
+        "data": DATA_NOTE + ", L2 flushed (256 MB write) between timed steps",
+        "config": config_dict(cfg_name, mode),
+        "quality": {"recall_at_10": round(recall, 4), "recall_queries": n_gt, "nprobe_sweep": sweep},
+        "build": {"seconds": round(build_s, 3), "stage_seconds": {k2: round(v, 3) for k2, v in build_stages.items()},
+                  "note": "build_index_device on the device-resident dataset (H2D excluded, cli.py:78-80)"},
+        "stage_ms_per_step": {k2: round(v / args.steps, 4) for k2, v in stage_ms.items()},
         "e2e": {
             "value": round(world * NQ / e2e_s, 1),
             "unit": "queries/s",
@@ -467,7 +478,8 @@ def run_ours(args, cfg_name: str) -> dict:
         "clocks": clocks.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        result["cpu_baseline"] = cpu_baseline(index, q_host, gt, sp, budget_s=args.cpu_budget)
+        result["gt_parity"] = gt_parity(x, queries, gt_ids, n_check=args.gt_check)
+        result["cpu_baseline"] = cpu_baseline(index, q_host, gt, sp, res_ids, res_dists, budget_s=args.cpu_budget)
     if world > 1:
         tdist.destroy_process_group()
     return result if rank == 0 else {}
@@ -483,8 +495,22 @@ def _host_index_arrays(index) -> dict:
     )
 
 
-def cpu_baseline(index, q_host, gt, sp, budget_s=20.0) -> dict:
-    """The oracle (NumPy restatement of the reference) on a bounded query sample, 1 host thread."""
+def gt_parity(x, queries, gt_ids, n_check: int = 100) -> dict:
+    """exact_knn_device against the oracle's float64 brute force on the first n_check queries."""
+    from oracle import ivrq_oracle as orc
+
+    if n_check <= 0:
+        return {"queries": 0}
+    t = time.perf_counter()
+    ids_o, _ = orc.exact_knn(x.cpu().numpy(), queries[:n_check].cpu().numpy().astype(np.float64), K)
+    got = gt_ids[:n_check].cpu().numpy()
+    return {"queries": int(n_check), "id_mismatch_rows": int((ids_o != got).any(axis=1).sum()),
+            "oracle_seconds": round(time.perf_counter() - t, 1)}
+
+
+def cpu_baseline(index, q_host, gt, sp, gpu_ids, gpu_dists, budget_s=20.0) -> dict:
+    """The oracle (NumPy restatement of the reference) on a bounded query sample, 1 host thread,
+    with its results compared id for id against the GPU search of the same queries."""
     from oracle import ivrq_oracle as orc
 
     from threadpoolctl import threadpool_limits
@@ -492,50 +518,77 @@ def cpu_baseline(index, q_host, gt, sp, budget_s=20.0) -> dict:
     ix = _host_index_arrays(index)
     codes = orc.decode_codes(ix) if ix["bits"] > 1 else None
     with threadpool_limits(1):  # 1 host thread, BLAS included (the reference default, IVRQ_THREADS=1)
-        return _cpu_baseline_timed(orc, ix, codes, q_host, gt, sp, budget_s)
+        out = _cpu_baseline_timed(orc, ix, codes, q_host, gt, sp, budget_s, gpu_ids, gpu_dists)
+    return out
 
 
-def _cpu_baseline_timed(orc, ix, codes, q_host, gt, sp, budget_s) -> dict:
+def _cpu_baseline_timed(orc, ix, codes, q_host, gt, sp, budget_s, gpu_ids, gpu_dists) -> dict:
+    kw = dict(ip_mode=sp.ip_mode, query_bits=sp.query_bits, codes=codes)
     t = time.perf_counter()
-    orc.search(q_host[:4], ix, sp.k, sp.n_probe, ip_mode=sp.ip_mode, query_bits=sp.query_bits, codes=codes)
+    orc.search(q_host[:4], ix, sp.k, sp.n_probe, **kw)
     per_q = max((time.perf_counter() - t) / 4, 1e-4)
     m = int(min(len(q_host), max(8, budget_s / per_q)))
     t = time.perf_counter()
-    res = orc.search(q_host[:m], ix, sp.k, sp.n_probe, ip_mode=sp.ip_mode, query_bits=sp.query_bits, codes=codes)
+    res = orc.search(q_host[:m], ix, sp.k, sp.n_probe, **kw)
     dt = time.perf_counter() - t
     ids = np.full((m, sp.k), -1, dtype=np.int64)
-    for i, (a, _) in enumerate(res):
+    dists = np.full((m, sp.k), np.inf)
+    for i, (a, b) in enumerate(res):
         ids[i, : len(a)] = a
+        dists[i, : len(b)] = b
+    bad = np.flatnonzero((ids != gpu_ids[:m]).any(axis=1))
+    fin = np.isfinite(dists) & (ids == gpu_ids[:m])
+    rel = np.abs(dists[fin] - gpu_dists[:m][fin]) / np.maximum(np.abs(dists[fin]), 1e-300)
+    parity = {"queries": m, "id_mismatch": int(bad.size), "max_rel_dist": float(rel.max()) if rel.size else 0.0,
+              "note": "oracle search on the host (its own float64 query rotation) vs the GPU search, same index"}
     return {
         "value": round(m / dt, 2),
         "unit": "queries/s",
         "cores": 1,
         "kind": "port",
         "sample": f"first {m} of {len(q_host)} queries, same index/params (oracle/ivrq_oracle.py search)",
-        "recall_at_10_sample": round(recall_at_k(ids, gt[:m], K), 4),
+        "recall_at_10_sample": round(recall_at_k(ids, gt[:m], K), 4) if m <= len(gt) else None,
+        "parity": parity,
     }
 
 
 # ---------------------------------------------------------------- reference arm
 
 
-_REF_INDEX: dict = {}  # set before the worker pool forks: the index is inherited, never pickled per task
+_REF: dict = {}  # set before the worker pool forks: the index is inherited, never pickled per task
+
+
+def _ref_import():
+    """The unmodified reference package from baseline/_ref (pip install --target), or None."""
+    ref_dir = ROOT / "baseline" / "_ref"
+    if (ref_dir / "ivfrabitq" / "__init__.py").exists():
+        sys.path.insert(0, str(ref_dir))
+        import ivfrabitq
+
+        return ivfrabitq
+    return None
 
 
 def _ref_worker(payload):
-    from oracle import ivrq_oracle as orc
-
     from threadpoolctl import threadpool_limits
 
     qs, k, nprobe, mode, qbits = payload
     with threadpool_limits(1):  # one BLAS thread per process (the reference's fastest setting, SURVEY §0.5)
         t = time.perf_counter()
-        orc.search(qs, _REF_INDEX["ix"], k, nprobe, ip_mode=mode, query_bits=qbits, codes=_REF_INDEX["codes"])
+        ref = _REF.get("pkg")
+        if ref is not None:
+            sp = ref.SearchParams(k=k, n_probe=nprobe, ip_mode=mode, query_bits=qbits)
+            ref.search_batch(qs, _REF["index"], sp, workers=1)
+        else:
+            from oracle import ivrq_oracle as orc
+
+            orc.search(qs, _REF["ix"], k, nprobe, ip_mode=mode, query_bits=qbits, codes=_REF["codes"])
         return len(qs), time.perf_counter() - t
 
 
 def run_reference(args, cfg_name: str) -> dict:
-    """The reference algorithm on the host (oracle port), all cores, bounded query samples."""
+    """The reference on the host: its build (or the oracle port's, parallel) and its own search_batch,
+    one forked process per host core over bounded query samples.  Does not import the product package."""
     world, rank, local = dist_setup()
     if rank != 0:
         return {}
@@ -543,33 +596,55 @@ def run_reference(args, cfg_name: str) -> dict:
 
     import torch
 
-    import paper_2602_23999_b200 as iv
     from oracle import ivrq_oracle as orc
-    from paper_2602_23999_b200.index import build_index_device
 
     cfg = CONFIGS[cfg_name]
-    n, d, nlist, bits = cfg["n"], cfg["d"], cfg["nlist"], cfg["bits"]
+    n, d, nlist, bits, nprobe = cfg["n"], cfg["d"], cfg["nlist"], cfg["bits"], cfg["nprobe"]
+    cores = os.cpu_count() or 1
     device = torch.device("cuda", local)
     torch.cuda.set_device(local)
-    x, queries = make_dataset_gpu(n, NQ, d, device)
-    params = iv.BuildParams(
-        n_clusters=nlist, quant=iv.QuantizationParams(bits=bits), kmeans_iters=25,
-        train_fraction=train_fraction(n, nlist), seed=0,
-    )
-    # untimed setup: the index arrays (identical to the reference's build up to
-    # float ulps, see tests/test_gpu_parity.py), handed to the CPU search
-    index = build_index_device(x, params)
-    ix = _host_index_arrays(index)
-    q_host = queries.cpu().numpy()
-    nprobe = cfg["nprobe"] or args.ref_nprobe
-    codes = orc.decode_codes(ix) if bits > 1 else None
-    cores = os.cpu_count() or 1
+    xt, qt = make_dataset_gpu(n, NQ, d, device)  # the same synthetic data as our arm (torch RNG only)
+    x, q_host = xt.cpu().numpy(), qt.cpu().numpy()
+    del xt, qt
+    torch.cuda.empty_cache()
+    ref = _ref_import()
+    tf = train_fraction(n, nlist)
+    tb = time.perf_counter()
+    stages: dict = {}
+    if ref is not None and n <= 200_000:
+        # the reference's own build_index (small config: minutes would be needed at 1M rows)
+        index = ref.build_index(x, ref.BuildParams(n_clusters=nlist, quant=ref.QuantizationParams(bits=bits),
+                                                   kmeans_iters=25, train_fraction=tf, seed=0), workers=1)
+        build_kind, build_cores = "reference build_index (baseline/_ref)", 1
+        ix = None
+    else:
+        ix = orc.build(x, nlist, bits, 25, tf, 0, workers=cores, timings=stages)
+        build_kind, build_cores = "port (oracle build: k-means++ passes on a thread pool, per-list encoder " \
+                                  "in forked processes)", cores
+        index = None
+    build_s = time.perf_counter() - tb
+    log(f"[bench:reference] build {build_s:.1f}s ({build_kind})")
+    if ref is not None:
+        if index is None:
+            index = ref.IvfRabitqIndex(
+                dims=d, bits=bits, n_clusters=nlist, size=n, eps_bound=float(ix["eps_bound"]), seed=0,
+                rotation=ix["rotation"], centroids=ref.Centroids.from_values(ix["centroids"]),
+                offsets=ix["offsets"], packed_msb=ix["packed_msb"], excodes=ix["excodes"],
+                short_factors=ix["short_factors"], long_factors=ix["long_factors"], pids=ix["pids"],
+            )
+        if bits > 1:
+            _ = index.code_values  # materialised once, inherited by the forked workers
+        if args.mode == "lut":
+            _ = index.msb_nibbles
+        _REF["pkg"], _REF["index"] = ref, index
+        search_kind = "reference search_batch (baseline/_ref, unmodified)"
+    else:
+        _REF["ix"], _REF["codes"] = ix, (orc.decode_codes(ix) if bits > 1 else None)
+        search_kind = "port (oracle/ivrq_oracle.py search; baseline/_ref not installed)"
     os.environ["OPENBLAS_NUM_THREADS"] = "1"
     per_step = max(cores, int(args.ref_queries_per_step))
-    ctx = mp.get_context("fork")
     step_qps = []
-    _REF_INDEX["ix"], _REF_INDEX["codes"] = ix, codes
-    with ctx.Pool(cores) as pool:
+    with mp.get_context("fork").Pool(cores) as pool:
         for step in range(args.warmup + args.steps):
             lo = (step * per_step) % NQ
             qs = q_host[lo : lo + per_step]
@@ -580,22 +655,30 @@ def run_reference(args, cfg_name: str) -> dict:
             if step >= args.warmup:
                 step_qps.append(len(qs) / dt)
     value = float(np.mean(step_qps))
+    kind = "reference" if ref is not None else "port"
     return {
         "impl": "reference",
-        "metric": "search QPS @ recall@10~0.95 (10K-query batch)",
+        "metric": METRIC,
         "value": round(value, 2),
         "unit": "queries/s",
         "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
+        "ms_per_step": round(1e3 * per_step / value, 3),
         "higher_is_better": True,
-        "config": {"workload": cfg_name + ": " + cfg["desc"], "n_probe": nprobe, "k": K, "ip_mode": args.mode},
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64 estimator / int popcount / u8 codes",
+        "data": DATA_NOTE + " (copied to the host)",
+        "config": config_dict(cfg_name, args.mode),
+        "build": {"seconds": round(build_s, 3), "kind": build_kind, "cores": build_cores,
+                  "stage_seconds": stages},
         "cpu_baseline": {
             "value": round(value, 2),
             "unit": "queries/s",
             "cores": cores,
-            "kind": "port",
-            "sample": f"{per_step} queries per step across {cores} processes (oracle/ivrq_oracle.py search)",
+            "kind": kind,
+            "sample": f"{per_step} queries per step across {cores} forked processes ({search_kind})",
         },
         "e2e": {"value": round(value, 2), "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -609,11 +692,11 @@ def main() -> None:
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--mode", default="bitwise", choices=("bitwise", "lut"))
-    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--ref-nprobe", type=int, default=8)
     ap.add_argument("--ref-queries-per-step", type=int, default=1024)
-    ap.add_argument("--gt-queries", type=int, default=0, help="queries with exact ground truth (0 = all)")
+    ap.add_argument("--gt-queries", type=int, default=2000, help="queries with exact ground truth (0 = all)")
+    ap.add_argument("--gt-check", type=int, default=100, help="ground-truth rows checked against the oracle")
     ap.add_argument("--build-breakdown", action="store_true", help="rebuild once with per-stage timings")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)

@@ -113,6 +113,12 @@ IVRQ_API const char* ivrq_last_error(void);
 /* Number of SMs of `device` (synchronous; for host-side grid sizing). */
 IVRQ_API int ivrq_device_sm_count(int device, int* out);
 
+/* Return the library's cached scratch memory on the current device to the driver
+ * (synchronises `stream` first).  Scratch comes from a private stream-ordered pool
+ * that keeps up to IVRQ_POOL_KEEP_BYTES (default 4 GiB) mapped between calls; the
+ * process-wide default CUDA pool is never reconfigured. */
+IVRQ_API int ivrq_release_memory(void* stream);
+
 /* Bytes per vector of the rcodes layout (0 for bits == 1). */
 IVRQ_API int64_t ivrq_rcode_row_bytes(int32_t dims, int32_t bits);
 
@@ -150,6 +156,13 @@ IVRQ_API int ivrq_select_clusters_ordered(const double* q_rot, int64_t nq, int32
                                  int32_t n_clusters, int32_t n_probe, int32_t order_by_id,
                                  int64_t* ids, double* d2, void* workspace,
                                  size_t workspace_bytes, void* stream);
+
+/* Same selection against float64 centroids (select_clusters takes any Centroids,
+ * e.g. train_kmeans' float64 output): the float64 GEMM (DMMA) path. */
+IVRQ_API int ivrq_select_clusters_f64(const double* q_rot, int64_t nq, int32_t dims, const double* centroids,
+                                      const double* centroid_sqnorms, int32_t n_clusters, int32_t n_probe,
+                                      int32_t order_by_id, int64_t* ids, double* d2, void* workspace,
+                                      size_t workspace_bytes, void* stream);
 
 /* Per-query state (_prepare_from_rotated, search.py:186-214; build_luts 115-132).
  * scalars: double[nq*IVRQ_QS_COUNT]; planes: uint32[nq*query_bits*g] (bitwise
@@ -199,6 +212,66 @@ IVRQ_API int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list_l
 IVRQ_API int ivrq_merge_topk(const int64_t* ids, const double* dists, const int32_t* counts,
                              int64_t nq, int32_t parts, int32_t k, int64_t* out_ids,
                              double* out_dists, int32_t* out_counts, void* stream);
+
+/* ---------------------------------------------------------------- sub-operators
+ * The reference's finer-grained API (search.py:84-375, codec.py:118-151, 262-303,
+ * 383-401), one call per operator.  All pointers are device pointers. */
+
+/* ip_bitwise (search.py:163-183): words uint32[groups*n] laid out (groups, n)
+ * (a list's interleaved slice), planes uint32[query_bits*groups]; out int64[n]. */
+IVRQ_API int ivrq_ip_bitwise(const uint32_t* words, int32_t groups, int64_t n, const uint32_t* planes,
+                             int32_t query_bits, int64_t* out, void* stream);
+
+/* ip_lut (search.py:146-160): nibbles uint8[n*blocks], luts float[blocks*16]; out double[n]. */
+IVRQ_API int ivrq_ip_lut(const uint8_t* nibbles, int64_t n, int32_t blocks, const float* luts, double* out,
+                         void* stream);
+
+/* estimate_stage1 (search.py:270-287): ip double[n], short_factors double[n*3]
+ * (add, scale, err), d_qc2 double[n]; est2/lb2 double[n]. */
+IVRQ_API int ivrq_estimate_stage1(const double* ip, const double* short_factors, int64_t n, const double* d_qc2,
+                                  double code_sum_q, double ip_margin, double* est2, double* lb2, void* stream);
+
+/* refine_stage2 (search.py:290-310): ex double[n*dims] ex-code values, ip_binary
+ * double[n], long_factors double[n*2], q_rot double[dims], d_qc2 double[n]; out double[n].
+ * bits < 2 -> IVRQ_EINVAL (no ex-code exists for 1-bit indexes). */
+IVRQ_API int ivrq_refine_stage2(const double* ex, int64_t n, int32_t dims, const double* ip_binary,
+                                const double* long_factors, const double* q_rot, double sum_q, const double* d_qc2,
+                                int32_t bits, double* out, void* stream);
+
+/* cluster_local_search (search.py:326-375) for one query and one cluster: stage-1
+ * estimates, prune lb2 <= threshold, refinement of the survivors, local top-k by
+ * (dist, pid).  qstate: HOST double[IVRQ_QS_COUNT] (sum_q, delta, code_sum, ip_margin);
+ * planes (bitwise) / luts (lut) as ivrq_prepare_queries writes them for one query
+ * (device); d_qc2: HOST pointer to the squared query-centroid distance, or NULL
+ * (then computed on the device from the centroid).  Outputs out_ids int64[k],
+ * out_dists double[k], out_count int32[1].  list_size = the cluster's row count;
+ * workspace: ivrq_cluster_local_search_workspace(list_size) bytes. */
+IVRQ_API size_t ivrq_cluster_local_search_workspace(int64_t list_size);
+IVRQ_API int ivrq_cluster_local_search(const ivrq_index_view* index, int64_t cluster, const double* q_rot,
+                                       const uint32_t* planes, const float* luts, const double* qstate,
+                                       const ivrq_search_params* params, double threshold, const double* d_qc2,
+                                       int64_t* out_ids, double* out_dists, int32_t* out_count, void* workspace,
+                                       size_t workspace_bytes, int64_t list_size, void* stream);
+
+/* compute_factors_batch (codec.py:322-380): u uint8[n*dims], o double[n*dims],
+ * dist double[n], c_rot double[n*dims]; short_factors double[n*3], long_factors
+ * double[n*2], low_quality uint8[n]. */
+IVRQ_API int ivrq_compute_factors(const uint8_t* u, const double* o, const double* dist, const double* c_rot,
+                                  int64_t n, int32_t dims, int32_t bits, double eps_bound, double* short_factors,
+                                  double* long_factors, uint8_t* low_quality, void* stream);
+
+/* normalize_residuals (codec.py:138-151; dd_norm = 0, einsum-order norm) and
+ * normalize_residual (codec.py:118-135; dd_norm = 1, the norm as a double-double
+ * dot rounded once): x, c double[n*dims]; o double[n*dims], dist double[n]. */
+IVRQ_API int ivrq_normalize_residuals(const double* x, const double* c, int64_t n, int32_t dims, int32_t dd_norm,
+                                      double* o, double* dist, void* stream);
+
+/* quantize_oracle (codec.py:262-303) for one vector o double[dims]: out uint8[dims].
+ * The host enforces the reference's enumeration guard dims*2^(bits-1) <= 2^15.
+ * workspace: ivrq_quantize_oracle_workspace(dims, bits) bytes. */
+IVRQ_API size_t ivrq_quantize_oracle_workspace(int32_t dims, int32_t bits);
+IVRQ_API int ivrq_quantize_oracle(const double* o, int32_t dims, int32_t bits, uint8_t* out, void* workspace,
+                                  size_t workspace_bytes, void* stream);
 
 /* ---------------------------------------------------------------- build */
 /* k-means++ seeding (_kmeans_pp_init, clustering.py:60-79) on x float[n*d]

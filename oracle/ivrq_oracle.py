@@ -50,13 +50,29 @@ def nearest_centre(x64: np.ndarray, centres: np.ndarray, c_sq: np.ndarray, block
     return lab, best
 
 
-def seed_centres(x64: np.ndarray, k: int, rng: np.random.Generator) -> np.ndarray:
+def _sqdist_rows(x64: np.ndarray, c: np.ndarray, pool=None) -> np.ndarray:
+    """rowdot(x - c, x - c); with a thread pool, row blocks in parallel (rows are independent,
+    so the values are those of the single call -- einsum drops the GIL in its inner loop)."""
+    if pool is None:
+        gap = x64 - c
+        return rowdot(gap, gap)
+    out = np.empty(x64.shape[0])
+    bounds = np.linspace(0, x64.shape[0], 4 * pool._max_workers + 1).astype(np.int64)
+
+    def part(a, b):
+        g = x64[a:b] - c
+        out[a:b] = rowdot(g, g)
+
+    list(pool.map(lambda ab: part(*ab), zip(bounds[:-1], bounds[1:])))
+    return out
+
+
+def seed_centres(x64: np.ndarray, k: int, rng: np.random.Generator, pool=None) -> np.ndarray:
     """k-means++ seeding (clustering.py:60-79)."""
     n, d = x64.shape
     out = np.empty((k, d))
     out[0] = x64[int(rng.integers(n))]
-    gap = x64 - out[0]
-    dmin = rowdot(gap, gap)
+    dmin = _sqdist_rows(x64, out[0], pool)
     for j in range(1, k):
         tot = float(dmin.sum())
         if tot > 0.0:
@@ -64,17 +80,16 @@ def seed_centres(x64: np.ndarray, k: int, rng: np.random.Generator) -> np.ndarra
         else:
             pick = int(rng.integers(n))
         out[j] = x64[pick]
-        gap = x64 - out[j]
-        np.minimum(dmin, rowdot(gap, gap), out=dmin)
+        np.minimum(dmin, _sqdist_rows(x64, out[j], pool), out=dmin)
     return out
 
 
-def kmeans(x: np.ndarray, k: int, iters: int, seed: int) -> np.ndarray:
+def kmeans(x: np.ndarray, k: int, iters: int, seed: int, pool=None) -> np.ndarray:
     """Lloyd iterations with empty-cluster reseeding (clustering.py:82-113); float64 centres."""
     x64 = np.ascontiguousarray(x, dtype=np.float64)
     n = x64.shape[0]
     rng = np.random.default_rng(seed)
-    centres = seed_centres(x64, k, rng)
+    centres = seed_centres(x64, k, rng, pool)
     for _ in range(iters):
         lab, dmin = nearest_centre(x64, centres, rowdot(centres, centres))
         cnt = np.bincount(lab, minlength=k)
@@ -205,9 +220,69 @@ def ex_bytes(ex: np.ndarray, bits: int) -> np.ndarray:
 # ---------------------------------------------------------------- build (index.py:190-281)
 
 
-def build(x, nlist, bits, iters=25, train_fraction=1.0, seed=0, n_coarse=64, n_fine=32, eps=1.9, inject=None):
-    """Index arrays of ``build_index``; ``inject`` may pin centroids64/rotation/cent_rot/o_rot."""
+def _encode_lists(c_lo, c_hi, offsets, o_rot, d, crot, bits, n_coarse, n_fine, eps, g, out):
+    """Encode lists [c_lo, c_hi) into the output arrays (index.py:247-264, one _quantize_cluster each)."""
+    dims = o_rot.shape[1]
+    packed, exb, short, long, codes = out
+    for c in range(c_lo, c_hi):
+        lo, hi = int(offsets[c]), int(offsets[c + 1])
+        if hi == lo:
+            continue
+        u, _ = quantize(o_rot[lo:hi], bits, n_coarse, n_fine)
+        if codes is not None:
+            codes[lo:hi] = u
+        sh, lg = factors(u, o_rot[lo:hi], d[lo:hi], np.broadcast_to(crot[c].astype(np.float64), (hi - lo, dims)), bits, eps)
+        packed[lo * g : hi * g] = msb_words(u >> (bits - 1))
+        exb[lo:hi] = ex_bytes(u & ((1 << (bits - 1)) - 1), bits)
+        short[lo:hi] = sh
+        long[lo:hi] = lg
+
+
+_FORK_STATE: dict = {}
+
+
+def _encode_worker(span):
+    st = _FORK_STATE
+    _encode_lists(span[0], span[1], st["offsets"], st["o_rot"], st["d"], st["crot"], st["bits"], st["n_coarse"],
+                  st["n_fine"], st["eps"], st["g"], st["out"])
+    return span
+
+
+def _shared(shape, dtype):
+    """A zeroed array in anonymous shared memory (visible to forked workers)."""
+    import mmap
+
+    nbytes = max(1, int(np.prod(shape, dtype=np.int64)) * np.dtype(dtype).itemsize)
+    buf = mmap.mmap(-1, nbytes)
+    return np.frombuffer(buf, dtype=dtype, count=int(np.prod(shape, dtype=np.int64))).reshape(shape)
+
+
+def build(x, nlist, bits, iters=25, train_fraction=1.0, seed=0, n_coarse=64, n_fine=32, eps=1.9, inject=None,
+          workers=1, timings=None):
+    """Index arrays of ``build_index``; ``inject`` may pin centroids64/rotation/cent_rot/o_rot.
+
+    ``workers > 1`` (bench.py's CPU arm only): the k-means++ distance passes run on a thread
+    pool and the per-list encoder on forked processes writing shared memory -- every value is
+    computed by the same expressions on the same rows, so the arrays equal ``workers=1``'s
+    (the reference's own build parallelises the same per-list loop, index.py:259-264).
+    """
+    import time as _time
+
     inject = inject or {}
+    tick = _time.perf_counter()
+
+    def lap(name):
+        nonlocal tick
+        if timings is not None:
+            now = _time.perf_counter()
+            timings[name] = round(now - tick, 3)
+            tick = now
+
+    pool = None
+    if workers > 1:
+        from concurrent.futures import ThreadPoolExecutor
+
+        pool = ThreadPoolExecutor(workers)
     x = np.ascontiguousarray(np.atleast_2d(x), dtype=np.float32)
     n, dims = x.shape
     seeds = np.random.SeedSequence(seed).spawn(2)
@@ -220,8 +295,10 @@ def build(x, nlist, bits, iters=25, train_fraction=1.0, seed=0, n_coarse=64, n_f
             xt = x[rows]
         else:
             xt = x
-        centres = kmeans(xt, nlist, iters, int(seeds[1].generate_state(1)[0]))
+        centres = kmeans(xt, nlist, iters, int(seeds[1].generate_state(1)[0]), pool)
+    lap("kmeans")
     lab, _ = nearest_centre(x.astype(np.float64), centres, rowdot(centres, centres))
+    lap("assign")
     cnt = np.bincount(lab, minlength=nlist)
     offsets = np.concatenate(([0], np.cumsum(cnt))).astype(np.uint64)
     perm = np.argsort(lab, kind="stable")
@@ -233,24 +310,31 @@ def build(x, nlist, bits, iters=25, train_fraction=1.0, seed=0, n_coarse=64, n_f
     o, d = normalise(x[perm], c32[lab[perm]])
     o_rot = inject.get("o_rot")
     o_rot = np.asarray(o_rot, dtype=np.float32) if o_rot is not None else (o @ rot.T.astype(np.float64)).astype(np.float32)
+    lap("normalize_rotate")
     g = (dims + 31) // 32
     bpv = (dims * (bits - 1) + 7) // 8
-    packed = np.zeros(n * g, dtype=np.uint32)
-    exb = np.zeros((n, bpv), dtype=np.uint8)
-    short = np.zeros((n, 3), dtype=np.float32)
-    long = np.zeros((n, 2), dtype=np.float32)
-    codes = np.zeros((n, dims), dtype=np.uint8)
-    for c in range(nlist):
-        lo, hi = int(offsets[c]), int(offsets[c + 1])
-        if hi == lo:
-            continue
-        u, _ = quantize(o_rot[lo:hi], bits, n_coarse, n_fine)
-        codes[lo:hi] = u
-        sh, lg = factors(u, o_rot[lo:hi], d[lo:hi], np.broadcast_to(crot[c].astype(np.float64), (hi - lo, dims)), bits, eps)
-        packed[lo * g : hi * g] = msb_words(u >> (bits - 1))
-        exb[lo:hi] = ex_bytes(u & ((1 << (bits - 1)) - 1), bits)
-        short[lo:hi] = sh
-        long[lo:hi] = lg
+    alloc = _shared if workers > 1 else (lambda shape, dt: np.zeros(shape, dtype=dt))
+    packed = alloc((n * g,), np.uint32)
+    exb = alloc((n, bpv), np.uint8)
+    short = alloc((n, 3), np.float32)
+    long = alloc((n, 2), np.float32)
+    codes = alloc((n, dims), np.uint8) if workers == 1 else None
+    out = (packed, exb, short, long, codes)
+    if workers > 1:
+        import multiprocessing as mp
+
+        _FORK_STATE.update(offsets=offsets, o_rot=o_rot, d=d, crot=crot, bits=bits, n_coarse=n_coarse,
+                           n_fine=n_fine, eps=eps, g=g, out=out)
+        # lists in contiguous spans of about equal row count, several per worker
+        cuts = np.searchsorted(offsets.astype(np.int64), np.linspace(0, n, 8 * workers + 1)[1:-1])
+        edges = np.unique(np.concatenate(([0], cuts, [nlist])))
+        with mp.get_context("fork").Pool(workers) as pp:
+            list(pp.imap_unordered(_encode_worker, list(zip(edges[:-1], edges[1:]))))
+        _FORK_STATE.clear()
+        pool.shutdown()
+    else:
+        _encode_lists(0, nlist, offsets, o_rot, d, crot, bits, n_coarse, n_fine, eps, g, out)
+    lap("encode")
     return dict(
         dims=dims, bits=bits, n_clusters=nlist, size=n, eps_bound=eps, rotation=rot, centroids=crot,
         centroid_sqnorms=rowdot(crot.astype(np.float64), crot.astype(np.float64)), offsets=offsets,

@@ -72,6 +72,7 @@ _SIGNATURES: dict[str, tuple[object, list[object]]] = {
     "ivrq_kernel_time": (c_int, [ctypes.c_char_p, POINTER(ctypes.c_double), POINTER(ctypes.c_int64)]),
     "ivrq_last_error": (ctypes.c_char_p, []),
     "ivrq_device_sm_count": (c_int, [c_int, POINTER(c_int)]),
+    "ivrq_release_memory": (c_int, [P]),
     "ivrq_row_sqnorms": (c_int, [P, c_int, c_int64, c_int32, P, P]),
     "ivrq_matmul_nt": (c_int, [P, c_int, P, c_int, c_int64, c_int64, c_int32, P, P]),
     "ivrq_rotate_queries": (c_int, [P, c_int, c_int64, c_int32, P, P, P]),
@@ -81,6 +82,10 @@ _SIGNATURES: dict[str, tuple[object, list[object]]] = {
         [P, c_int64, c_int32, P, P, c_int32, c_int32, P, P, P, c_size_t, P],
     ),
     "ivrq_select_clusters_ordered": (
+        c_int,
+        [P, c_int64, c_int32, P, P, c_int32, c_int32, c_int32, P, P, P, c_size_t, P],
+    ),
+    "ivrq_select_clusters_f64": (
         c_int,
         [P, c_int64, c_int32, P, P, c_int32, c_int32, c_int32, P, P, P, c_size_t, P],
     ),
@@ -98,6 +103,20 @@ _SIGNATURES: dict[str, tuple[object, list[object]]] = {
          P, P, P, P, P, P, P, P],
     ),
     "ivrq_merge_topk": (c_int, [P, P, P, c_int64, c_int32, c_int32, P, P, P, P]),
+    "ivrq_ip_bitwise": (c_int, [P, c_int32, c_int64, P, c_int32, P, P]),
+    "ivrq_ip_lut": (c_int, [P, c_int64, c_int32, P, P, P]),
+    "ivrq_estimate_stage1": (c_int, [P, P, c_int64, P, c_double, c_double, P, P, P]),
+    "ivrq_refine_stage2": (c_int, [P, c_int64, c_int32, P, P, P, c_double, P, c_int32, P, P]),
+    "ivrq_cluster_local_search_workspace": (c_size_t, [c_int64]),
+    "ivrq_cluster_local_search": (
+        c_int,
+        [POINTER(IndexView), c_int64, P, P, P, POINTER(c_double), POINTER(SearchParamsC), c_double,
+         POINTER(c_double), P, P, P, P, c_size_t, c_int64, P],
+    ),
+    "ivrq_compute_factors": (c_int, [P, P, P, P, c_int64, c_int32, c_int32, c_double, P, P, P, P]),
+    "ivrq_normalize_residuals": (c_int, [P, P, c_int64, c_int32, c_int32, P, P, P]),
+    "ivrq_quantize_oracle_workspace": (c_size_t, [c_int32, c_int32]),
+    "ivrq_quantize_oracle": (c_int, [P, c_int32, c_int32, P, P, c_size_t, P]),
     "ivrq_rcode_row_bytes": (c_int64, [c_int32, c_int32]),
     "ivrq_make_rcodes": (c_int, [P, P, c_int32, P, c_int64, c_int32, c_int32, P, P]),
     "ivrq_kmeanspp": (

@@ -32,9 +32,16 @@ __all__ = [
     "unpack_excodes",
     "quantize_batch",
     "quantize_vector",
+    "quantize_oracle",
+    "normalize_residual",
+    "normalize_residuals",
+    "compute_factors",
+    "compute_factors_batch",
     "encode_rows",
     "rcode_row_bytes",
 ]
+
+_ORACLE_MAX_FACTORS = 1 << 15
 
 
 @dataclass(frozen=True)
@@ -284,3 +291,92 @@ def quantize_vector(o_prime: np.ndarray, params: QuantizationParams) -> tuple[np
         raise ValueError(f"expected a 1-d vector, got shape {v.shape}")
     u, t = quantize_batch(v[np.newaxis, :], params)
     return u[0], float(t[0])
+
+
+# ---------------------------------------------------------------- per-vector sub-operators
+
+
+def _check_finite_pair(a: np.ndarray, b: np.ndarray) -> None:
+    if a.shape != b.shape:
+        raise ValueError(f"shape mismatch: {a.shape} vs {b.shape}")
+    if not (np.isfinite(a).all() and np.isfinite(b).all()):
+        raise ValueError("non-finite input")
+
+
+def _normalize(x: np.ndarray, c: np.ndarray, dd_norm: int) -> tuple[np.ndarray, np.ndarray]:
+    n, d = x.shape
+    device = dev.require_cuda()
+    o = torch.empty((n, d), dtype=torch.float64, device=device)
+    dist = torch.empty(n, dtype=torch.float64, device=device)
+    if n:
+        xd, cd = dev.to_device(x, device), dev.to_device(c, device)  # alive until the launch is queued
+        _lib.call("ivrq_normalize_residuals", dev.ptr(xd), dev.ptr(cd), n, d, dd_norm, dev.ptr(o), dev.ptr(dist),
+                  dev.stream_ptr())
+    return dev.to_host(o), dev.to_host(dist)
+
+
+def normalize_residual(o_r: np.ndarray, c: np.ndarray) -> tuple[np.ndarray, float]:
+    """Unit direction and distance of ``o_r`` from ``c``; zero vector when d == 0 (codec.py:118-135)."""
+    x = np.asarray(o_r, dtype=np.float64)
+    cc = np.asarray(c, dtype=np.float64)
+    _check_finite_pair(x, cc)
+    o, d = _normalize(np.ascontiguousarray(x.reshape(1, -1)), np.ascontiguousarray(cc.reshape(1, -1)), 1)
+    return o[0].reshape(x.shape), float(d[0])
+
+
+def normalize_residuals(x: np.ndarray, centers: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
+    """Row-wise :func:`normalize_residual`, einsum-order norms (codec.py:138-151)."""
+    xx = np.ascontiguousarray(np.atleast_2d(np.asarray(x, dtype=np.float64)))
+    cc = np.ascontiguousarray(np.atleast_2d(np.asarray(centers, dtype=np.float64)))
+    _check_finite_pair(xx, cc)
+    return _normalize(xx, cc, 0)
+
+
+def compute_factors_batch(u: np.ndarray, o: np.ndarray, d: np.ndarray, c_prime: np.ndarray, params: QuantizationParams):
+    """Per-vector estimator factors ``(short (n,3), long (n,2), low_quality)`` in float64 (codec.py:322-380)."""
+    uu = np.ascontiguousarray(np.atleast_2d(np.asarray(u, dtype=np.uint8)))
+    oo = np.ascontiguousarray(np.atleast_2d(np.asarray(o, dtype=np.float64)))
+    cc = np.ascontiguousarray(np.atleast_2d(np.asarray(c_prime, dtype=np.float64)))
+    dd = np.ascontiguousarray(np.atleast_1d(np.asarray(d, dtype=np.float64)))
+    n, dims = oo.shape
+    if uu.shape != (n, dims) or cc.shape != (n, dims) or dd.shape != (n,):
+        raise ValueError("inconsistent shapes across codes, vectors, and centers")
+    device = dev.require_cuda()
+    short = torch.zeros((n, 3), dtype=torch.float64, device=device)
+    long = torch.zeros((n, 2), dtype=torch.float64, device=device)
+    lowq = torch.zeros(n, dtype=torch.uint8, device=device)
+    if n:
+        ud, od, ddd, cd = (dev.to_device(a, device) for a in (uu, oo, dd, cc))
+        _lib.call("ivrq_compute_factors", dev.ptr(ud), dev.ptr(od), dev.ptr(ddd), dev.ptr(cd), n, dims, params.bits,
+                  float(params.eps_bound), dev.ptr(short), dev.ptr(long), dev.ptr(lowq), dev.stream_ptr())
+    return dev.to_host(short), dev.to_host(long), dev.to_host(lowq).astype(bool)
+
+
+def compute_factors(u: np.ndarray, o_prime: np.ndarray, d: float, c_prime: np.ndarray, params: QuantizationParams):
+    """Single-vector :func:`compute_factors_batch` (codec.py:383-401)."""
+    short, long, _ = compute_factors_batch(np.asarray(u)[None, :], np.asarray(o_prime)[None, :], np.array([d]),
+                                           np.asarray(c_prime)[None, :], params)
+    return (
+        ShortFactors(add=float(short[0, 0]), scale=float(short[0, 1]), err=float(short[0, 2])),
+        LongFactors(add=float(long[0, 0]), scale=float(long[0, 1])),
+    )
+
+
+def quantize_oracle(o_prime: np.ndarray, bits: int) -> np.ndarray:
+    """Exhaustive critical-factor quantizer of one vector (codec.py:262-303), one CTA on the GPU."""
+    o = np.ascontiguousarray(np.asarray(o_prime, dtype=np.float64))
+    if o.ndim != 1:
+        raise ValueError(f"expected a 1-d vector, got shape {o.shape}")
+    dims = o.size
+    if dims * 2 ** (bits - 1) > _ORACLE_MAX_FACTORS:
+        raise ValueError(
+            f"critical-factor count {dims * 2 ** (bits - 1)} exceeds the enumeration guard ({_ORACLE_MAX_FACTORS})"
+        )
+    device = dev.require_cuda()
+    out = torch.empty(dims, dtype=torch.uint8, device=device)
+    ws_bytes = int(_lib.load().ivrq_quantize_oracle_workspace(dims, bits))
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=device)
+    od = dev.to_device(o, device)
+    _lib.call("ivrq_quantize_oracle", dev.ptr(od), dims, bits, dev.ptr(out), dev.ptr(ws),
+              ws_bytes, dev.stream_ptr())
+    return dev.to_host(out)

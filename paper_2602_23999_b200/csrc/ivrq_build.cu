@@ -15,8 +15,11 @@ namespace ivrq {
 template <typename T>
 static int dalloc(T** p, size_t count, cudaStream_t s, const char* what) {
   if (count == 0) count = 1;
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(p), count * sizeof(T), s);
-  if (e != cudaSuccess) return fail(IVRQ_ENOMEM, std::string(what) + ": cudaMallocAsync failed");
+  cudaError_t e = pool_malloc(reinterpret_cast<void**>(p), count * sizeof(T), s);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(IVRQ_ENOMEM, std::string(what) + ": stream-ordered allocation failed");
+  }
   return IVRQ_OK;
 }
 

@@ -27,11 +27,76 @@ namespace ivrq {
 void set_error(const std::string& msg);
 int fail(int code, const std::string& msg);
 int check_launch(const char* what);
-// Keep freed stream-ordered (cudaMallocAsync) memory in the device's default
-// pool across synchronisations instead of returning it to the driver, so the
-// per-call workspaces of the search do not re-map pages every call.
-void retain_async_pool(cudaStream_t s);
+// The library's own stream-ordered memory pool on the current device (never the
+// process-wide default pool): freed workspace stays mapped up to a bounded
+// release threshold (IVRQ_POOL_KEEP_BYTES), so per-call workspaces do not
+// re-map pages every call, and ivrq_release_memory() trims it.
+cudaMemPool_t library_pool();
+cudaError_t pool_malloc(void** p, size_t bytes, cudaStream_t s);
 int sm_count_of_current_device();
+
+// Scratch memory of one C-ABI call: every block allocated through it is freed
+// (stream-ordered, on the stream given at construction) when it goes out of
+// scope, on the success path and on every early error return alike.
+class Workspace {
+ public:
+  explicit Workspace(cudaStream_t s) : s_(s) {}
+  Workspace(const Workspace&) = delete;
+  Workspace& operator=(const Workspace&) = delete;
+  ~Workspace() {
+    for (int i = 0; i < n_; ++i) cudaFreeAsync(p_[i], s_);
+  }
+  // count elements of T (at least one); false (with the error set) on failure
+  template <typename T>
+  bool alloc(T*& out, size_t count, cudaStream_t on = nullptr) {
+    out = nullptr;
+    if (n_ == kMax) return false;
+    void* p = nullptr;
+    if (pool_malloc(&p, (count ? count : 1) * sizeof(T), on ? on : s_) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    p_[n_++] = p;
+    out = static_cast<T*>(p);
+    return true;
+  }
+
+ private:
+  static constexpr int kMax = 48;
+  cudaStream_t s_;
+  void* p_[kMax] = {};
+  int n_ = 0;
+};
+
+// Fork/join of a side stream inside one call: join() makes `main` wait for the
+// side stream's work; the destructor joins too, so an early return never leaves
+// work on the side stream that the caller's stream does not wait for.
+class StreamFork {
+ public:
+  StreamFork(cudaStream_t main, cudaStream_t side) : main_(main), side_(side) {
+    if (side_ && cudaEventCreateWithFlags(&ev_, cudaEventDisableTiming) == cudaSuccess) {
+      cudaEventRecord(ev_, main_);
+      cudaStreamWaitEvent(side_, ev_, 0);
+    } else {
+      side_ = nullptr;
+    }
+  }
+  StreamFork(const StreamFork&) = delete;
+  StreamFork& operator=(const StreamFork&) = delete;
+  ~StreamFork() { join(); }
+  cudaStream_t side() const { return side_ ? side_ : main_; }
+  void join() {
+    if (!side_) return;
+    cudaEventRecord(ev_, side_);
+    cudaStreamWaitEvent(main_, ev_, 0);
+    cudaEventDestroy(ev_);
+    side_ = nullptr;
+  }
+
+ private:
+  cudaStream_t main_, side_;
+  cudaEvent_t ev_ = nullptr;
+};
 // A non-blocking stream per device (and host thread) for intra-call fork/join.
 cudaStream_t side_stream();
 

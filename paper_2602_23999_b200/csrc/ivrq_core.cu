@@ -2,6 +2,7 @@
 #include <cudaTypedefs.h>
 
 #include <atomic>
+#include <cstdlib>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -29,16 +30,35 @@ int check_launch(const char* what) {
   return IVRQ_OK;
 }
 
-void retain_async_pool(cudaStream_t) {
-  static thread_local int done_mask = 0;  // devices 0..31 handled by this thread
+cudaMemPool_t library_pool() {
+  static std::mutex mu;
+  static cudaMemPool_t pools[64] = {};
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev >= 32 || (done_mask >> dev) & 1) return;
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-    uint64_t thr = ~0ULL;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!pools[dev]) {
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    cudaMemPool_t pool = nullptr;
+    if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    // keep up to 4 GiB of freed workspace mapped (a C3 search uses ~1.3 GB per call)
+    const char* env = getenv("IVRQ_POOL_KEEP_BYTES");
+    uint64_t keep = env ? strtoull(env, nullptr, 10) : (uint64_t(4) << 30);
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    pools[dev] = pool;
   }
-  done_mask |= 1 << dev;
+  return pools[dev];
+}
+
+cudaError_t pool_malloc(void** p, size_t bytes, cudaStream_t s) {
+  cudaMemPool_t pool = library_pool();
+  if (!pool) return cudaMallocAsync(p, bytes, s);
+  return cudaMallocFromPoolAsync(p, bytes, pool, s);
 }
 
 namespace tc {
@@ -163,6 +183,14 @@ extern "C" int ivrq_kernel_time(const char* name, double* total_ms, int64_t* lau
 }
 
 extern "C" const char* ivrq_last_error(void) { return g_last_error.c_str(); }
+
+extern "C" int ivrq_release_memory(void* stream) {
+  cudaMemPool_t pool = library_pool();
+  if (!pool) return IVRQ_OK;
+  if (cudaStreamSynchronize(as_stream(stream)) != cudaSuccess || cudaMemPoolTrimTo(pool, 0) != cudaSuccess)
+    return fail(IVRQ_ECUDA, "ivrq_release_memory: pool trim failed");
+  return IVRQ_OK;
+}
 
 extern "C" int ivrq_device_sm_count(int device, int* out) {
   int v = 0;

@@ -603,24 +603,15 @@ int probe_tc(const double* q_rot, int64_t nq, int32_t dims, const float* centroi
   double *ql1 = nullptr, *cl1 = nullptr;
   float* bounds = nullptr;
   const int64_t rows = std::max<int64_t>(128, std::min<int64_t>(nq, ((int64_t)256 << 20) / ((int64_t)n_clusters * 8)));
-  static const bool want_stats = getenv("IVRQ_PROBE_STATS") != nullptr;
-  unsigned long long* pstats = nullptr;
-  if (want_stats) {
-    cudaMalloc(reinterpret_cast<void**>(&pstats), 16);
-    cudaMemset(pstats, 0, 16);
-  }
-  if (cudaMallocAsync(reinterpret_cast<void**>(&qd), (size_t)4 * nq * kp, s) != cudaSuccess ||
-      cudaMallocAsync(reinterpret_cast<void**>(&cd), (size_t)4 * n_clusters * kp, s) != cudaSuccess ||
-      cudaMallocAsync(reinterpret_cast<void**>(&qe), nq * sizeof(int32_t), s) != cudaSuccess ||
-      cudaMallocAsync(reinterpret_cast<void**>(&ce), n_clusters * sizeof(int32_t), s) != cudaSuccess ||
-      cudaMallocAsync(reinterpret_cast<void**>(&ql1), nq * sizeof(double), s) != cudaSuccess ||
-      cudaMallocAsync(reinterpret_cast<void**>(&cl1), n_clusters * sizeof(double), s) != cudaSuccess ||
-      cudaMallocAsync(reinterpret_cast<void**>(&bounds), (size_t)rows * n_clusters * 2 * sizeof(float), s) != cudaSuccess)
+  Workspace ws(s);
+  if (!ws.alloc(qd, (size_t)4 * nq * kp) || !ws.alloc(cd, (size_t)4 * n_clusters * kp) || !ws.alloc(qe, nq) ||
+      !ws.alloc(ce, n_clusters) || !ws.alloc(ql1, nq) || !ws.alloc(cl1, n_clusters) ||
+      !ws.alloc(bounds, (size_t)rows * n_clusters * 2))
     return fail(IVRQ_ENOMEM, "ivrq_select_clusters: workspace allocation failed");
-  static const int ndig = getenv("IVRQ_PROBE_DIGITS") ? atoi(getenv("IVRQ_PROBE_DIGITS")) : 2;
-  const int QT = ndig == 4 ? QT_<4> : QT_<2>, CT = ndig == 4 ? CT_<4> : CT_<2>;
-  auto dq = ndig == 4 ? digits_kernel<double, 4> : digits_kernel<double, 2>;
-  auto dc = ndig == 4 ? digits_kernel<float, 4> : digits_kernel<float, 2>;
+  constexpr int ndig = 2;  // 14-bit fixed point per side
+  const int QT = QT_<ndig>, CT = CT_<ndig>;
+  auto dq = digits_kernel<double, ndig>;
+  auto dc = digits_kernel<float, ndig>;
   dq<<<(unsigned)ceil_div(nq, 8), 256, 0, s>>>(q_rot, nq, dims, kp, 0, qd, qe, ql1);
   dc<<<(unsigned)ceil_div(n_clusters, 8), 256, 0, s>>>(centroids, n_clusters, dims, kp, 0, cd, ce, cl1);
   IVRQ_TRY(check_launch("ivrq_select_clusters(digits)"));
@@ -640,7 +631,7 @@ int probe_tc(const double* q_rot, int64_t nq, int32_t dims, const float* centroi
   ta.c_l1 = cl1;
   ta.bnd = bounds;
   const size_t sm = tp_smem_bytes();
-  auto tk = ndig == 4 ? tc_probe_kernel<4> : tc_probe_kernel<2>;
+  auto tk = tc_probe_kernel<ndig>;
   if (cudaFuncSetAttribute(tk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess ||
       cudaFuncSetAttribute(probe_rescore_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ROW * 4) !=
           cudaSuccess)
@@ -656,22 +647,8 @@ int probe_tc(const double* q_rot, int64_t nq, int32_t dims, const float* centroi
     const size_t rsm =
         n_clusters <= SMEM_ROW && !rs_fast_tau(n_clusters, n_probe) ? (size_t)n_clusters * sizeof(float) : 0;
     probe_rescore_kernel<<<(unsigned)rn, RS_THREADS, rsm, s>>>(bounds, r0, n_clusters, n_probe, order_by_id, q_rot,
-                                                               centroids, dims, q_sq, centroid_sqnorms, ids, d2, pstats);
+                                                               centroids, dims, q_sq, centroid_sqnorms, ids, d2, nullptr);
     IVRQ_TRY(check_launch("ivrq_select_clusters(rescore)"));
-  }
-  cudaFreeAsync(qd, s);
-  cudaFreeAsync(cd, s);
-  cudaFreeAsync(qe, s);
-  cudaFreeAsync(ce, s);
-  cudaFreeAsync(ql1, s);
-  cudaFreeAsync(cl1, s);
-  cudaFreeAsync(bounds, s);
-  if (pstats) {  // debugging aid: mean candidates per query and overflows (synchronises)
-    unsigned long long h[2];
-    cudaMemcpy(h, pstats, 16, cudaMemcpyDeviceToHost);
-    fprintf(stderr, "[ivrq probe] nq=%lld nlist=%d nprobe=%d candidates/query=%.2f overflow=%llu\n", (long long)nq,
-            n_clusters, n_probe, (double)h[0] / (double)nq, h[1]);
-    cudaFree(pstats);
   }
   return IVRQ_OK;
 }

@@ -1718,7 +1718,8 @@ __global__ void __launch_bounds__(1024) pair_plan_kernel(const int64_t* __restri
     if (c < nlist) {
       const int64_t n_c = offsets[c + 1] - offsets[c], cnt = poff[c + 1] - poff[c];
       e = cnt * ip_row_stride(n_c);
-      t = (n_c > 0 && cnt > 0) ? ceil_div(cnt, grp) : 0;
+      // grp > 0: groups of grp pairs; grp < 0: tiles of -grp rows of the list (lists with pairs)
+      t = (n_c > 0 && cnt > 0) ? (grp > 0 ? ceil_div(cnt, grp) : ceil_div(n_c, -grp)) : 0;
     }
     int64_t ie = e, it = t;  // inclusive warp scans
 #pragma unroll
@@ -1964,17 +1965,24 @@ __global__ void __launch_bounds__(THREADS, 2) first_dist_kernel(FdArgs a) {
 // (list, query) pair, list-major on the 5th-generation tensor cores: for a
 // list c and a group of G queries probing it, D[v][(j, s)] = <u_v, digit_s of
 // q_j> is one int8 GEMM (M = 128 vectors per TMEM tile, N = 8 G digit slices,
-// K = kpad) with the accumulator in TMEM.  Warp roles per CTA:
-//   warps 0-3  stage rcode tiles (128 rows x 128 B per stage) into a ring,
+// K = kpad) with the accumulator in TMEM.  The group's digit slices stay
+// resident in shared memory while the list's rcode rows stream past them.
+// Warp roles per CTA:
+//   warps 0-3  stage rcode tiles (128 rows x 128 B per stage) into a ring
+//              (one TMA lane for 8-bit codes; all four warps unpack 4-bit codes),
+//   warp 1     also loads the next group's digit slices: one 1-D bulk copy of
+//              nkc KB per query from the pre-swizzled slice array, as soon as
+//              the previous group's MMAs retire (no CTA barrier between groups),
 //   warp 4     issues tcgen05.mma (one elected lane) and commits,
-//   warps 5-8  read the accumulator (tcgen05.ld), assemble each query's 8
-//              digit dots exactly in int64, round once to float64 and write
-//              the refined distance with refine_chunk's arithmetic.
-// The per-query pass (scan_warp_kernel) then only streams stage-1 inputs and
+//   warps 5-12 read the accumulator (tcgen05.ld; two warps per TMEM lane
+//              quarter, each half of the group's queries), assemble each
+//              query's 8 digit dots exactly in int64, round once to float64 and
+//              write the refined distance with refine_chunk's arithmetic.
+// The per-query pass (scan_rd_kernel) then only streams stage-1 inputs and
 // reads the refined distance of its survivors.
 constexpr int TCM = 128;     // vectors per tile = TMEM lanes
 constexpr int TCKC = 128;    // K bytes per A stage (4 MMAs of K = 32)
-constexpr int TCST = 6;      // A stages
+constexpr int TCST = 6;      // A stages (tc_ip_kernel)
 constexpr int TC_PROD = 4;  // producer warps
 constexpr int TC_THREADS = 32 * (TC_PROD + 1 + 4);
 constexpr int TCR_EPI = 8;  // tc_refine epilogue warps: 2 per TMEM lane quarter, each half of the group's queries
@@ -1982,9 +1990,9 @@ constexpr int TCR_THREADS = 32 * (TC_PROD + 1 + TCR_EPI);
 
 struct TcArgs {
   CUtensorMap map_a;        // rcodes [N rows x rcode_bytes] (8-bit codes), box 128 B x 128 rows, 128B swizzle
-  CUtensorMap map_b;        // tc-ordered slices [nq * 8 rows x kpad], box 128 B x 8 rows
+  const int8_t* bslices;    // [nq][nkc][8 rows x 128 B] pre-swizzled digit slices (tc_slices_kernel)
   ivrq_index_view ix;
-  int kpad, G, nib;
+  int kpad, G, nst, nib;
   const double* scalars;
   const double* probe_d2;
   int nprobe, nlist;
@@ -1993,23 +2001,34 @@ struct TcArgs {
   const int64_t* pair_base; // [nlist + 1]
   const int32_t* gpre;      // [nlist + 1] prefix of ceil(bucket / G)
   double* rdist;
-  unsigned long long* prof;  // optional wait-cycle counters (IVRQ_TC_PROF)
-  int nst;                   // A stages
-  int w1;                    // one polling lane per waiting warp
-  int dbg;                   // IVRQ_TC_DBG (diagnostics only, results invalid): 1 = no epilogue math/stores, 2 = no MMAs
 };
 
-// digit slices in rcode byte order: out[q][s][P] = qslices[q][s][perm(P)] with
-// perm(64p + 16t + 4h + j) = 64p + 16h + 4t + j (the mma.sync fragment order transposed)
-__global__ void tc_slices_kernel(const int8_t* __restrict__ qslices, int64_t nq, int kp, int8_t* __restrict__ out) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // one 16-byte chunk
-  const int64_t nchunk = nq * SLICES * (kp / 16);
-  if (i >= nchunk) return;
-  const int64_t row = i / (kp / 16);
-  const int P0 = 16 * (int)(i % (kp / 16));
-  const int p64 = P0 >> 6, t4 = (P0 >> 4) & 3;
-  const uint32_t* src = reinterpret_cast<const uint32_t*>(qslices + row * kp + 64 * p64 + 4 * t4);
-  *reinterpret_cast<uint4*>(out + row * kp + P0) = make_uint4(src[0], src[4], src[8], src[12]);
+// byte offset of (row R, byte k < 128) in a 128B-swizzled K-major tile (8-row atoms of 1024 B)
+__host__ __device__ inline uint32_t sw128_offset(int R, int k) {
+  return (uint32_t)((R >> 3) * 1024 + (R & 7) * 128 + ((((k >> 4) ^ (R & 7)) & 7) << 4) + (k & 15));
+}
+
+// The refine's B operand, laid out for one bulk copy per query: out[q][kc] is the 1 KB
+// 128B-swizzled atom of digit rows s = 0..7, K bytes [128 kc, 128 kc + 128) in rcode
+// byte order P, with qslices' mma.sync fragment order transposed:
+// value(P = 64p + 16t + 4h + j) = qslices[q][s][64p + 16h + 4t + j]; zero past kpad.
+__global__ void tc_slices_kernel(const int8_t* __restrict__ qslices, int64_t nq, int kp, int nkc,
+                                 int8_t* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // one 16-byte group of one row
+  const int64_t ngroups = nq * nkc * 64;
+  if (i >= ngroups) return;
+  const int64_t atom = i >> 6;  // (q, kc)
+  const int w = (int)(i & 63), s = w >> 3, c16 = w & 7;
+  const int64_t q = atom / nkc;
+  const int kc = (int)(atom % nkc);
+  const int P0 = kc * TCKC + 16 * c16;
+  uint4 v = make_uint4(0u, 0u, 0u, 0u);
+  if (P0 < kp) {
+    const int p64 = P0 >> 6, t4 = (P0 >> 4) & 3;
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(qslices + (q * SLICES + s) * kp + 64 * p64 + 4 * t4);
+    v = make_uint4(src[0], src[4], src[8], src[12]);
+  }
+  *reinterpret_cast<uint4*>(out + atom * 1024 + sw128_offset(s, 16 * c16)) = v;
 }
 
 __host__ __device__ inline uint32_t tmem_cols(int n) {  // power of two >= 32 (<= 512)
@@ -2018,50 +2037,32 @@ __host__ __device__ inline uint32_t tmem_cols(int n) {  // power of two >= 32 (<
 
 size_t tc_smem_bytes(int kpad, int G, int nst) {
   const int nkc = (kpad + TCKC - 1) / TCKC;
-  return 1024 + (size_t)nkc * 8 * G * TCKC + (size_t)nst * TCM * TCKC + 128 * G + 256;
-}
-
-// byte offset of (row R, byte k < 128) in a 128B-swizzled K-major tile (8-row atoms of 1024 B)
-__device__ __forceinline__ uint32_t sw128_offset(int R, int k) {
-  return (uint32_t)((R >> 3) * 1024 + (R & 7) * 128 + ((((k >> 4) ^ (R & 7)) & 7) << 4) + (k & 15));
+  return 1024 + (size_t)nkc * 8 * G * TCKC + (size_t)nst * TCM * TCKC + 256;
 }
 
 __global__ void __launch_bounds__(TCR_THREADS, 1) tc_refine_kernel(const __grid_constant__ TcArgs a) {
   extern __shared__ __align__(1024) unsigned char tsm_raw[];
   unsigned char* tsm = reinterpret_cast<unsigned char*>(((uintptr_t)tsm_raw + 1023) & ~(uintptr_t)1023);
-  const int G = a.G, N = 8 * G, kp = a.kpad;
-  const int TCST = a.nst;  // A ring depth (runtime: traded against the group size for shared memory)
+  const int G = a.G, N = 8 * G, kp = a.kpad, NST = a.nst;
   const int nkc = (kp + TCKC - 1) / TCKC;  // 128-byte K chunks
-  int8_t* sB = reinterpret_cast<int8_t*>(tsm);                                   // [nkc][N rows x 128 B] swizzled
-  uint8_t* sA = reinterpret_cast<uint8_t*>(tsm + (size_t)nkc * N * TCKC);        // [TCST][128 rows x 128 B] swizzled
-  // per-query scalars of a group, double-buffered by group parity: [2][G] each
-  double* s_dq = reinterpret_cast<double*>(sA + TCST * TCM * TCKC);
-  double* s_kb = s_dq + 2 * G;
-  double* s_hs = s_kb + 2 * G;
-  double* s_ls = s_hs + 2 * G;
-  int64_t* s_row = reinterpret_cast<int64_t*>(s_ls + 2 * G);                     // rdist row of query j
-  uint64_t* bars = reinterpret_cast<uint64_t*>(s_row + 2 * G);
-  uint64_t* full = bars;                      // [TCST]
-  uint64_t* empty = bars + TCST;              // [TCST]
-  uint64_t* accf = bars + 2 * TCST;           // [2]
-  uint64_t* acce = bars + 2 * TCST + 2;       // [2]
-  uint64_t* bfull = bars + 2 * TCST + 4;      // [1]
-  uint64_t* bempty = bars + 2 * TCST + 5;     // [1] the group's MMAs are done with sB
-  uint64_t* scf = bars + 2 * TCST + 6;        // [2] scalars of buffer i written
-  uint64_t* sce = bars + 2 * TCST + 8;        // [2] scalars of buffer i consumed by the epilogue
-  uint32_t* s_taddr = reinterpret_cast<uint32_t*>(bars + 2 * TCST + 10);
-  // 8-bit codes: query groups hand over through mbarriers (B reloaded as soon as the previous
-  // group's MMAs retire, scalars double-buffered) instead of a CTA barrier that drains the
-  // pipeline at every group; the 4-bit path (all producer warps unpacking) keeps the barrier
-  const bool async_grp = !a.nib;
+  int8_t* sB = reinterpret_cast<int8_t*>(tsm);                                   // [G][nkc][8 rows x 128 B]
+  uint8_t* sA = reinterpret_cast<uint8_t*>(tsm + (size_t)nkc * N * TCKC);        // [NST][128 rows x 128 B] swizzled
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sA + (size_t)NST * TCM * TCKC);
+  uint64_t* full = bars;                      // [NST]
+  uint64_t* empty = bars + NST;               // [NST]
+  uint64_t* accf = bars + 2 * NST;            // [2]
+  uint64_t* acce = bars + 2 * NST + 2;        // [2]
+  uint64_t* bfull = bars + 2 * NST + 4;       // [1]
+  uint64_t* bempty = bars + 2 * NST + 5;      // [1] the group's MMAs are done with sB
+  uint32_t* s_taddr = reinterpret_cast<uint32_t*>(bars + 2 * NST + 6);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  // a whole warp waiting on an mbarrier: one lane polls (a.w1), the warp then re-converges
+  // a whole warp waiting on an mbarrier: one lane polls, the warp then re-converges
   auto wait1 = [&](uint64_t* bar, uint32_t parity) {
-    if (!a.w1 || lane == 0) tc::mbar_wait(bar, parity);
+    if (lane == 0) tc::mbar_wait(bar, parity);
     __syncwarp();
   };
   if (tid == 0) {
-    for (int i = 0; i < TCST; ++i) {
+    for (int i = 0; i < NST; ++i) {
       tc::mbar_init(&full[i], a.nib ? 32 * TC_PROD : 1);
       tc::mbar_init(&empty[i], 1);
     }
@@ -2071,10 +2072,6 @@ __global__ void __launch_bounds__(TCR_THREADS, 1) tc_refine_kernel(const __grid_
     }
     tc::mbar_init(bfull, 1);
     tc::mbar_init(bempty, 1);
-    for (int i = 0; i < 2; ++i) {
-      tc::mbar_init(&scf[i], 1);
-      tc::mbar_init(&sce[i], 32 * TCR_EPI);
-    }
     tc::fence_mbar_init();
   }
   if (wid == TC_PROD) tc::tmem_alloc(s_taddr, tmem_cols(2 * N));
@@ -2083,9 +2080,8 @@ __global__ void __launch_bounds__(TCR_THREADS, 1) tc_refine_kernel(const __grid_
   tc::fence_after_sync();
   const uint32_t tbase = *s_taddr;
   const int64_t rb = a.ix.rcode_bytes;
+  const uint32_t bq_bytes = (uint32_t)nkc * 1024;  // one query's slices
   uint32_t it_prod = 0, it_mma = 0, tile_mma = 0, tile_epi = 0, grp = 0;
-  const long long t_start = a.prof ? clock64() : 0;
-  long long a_grp_end = 0;
   const int total = a.gpre[a.nlist];
   for (int b = blockIdx.x; b < total; b += gridDim.x, ++grp) {
     int lo_c = 0, hi_c = a.nlist;
@@ -2097,57 +2093,26 @@ __global__ void __launch_bounds__(TCR_THREADS, 1) tc_refine_kernel(const __grid_
     const int64_t lo = a.ix.offsets[c], n_c = a.ix.offsets[c + 1] - lo;
     const int64_t ps = a.poff[c] + (int64_t)(b - a.gpre[c]) * G;
     const int nqg = (int)min((int64_t)G, a.poff[c + 1] - ps);
-    const int64_t rs = ip_row_stride(n_c);
     const int ntile = (int)ceil_div(n_c, TCM);
-    const int sb = (int)(grp & 1);  // scalar buffer of this group
-    if (!async_grp) __syncthreads();  // previous group's MMAs completed (its epilogue waited on them), scalars consumed
-    if (a.prof && wid == TC_PROD && lane == 0 && a_grp_end) atomicAdd(a.prof + 5, (unsigned long long)(clock64() - a_grp_end));
-    if (wid == (async_grp ? 1 : 0)) {
-      // group scalars (lane j: query j), then the group operand: the G queries' digit slices,
-      // 8 rows per query, by TMA (one lane per query)
-      if (async_grp) wait1(&sce[sb], ((grp >> 1) & 1) ^ 1);  // the epilogue is done with group grp - 2
-      if (lane < G) {
-        double dq = 0.0, kb = 0.0;
-        int e = 0;
-        int64_t row = 0;
-        if (lane < nqg) {
-          const int64_t pr = a.porder[ps + lane];
-          const int64_t q = pr / a.nprobe;
-          dq = a.probe_d2[pr];
-          kb = a.scalars[q * IVRQ_QS_COUNT + IVRQ_QS_KB_SUM];
-          e = (int)a.scalars[q * IVRQ_QS_COUNT + IVRQ_QS_SLICE_EXP];
-          row = a.pair_base[c] + (ps + lane - a.poff[c]) * rs;
-        }
-        s_dq[sb * G + lane] = dq;
-        s_kb[sb * G + lane] = kb;
-        s_hs[sb * G + lane] = ldexp(1.0, e - 26);
-        s_ls[sb * G + lane] = ldexp(1.0, e - 54);
-        s_row[sb * G + lane] = row;
-      }
-      __syncwarp();
-      if (async_grp) {
-        if (lane == 0) tc::mbar_arrive(&scf[sb]);
-        wait1(bempty, (grp & 1) ^ 1);  // the previous group's MMAs no longer read sB
-      }
-      if (lane == 0) tc::mbar_expect_tx(bfull, (uint32_t)(nqg * nkc * 8 * TCKC));
+    if (wid == 1) {
+      // the group operand: each query's digit slices (nkc KB, pre-swizzled) by one bulk copy,
+      // issued once the previous group's MMAs no longer read sB
+      wait1(bempty, (grp & 1) ^ 1);
+      if (lane == 0) tc::mbar_expect_tx(bfull, (uint32_t)nqg * bq_bytes);
       __syncwarp();
       if (lane < nqg) {
-        const int q8 = (int)((a.porder[ps + lane] / a.nprobe) * SLICES);
-        for (int kc = 0; kc < nkc; ++kc)
-          tc::tma_load_2d(sB + kc * N * TCKC + lane * 8 * TCKC, &a.map_b, kc * TCKC, q8, bfull);
+        const int64_t q = a.porder[ps + lane] / a.nprobe;
+        tc::bulk_load(sB + (size_t)lane * bq_bytes, a.bslices + q * bq_bytes, bq_bytes, bfull, tc::kL2EvictLast);
       }
     }
-    if (!async_grp) __syncthreads();
     if (wid < TC_PROD) {
       // ---- producers: rcode tiles -> A ring
       if (!a.nib) {
         if (tid == 0) {
           for (int t = 0; t < ntile; ++t)
             for (int kc = 0; kc < nkc; ++kc, ++it_prod) {
-              const int st = it_prod % TCST;
-              const long long tw = a.prof ? clock64() : 0;
-              tc::mbar_wait(&empty[st], ((it_prod / TCST) & 1) ^ 1);
-              if (a.prof) atomicAdd(a.prof + 6, (unsigned long long)(clock64() - tw));
+              const int st = it_prod % NST;
+              tc::mbar_wait(&empty[st], ((it_prod / NST) & 1) ^ 1);
               tc::mbar_expect_tx(&full[st], TCM * TCKC);
               tc::tma_load_2d(sA + st * TCM * TCKC, &a.map_a, kc * TCKC, (int)(lo + (int64_t)t * TCM), &full[st]);
             }
@@ -2169,16 +2134,16 @@ __global__ void __launch_bounds__(TCR_THREADS, 1) tc_refine_kernel(const __grid_
                                               : make_uint2(0u, 0u);
           }
         };
-        const int nst = ntile * nkc;
+        const int nsx = ntile * nkc;
         uint2 xn[PER];
-        if (nst > 0) load_stage(0, xn);
-        for (int sidx = 0; sidx < nst; ++sidx, ++it_prod) {
+        if (nsx > 0) load_stage(0, xn);
+        for (int sidx = 0; sidx < nsx; ++sidx, ++it_prod) {
           uint2 xc[PER];
 #pragma unroll
           for (int e = 0; e < PER; ++e) xc[e] = xn[e];
-          if (sidx + 1 < nst) load_stage(sidx + 1, xn);
-          const int st = it_prod % TCST;
-          tc::mbar_wait(&empty[st], ((it_prod / TCST) & 1) ^ 1);
+          if (sidx + 1 < nsx) load_stage(sidx + 1, xn);
+          const int st = it_prod % NST;
+          tc::mbar_wait(&empty[st], ((it_prod / NST) & 1) ^ 1);
           uint8_t* dst = sA + st * TCM * TCKC;
 #pragma unroll
           for (int e = 0; e < PER; ++e) {
@@ -2193,332 +2158,90 @@ __global__ void __launch_bounds__(TCR_THREADS, 1) tc_refine_kernel(const __grid_
         }
       }
     } else if (wid == TC_PROD) {
-      // ---- MMA issuer (optionally timing its waits: a.prof[0..3] = B, accumulator, A, total cycles)
-      // N of this group's MMAs: its queries' 8 digit rows, rounded to 16 (lists probed by few queries
-      // do not pay for a full group)
+      // ---- MMA issuer.  N = the group's 8 digit rows per query, rounded to 16 (a list probed by
+      // few queries does not pay for a full group)
       const uint32_t idesc = tc::idesc_i8(TCM, 8 * ((nqg + 1) & ~1), false, true);
-      long long t0 = a.prof ? clock64() : 0;
       wait1(bfull, grp & 1);
-      long long t1 = a.prof ? clock64() : 0;
-      if (a.prof && lane == 0) atomicAdd(a.prof + 0, (unsigned long long)(t1 - t0));
       for (int t = 0; t < ntile; ++t, ++tile_mma) {
         const int ab = tile_mma & 1;
-        t0 = a.prof ? clock64() : 0;
         wait1(&acce[ab], ((tile_mma >> 1) & 1) ^ 1);
-        if (a.prof && lane == 0) atomicAdd(a.prof + 1, (unsigned long long)(clock64() - t0));
         tc::fence_after_sync();
         for (int kc = 0; kc < nkc; ++kc, ++it_mma) {
-          const int st = it_mma % TCST;
-          t0 = a.prof ? clock64() : 0;
-          wait1(&full[st], (it_mma / TCST) & 1);
-          if (a.prof && lane == 0) atomicAdd(a.prof + 2, (unsigned long long)(clock64() - t0));
+          const int st = it_mma % NST;
+          wait1(&full[st], (it_mma / NST) & 1);
           tc::fence_after_sync();
           if (lane == 0) {
-            const long long ti = a.prof ? clock64() : 0;
             const int ks = min(TCKC, kp - kc * TCKC) / 32;
-            for (int s2 = 0; s2 < ks && a.dbg != 2 && a.dbg != 3; ++s2) {
+            for (int s2 = 0; s2 < ks; ++s2) {
               const uint64_t ad = tc::smem_desc_sw128(sA + st * TCM * TCKC + 32 * s2);
-              const uint64_t bd = tc::smem_desc_sw128(sB + kc * N * TCKC + 32 * s2);
+              const uint64_t bd = tc::smem_desc_sw128_sbo(sB + kc * 1024 + 32 * s2, bq_bytes);
               tc::mma_i8(tbase + ab * N, ad, bd, idesc, kc > 0 || s2 > 0);
             }
             tc::commit(&empty[st]);
             if (kc == nkc - 1) tc::commit(&accf[ab]);
-            if (a.prof) atomicAdd(a.prof + 4, (unsigned long long)(clock64() - ti));
           }
           __syncwarp();
         }
       }
-      if (async_grp && lane == 0) tc::commit(bempty);  // sB free once this group's MMAs retire
+      if (lane == 0) tc::commit(bempty);  // sB free once this group's MMAs retire
       __syncwarp();
-      if (a.prof && lane == 0) a_grp_end = clock64();
     } else {
       // ---- epilogue: row r of the tile is TMEM lane r (a warp reads lane quarter wid % 4); the two
-      // warps of a quarter split the group's queries
+      // warps of a quarter split the group's queries.  Per-query scalars: lane i holds query j_lo + i.
       const int quarter = wid & 3;
       const int r = quarter * 32 + lane;
       const int jh = ((G >> 1) + 3) & ~3;
-      const int j_lo = ((wid - (TC_PROD + 1)) >> 2) * jh, j_hi = min(G, j_lo + jh);
-      if (async_grp) wait1(&scf[sb], (grp >> 1) & 1);
+      const int j_lo = ((wid - (TC_PROD + 1)) >> 2) * jh, j_hi = min(nqg, j_lo + jh);
+      const int64_t rs = ip_row_stride(n_c);
+      double dq = 0.0, kb = 0.0, hs = 0.0, ls = 0.0;
+      int64_t rowb = 0;
+      if (j_lo + lane < j_hi) {
+        const int64_t pi = ps + j_lo + lane;
+        const int64_t pr = a.porder[pi];
+        const int64_t q = pr / a.nprobe;
+        dq = a.probe_d2[pr];
+        kb = a.scalars[q * IVRQ_QS_COUNT + IVRQ_QS_KB_SUM];
+        const int e = (int)a.scalars[q * IVRQ_QS_COUNT + IVRQ_QS_SLICE_EXP];
+        hs = ldexp(1.0, e - 26);
+        ls = ldexp(1.0, e - 54);
+        rowb = a.pair_base[c] + (pi - a.poff[c]) * rs;
+      }
       for (int t = 0; t < ntile; ++t, ++tile_epi) {
         const int ab = tile_epi & 1;
         const int64_t v = (int64_t)t * TCM + r;
         float2 lf = make_float2(0.f, 0.f);
         if (v < n_c) lf = __ldg(reinterpret_cast<const float2*>(a.ix.long_factors) + lo + v);
-        const long long te = a.prof ? clock64() : 0;
         wait1(&accf[ab], (tile_epi >> 1) & 1);
-        if (a.prof && tid == 32 * (TC_PROD + 1)) atomicAdd(a.prof + 7, (unsigned long long)(clock64() - te));
         tc::fence_after_sync();
-        for (int j0 = j_lo; j0 < j_hi && a.dbg != 1 && a.dbg != 3; j0 += 4) {
+        for (int j0 = j_lo; j0 < j_hi; j0 += 4) {
           uint32_t d[32];
           tc::tmem_ld32(tbase + ((uint32_t)(quarter * 32) << 16) + ab * N + 8 * j0, d);
           tc::tmem_ld_wait();
 #pragma unroll
           for (int jj = 0; jj < 4; ++jj) {
             const int j = j0 + jj;
-            if (j < nqg && v < n_c) {
+            const int src = (j - j_lo) & 31;
+            const double q_dq = __shfl_sync(FULL, dq, src), q_kb = __shfl_sync(FULL, kb, src);
+            const double q_hs = __shfl_sync(FULL, hs, src), q_ls = __shfl_sync(FULL, ls, src);
+            const int64_t q_row = __shfl_sync(FULL, rowb, src);
+            if (j < j_hi && v < n_c) {
               const int* D = reinterpret_cast<const int*>(d + 8 * jj);
               const long long hi = (long long)D[0] * 2097152LL + (long long)D[1] * 16384LL + (long long)D[2] * 128LL + D[3];
               const long long lw = (long long)D[4] * 2097152LL + (long long)D[5] * 16384LL + (long long)D[6] * 128LL + D[7];
-              const int js = sb * G + j;
-              const double ip = dadd(dmul((double)hi, s_hs[js]), dmul((double)lw, s_ls[js]));
-              a.rdist[s_row[js] + v] =
-                  dmax(dsub(dadd((double)lf.x, s_dq[js]), dmul((double)lf.y, dsub(ip, s_kb[js]))), 0.0);
+              const double ip = dadd(dmul((double)hi, q_hs), dmul((double)lw, q_ls));
+              // streaming store: written once, read once by scan_rd
+              __stcs(a.rdist + q_row + v, dmax(dsub(dadd((double)lf.x, q_dq), dmul((double)lf.y, dsub(ip, q_kb))), 0.0));
             }
           }
         }
         tc::fence_before_sync();
         tc::mbar_arrive(&acce[ab]);
       }
-      if (async_grp) tc::mbar_arrive(&sce[sb]);  // this group's scalars may be overwritten
     }
   }
   tc::fence_before_sync();
   __syncthreads();
-  if (a.prof && tid == 0) atomicAdd(a.prof + 3, (unsigned long long)(clock64() - t_start));
   if (wid == TC_PROD) tc::tmem_dealloc(tbase, tmem_cols(2 * N));
-}
-
-// ------------------------------------------------------------ refine, A operand in TMEM (TS form)
-// Same result as tc_refine_kernel with the roles swapped so the tensor core reads
-// only one operand from shared memory: the group's digit slices (M = 128 rows =
-// 16 queries x 8 digits) are staged once per group by TMA and copied into TMEM
-// (tcgen05.cp); every rcode tile (N = 128 vectors, TMA ring) then meets them in a
-// TS-form MMA.  Per MMA the SMEM traffic is the rcode tile only (written by TMA,
-// read once), which the int8 peak can sustain; the SS form also re-read the
-// resident slices.  The epilogue thread of TMEM lane 8 j + s holds digit s of
-// query j for 32 vectors at a time; the 8 digit lanes of a query are reduced by
-// a transposed shuffle tree (hi = digits 0-3, lo = digits 4-7, exact int64) and
-// each lane finishes 4 vectors with refine_chunk's float64 arithmetic.
-constexpr int TSG = 16;  // queries per group: M = 128 digit rows
-
-size_t tc_ts_smem_bytes(int kpad) {
-  const int nkc = (kpad + TCKC - 1) / TCKC;
-  return 1024 + (size_t)nkc * 128 * TCKC + (size_t)TCST * TCM * TCKC + 64 * TSG + 256 + 2 * TCM * 8;
-}
-
-__global__ void __launch_bounds__(TC_THREADS, 1) tc_refine_ts_kernel(const __grid_constant__ TcArgs a) {
-  extern __shared__ __align__(1024) unsigned char tsm_raw[];
-  unsigned char* tsm = reinterpret_cast<unsigned char*>(((uintptr_t)tsm_raw + 1023) & ~(uintptr_t)1023);
-  const int kp = a.kpad;
-  const int nkc = (kp + TCKC - 1) / TCKC;
-  int8_t* sB = reinterpret_cast<int8_t*>(tsm);                                   // [nkc][128 rows x 128 B] slices
-  uint8_t* sA = reinterpret_cast<uint8_t*>(tsm + (size_t)nkc * 128 * TCKC);      // [TCST][128 vectors x 128 B]
-  double* s_dq = reinterpret_cast<double*>(sA + TCST * TCM * TCKC);              // [TSG]
-  double* s_kb = s_dq + TSG;
-  double* s_hs = s_kb + TSG;
-  double* s_ls = s_hs + TSG;
-  int64_t* s_row = reinterpret_cast<int64_t*>(s_ls + TSG);
-  float2* s_lf = reinterpret_cast<float2*>(s_row + TSG);                         // [2][TCM] long factors of the tile
-  uint64_t* bars = reinterpret_cast<uint64_t*>(s_lf + 2 * TCM);
-  uint64_t* full = bars;
-  uint64_t* empty = bars + TCST;
-  uint64_t* accf = bars + 2 * TCST;
-  uint64_t* acce = bars + 2 * TCST + 2;
-  uint64_t* bfull = bars + 2 * TCST + 4;
-  uint32_t* s_taddr = reinterpret_cast<uint32_t*>(bars + 2 * TCST + 5);
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  if (tid == 0) {
-    for (int i = 0; i < TCST; ++i) {
-      tc::mbar_init(&full[i], a.nib ? 32 * TC_PROD : 1);
-      tc::mbar_init(&empty[i], 1);
-    }
-    for (int i = 0; i < 2; ++i) {
-      tc::mbar_init(&accf[i], 1);
-      tc::mbar_init(&acce[i], 128);
-    }
-    tc::mbar_init(bfull, 1);
-    tc::fence_mbar_init();
-  }
-  if (wid == TC_PROD) tc::tmem_alloc(s_taddr, 512);
-  tc::fence_before_sync();
-  __syncthreads();
-  tc::fence_after_sync();
-  const uint32_t tbase = *s_taddr;      // accumulators: columns [0, 256)
-  const uint32_t tslices = tbase + 256; // the group's digit slices: kpad / 4 columns
-  const int64_t rb = a.ix.rcode_bytes;
-  const uint32_t idesc = tc::idesc_i8(128, TCM, true, false);  // A = slices (s8), B = rcodes (u8)
-  uint32_t it_prod = 0, it_mma = 0, tile_mma = 0, tile_epi = 0, grp = 0;
-  const int total = a.gpre[a.nlist];
-  for (int b = blockIdx.x; b < total; b += gridDim.x, ++grp) {
-    int lo_c = 0, hi_c = a.nlist;
-    while (hi_c - lo_c > 1) {
-      const int mid = (lo_c + hi_c) >> 1;
-      if (a.gpre[mid] <= b) lo_c = mid; else hi_c = mid;
-    }
-    const int c = lo_c;
-    const int64_t lo = a.ix.offsets[c], n_c = a.ix.offsets[c + 1] - lo;
-    const int64_t ps = a.poff[c] + (int64_t)(b - a.gpre[c]) * TSG;
-    const int nqg = (int)min((int64_t)TSG, a.poff[c + 1] - ps);
-    const int64_t rs = ip_row_stride(n_c);
-    const int ntile = (int)ceil_div(n_c, TCM);
-    __syncthreads();  // previous group's MMAs (and slice copies) completed, scalars consumed
-    if (wid == 0) {   // the group's digit slices: 8 rows per query, by TMA (one lane per query)
-      if (lane == 0) tc::mbar_expect_tx(bfull, (uint32_t)(nqg * nkc * 8 * TCKC));
-      __syncwarp();
-      if (lane < nqg) {
-        const int q8 = (int)((a.porder[ps + lane] / a.nprobe) * SLICES);
-        for (int kc = 0; kc < nkc; ++kc)
-          tc::tma_load_2d(sB + kc * 128 * TCKC + lane * 8 * TCKC, &a.map_b, kc * TCKC, q8, bfull);
-      }
-    }
-    if (tid < TSG) {
-      double dq = 0.0, kb = 0.0;
-      int e = 0;
-      int64_t row = 0;
-      if (tid < nqg) {
-        const int64_t pr = a.porder[ps + tid];
-        const int64_t q = pr / a.nprobe;
-        dq = a.probe_d2[pr];
-        kb = a.scalars[q * IVRQ_QS_COUNT + IVRQ_QS_KB_SUM];
-        e = (int)a.scalars[q * IVRQ_QS_COUNT + IVRQ_QS_SLICE_EXP];
-        row = a.pair_base[c] + (ps + tid - a.poff[c]) * rs;
-      }
-      s_dq[tid] = dq;
-      s_kb[tid] = kb;
-      s_hs[tid] = ldexp(1.0, e - 26);
-      s_ls[tid] = ldexp(1.0, e - 54);
-      s_row[tid] = row;
-    }
-    __syncthreads();
-    if (wid < TC_PROD) {
-      if (!a.nib) {
-        if (tid == 0) {
-          for (int t = 0; t < ntile; ++t)
-            for (int kc = 0; kc < nkc; ++kc, ++it_prod) {
-              const int st = it_prod % TCST;
-              tc::mbar_wait(&empty[st], ((it_prod / TCST) & 1) ^ 1);
-              tc::mbar_expect_tx(&full[st], TCM * TCKC);
-              tc::tma_load_2d(sA + st * TCM * TCKC, &a.map_a, kc * TCKC, (int)(lo + (int64_t)t * TCM), &full[st]);
-            }
-        }
-      } else {
-        const int pl = wid * 32 + lane;
-        const uint8_t* rows = a.ix.rcodes + lo * rb;
-        constexpr int PER = TCM * (TCKC / 16) / (32 * TC_PROD);
-        auto load_stage = [&](int sidx, uint2 (&x)[PER]) {
-          const int t = sidx / nkc, kb0 = (sidx % nkc) * TCKC;
-#pragma unroll
-          for (int e = 0; e < PER; ++e) {
-            const int i = pl + e * 32 * TC_PROD;
-            const int r = i / (TCKC / 16), pc = 16 * (i % (TCKC / 16));
-            const int64_t v = (int64_t)t * TCM + r;
-            x[e] = (v < n_c && kb0 + pc < kp) ? __ldg(reinterpret_cast<const uint2*>(rows + v * rb + (kb0 + pc) / 2))
-                                              : make_uint2(0u, 0u);
-          }
-        };
-        const int nst = ntile * nkc;
-        uint2 xn[PER];
-        if (nst > 0) load_stage(0, xn);
-        for (int sidx = 0; sidx < nst; ++sidx, ++it_prod) {
-          uint2 xc[PER];
-#pragma unroll
-          for (int e = 0; e < PER; ++e) xc[e] = xn[e];
-          if (sidx + 1 < nst) load_stage(sidx + 1, xn);
-          const int st = it_prod % TCST;
-          tc::mbar_wait(&empty[st], ((it_prod / TCST) & 1) ^ 1);
-          uint8_t* dst = sA + st * TCM * TCKC;
-#pragma unroll
-          for (int e = 0; e < PER; ++e) {
-            const int i = pl + e * 32 * TC_PROD;
-            const int r = i / (TCKC / 16), pc = 16 * (i % (TCKC / 16));
-            const uint2 x = xc[e];
-            *reinterpret_cast<uint4*>(dst + sw128_offset(r, pc)) =
-                make_uint4(x.x & 0x0F0F0F0Fu, (x.x >> 4) & 0x0F0F0F0Fu, x.y & 0x0F0F0F0Fu, (x.y >> 4) & 0x0F0F0F0Fu);
-          }
-          tc::fence_smem_async();
-          tc::mbar_arrive(&full[st]);
-        }
-      }
-    } else if (wid == TC_PROD) {
-      // ---- MMA issuer: slices -> TMEM once per group, then a TS MMA per 32 dims of every rcode tile
-      tc::mbar_wait(bfull, grp & 1);
-      tc::fence_after_sync();
-      if (lane == 0)
-        for (int s2 = 0; s2 < kp / 32; ++s2)
-          tc::tmem_cp_128x256b(tslices + 8 * s2, tc::smem_desc_sw128(sB + (s2 / 4) * 128 * TCKC + 32 * (s2 % 4)));
-      __syncwarp();
-      for (int t = 0; t < ntile; ++t, ++tile_mma) {
-        const int ab = tile_mma & 1;
-        tc::mbar_wait(&acce[ab], ((tile_mma >> 1) & 1) ^ 1);
-        tc::fence_after_sync();
-        for (int kc = 0; kc < nkc; ++kc, ++it_mma) {
-          const int st = it_mma % TCST;
-          tc::mbar_wait(&full[st], (it_mma / TCST) & 1);
-          tc::fence_after_sync();
-          if (lane == 0) {
-            const int ks = min(TCKC, kp - kc * TCKC) / 32;
-            for (int s2 = 0; s2 < ks; ++s2) {
-              const uint64_t bd = tc::smem_desc_sw128(sA + st * TCM * TCKC + 32 * s2);
-              tc::mma_i8_ts(tbase + ab * TCM, tslices + 8 * (kc * 4 + s2), bd, idesc, kc > 0 || s2 > 0);
-            }
-            tc::commit(&empty[st]);
-            if (kc == nkc - 1) tc::commit(&accf[ab]);
-          }
-          __syncwarp();
-        }
-      }
-    } else {
-      // ---- epilogue: TMEM lane 8 j + s (query j, digit s), columns = the tile's 128 vectors
-      const int quarter = wid & 3;
-      const int row = quarter * 32 + lane;
-      const int j = row >> 3, s = row & 7;
-      const int b0 = s & 1, b1 = (s >> 1) & 1, b2 = s >> 2;
-      const int wsh = 7 * (3 - (s & 3));  // digit weight inside its half: 128^(3 - s mod 4)
-      for (int t = 0; t < ntile; ++t, ++tile_epi) {
-        const int ab = tile_epi & 1;
-        {  // the tile's long factors, staged while the MMAs run (double-buffered by tile parity)
-          const int et = tid - 32 * (TC_PROD + 1);  // 0..127
-          const int64_t v = (int64_t)t * TCM + et;
-          s_lf[ab * TCM + et] = v < n_c ? __ldg(reinterpret_cast<const float2*>(a.ix.long_factors) + lo + v)
-                                        : make_float2(0.f, 0.f);
-          asm volatile("bar.sync 1, 128;" ::: "memory");  // epilogue warps only
-        }
-        tc::mbar_wait(&accf[ab], (tile_epi >> 1) & 1);
-        tc::fence_after_sync();
-        for (int v0 = 0; v0 < TCM; v0 += 32) {
-          uint32_t d[32];
-          tc::tmem_ld32(tbase + ((uint32_t)(quarter * 32) << 16) + ab * TCM + v0, d);
-          tc::tmem_ld_wait();
-          long long X[32];
-#pragma unroll
-          for (int i = 0; i < 32; ++i) X[i] = ((long long)(int)d[i]) << wsh;
-          // (register arrays indexed at compile time only; the lane's half is chosen by selects)
-          long long Y[16];
-#pragma unroll
-          for (int m = 0; m < 16; ++m) {
-            const long long keep = b0 ? X[16 + m] : X[m], give = b0 ? X[m] : X[16 + m];
-            Y[m] = keep + __shfl_xor_sync(0xffffffffu, give, 1);
-          }
-          long long Z[8];
-#pragma unroll
-          for (int m = 0; m < 8; ++m) {
-            const long long keep = b1 ? Y[8 + m] : Y[m], give = b1 ? Y[m] : Y[8 + m];
-            Z[m] = keep + __shfl_xor_sync(0xffffffffu, give, 2);
-          }
-          // lanes s and s^4 hold the hi (digits 0-3) and lo (4-7) sums of the same 8 vectors
-#pragma unroll
-          for (int m = 0; m < 4; ++m) {
-            const long long mine = b2 ? Z[4 + m] : Z[m];
-            const long long other = __shfl_xor_sync(0xffffffffu, b2 ? Z[m] : Z[4 + m], 4);
-            const long long hi = b2 ? other : mine, lw = b2 ? mine : other;
-            const int vl = v0 + 16 * b0 + 8 * b1 + 4 * b2 + m;
-            const int64_t v = (int64_t)t * TCM + vl;
-            if (j < nqg && v < n_c) {
-              const float2 lf = s_lf[ab * TCM + vl];
-              const double ip = dadd(dmul((double)hi, s_hs[j]), dmul((double)lw, s_ls[j]));
-              a.rdist[s_row[j] + v] =
-                  dmax(dsub(dadd((double)lf.x, s_dq[j]), dmul((double)lf.y, dsub(ip, s_kb[j]))), 0.0);
-            }
-          }
-        }
-        tc::fence_before_sync();
-        tc::mbar_arrive(&acce[ab]);
-      }
-    }
-  }
-  tc::fence_before_sync();
-  __syncthreads();
-  if (wid == TC_PROD) tc::tmem_dealloc(tbase, 512);
 }
 
 // ------------------------------------------------------------ stage-1 inner products on tcgen05
@@ -2808,13 +2531,8 @@ inline auto rd_kernel_for(bool refine, int ipb) {
 }
 
 inline int launch_rd(const Args& a, bool refine, int ipb, cudaStream_t s) {
-  static const int rsub = getenv("IVRQ_RD_SUB") ? atoi(getenv("IVRQ_RD_SUB")) : 4;  // 32-vector sub-chunks per batch
-  static const int rminb = getenv("IVRQ_RD_MINB") ? atoi(getenv("IVRQ_RD_MINB")) : 6;  // B200 A/B: 1, 6, 8
-  auto kern = rsub == 8 ? rd_kernel_for<8>(refine, ipb)
-              : rsub == 2 ? (rminb == 8 ? rd_kernel_for<2, 8>(refine, ipb) : rd_kernel_for<2>(refine, ipb))
-              : rminb == 8 ? rd_kernel_for<4, 8>(refine, ipb)
-              : rminb == 6 ? rd_kernel_for<4, 6>(refine, ipb)
-                           : rd_kernel_for<4>(refine, ipb);
+  // 4 sub-chunks of 32 vectors per batch, register budget for 6 resident CTAs (B200 A/B: 1, 6, 8)
+  auto kern = rd_kernel_for<4, 6>(refine, ipb);
   {
     KernelTimer kt("scan_rd_kernel", s);
     kern<<<(unsigned)ceil_div(a.nq, RDW), RDW * 32, 0, s>>>(a);
@@ -2827,12 +2545,9 @@ int launch_warp(const Args& a, int ipb, cudaStream_t s) {
   const size_t sm = warp_smem_bytes(a.kpad, REFINE);
   // wide rows (D >= 1024: the digit slices take ~12 KB of shared memory per warp) trade residency
   // for registers: C5 (D = 1536) scan 15.4 ms at 6 vs 16.8 at 8; C4 (D = 96) 8.6 at 8 vs 10.0 at 6
-  static const int minb_env = getenv("IVRQ_WARP_MINB") ? atoi(getenv("IVRQ_WARP_MINB")) : 0;
-  const int minb = minb_env ? minb_env : (a.kpad >= 1024 ? 6 : WQ_MINB);
-  auto kern = minb == 16  ? (ipb == 2 ? scan_warp_kernel<REFINE, NIB, 2, 16> : scan_warp_kernel<REFINE, NIB, 4, 16>)
-              : minb == 12 ? (ipb == 2 ? scan_warp_kernel<REFINE, NIB, 2, 12> : scan_warp_kernel<REFINE, NIB, 4, 12>)
-              : minb == 6 ? (ipb == 2 ? scan_warp_kernel<REFINE, NIB, 2, 6> : scan_warp_kernel<REFINE, NIB, 4, 6>)
-                          : (ipb == 2 ? scan_warp_kernel<REFINE, NIB, 2, WQ_MINB> : scan_warp_kernel<REFINE, NIB, 4, WQ_MINB>);
+  auto kern = a.kpad >= 1024 ? (ipb == 2 ? scan_warp_kernel<REFINE, NIB, 2, 6> : scan_warp_kernel<REFINE, NIB, 4, 6>)
+                             : (ipb == 2 ? scan_warp_kernel<REFINE, NIB, 2, WQ_MINB>
+                                         : scan_warp_kernel<REFINE, NIB, 4, WQ_MINB>);
   if (sm > 48 * 1024 && cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess)
     return fail(IVRQ_EUNSUP, "ivrq_search_scan: shared memory request too large");
   {
@@ -2866,6 +2581,53 @@ int launch_mode(const Args& a, bool refine, bool nib, int ipb, cudaStream_t s) {
   return nib ? launch_t<MODE, true, true>(a, ipb, s) : launch_t<MODE, true, false>(a, ipb, s);
 }
 
+// Path selection.  Every path computes the reference's arithmetic exactly, so
+// they return identical ids, distances and survivor counts (tests/
+// test_gpu_parity.py::test_tensor_core_stage1_matches_popcount_path); the
+// defaults are the measured fastest per configuration.  The
+// environment variables only force a path, for those equivalence tests.
+struct ScanPolicy {
+  bool tc_path, warp_path, rd_path, first_phase, first_dist, tc_ip;
+};
+
+static int env_flag(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : dflt;
+}
+
+static ScanPolicy scan_policy(const ivrq_index_view& ix, const ivrq_search_params& p, bool refine, bool chained,
+                              int64_t nl) {
+  ScanPolicy sp{};
+  // bitwise mode, k <= 32: stage-1 inner products list-major on the tensor cores, then one
+  // warp per query (first lists included)
+  sp.tc_path = p.ip_mode == IVRQ_IP_BITWISE && p.k <= 32 && env_flag("IVRQ_TC_STAGE1", 1) != 0 && nl >= 1;
+  sp.warp_path = sp.tc_path && env_flag("IVRQ_WARP_SCAN", 1) != 0;
+  // every probed pair refined list-major on tcgen05 (then a streaming per-query pass): dense
+  // refine costs (probed vectors) x kpad MACs against (survivors) x kpad gathered by the in-warp
+  // refine; measured on the B200: dense wins for 8-bit codes at D <= 768 (C3), the survivor-only
+  // path for 4-bit codes (C2, C4: few survivors, 64-byte rows) and at D = 1536 (C5).
+  const int tr = env_flag("IVRQ_TC_REFINE", -1);
+  const bool dense = tr >= 0 ? tr != 0 : (!rcode_nibbles(ix.bits) && kpad64(ix.dims) <= 768);
+  sp.rd_path = sp.warp_path && (!refine || (ix.rcodes && dense));
+  sp.first_phase = refine && p.k <= 32 && !chained && env_flag("IVRQ_FIRST_LIST", !sp.warp_path) != 0;
+  sp.first_dist = sp.warp_path && !sp.rd_path && refine && !chained && env_flag("IVRQ_FIRST_DIST", 1) != 0;
+  // tcgen05 stage 1 for long codes; mma.sync tiles win for short ones (D <= 224)
+  sp.tc_ip = env_flag("IVRQ_TC_IP", words_per_vector(ix.dims) >= 8 ? 1 : 0) != 0;
+  return sp;
+}
+
+// tc_refine group size and A ring depth: the largest query group whose digit slices fit beside
+// a ring of >= 3 A stages (C3, D = 768: G = 28, 3 stages; scan stage measured 2.72 ms against
+// 2.78 (G = 24, 4 stages), 2.88 (20, 5), 3.19 (16, 6), 3.64 (12, 8))
+static bool tc_refine_shape(int kpad, int& G, int& nst) {
+  const size_t cap = 227 * 1024;
+  for (G = 32; G >= 4; G -= 4) {
+    for (nst = 8; nst >= 3; --nst)
+      if (tc_smem_bytes(kpad, G, nst) <= cap) return true;
+  }
+  return false;
+}
+
 }  // namespace scan
 }  // namespace ivrq
 
@@ -2895,9 +2657,9 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
   if (params->k < 1) return fail(IVRQ_EINVAL, "k must be >= 1");
   if (params->k > 4096) return fail(IVRQ_EUNSUP, "ivrq_search_scan: k > 4096 not supported");
   if (index->bits < 1 || index->bits > 8) return fail(IVRQ_EINVAL, "index bits out of range");
+  if (nq == 0) return IVRQ_OK;
   const bool refine = params->refine && index->bits >= 2;
   if (refine && (!qslices || !index->rcodes)) return fail(IVRQ_EINVAL, "refine needs qslices and rcodes");
-  if (nq == 0) return IVRQ_OK;
   scan::Args a{};
   a.ix = *index;
   a.probe_ids = probe_ids;
@@ -2925,62 +2687,36 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
   a.out_dists = out_dists;
   a.out_counts = out_counts;
   a.stats = stats;
+  a.l2_prefetch = 0;  // measured neutral
+  a.rd_prefetch = 1;  // scan_rd: refined distances read with the stage-1 inputs (fewer dependent loads)
   const bool nib = rcode_nibbles(index->bits);
-  const char* pf_env = getenv("IVRQ_L2_PREFETCH");
-  a.l2_prefetch = pf_env ? atoi(pf_env) : 0;
-  const char* rp_env = getenv("IVRQ_RD_PREFETCH");
-  a.rd_prefetch = rp_env ? atoi(rp_env) : 1;
   cudaStream_t s = as_stream(stream);
-  retain_async_pool(s);
-  // Schedule queries grouped by their first (lowest-id) probed list: that list
-  // is refined in full (the threshold is still +inf), so neighbours in the
-  // grid share it through L2.  Results do not depend on the order.
-  int32_t* first = nullptr;
-  int64_t *cnt = nullptr, *off = nullptr, *order = nullptr;
-  const char* ord_env = getenv("IVRQ_SCAN_ORDER");
-  const bool grouped = ord_env ? atoi(ord_env) != 0 : true;
   const int64_t nl = index->n_clusters;
-  int32_t* gpre = nullptr;
-  int64_t* pool_ids = nullptr;
-  double* pool_d = nullptr;
-  int32_t* pool_n = nullptr;
-  const char* fl_env = getenv("IVRQ_FIRST_LIST");
-  const char* tc_env = getenv("IVRQ_TC_STAGE1");
-  const char* wenv = getenv("IVRQ_WARP_SCAN");
-  // bitwise mode, k <= 32: stage-1 inner products list-major on the tensor
-  // cores, then one warp per query (first lists included)
-  const bool tc_path = params->ip_mode == IVRQ_IP_BITWISE && a.k <= 32 && (tc_env ? atoi(tc_env) != 0 : true) && nl >= 1;
-  const bool warp_path = tc_path && (wenv ? atoi(wenv) != 0 : true);
-  // ... with every probed pair refined list-major on tcgen05 and a streaming per-query pass
-  const char* tr_env = getenv("IVRQ_TC_REFINE");
-  // Dense refine costs (probed vectors) x kpad MACs against (survivors) x kpad gathered for the
-  // in-warp refine: at D <= 768 the tensor cores win, at D = 1536 (5x more probed than surviving
-  // vectors) the survivor-only path does.  IVRQ_TC_REFINE=0/1 forces either.
-  // Measured (B200, bench configs): dense wins at C3 (8-bit codes, D = 768); the survivor-only
-  // path wins for 4-bit codes (C2, C4: few survivors, 64-byte rows) and at D = 1536 (C5).
-  // (1-bit indexes have nothing to refine: the streaming pass alone.)
-  const bool rd_path = warp_path && (!refine || (index->rcodes && (tr_env ? atoi(tr_env) != 0
-                                                                          : (!rcode_nibbles(index->bits) &&
-                                                                             kpad64(index->dims) <= 768))));
-  const bool first_phase = grouped && refine && a.k <= 32 && !init_counts &&
-                           (fl_env ? atoi(fl_env) != 0 : !warp_path);
-  if (grouped && nq > 1 && nl >= 1) {
-    if (cudaMallocAsync(reinterpret_cast<void**>(&first), nq * sizeof(int32_t), s) != cudaSuccess ||
-        cudaMallocAsync(reinterpret_cast<void**>(&cnt), (nl + 1) * sizeof(int64_t), s) != cudaSuccess ||
-        cudaMallocAsync(reinterpret_cast<void**>(&off), (nl + 2) * sizeof(int64_t), s) != cudaSuccess ||
-        cudaMallocAsync(reinterpret_cast<void**>(&order), nq * sizeof(int64_t), s) != cudaSuccess)
-      return fail(IVRQ_ENOMEM, "ivrq_search_scan: workspace allocation failed");
+  const scan::ScanPolicy pol = scan::scan_policy(*index, *params, refine, init_counts != nullptr, nl);
+  Workspace ws(s);  // every scratch block below is freed when the call returns, on any path
+  auto oom = [](const char* what) { return fail(IVRQ_ENOMEM, std::string("ivrq_search_scan: ") + what); };
+  // Queries grouped by their first (lowest-id) probed list: that list is refined in full
+  // (the threshold is still +inf), so neighbours in the grid share it through L2.  Results
+  // do not depend on the order.
+  int64_t *off = nullptr;
+  if (nq > 1 && nl >= 1) {
+    int32_t* first = nullptr;
+    int64_t *cnt = nullptr, *order = nullptr;
+    if (!ws.alloc(first, nq) || !ws.alloc(cnt, nl + 1) || !ws.alloc(off, nl + 2) || !ws.alloc(order, nq))
+      return oom("workspace allocation failed");
     scan::first_probe_kernel<<<(unsigned)ceil_div(nq, 256), 256, 0, s>>>(probe_ids, nq, a.nprobe, list_lo, list_hi,
                                                                          first);
     IVRQ_TRY(check_launch("ivrq_search_scan(order)"));
     IVRQ_TRY(ivrq_counting_sort(first, nq, (int32_t)(nl + 1), cnt, off, order, stream));
     a.qorder = order;
-    if (first_phase) {
-      if (cudaMallocAsync(reinterpret_cast<void**>(&gpre), (nl + 1) * sizeof(int32_t), s) != cudaSuccess ||
-          cudaMallocAsync(reinterpret_cast<void**>(&pool_ids), nq * a.k * sizeof(int64_t), s) != cudaSuccess ||
-          cudaMallocAsync(reinterpret_cast<void**>(&pool_d), nq * a.k * sizeof(double), s) != cudaSuccess ||
-          cudaMallocAsync(reinterpret_cast<void**>(&pool_n), nq * sizeof(int32_t), s) != cudaSuccess)
-        return fail(IVRQ_ENOMEM, "ivrq_search_scan: workspace allocation failed");
+    if (pol.first_phase) {
+      int32_t* gpre = nullptr;
+      int64_t* pool_ids = nullptr;
+      double* pool_d = nullptr;
+      int32_t* pool_n = nullptr;
+      if (!ws.alloc(gpre, nl + 1) || !ws.alloc(pool_ids, nq * a.k) || !ws.alloc(pool_d, nq * a.k) ||
+          !ws.alloc(pool_n, nq))
+        return oom("workspace allocation failed");
       cudaMemsetAsync(pool_n, 0, nq * sizeof(int32_t), s);
       if (stats) cudaMemsetAsync(stats, 0, 2 * nq * sizeof(int64_t), s);
       scan::group_prefix_kernel<<<1, 1, 0, s>>>(off, (int)nl, gpre);
@@ -3008,8 +2744,7 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
       if (fsm > 48 * 1024 &&
           cudaFuncSetAttribute(fk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm) != cudaSuccess)
         return fail(IVRQ_EUNSUP, "ivrq_search_scan: dims too large for the first-list phase");
-      const unsigned grid = (unsigned)(ceil_div(nq, scan::QG) + nl);
-      fk<<<grid, scan::THREADS, fsm, s>>>(fa);
+      fk<<<(unsigned)(ceil_div(nq, scan::QG) + nl), scan::THREADS, fsm, s>>>(fa);
       IVRQ_TRY(check_launch("ivrq_search_scan(first lists)"));
       a.init_ids = pool_ids;
       a.init_dists = pool_d;
@@ -3017,18 +2752,14 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
       a.skip_first = 1;
     }
   }
-  // first lists refined list-major for the warp-per-query kernel (launched
-  // below, concurrently with the stage-1 inner products on a side stream)
-  std::function<int()> fd_launch;
-  int64_t *fbase = nullptr, *ftot = nullptr;
-  int32_t* fgpre = nullptr;
-  double* fdist = nullptr;
-  const char* fd_env = getenv("IVRQ_FIRST_DIST");
-  if (warp_path && !rd_path && refine && a.qorder && !init_counts && (fd_env ? atoi(fd_env) != 0 : true)) {
-    if (cudaMallocAsync(reinterpret_cast<void**>(&fbase), (nl + 1) * sizeof(int64_t), s) != cudaSuccess ||
-        cudaMallocAsync(reinterpret_cast<void**>(&fgpre), (nl + 1) * sizeof(int32_t), s) != cudaSuccess ||
-        cudaMallocAsync(reinterpret_cast<void**>(&ftot), 2 * sizeof(int64_t), s) != cudaSuccess)
-      return fail(IVRQ_ENOMEM, "ivrq_search_scan: workspace allocation failed");
+  // first lists refined list-major for the warp-per-query kernel (run on the main stream,
+  // concurrently with the stage-1 inner products on the side stream)
+  std::function<int()> refine_launch;
+  if (pol.first_dist && a.qorder) {
+    int64_t *fbase = nullptr, *ftot = nullptr;
+    int32_t* fgpre = nullptr;
+    if (!ws.alloc(fbase, nl + 1) || !ws.alloc(fgpre, nl + 1) || !ws.alloc(ftot, 2))
+      return oom("workspace allocation failed");
     scan::pair_plan_kernel<<<1, 1024, 0, s>>>(index->offsets, off, (int)nl, scan::FQ, fbase, fgpre, ftot);
     IVRQ_TRY(check_launch("ivrq_search_scan(first-list plan)"));
     int64_t tot[2] = {0, 0};
@@ -3039,8 +2770,8 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
       return fail(IVRQ_ECUDA, "ivrq_search_scan: first-list plan readback failed");
     }
     if (tot[0] > 0) {
-      if (cudaMallocAsync(reinterpret_cast<void**>(&fdist), (size_t)tot[0] * sizeof(double), s) != cudaSuccess)
-        return fail(IVRQ_ENOMEM, "ivrq_search_scan: first-list distance buffer allocation failed");
+      double* fdist = nullptr;
+      if (!ws.alloc(fdist, (size_t)tot[0])) return oom("first-list distance buffer allocation failed");
       scan::FdArgs fa{};
       fa.ix = *index;
       fa.list_lo = list_lo;
@@ -3062,7 +2793,7 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
       if (fsm > 48 * 1024 &&
           cudaFuncSetAttribute(fk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm) != cudaSuccess)
         return fail(IVRQ_EUNSUP, "ivrq_search_scan: dims too large for the first-list refine");
-      fd_launch = [fk, fa, fsm, s]() {
+      refine_launch = [fk, fa, fsm, s]() {
         fk<<<(unsigned)(2 * sm_count_of_current_device()), scan::THREADS, fsm, s>>>(fa);
         return check_launch("ivrq_search_scan(first-list refine)");
       };
@@ -3073,32 +2804,19 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
   }
   // list-major stage-1 inner products on the int8 tensor cores (bitwise mode, k <= 32)
   int ipb = 0;
-  double* rdist = nullptr;
-  int8_t* tcsl = nullptr;
-  int8_t* qpairs = nullptr;
-  int32_t* igpre = nullptr;
-  int64_t* iscratch = nullptr;
-  int32_t* rgpre = nullptr;
-  int64_t* rscratch = nullptr;
-  int32_t *pkeys = nullptr, *pslot = nullptr, *tpre = nullptr;
-  int64_t *pcnt = nullptr, *poff = nullptr, *porder = nullptr, *pbase = nullptr, *ptot = nullptr;
-  void* ipbuf = nullptr;
   const int64_t ipmax = (int64_t)words_per_vector(index->dims) * 32 << (params->query_bits - 1);
-  if (tc_path) {
+  if (pol.tc_path) {
     ipb = ipmax <= 32768 ? 2 : 4;
     const int64_t npairs = nq * a.nprobe;
-    const int excl = rd_path     ? 0
-                     : warp_path ? (refine && !a.prune ? 2 : (refine && !init_counts ? 1 : 0))
-                                 : (a.skip_first ? 1 : 0);
-    if (cudaMallocAsync(reinterpret_cast<void**>(&pkeys), npairs * sizeof(int32_t), s) != cudaSuccess ||
-        cudaMallocAsync(reinterpret_cast<void**>(&pslot), npairs * sizeof(int32_t), s) != cudaSuccess ||
-        cudaMallocAsync(reinterpret_cast<void**>(&porder), npairs * sizeof(int64_t), s) != cudaSuccess ||
-        cudaMallocAsync(reinterpret_cast<void**>(&pcnt), (nl + 1) * sizeof(int64_t), s) != cudaSuccess ||
-        cudaMallocAsync(reinterpret_cast<void**>(&poff), (nl + 2) * sizeof(int64_t), s) != cudaSuccess ||
-        cudaMallocAsync(reinterpret_cast<void**>(&pbase), (nl + 1) * sizeof(int64_t), s) != cudaSuccess ||
-        cudaMallocAsync(reinterpret_cast<void**>(&tpre), (nl + 1) * sizeof(int32_t), s) != cudaSuccess ||
-        cudaMallocAsync(reinterpret_cast<void**>(&ptot), 2 * sizeof(int64_t), s) != cudaSuccess)
-      return fail(IVRQ_ENOMEM, "ivrq_search_scan: workspace allocation failed");
+    const int excl = pol.rd_path     ? 0
+                     : pol.warp_path ? (refine && !a.prune ? 2 : (refine && !init_counts ? 1 : 0))
+                                     : (a.skip_first ? 1 : 0);
+    int32_t *pkeys = nullptr, *pslot = nullptr, *tpre = nullptr;
+    int64_t *pcnt = nullptr, *poff = nullptr, *porder = nullptr, *pbase = nullptr, *ptot = nullptr;
+    if (!ws.alloc(pkeys, npairs) || !ws.alloc(pslot, npairs) || !ws.alloc(porder, npairs) ||
+        !ws.alloc(pcnt, nl + 1) || !ws.alloc(poff, nl + 2) || !ws.alloc(pbase, nl + 1) || !ws.alloc(tpre, nl + 1) ||
+        !ws.alloc(ptot, 2))
+      return oom("workspace allocation failed");
     scan::pair_key_kernel<<<(unsigned)ceil_div(nq, 256), 256, 0, s>>>(probe_ids, nq, a.nprobe, list_lo, list_hi,
                                                                       excl, pkeys);
     IVRQ_TRY(check_launch("ivrq_search_scan(pair keys)"));
@@ -3107,77 +2825,52 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
                                                                           (int32_t)nl, pslot);
     scan::pair_plan_kernel<<<1, 1024, 0, s>>>(index->offsets, poff, (int)nl, scan::TQ, pbase, tpre, ptot);
     IVRQ_TRY(check_launch("ivrq_search_scan(pair plan)"));
-    // ip buffer: bounded by every pair owning a row of the largest list (no
-    // host round trip), or the exact total read back when the bound is unknown
+    // ip buffer: bounded by every pair owning a row of the largest list (no host round trip)
+    // while the buffers stay within 8 GiB of the 180 GB of HBM, else the exact total read back
     int64_t tot[2] = {0, 0};
     if (excl == 2) {
       tot[0] = 0;
     } else if (index->max_list > 0 &&
-               npairs * scan::ip_row_stride(index->max_list) * (ipb + (rd_path && refine ? 8 : 0)) <=
+               npairs * scan::ip_row_stride(index->max_list) * (ipb + (pol.rd_path && refine ? 8 : 0)) <=
                    (int64_t(8) << 30)) {
-      // bound without a host round trip while the buffers stay within 8 GiB of the 180 GB of HBM
       tot[0] = npairs * scan::ip_row_stride(index->max_list);
     } else if (cudaMemcpyAsync(tot, ptot, sizeof(tot), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
                cudaStreamSynchronize(s) != cudaSuccess) {
       return fail(IVRQ_ECUDA, "ivrq_search_scan: pair plan readback failed");
     }
     if (tot[0] > 0) {
-      if (cudaMallocAsync(&ipbuf, (size_t)tot[0] * ipb, s) != cudaSuccess)
-        return fail(IVRQ_ENOMEM, "ivrq_search_scan: inner-product buffer allocation failed");
+      uint8_t* ipbuf = nullptr;
       int8_t* qhat = nullptr;
-      if (cudaMallocAsync(reinterpret_cast<void**>(&qhat), (size_t)nq * 32 * a.g, s) != cudaSuccess)
-        return fail(IVRQ_ENOMEM, "ivrq_search_scan: workspace allocation failed");
-      scan::IpArgs ia{};
-      ia.ix = *index;
-      ia.qhat = qhat;
-      ia.g = a.g;
-      ia.nprobe = a.nprobe;
-      ia.nlist = (int)nl;
-      ia.porder = porder;
-      ia.poff = poff;
-      ia.pair_base = pbase;
-      ia.tpre = tpre;
-      ia.ipbuf = ipbuf;
-      const size_t ism = (size_t)scan::TQ * (32 * a.g + scan::TQ_PAD) + 2 * sizeof(uint32_t) * scan::KCH * scan::TV;
-      auto ik = ipb == 2 ? scan::ip_list_kernel<int16_t> : scan::ip_list_kernel<int32_t>;
-      if (ism > 48 * 1024 &&
-          cudaFuncSetAttribute(ik, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ism) != cudaSuccess)
-        return fail(IVRQ_EUNSUP, "ivrq_search_scan: dims too large for the tensor-core stage 1");
-      if (rd_path && refine) {
-        // refined distance of every probed pair on tcgen05 (concurrent with the inner products)
-        // group size: the rcode tiles of a list are streamed once per group, so the largest group whose
-        // digit slices fit next to a ring of >= 3 A stages (C3, D = 768: G = 28, 3 stages; scan stage
-        // measured 2.72 ms against 2.78 (G = 24, 4 stages), 2.88 (20, 5), 3.19 (16, 6), 3.64 (12, 8))
-        const size_t smem_cap = 227 * 1024;
-        int G = 32;
-        while (G > 4 && scan::tc_smem_bytes(a.kpad, G, 3) > smem_cap) G -= 4;
-        int nst = scan::TCST;
-        while (nst > 2 && scan::tc_smem_bytes(a.kpad, G, nst) > smem_cap) --nst;
-        if (getenv("IVRQ_TC_G")) G = atoi(getenv("IVRQ_TC_G"));  // A/B: group size (multiple of 2) and A stages
-        if (getenv("IVRQ_TC_ST")) nst = atoi(getenv("IVRQ_TC_ST"));
-        if (G < 4 || G > 32 || (G & 3) || nst < 2 || nst > 8 || scan::tc_smem_bytes(a.kpad, G, nst) > smem_cap)
-          return fail(IVRQ_EINVAL, "ivrq_search_scan: tensor-core refine group/stage configuration does not fit");
-        if (cudaMallocAsync(reinterpret_cast<void**>(&rdist), (size_t)tot[0] * sizeof(double), s) != cudaSuccess ||
-            cudaMallocAsync(reinterpret_cast<void**>(&rgpre), (nl + 1) * sizeof(int32_t), s) != cudaSuccess ||
-            cudaMallocAsync(reinterpret_cast<void**>(&rscratch), (nl + 3) * sizeof(int64_t), s) != cudaSuccess)
-          return fail(IVRQ_ENOMEM, "ivrq_search_scan: refined-distance buffer allocation failed");
+      if (!ws.alloc(ipbuf, (size_t)tot[0] * ipb) || !ws.alloc(qhat, (size_t)nq * 32 * a.g))
+        return oom("inner-product buffer allocation failed");
+      if (pol.rd_path && refine) {
+        // refined distance of every probed pair on tcgen05 (concurrent with the inner products):
+        // one work item per (list, group of G queries probing it)
+        int G = 0, nb = 0;
+        if (!scan::tc_refine_shape(a.kpad, G, nb))
+          return fail(IVRQ_EUNSUP, "ivrq_search_scan: dims too large for the tensor-core refine");
+        double* rdist = nullptr;
+        int32_t* rgpre = nullptr;
+        int64_t* rscratch = nullptr;
+        int8_t* tcsl = nullptr;
+        const int nkc = (a.kpad + scan::TCKC - 1) / scan::TCKC;
+        if (!ws.alloc(rdist, (size_t)tot[0]) || !ws.alloc(rgpre, nl + 1) || !ws.alloc(rscratch, nl + 3) ||
+            !ws.alloc(tcsl, (size_t)nq * nkc * 1024))
+          return oom("refined-distance buffer allocation failed");
         scan::pair_plan_kernel<<<1, 1024, 0, s>>>(index->offsets, poff, (int)nl, G, rscratch, rgpre, rscratch + nl + 1);
         IVRQ_TRY(check_launch("ivrq_search_scan(refine plan)"));
-        if (cudaMallocAsync(reinterpret_cast<void**>(&tcsl), (size_t)nq * scan::SLICES * a.kpad, s) != cudaSuccess)
-          return fail(IVRQ_ENOMEM, "ivrq_search_scan: workspace allocation failed");
-        scan::tc_slices_kernel<<<(unsigned)ceil_div(nq * scan::SLICES * (a.kpad / 16), 256), 256, 0, s>>>(
-            qslices, nq, a.kpad, tcsl);
+        scan::tc_slices_kernel<<<(unsigned)ceil_div(nq * nkc * 64, 256), 256, 0, s>>>(qslices, nq, a.kpad, nkc, tcsl);
         scan::TcArgs ta{};
         // A: the rcode rows (8-bit codes; 4-bit indexes are unpacked by the producer warps instead)
-        if ((!nib && !tc::make_tmap_u8_sw128(&ta.map_a, index->rcodes, (uint64_t)index->rcode_bytes,
-                                             (uint64_t)index->size, (uint64_t)index->rcode_bytes, scan::TCKC,
-                                             scan::TCM)) ||
-            !tc::make_tmap_u8_sw128(&ta.map_b, tcsl, (uint64_t)a.kpad, (uint64_t)nq * scan::SLICES, (uint64_t)a.kpad,
-                                    scan::TCKC, 8))
+        if (!nib && !tc::make_tmap_u8_sw128(&ta.map_a, index->rcodes, (uint64_t)index->rcode_bytes,
+                                            (uint64_t)index->size, (uint64_t)index->rcode_bytes, scan::TCKC,
+                                            scan::TCM))
           return fail(IVRQ_ECUDA, "ivrq_search_scan: TMA tensor map encoding failed");
+        ta.bslices = tcsl;
         ta.ix = *index;
         ta.kpad = a.kpad;
         ta.G = G;
+        ta.nst = nb;
         ta.nib = nib ? 1 : 0;
         ta.scalars = scalars;
         ta.probe_d2 = probe_d2;
@@ -3188,185 +2881,107 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
         ta.pair_base = pbase;
         ta.gpre = rgpre;
         ta.rdist = rdist;
-        ta.dbg = getenv("IVRQ_TC_DBG") ? atoi(getenv("IVRQ_TC_DBG")) : 0;
-        ta.nst = nst;
-        ta.w1 = getenv("IVRQ_TC_W1") ? atoi(getenv("IVRQ_TC_W1")) : 1;
-        const size_t tsm = scan::tc_smem_bytes(a.kpad, G, nst);
+        const size_t tsm = scan::tc_smem_bytes(a.kpad, G, nb);
         if (cudaFuncSetAttribute(scan::tc_refine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm) !=
             cudaSuccess)
           return fail(IVRQ_EUNSUP, "ivrq_search_scan: dims too large for the tensor-core refine");
-        static const bool tprof = getenv("IVRQ_TC_PROF") != nullptr;
-        if (tprof) {
-          cudaMalloc(reinterpret_cast<void**>(&ta.prof), 8 * sizeof(unsigned long long));
-          cudaMemset(ta.prof, 0, 8 * sizeof(unsigned long long));
-        }
-        const char* ts_env = getenv("IVRQ_TC_TS");
-        // TS form measured slower at C3 (1.96 vs 1.78 ms per search on the B200): opt-in only
-        const bool ts = (ts_env ? atoi(ts_env) != 0 : false) && a.kpad <= 768;
-        if (ts) {
-          // TS form: 16-query groups, slices staged as 128 rows per 128-dim chunk
-          ta.G = scan::TSG;
-          scan::pair_plan_kernel<<<1, 1024, 0, s>>>(index->offsets, poff, (int)nl, scan::TSG, rscratch, rgpre,
-                                                     rscratch + nl + 1);
-          const size_t tss = scan::tc_ts_smem_bytes(a.kpad);
-          if (cudaFuncSetAttribute(scan::tc_refine_ts_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)tss) != cudaSuccess)
-            return fail(IVRQ_EUNSUP, "ivrq_search_scan: dims too large for the tensor-core refine");
-          fd_launch = [ta, tss, s]() {
-            scan::tc_refine_ts_kernel<<<(unsigned)sm_count_of_current_device(), scan::TC_THREADS, tss, s>>>(ta);
-            return check_launch("ivrq_search_scan(tensor-core refine)");
-          };
-        } else
-        fd_launch = [ta, tsm, s]() {
+        refine_launch = [ta, tsm, s]() {
           {
             KernelTimer kt("tc_refine_kernel", s);
             scan::tc_refine_kernel<<<(unsigned)sm_count_of_current_device(), scan::TCR_THREADS, tsm, s>>>(ta);
           }
-          const int rc = check_launch("ivrq_search_scan(tensor-core refine)");
-          if (ta.prof) {  // debugging aid (synchronises): where the MMA lane waited
-            unsigned long long h[8];
-            cudaMemcpy(h, ta.prof, sizeof(h), cudaMemcpyDeviceToHost);
-            const double tot = (double)h[3];
-            fprintf(stderr,
-                    "[ivrq tc_refine] MMA lane (share of CTA cycles): wait B %.3f, wait accumulator %.3f, wait A %.3f, "
-                    "issue %.3f, group switch %.3f; producer wait-empty %.3f; epilogue wait-accf %.3f\n",
-                    h[0] / tot, h[1] / tot, h[2] / tot, h[4] / tot, h[5] / tot, h[6] / tot, h[7] / tot);
-            cudaFree(ta.prof);
-          }
-          return rc;
+          return check_launch("ivrq_search_scan(tensor-core refine)");
         };
         a.rdist = rdist;
       }
-      // fork: the stage-1 inner products on the side stream, the first-list
-      // refine on s; both only read the index and the prepared queries
-      cudaStream_t s2 = side_stream();
-      cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-      if (fd_launch && s2) {
-        cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming);
-        cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming);
-        cudaEventRecord(ev_fork, s);
-        cudaStreamWaitEvent(s2, ev_fork, 0);
-      }
-      cudaStream_t si = (fd_launch && s2) ? s2 : s;
-      scan::qhat_kernel<<<(unsigned)ceil_div(nq * a.g, 256), 256, 0, si>>>(planes, nq, a.g, a.qbits, qhat);
-      const char* ti_env = getenv("IVRQ_TC_IP");
-      if (ti_env ? atoi(ti_env) != 0 : a.g >= 8) {  // mma.sync tiles win for short codes (D <= 224)
-        // stage-1 inner products on tcgen05: qhat rows gathered into pair order, then list-major GEMM tiles
-        const int rowb = 32 * a.g;
-        if (cudaMallocAsync(reinterpret_cast<void**>(&qpairs), (size_t)npairs * rowb, si) != cudaSuccess ||
-            cudaMallocAsync(reinterpret_cast<void**>(&igpre), (nl + 1) * sizeof(int32_t), si) != cudaSuccess ||
-            cudaMallocAsync(reinterpret_cast<void**>(&iscratch), (nl + 3) * sizeof(int64_t), si) != cudaSuccess)
-          return fail(IVRQ_ENOMEM, "ivrq_search_scan: workspace allocation failed");
-        const int ipq = scan::ip_group_size(a.g);
-        scan::pair_plan_kernel<<<1, 1024, 0, si>>>(index->offsets, poff, (int)nl, ipq, iscratch, igpre,
-                                                    iscratch + nl + 1);
-        scan::qhat_pairs_kernel<<<(unsigned)(4 * sm_count_of_current_device()), 256, 0, si>>>(
-            qhat, porder, poff, (int)nl, a.nprobe, rowb, qpairs);
-        scan::TcIpArgs ta{};
-        if (!tc::make_tmap_u8_sw128(&ta.map_b, qpairs, (uint64_t)rowb, (uint64_t)npairs, (uint64_t)rowb, scan::TCKC,
-                                    ipq))
-          return fail(IVRQ_ECUDA, "ivrq_search_scan: TMA tensor map encoding failed");
-        ta.ix = *index;
-        ta.g = a.g;
-        ta.nlist = (int)nl;
-        ta.ip32 = ipb == 4 ? 1 : 0;
-        ta.ipq = ipq;
-        ta.poff = poff;
-        ta.pair_base = pbase;
-        ta.gpre = igpre;
-        ta.ipbuf = ipbuf;
-        const size_t tsm = scan::tc_ip_smem_bytes(a.g);
-        if (cudaFuncSetAttribute(scan::tc_ip_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm) !=
-            cudaSuccess)
-          return fail(IVRQ_EUNSUP, "ivrq_search_scan: dims too large for the tensor-core stage 1");
-        KernelTimer kt("tc_ip_kernel", si);
-        scan::tc_ip_kernel<<<(unsigned)sm_count_of_current_device(), scan::TC_THREADS, tsm, si>>>(ta);
-      } else {
-        KernelTimer kt("ip_list_kernel", si);
-        ik<<<(unsigned)(2 * sm_count_of_current_device()), scan::THREADS, ism, si>>>(ia);
-      }
-      IVRQ_TRY(check_launch("ivrq_search_scan(stage-1 tiles)"));
-      if (fd_launch) {
-        IVRQ_TRY(fd_launch());
-        fd_launch = nullptr;
-      }
-      if (ev_join) {
-        cudaEventRecord(ev_join, s2);
-        cudaStreamWaitEvent(s, ev_join, 0);
-        cudaEventDestroy(ev_fork);
-        cudaEventDestroy(ev_join);
-      }
-      cudaFreeAsync(qhat, s);
+      {
+        // fork: the stage-1 inner products on the side stream, the refine on s; both only read
+        // the index and the prepared queries.  The fork joins on every return path.
+        StreamFork fork(s, refine_launch ? side_stream() : nullptr);
+        cudaStream_t si = fork.side();
+        scan::qhat_kernel<<<(unsigned)ceil_div(nq * a.g, 256), 256, 0, si>>>(planes, nq, a.g, a.qbits, qhat);
+        if (pol.tc_ip) {
+          // stage-1 inner products on tcgen05: qhat rows gathered into pair order, then list-major GEMM tiles
+          const int rowb = 32 * a.g;
+          int8_t* qpairs = nullptr;
+          int32_t* igpre = nullptr;
+          int64_t* iscratch = nullptr;
+          if (!ws.alloc(qpairs, (size_t)npairs * rowb, si) || !ws.alloc(igpre, nl + 1, si) ||
+              !ws.alloc(iscratch, nl + 3, si))
+            return oom("workspace allocation failed");
+          const int ipq = scan::ip_group_size(a.g);
+          scan::pair_plan_kernel<<<1, 1024, 0, si>>>(index->offsets, poff, (int)nl, ipq, iscratch, igpre,
+                                                      iscratch + nl + 1);
+          scan::qhat_pairs_kernel<<<(unsigned)(4 * sm_count_of_current_device()), 256, 0, si>>>(
+              qhat, porder, poff, (int)nl, a.nprobe, rowb, qpairs);
+          scan::TcIpArgs ta{};
+          if (!tc::make_tmap_u8_sw128(&ta.map_b, qpairs, (uint64_t)rowb, (uint64_t)npairs, (uint64_t)rowb,
+                                      scan::TCKC, ipq))
+            return fail(IVRQ_ECUDA, "ivrq_search_scan: TMA tensor map encoding failed");
+          ta.ix = *index;
+          ta.g = a.g;
+          ta.nlist = (int)nl;
+          ta.ip32 = ipb == 4 ? 1 : 0;
+          ta.ipq = ipq;
+          ta.poff = poff;
+          ta.pair_base = pbase;
+          ta.gpre = igpre;
+          ta.ipbuf = ipbuf;
+          const size_t tsm = scan::tc_ip_smem_bytes(a.g);
+          if (cudaFuncSetAttribute(scan::tc_ip_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm) !=
+              cudaSuccess)
+            return fail(IVRQ_EUNSUP, "ivrq_search_scan: dims too large for the tensor-core stage 1");
+          KernelTimer kt("tc_ip_kernel", si);
+          scan::tc_ip_kernel<<<(unsigned)sm_count_of_current_device(), scan::TC_THREADS, tsm, si>>>(ta);
+        } else {
+          scan::IpArgs ia{};
+          ia.ix = *index;
+          ia.qhat = qhat;
+          ia.g = a.g;
+          ia.nprobe = a.nprobe;
+          ia.nlist = (int)nl;
+          ia.porder = porder;
+          ia.poff = poff;
+          ia.pair_base = pbase;
+          ia.tpre = tpre;
+          ia.ipbuf = ipbuf;
+          const size_t ism =
+              (size_t)scan::TQ * (32 * a.g + scan::TQ_PAD) + 2 * sizeof(uint32_t) * scan::KCH * scan::TV;
+          auto ik = ipb == 2 ? scan::ip_list_kernel<int16_t> : scan::ip_list_kernel<int32_t>;
+          if (ism > 48 * 1024 &&
+              cudaFuncSetAttribute(ik, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ism) != cudaSuccess)
+            return fail(IVRQ_EUNSUP, "ivrq_search_scan: dims too large for the tensor-core stage 1");
+          KernelTimer kt("ip_list_kernel", si);
+          ik<<<(unsigned)(2 * sm_count_of_current_device()), scan::THREADS, ism, si>>>(ia);
+        }
+        IVRQ_TRY(check_launch("ivrq_search_scan(stage-1 tiles)"));
+        if (refine_launch) {
+          IVRQ_TRY(refine_launch());
+          refine_launch = nullptr;
+        }
+      }  // joined
+      a.ipbuf = ipbuf;
+      a.pslot = pslot;
+      a.pair_base = pbase;
     }
-    a.ipbuf = ipbuf;
-    a.pslot = pslot;
-    a.pair_base = pbase;
   }
-  if (fd_launch) IVRQ_TRY(fd_launch());
-  int64_t *m_lo = nullptr, *m_base = nullptr;
-  int32_t* m_nc = nullptr;
-  if (warp_path) {  // both warp kernels walk the per-probe metadata
+  if (refine_launch) IVRQ_TRY(refine_launch());
+  if (pol.warp_path) {  // both warp kernels walk the per-probe metadata
     const int64_t np = nq * a.nprobe;
-    if (cudaMallocAsync(reinterpret_cast<void**>(&m_lo), np * sizeof(int64_t), s) != cudaSuccess ||
-        cudaMallocAsync(reinterpret_cast<void**>(&m_base), np * sizeof(int64_t), s) != cudaSuccess ||
-        cudaMallocAsync(reinterpret_cast<void**>(&m_nc), np * sizeof(int32_t), s) != cudaSuccess)
-      return fail(IVRQ_ENOMEM, "ivrq_search_scan: workspace allocation failed");
+    int64_t *m_lo = nullptr, *m_base = nullptr;
+    int32_t* m_nc = nullptr;
+    if (!ws.alloc(m_lo, np) || !ws.alloc(m_base, np) || !ws.alloc(m_nc, np)) return oom("workspace allocation failed");
     scan::probe_meta_kernel<<<(unsigned)ceil_div(np, 256), 256, 0, s>>>(a, m_lo, m_nc, m_base);
     IVRQ_TRY(check_launch("ivrq_search_scan(probe metadata)"));
     a.m_lo = m_lo;
     a.m_nc = m_nc;
     a.m_base = m_base;
   }
-  const int rc = params->ip_mode == IVRQ_IP_BITWISE
-                     ? (rd_path && a.ipbuf ? scan::launch_rd(a, refine, ipb, s)
-                                           : scan::launch_mode<IVRQ_IP_BITWISE>(a, refine, nib, warp_path ? -ipb : ipb, s))
-                                                    : scan::launch_mode<IVRQ_IP_LUT>(a, refine, nib, 0, s);
-  if (m_lo) {
-    cudaFreeAsync(m_lo, s);
-    cudaFreeAsync(m_base, s);
-    cudaFreeAsync(m_nc, s);
+  if (params->ip_mode == IVRQ_IP_BITWISE) {
+    if (pol.rd_path && a.ipbuf) return scan::launch_rd(a, refine, ipb, s);
+    return scan::launch_mode<IVRQ_IP_BITWISE>(a, refine, nib, pol.warp_path ? -ipb : ipb, s);
   }
-  if (tcsl) cudaFreeAsync(tcsl, s);
-  if (qpairs) {
-    cudaFreeAsync(qpairs, s);
-    cudaFreeAsync(igpre, s);
-    cudaFreeAsync(iscratch, s);
-  }
-  if (rdist) {
-    cudaFreeAsync(rdist, s);
-    cudaFreeAsync(rgpre, s);
-    cudaFreeAsync(rscratch, s);
-  }
-  if (fbase) {
-    cudaFreeAsync(fbase, s);
-    cudaFreeAsync(fgpre, s);
-    cudaFreeAsync(ftot, s);
-    if (fdist) cudaFreeAsync(fdist, s);
-  }
-  if (pkeys) {
-    cudaFreeAsync(pkeys, s);
-    cudaFreeAsync(pslot, s);
-    cudaFreeAsync(porder, s);
-    cudaFreeAsync(pcnt, s);
-    cudaFreeAsync(poff, s);
-    cudaFreeAsync(pbase, s);
-    cudaFreeAsync(tpre, s);
-    cudaFreeAsync(ptot, s);
-    if (ipbuf) cudaFreeAsync(ipbuf, s);
-  }
-  if (first) {
-    cudaFreeAsync(first, s);
-    cudaFreeAsync(cnt, s);
-    cudaFreeAsync(off, s);
-    cudaFreeAsync(order, s);
-  }
-  if (gpre) {
-    cudaFreeAsync(gpre, s);
-    cudaFreeAsync(pool_ids, s);
-    cudaFreeAsync(pool_d, s);
-    cudaFreeAsync(pool_n, s);
-  }
-  return rc;
+  return scan::launch_mode<IVRQ_IP_LUT>(a, refine, nib, 0, s);
 }
 
 extern "C" int ivrq_merge_topk(const int64_t* ids, const double* dists, const int32_t* counts, int64_t nq,

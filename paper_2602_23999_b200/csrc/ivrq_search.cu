@@ -293,6 +293,11 @@ static int64_t probe_chunk_rows(int64_t nq, int32_t n_clusters) {
   return std::min<int64_t>(rows, std::max<int64_t>(nq, 1));
 }
 
+template <typename TC>
+static int probe_gemm_select(const double* q_rot, int64_t nq, int32_t dims, const TC* centroids,
+                             const double* centroid_sqnorms, int32_t n_clusters, int32_t n_probe, int32_t order_by_id,
+                             int64_t* ids, double* d2, double* dist, const double* q_sq, int64_t rows, cudaStream_t s);
+
 extern "C" size_t ivrq_select_clusters_workspace(int64_t nq, int32_t n_clusters) {
   int64_t rows = probe_chunk_rows(nq, n_clusters);
   return (size_t)(rows * n_clusters * 8 + nq * 8 + 256);
@@ -322,12 +327,41 @@ extern "C" int ivrq_select_clusters_ordered(const double* q_rot, int64_t nq, int
   double* dist = reinterpret_cast<double*>(workspace);
   double* q_sq = dist + rows * n_clusters;
   IVRQ_TRY(ivrq_row_sqnorms(q_rot, 1, nq, dims, q_sq, stream));
-  const char* tp_env = getenv("IVRQ_TC_PROBE");
-  if (tp_env ? atoi(tp_env) != 0 : true) {
-    retain_async_pool(s);
+  // path switch for tests (both paths select the same clusters): IVRQ_TC_PROBE=0 forces the float64 GEMM
+  const bool tc_probe = getenv("IVRQ_TC_PROBE") ? atoi(getenv("IVRQ_TC_PROBE")) != 0 : true;
+  if (tc_probe) {
     return probe_tc(q_rot, nq, dims, centroids, centroid_sqnorms, n_clusters, n_probe, order_by_id, ids, d2, q_sq, s);
   }
-  gemm::RowMajor<float> lb{centroids, n_clusters, dims};
+  return probe_gemm_select(q_rot, nq, dims, centroids, centroid_sqnorms, n_clusters, n_probe, order_by_id, ids, d2,
+                           dist, q_sq, rows, s);
+}
+
+extern "C" int ivrq_select_clusters_f64(const double* q_rot, int64_t nq, int32_t dims, const double* centroids,
+                                        const double* centroid_sqnorms, int32_t n_clusters, int32_t n_probe,
+                                        int32_t order_by_id, int64_t* ids, double* d2, void* workspace,
+                                        size_t workspace_bytes, void* stream) {
+  if (n_probe < 1 || n_probe > n_clusters)
+    return fail(IVRQ_EINVAL, "n_probe=" + std::to_string(n_probe) + " exceeds " + std::to_string(n_clusters) +
+                                 " clusters");
+  if (nq == 0) return IVRQ_OK;
+  if (workspace_bytes < ivrq_select_clusters_workspace(nq, n_clusters))
+    return fail(IVRQ_ENOMEM, "ivrq_select_clusters: workspace too small");
+  cudaStream_t s = as_stream(stream);
+  const int64_t rows = probe_chunk_rows(nq, n_clusters);
+  double* dist = reinterpret_cast<double*>(workspace);
+  double* q_sq = dist + rows * n_clusters;
+  IVRQ_TRY(ivrq_row_sqnorms(q_rot, 1, nq, dims, q_sq, stream));
+  return probe_gemm_select(q_rot, nq, dims, centroids, centroid_sqnorms, n_clusters, n_probe, order_by_id, ids, d2,
+                           dist, q_sq, rows, s);
+}
+
+// float64 GEMM probe (DMMA) + exact selection, centroids of type TC
+template <typename TC>
+static int probe_gemm_select(const double* q_rot, int64_t nq, int32_t dims, const TC* centroids,
+                             const double* centroid_sqnorms, int32_t n_clusters, int32_t n_probe, int32_t order_by_id,
+                             int64_t* ids, double* d2, double* dist, const double* q_sq, int64_t rows,
+                             cudaStream_t s) {
+  gemm::RowMajor<TC> lb{centroids, n_clusters, dims};
   size_t sel_smem = order_by_id ? 0 : (size_t)n_probe * 16;
   if (sel_smem > 48 * 1024) {
     if (cudaFuncSetAttribute(probe_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sel_smem) !=

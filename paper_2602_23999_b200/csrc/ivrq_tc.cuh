@@ -47,6 +47,19 @@ __device__ __forceinline__ uint64_t smem_desc_sw128(const void* smem_ptr) {
   return d;
 }
 
+// same with an explicit stride between 8-row atoms (atoms of one K chunk interleaved
+// with the other chunks of the same rows: SBO = chunks x 1024)
+__device__ __forceinline__ uint64_t smem_desc_sw128_sbo(const void* smem_ptr, uint32_t sbo_bytes) {
+  const uint32_t addr = (uint32_t)__cvta_generic_to_shared(smem_ptr);
+  uint64_t d = 0;
+  d |= (uint64_t)((addr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
 // instruction descriptor, kind::i8: D s32, A/B u8 (0) or s8 (1), both K-major
 __host__ __device__ constexpr uint32_t idesc_i8(int M, int N, bool a_signed, bool b_signed) {
   return (2u << 4)                          // c_format = S32
@@ -127,6 +140,29 @@ __device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* m
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
           (uint32_t)__cvta_generic_to_shared(smem_dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"((uint32_t)__cvta_generic_to_shared(mbar))
+      : "memory");
+}
+
+// L2 eviction-priority policies for TMA (the createpolicy encodings CUTLASS uses)
+constexpr uint64_t kL2EvictFirst = 0x12F0000000000000ull;  // streamed once: do not displace reused data
+constexpr uint64_t kL2EvictLast = 0x14F0000000000000ull;   // re-read across tiles: keep in L2
+
+__device__ __forceinline__ void tma_load_2d_hint(void* smem_dst, const CUtensorMap* map, int x, int y, uint64_t* mbar,
+                                                 uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"((uint32_t)__cvta_generic_to_shared(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"((uint32_t)__cvta_generic_to_shared(mbar)), "l"(policy)
+      : "memory");
+}
+
+// 1-D bulk copy global -> shared (16-byte aligned, size a multiple of 16) completing on mbar
+__device__ __forceinline__ void bulk_load(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* mbar,
+                                          uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          (uint32_t)__cvta_generic_to_shared(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(gsrc)), "r"(bytes), "r"((uint32_t)__cvta_generic_to_shared(mbar)), "l"(policy)
       : "memory");
 }
 

@@ -18,6 +18,7 @@ threshold trajectory).
 
 from __future__ import annotations
 
+import math
 from dataclasses import dataclass
 
 import numpy as np
@@ -30,6 +31,15 @@ from paper_2602_23999_b200.index import IvfRabitqIndex, default_workers
 
 __all__ = [
     "SearchParams",
+    "QueryState",
+    "build_luts",
+    "nibbles_from_bits",
+    "ip_lut",
+    "ip_bitwise",
+    "prepare_query",
+    "estimate_stage1",
+    "refine_stage2",
+    "cluster_local_search",
     "select_clusters",
     "search_batch",
     "search_device",
@@ -88,6 +98,248 @@ def merge_topk(lists, k: int):
     return ids[order], dists[order]
 
 
+# ---------------------------------------------------------------- per-query sub-operators
+# The reference exports the pieces of its per-query scan (search.py:84-375).  Each
+# one here is a launch of libivrq_b200.so on the current stream (ivrq_ops.cu);
+# host code only validates shapes and moves the small operands.
+
+_LUT_BLOCK = 4
+
+
+@dataclass
+class QueryState:
+    """Per-query derived data reused across the query's probes (search.py:84-104)."""
+
+    q_rot: np.ndarray
+    sum_q: float
+    delta_q: float = 1.0
+    q_hat: np.ndarray | None = None
+    planes: np.ndarray | None = None
+    luts: np.ndarray | None = None
+    code_sum_q: float = 0.0
+    ip_margin: float = 0.0
+    threshold: float = math.inf
+
+    def __post_init__(self) -> None:
+        if not self.code_sum_q:
+            self.code_sum_q = self.sum_q
+
+    def scalars(self) -> np.ndarray:
+        sc = np.zeros(_lib.QS_COUNT, dtype=np.float64)
+        sc[_lib.QS_SUM_Q] = self.sum_q
+        sc[_lib.QS_DELTA] = self.delta_q
+        sc[_lib.QS_CODE_SUM] = self.code_sum_q
+        sc[_lib.QS_IP_MARGIN] = self.ip_margin
+        return sc
+
+
+def _prepare_one(q_rot: np.ndarray, params: SearchParams, eps_bound: float, bits: int = 1):
+    """ivrq_prepare_queries for one rotated query; host copies of scalars / planes / luts."""
+    q = np.ascontiguousarray(np.asarray(q_rot, dtype=np.float64).reshape(1, -1))
+    d = q.shape[1]
+    g = (d + 31) // 32
+    device = dev.require_cuda()
+    qd = dev.to_device(q, device)
+    scal = torch.empty((1, _lib.QS_COUNT), dtype=torch.float64, device=device)
+    planes = luts = None
+    if params.ip_mode == "bitwise":
+        planes = torch.empty((params.query_bits, g), dtype=torch.int32, device=device)
+    else:
+        luts = torch.empty((8 * g, 16), dtype=torch.float32, device=device)
+    cp = _lib.SearchParamsC(k=params.k, n_probe=params.n_probe,
+                            ip_mode=_lib.IVRQ_IP_BITWISE if params.ip_mode == "bitwise" else _lib.IVRQ_IP_LUT,
+                            query_bits=params.query_bits, refine=0, prune=1 if params.prune else 0)
+    _lib.call("ivrq_prepare_queries", dev.ptr(qd), 1, d, cp, bits, float(eps_bound), dev.ptr(scal), dev.ptr(planes),
+              dev.ptr(luts), None, dev.stream_ptr())
+    sc = dev.to_host(scal)[0]
+    return sc, (dev.to_host(planes).view(np.uint32) if planes is not None else None), (
+        dev.to_host(luts) if luts is not None else None)
+
+
+def _q_hat_from_planes(planes: np.ndarray, dims: int, qb: int) -> np.ndarray:
+    """The quantized query from its two's-complement bit planes (format view)."""
+    bits = np.unpackbits(np.ascontiguousarray(planes).view(np.uint8).reshape(qb, -1), axis=1,
+                         bitorder="little")[:, :dims].astype(np.int32)
+    w = (1 << np.arange(qb, dtype=np.int32))
+    w[-1] = -w[-1]
+    return (w[:, None] * bits).sum(axis=0).astype(np.int32)
+
+
+def _prepare_from_rotated(q_rot: np.ndarray, dims: int, params: SearchParams, eps_bound: float = 0.0) -> QueryState:
+    """QueryState of an already rotated query (search.py:186-214) on the GPU."""
+    q_rot = np.asarray(q_rot, dtype=np.float64)
+    sc, planes, luts = _prepare_one(q_rot, params, eps_bound)
+    st = QueryState(q_rot=q_rot, sum_q=float(sc[_lib.QS_SUM_Q]))
+    if params.ip_mode == "lut":
+        st.luts = luts
+        return st
+    st.delta_q = float(sc[_lib.QS_DELTA])
+    st.planes = planes
+    st.q_hat = _q_hat_from_planes(planes, dims, params.query_bits)
+    st.code_sum_q = float(sc[_lib.QS_CODE_SUM])
+    st.ip_margin = float(sc[_lib.QS_IP_MARGIN])
+    return st
+
+
+def prepare_query(q: np.ndarray, index: IvfRabitqIndex, params: SearchParams) -> QueryState:
+    """Rotate one query on the GPU and derive its QueryState (search.py:217-223)."""
+    q = np.asarray(q, dtype=np.float64)
+    if q.shape != (index.dims,):
+        raise ValueError(f"query shape {q.shape} != ({index.dims},)")
+    qd = dev.to_device(np.ascontiguousarray(q[None, :]))
+    q_rot = dev.to_host(rotate_queries_device(qd, index))[0]
+    return _prepare_from_rotated(q_rot, index.dims, params, index.eps_bound)
+
+
+def build_luts(q_rot: np.ndarray, block: int = _LUT_BLOCK) -> np.ndarray:
+    """Per-query lookup tables ``L[j][key]`` over 4-dim blocks, float32 (search.py:115-132)."""
+    if block != _LUT_BLOCK:
+        raise ValueError(f"the packed-nibble layout uses {_LUT_BLOCK}-dim blocks, got block={block}")
+    q = np.asarray(q_rot, dtype=np.float64).ravel()
+    if q.size == 0:
+        return np.zeros((1, 16), dtype=np.float32)
+    _, _, luts = _prepare_one(q, SearchParams(k=1, n_probe=1, ip_mode="lut"), 0.0)
+    return luts
+
+
+def nibbles_from_bits(bits_matrix: np.ndarray) -> np.ndarray:
+    """(n, dims) 0/1 rows -> (n, blocks) 4-dim nibble keys, zero padded (search.py:135-143; format view)."""
+    m = np.atleast_2d(np.asarray(bits_matrix, dtype=np.uint8))
+    n, dims = m.shape
+    padded_dims = ((dims + 31) // 32) * 32 if dims % 32 else dims
+    buf = np.zeros((n, max(padded_dims, _LUT_BLOCK)), dtype=np.uint8)
+    buf[:, :dims] = m
+    return (buf.reshape(n, -1, _LUT_BLOCK) @ (1 << np.arange(_LUT_BLOCK)).astype(np.uint8)).astype(np.uint8)
+
+
+def ip_lut(nibbles: np.ndarray, luts: np.ndarray):
+    """Binary code x real query via table lookups (search.py:146-160); float64."""
+    nib = np.asarray(nibbles)
+    single = nib.ndim == 1
+    nib2 = np.ascontiguousarray(np.atleast_2d(nib).astype(np.uint8))
+    luts = np.ascontiguousarray(np.asarray(luts, dtype=np.float32))
+    blocks = luts.shape[0]
+    if nib2.shape[1] != blocks:
+        raise ValueError(f"nibble count {nib2.shape[1]} != table count {blocks}")
+    n = nib2.shape[0]
+    out = dev.empty(n, torch.float64)
+    nd, ld = dev.to_device(nib2), dev.to_device(luts)  # alive until the launch is queued
+    _lib.call("ivrq_ip_lut", dev.ptr(nd), n, blocks, dev.ptr(ld), dev.ptr(out), dev.stream_ptr())
+    res = dev.to_host(out)
+    return float(res[0]) if single else res
+
+
+def ip_bitwise(words: np.ndarray, planes: np.ndarray, query_bits: int):
+    """Binary code x quantized query via AND + popcount (search.py:163-183); exact int."""
+    w = np.asarray(words, dtype=np.uint32)
+    single = w.ndim == 1
+    w2 = w[:, None] if single else w
+    planes = np.asarray(planes, dtype=np.uint32)
+    if planes.shape != (query_bits, w2.shape[0]):
+        raise ValueError(f"planes shape {planes.shape} != ({query_bits}, {w2.shape[0]})")
+    groups, n = w2.shape
+    out = dev.empty(n, torch.int64)
+    wd, pd = dev.to_device(np.ascontiguousarray(w2)), dev.to_device(np.ascontiguousarray(planes))
+    _lib.call("ivrq_ip_bitwise", dev.ptr(wd), groups, n, dev.ptr(pd), query_bits, dev.ptr(out), dev.stream_ptr())
+    res = dev.to_host(out)
+    return int(res[0]) if single else res
+
+
+def _short_cols(sf) -> np.ndarray:
+    from paper_2602_23999_b200.codec import ShortFactors
+
+    if isinstance(sf, ShortFactors):
+        return np.array([sf.add, sf.scale, sf.err], dtype=np.float64)
+    return np.asarray(sf, dtype=np.float64)
+
+
+def _long_cols(lf) -> np.ndarray:
+    from paper_2602_23999_b200.codec import LongFactors
+
+    if isinstance(lf, LongFactors):
+        return np.array([lf.add, lf.scale], dtype=np.float64)
+    return np.asarray(lf, dtype=np.float64)
+
+
+def estimate_stage1(ip_binary, sf, state: QueryState, d_qc2):
+    """1-bit estimate and pruning lower bound, both clamped at 0 (search.py:270-287)."""
+    cols = _short_cols(sf)
+    ip = np.asarray(ip_binary, dtype=np.float64)
+    dq = np.asarray(d_qc2, dtype=np.float64)
+    shape = np.broadcast_shapes(ip.shape, cols.shape[:-1], dq.shape)
+    n = int(np.prod(shape, dtype=np.int64))
+    ipb = np.ascontiguousarray(np.broadcast_to(ip, shape).reshape(n))
+    sfb = np.ascontiguousarray(np.broadcast_to(cols, shape + (3,)).reshape(n, 3))
+    dqb = np.ascontiguousarray(np.broadcast_to(dq, shape).reshape(n))
+    est = dev.empty(n, torch.float64)
+    lb = dev.empty(n, torch.float64)
+    ipd, sfd, dqd = dev.to_device(ipb), dev.to_device(sfb), dev.to_device(dqb)
+    _lib.call("ivrq_estimate_stage1", dev.ptr(ipd), dev.ptr(sfd), n,
+              dev.ptr(dqd), float(state.code_sum_q), float(state.ip_margin or 0.0), dev.ptr(est),
+              dev.ptr(lb), dev.stream_ptr())
+    e, lo = dev.to_host(est).reshape(shape), dev.to_host(lb).reshape(shape)
+    if shape == ():
+        return np.float64(e), np.float64(lo)
+    return e, lo
+
+
+def refine_stage2(excode, ip_binary, lf, state: QueryState, d_qc2, bits: int):
+    """Refined estimate from the full code, clamped at 0 (search.py:290-310)."""
+    if bits < 2:
+        raise ValueError("refinement requires bits >= 2 (no ex-code exists for 1-bit indexes)")
+    ex = np.ascontiguousarray(np.atleast_2d(np.asarray(excode, dtype=np.float64)))
+    n, d = ex.shape
+    ipb = np.ascontiguousarray(np.broadcast_to(np.asarray(ip_binary, dtype=np.float64), (n,)))
+    lfb = np.ascontiguousarray(np.broadcast_to(_long_cols(lf), (n, 2)))
+    dqb = np.ascontiguousarray(np.broadcast_to(np.asarray(d_qc2, dtype=np.float64), (n,)))
+    q = np.ascontiguousarray(np.asarray(state.q_rot, dtype=np.float64))
+    out = dev.empty(n, torch.float64)
+    exd, ipd, lfd, qd, dqd = (dev.to_device(a) for a in (ex, ipb, lfb, q, dqb))
+    _lib.call("ivrq_refine_stage2", dev.ptr(exd), n, d, dev.ptr(ipd), dev.ptr(lfd), dev.ptr(qd), float(state.sum_q),
+              dev.ptr(dqd), bits, dev.ptr(out), dev.stream_ptr())
+    res = dev.to_host(out)
+    if np.asarray(excode).ndim == 1:
+        return float(res[0])
+    return res
+
+
+def cluster_local_search(
+    state: QueryState,
+    index: IvfRabitqIndex,
+    cluster: int,
+    params: SearchParams,
+    threshold: float = math.inf,
+    d_qc2: float | None = None,
+) -> tuple[np.ndarray, np.ndarray]:
+    """One query, one cluster: stage 1, prune, refine, local top-K by (dist, id) (search.py:326-375)."""
+    lo, hi = index.cluster_range(cluster)
+    n_c = hi - lo
+    if n_c == 0:
+        return np.empty(0, dtype=np.int64), np.empty(0, dtype=np.float64)
+    device = dev.require_cuda()
+    bitwise = params.ip_mode == "bitwise"
+    q = dev.to_device(np.ascontiguousarray(np.asarray(state.q_rot, dtype=np.float64)), device)
+    planes = dev.to_device(np.ascontiguousarray(state.planes, dtype=np.uint32), device) if bitwise else None
+    luts = None if bitwise else dev.to_device(np.ascontiguousarray(state.luts, dtype=np.float32), device)
+    if (planes if bitwise else luts) is None:
+        raise ValueError(f"the query state has no {'planes' if bitwise else 'tables'} for ip_mode={params.ip_mode!r}")
+    import ctypes
+
+    sc = (ctypes.c_double * _lib.QS_COUNT)(*state.scalars().tolist())  # host scalars
+    dq = ctypes.byref(ctypes.c_double(float(d_qc2))) if d_qc2 is not None else None
+    k = params.k
+    out_i = torch.empty(k, dtype=torch.int64, device=device)
+    out_d = torch.empty(k, dtype=torch.float64, device=device)
+    cnt = torch.zeros(1, dtype=torch.int32, device=device)
+    ws_bytes = int(_lib.load().ivrq_cluster_local_search_workspace(n_c))
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=device)
+    _lib.call("ivrq_cluster_local_search", index.view(), int(cluster), dev.ptr(q), dev.ptr(planes), dev.ptr(luts),
+              sc, params.to_c(), float(threshold), dq, dev.ptr(out_i), dev.ptr(out_d),
+              dev.ptr(cnt), dev.ptr(ws), ws_bytes, n_c, dev.stream_ptr())
+    m = int(cnt.item())
+    return dev.to_host(out_i[:m]).copy(), dev.to_host(out_d[:m]).copy()
+
+
 def _probe_device(q_rot: torch.Tensor, cent: torch.Tensor, c_sq: torch.Tensor, n_probe: int, order_by_id: bool):
     nq, d = q_rot.shape
     nlist = cent.shape[0]
@@ -111,12 +363,21 @@ def select_clusters(q_rot: np.ndarray, centroids: Centroids, n_probe: int) -> tu
         raise ValueError(f"n_probe={n_probe} exceeds {centroids.n_clusters} clusters")
     vals = np.asarray(centroids.values)
     v32 = vals.astype(np.float32)
-    if vals.dtype != np.float32 and not np.array_equal(v32.astype(vals.dtype), vals):
-        raise ValueError("select_clusters on the GPU takes float32-representable centroids")
     qd = dev.to_device(q)
-    cd = dev.to_device(v32)
     csq = dev.to_device(np.asarray(centroids.squared_norms, dtype=np.float64))
-    ids, d2 = _probe_device(qd, cd, csq, n_probe, order_by_id=False)
+    if vals.dtype == np.float32 or np.array_equal(v32.astype(vals.dtype), vals):
+        ids, d2 = _probe_device(qd, dev.to_device(v32), csq, n_probe, order_by_id=False)
+        return dev.to_host(ids), dev.to_host(d2)
+    # float64 centroids (e.g. train_kmeans output): the float64 GEMM probe
+    cd = dev.to_device(np.ascontiguousarray(vals, dtype=np.float64))
+    nq, d = q.shape
+    ncl = cd.shape[0]
+    ids = torch.empty((nq, n_probe), dtype=torch.int64, device=qd.device)
+    d2 = torch.empty((nq, n_probe), dtype=torch.float64, device=qd.device)
+    ws_bytes = int(_lib.load().ivrq_select_clusters_workspace(nq, ncl))
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=qd.device)
+    _lib.call("ivrq_select_clusters_f64", dev.ptr(qd), nq, d, dev.ptr(cd), dev.ptr(csq), ncl, n_probe, 0,
+              dev.ptr(ids), dev.ptr(d2), dev.ptr(ws), ws_bytes, dev.stream_ptr())
     return dev.to_host(ids), dev.to_host(d2)
 
 

@@ -12,7 +12,9 @@ ROOT = Path(__file__).resolve().parents[1]
 GOLDEN = ROOT / "tests" / "golden"
 sys.path.insert(0, str(ROOT))
 
-CASE_NAMES = ["b1_d32", "b4_d48", "b8_d128", "b3_d96", "b2_dup", "b6_d20"]
+CASE_NAMES = ["b1_d32", "b4_d48", "b8_d128", "b3_d96", "b2_dup", "b6_d20", "b8_d768", "b4_d1536", "b4_d96_l512"]
+# the headline-shape cases (D = 768 / 1536, nlist 512); slower on the CPU oracle
+BIG_CASES = {"b8_d768", "b4_d1536", "b4_d96_l512"}
 
 # must match SEARCHES in tests/golden/gen_golden.py
 SEARCHES = [
@@ -22,6 +24,8 @@ SEARCHES = [
     dict(k=7, n_probe=3, ip_mode="bitwise", query_bits=2, refine=False, prune=True),
     dict(k=10, n_probe=4, ip_mode="bitwise", query_bits=4, refine=True, prune=False),
     dict(k=40, n_probe=1, ip_mode="lut", query_bits=4, refine=True, prune=True),
+    dict(k=10, n_probe=16, ip_mode="bitwise", query_bits=4, refine=True, prune=True),
+    dict(k=10, n_probe=32, ip_mode="lut", query_bits=4, refine=True, prune=True),
 ]
 
 
@@ -31,7 +35,17 @@ def pytest_configure(config):
 
 def load_case(name: str) -> dict:
     with np.load(GOLDEN / f"{name}.npz") as z:
-        return {k: z[k] for k in z.files}
+        g = {k: z[k] for k in z.files}
+    if "x" not in g:  # seeded mixture, regenerated (tests/golden/datagen.py)
+        sys.path.insert(0, str(GOLDEN))
+        from datagen import mix_data
+
+        kind, n, nq, dims, seed = (str(v) for v in g["gen"])
+        assert kind == "mix"
+        x, q = mix_data(int(n), int(nq), int(dims), int(seed))
+        assert np.array_equal(q, g["queries"]), "regenerated queries differ from the stored ones"
+        g["x"] = x
+    return g
 
 
 def case_params(g: dict) -> dict:

@@ -23,6 +23,9 @@ import numpy as np
 
 HERE = Path(__file__).resolve().parent
 REF_TESTS = Path("/root/reference/pkg/tests")
+sys.path.insert(0, str(HERE))
+
+from datagen import mix_data  # noqa: E402
 
 import ivfrabitq  # noqa: E402  (the reference)
 from ivfrabitq import clustering as rc  # noqa: E402
@@ -47,6 +50,15 @@ CASES = [
     dict(name="b3_d96", gen="blobs", n=1600, nq=48, dims=96, nlist=10, bits=3, iters=5, tf=1.0, seed=7),
     dict(name="b2_dup", gen="dup", n=40, nq=8, dims=8, nlist=3, bits=2, iters=3, tf=1.0, seed=0),
     dict(name="b6_d20", gen="gauss", n=900, nq=32, dims=20, nlist=7, bits=6, iters=4, tf=0.7, seed=11),
+    # headline shapes (BASELINE.json C3 / C5 / C4), small n.  "mix" data is regenerated from its seed
+    # at test time (tests/golden/datagen.py), so x is not stored.
+    # D = 768, 8-bit: tcgen05 stage 1 (g = 24) and the 6-chunk tcgen05 dense refine, ~128 queries
+    # per list (several refine groups per list, several 128-row tiles per list)
+    dict(name="b8_d768", gen="mix", n=3000, nq=256, dims=768, nlist=8, bits=8, iters=4, tf=1.0, seed=21),
+    # D = 1536, 4-bit: tcgen05 stage 1 (g = 48) + the warp-per-query survivor refine on nibble codes
+    dict(name="b4_d1536", gen="mix", n=1500, nq=128, dims=1536, nlist=4, bits=4, iters=3, tf=1.0, seed=22),
+    # D = 96, nlist 512: many short lists, the tensor-core probe at n_probe 16 / 32
+    dict(name="b4_d96_l512", gen="mix", n=12000, nq=160, dims=96, nlist=512, bits=4, iters=3, tf=0.5, seed=23),
 ]
 
 SEARCHES = [
@@ -56,12 +68,16 @@ SEARCHES = [
     dict(k=7, n_probe=3, ip_mode="bitwise", query_bits=2, refine=False, prune=True),
     dict(k=10, n_probe=4, ip_mode="bitwise", query_bits=4, refine=True, prune=False),
     dict(k=40, n_probe=1, ip_mode="lut", query_bits=4, refine=True, prune=True),
+    dict(k=10, n_probe=16, ip_mode="bitwise", query_bits=4, refine=True, prune=True),
+    dict(k=10, n_probe=32, ip_mode="lut", query_bits=4, refine=True, prune=True),
 ]
 
 
 def _data(case, make_dataset):
     rng = np.random.default_rng(1000 + case["seed"])
     n, nq, d = case["n"], case["nq"], case["dims"]
+    if case["gen"] == "mix":
+        return mix_data(n, nq, d, case["seed"])
     if case["gen"] == "blobs":
         base, queries = make_dataset(n_base=n, n_queries=nq, dims=d, n_blobs=8, seed=20260810 + case["seed"])
         return base, queries.astype(np.float64)
@@ -125,9 +141,74 @@ def _stage_build(x, params):
     )
 
 
+def gen_subops(indexes: dict) -> None:
+    """Reference outputs of the per-call sub-operators (search.py:84-375, codec.py:118-151, 262-303, 322-401)."""
+    rng = np.random.default_rng(77)
+    out = {}
+    # quantize_oracle: small vectors, every width the enumeration guard admits
+    qo = []
+    for i, (dims, bits) in enumerate([(d, b) for d in (1, 3, 5, 8, 12, 31) for b in (1, 2, 3, 4, 6)]):
+        if dims * 2 ** (bits - 1) > rcodec._ORACLE_MAX_FACTORS:
+            continue
+        for j in range(4):
+            o = rng.standard_normal(dims)
+            if j == 1:
+                o[rng.integers(0, dims)] = 0.0  # a zero coordinate (u_zero)
+            if j == 3:
+                o = np.round(o * 2) / 2  # exact ties between coordinates
+            nrm = np.linalg.norm(o)
+            o = o / nrm if nrm > 0 else o
+            out[f"qo{len(qo)}_o"] = o
+            out[f"qo{len(qo)}_u"] = rcodec.quantize_oracle(o, bits)
+            qo.append(bits)
+    out["qo_bits"] = np.array(qo, dtype=np.int64)
+    # compute_factors_batch
+    for bits in (1, 4, 7):
+        n, dims = 40, 24
+        o = rng.standard_normal((n, dims))
+        o /= np.linalg.norm(o, axis=1)[:, None]
+        u, _ = rcodec.quantize_batch(o, rcodec.QuantizationParams(bits=bits))
+        dd = rng.uniform(0.0, 3.0, n)
+        dd[3] = 0.0
+        c = rng.standard_normal((n, dims))
+        sh, lg, lowq = rcodec.compute_factors_batch(u, o, dd, c, rcodec.QuantizationParams(bits=bits))
+        out.update({f"cf{bits}_u": u, f"cf{bits}_o": o, f"cf{bits}_d": dd, f"cf{bits}_c": c,
+                    f"cf{bits}_short": sh, f"cf{bits}_long": lg, f"cf{bits}_lowq": lowq})
+    # normalize_residuals (einsum order: host independent)
+    x = rng.standard_normal((30, 20))
+    c = rng.standard_normal((30, 20))
+    c[4] = x[4]
+    o, dd = rcodec.normalize_residuals(x, c)
+    out.update(nr_x=x, nr_c=c, nr_o=o, nr_d=dd)
+    # cluster_local_search on two golden indexes, both ip modes, open and finite thresholds
+    for name, (idx, queries) in indexes.items():
+        for mode in ("bitwise", "lut"):
+            sp = rs.SearchParams(k=7, n_probe=1, ip_mode=mode)
+            for qi in range(3):
+                st = rs.prepare_query(np.asarray(queries[qi], dtype=np.float64), idx, sp)
+                for cl in range(idx.n_clusters):
+                    for ti, thr in enumerate((math.inf, None)):
+                        if thr is None:  # a threshold that prunes part of the list
+                            ids0, d0 = rs.cluster_local_search(st, idx, cl, rs.SearchParams(k=1000, n_probe=1,
+                                                                                           ip_mode=mode))
+                            thr = float(np.median(d0)) if d0.size else 0.0
+                        ids, dists = rs.cluster_local_search(st, idx, cl, sp, thr)
+                        key = f"cls_{name}_{mode}_{qi}_{cl}_{ti}"
+                        out[key + "_thr"] = np.float64(thr)
+                        out[key + "_ids"] = ids
+                        out[key + "_dists"] = dists
+                out[f"cls_{name}_{mode}_{qi}_qrot"] = st.q_rot
+    np.savez_compressed(HERE / "subops.npz", **out)
+    print("subops ok", (HERE / "subops.npz").stat().st_size, "bytes")
+
+
 def main() -> None:
     make_dataset = _make_dataset()
+    only = set(sys.argv[1:])
+    sub_indexes = {}
     for case in CASES:
+        if only and case["name"] not in only and "subops" not in only:
+            continue
         x, queries = _data(case, make_dataset)
         params = rindex.BuildParams(
             n_clusters=case["nlist"],
@@ -137,11 +218,14 @@ def main() -> None:
             seed=case["seed"],
         )
         idx = rindex.build_index(x, params)
+        if case["name"] in ("b4_d48", "b8_d128"):
+            sub_indexes[case["name"]] = (idx, queries)
+        if only and case["name"] not in only:
+            continue
         st = _stage_build(x, params)
         # the staged pipeline must reproduce build_index bit for bit
         assert np.array_equal(st["order"].astype(np.uint64), idx.pids)
         out = {
-            "x": x,
             "queries": queries,
             "params": np.array(
                 [case["nlist"], case["bits"], case["iters"], case["seed"]], dtype=np.int64
@@ -158,6 +242,9 @@ def main() -> None:
             "long_factors": idx.long_factors,
             "pids": idx.pids,
         }
+        if case["gen"] != "mix":
+            out["x"] = x
+        out["gen"] = np.array([case["gen"], str(case["n"]), str(case["nq"]), str(case["dims"]), str(case["seed"])])
         for key, val in st.items():
             out["stage_" + key] = val
         q64 = np.ascontiguousarray(queries, dtype=np.float64)
@@ -196,10 +283,12 @@ def main() -> None:
             out[f"s{si}_qstate"] = scal
             if planes:
                 out[f"s{si}_planes"] = np.stack(planes)
-            if luts:
-                out[f"s{si}_luts"] = np.stack(luts)
+            if luts:  # 16 queries' tables are enough to pin build_luts (they dominate the fixture size)
+                out[f"s{si}_luts"] = np.stack(luts[:16])
         np.savez_compressed(HERE / f"{case['name']}.npz", **out)
         print(case["name"], "ok", (HERE / f"{case['name']}.npz").stat().st_size, "bytes")
+    if not only or "subops" in only:
+        gen_subops(sub_indexes)
     # known-answer vectors for the reduction orders (host-independent NumPy semantics)
     rng = np.random.default_rng(5)
     red = {}

@@ -198,3 +198,63 @@ def test_index_views_match_oracle_decode():
     lo, hi = ix.cluster_range(0)
     assert ix.cluster_words(0).shape == (ix.words_per_vector, hi - lo)
     assert ix.msb_nibbles.shape == (ix.size, 8 * ix.words_per_vector)
+
+
+# ---------------------------------------------------------------- drop-in API surface
+
+# the reference's public names (reference pkg/src/ivfrabitq/__init__.py:57-101)
+REFERENCE_ALL = [
+    "Centroids", "assign", "train_kmeans", "LongFactors", "PackedPlane", "QuantizationParams", "ShortFactors",
+    "compute_factors", "normalize_residual", "pack_excodes", "pack_interleaved", "quantize_oracle",
+    "quantize_vector", "split_planes", "unpack_excodes", "unpack_interleaved", "BuildParams", "IndexFormatError",
+    "IvfRabitqIndex", "build_index", "load_index", "save_index", "read_fvecs", "read_ivecs", "write_fvecs",
+    "write_ivecs", "Rotation", "exact_knn", "gen_rotation", "rotate", "QueryState", "SearchParams", "build_luts",
+    "cluster_local_search", "estimate_stage1", "ip_bitwise", "ip_lut", "merge_topk", "prepare_query",
+    "refine_stage2", "schedule_probes", "search_batch", "select_clusters",
+]
+
+
+def test_reference_public_names_all_exported():
+    missing = [n for n in REFERENCE_ALL if not hasattr(iv, n)]
+    assert not missing, missing
+    assert set(REFERENCE_ALL) <= set(iv.__all__)
+
+
+def test_query_state_defaults_follow_reference():
+    st = iv.QueryState(q_rot=np.ones(4), sum_q=4.0)
+    assert st.code_sum_q == 4.0 and st.delta_q == 1.0 and st.threshold == float("inf")
+    assert st.q_hat is None and st.planes is None and st.luts is None
+
+
+def test_nibbles_from_bits_layout():
+    bits = np.zeros((2, 8), dtype=np.uint8)
+    bits[0, 0] = 1
+    bits[1, 4:8] = 1
+    nib = iv.nibbles_from_bits(bits)
+    # 8 dims are padded to one 32-dim word: 8 nibbles per row
+    assert nib.shape == (2, 8)
+    assert nib[0, 0] == 1 and nib[1, 1] == 15 and nib[1, 0] == 0
+
+
+def test_fvecs_ivecs_round_trip_and_errors(tmp_path):
+    x = np.arange(12, dtype=np.float32).reshape(3, 4) / 7.0
+    p = tmp_path / "a.fvecs"
+    iv.write_fvecs(str(p), x)
+    np.testing.assert_array_equal(iv.read_fvecs(str(p)), x)
+    ids = np.arange(6, dtype=np.int32).reshape(2, 3)
+    pi = tmp_path / "a.ivecs"
+    iv.write_ivecs(str(pi), ids)
+    np.testing.assert_array_equal(iv.read_ivecs(str(pi)), ids)
+    # 4 + 4*4 bytes per record: drop the last 4 bytes -> truncated record at the second record's offset
+    raw = p.read_bytes()
+    bad = tmp_path / "bad.fvecs"
+    bad.write_bytes(raw[:-4])
+    with pytest.raises(ValueError, match="truncated record at byte offset 40"):
+        iv.read_fvecs(str(bad))
+    mixed = tmp_path / "mixed.fvecs"
+    mixed.write_bytes(raw[:20] + np.array([3], dtype="<i4").tobytes() + raw[24:])
+    with pytest.raises(ValueError, match="inconsistent dimension 3 at byte offset 20"):
+        iv.read_fvecs(str(mixed))
+    empty = tmp_path / "e.fvecs"
+    empty.write_bytes(b"")
+    assert iv.read_fvecs(str(empty)).shape == (0, 0)
