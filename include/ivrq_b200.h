@@ -315,6 +315,17 @@ IVRQ_API int ivrq_kmeans_reseed(int32_t* labels, double* dmin, int64_t n, int64_
 IVRQ_API int ivrq_kmeans_update(const float* x, int64_t n, const int64_t* order, const int64_t* offsets,
                        int32_t k, int32_t d, double* centers, void* stream);
 
+/* Data-parallel form of the centroid update for ranks that own ascending row blocks:
+ * per cluster c, the sequential sum continues from init_sums[c] (after init_counts[c]
+ * rows of earlier ranks; both NULL on the first rank) over this rank's rows of c
+ * (order/offsets from ivrq_counting_sort of the local labels), so the chain over ranks
+ * reproduces np.add.reduceat's row order exactly.  total_counts NULL: out = running
+ * sums double[k*d], out_counts = running counts (for the next rank); otherwise out =
+ * centres (sum / total_counts[c]). */
+IVRQ_API int ivrq_kmeans_chain_sums(const float* x, const int64_t* order, const int64_t* offsets, int32_t k,
+                                    int32_t d, const double* init_sums, const int64_t* init_counts,
+                                    const int64_t* total_counts, double* out, int64_t* out_counts, void* stream);
+
 /* Residual normalisation + rotation (normalize_residuals codec.py:138-151;
  * index.py:237-238): for output row r, source row s = order[r] and centroid
  * c = labels[s]: diff = x[s] - cent32[c] (float64), dist[r] = sqrt(einsum(diff,diff)),

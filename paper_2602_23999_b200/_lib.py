@@ -127,6 +127,7 @@ _SIGNATURES: dict[str, tuple[object, list[object]]] = {
     "ivrq_counting_sort": (c_int, [P, c_int64, c_int32, P, P, P, P]),
     "ivrq_kmeans_reseed": (c_int, [P, P, c_int64, P, c_int32, P, P]),
     "ivrq_kmeans_update": (c_int, [P, c_int64, P, P, c_int32, c_int32, P, P]),
+    "ivrq_kmeans_chain_sums": (c_int, [P, P, P, c_int32, c_int32, P, P, P, P, P, P]),
     "ivrq_normalize_rotate": (c_int, [P, P, P, P, P, c_int64, c_int32, P, P, P]),
     "ivrq_rotate_rows_f32": (c_int, [P, c_int64, c_int32, P, P, P]),
     "ivrq_encode": (

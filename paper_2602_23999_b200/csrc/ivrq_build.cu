@@ -520,6 +520,29 @@ __global__ void update_kernel(const float* __restrict__ x, int64_t n, const int6
   }
 }
 
+// Chained centroid sums for data-parallel Lloyd (np.add.reduceat over rows in ascending
+// order, clustering.py:108-112, split across ranks that own ascending row blocks): the
+// running per-cluster sum continues from the previous rank's (init_sums, init_counts) over
+// this rank's rows of the cluster, in order.  With total_counts the centres are written
+// (sum / count); otherwise the running sums and counts are handed on.
+__global__ void chain_sums_kernel(const float* __restrict__ x, const int64_t* __restrict__ order,
+                                  const int64_t* __restrict__ offsets, int k, int d,
+                                  const double* __restrict__ init_sums, const int64_t* __restrict__ init_counts,
+                                  const int64_t* __restrict__ total_counts, double* __restrict__ out,
+                                  int64_t* __restrict__ out_counts) {
+  const int c = blockIdx.x;
+  const int64_t s = offsets[c], e = offsets[c + 1];
+  const int64_t before = init_counts ? init_counts[c] : 0;
+  for (int j = threadIdx.x; j < d; j += blockDim.x) {
+    double acc = before > 0 ? init_sums[(int64_t)c * d + j] : 0.0;
+    int64_t r = s;
+    if (before == 0 && r < e) acc = (double)x[order[r++] * d + j];  // reduceat starts from the first row
+    for (; r < e; ++r) acc = dadd(acc, (double)x[order[r] * d + j]);
+    out[(int64_t)c * d + j] = total_counts ? ddiv(acc, (double)total_counts[c]) : acc;
+  }
+  if (threadIdx.x == 0 && out_counts) out_counts[c] = before + (e - s);
+}
+
 // ============================================================ normalise + rotate
 // dist[r] = sqrt(einsum(diff, diff)), diff = x[order[r]] - cent32[labels[order[r]]]
 __global__ void __launch_bounds__(rowchain::THREADS) resid_norm_kernel(const float* __restrict__ x,
@@ -1064,6 +1087,17 @@ extern "C" int ivrq_kmeans_reseed(int32_t* labels, double* dmin, int64_t n, int6
   if (n <= 0 || k < 1) return fail(IVRQ_EINVAL, "ivrq_kmeans_reseed: bad sizes");
   reseed_kernel<<<1, 1024, 0, as_stream(stream)>>>(labels, dmin, n, counts, k, n_empty_out);
   return check_launch("ivrq_kmeans_reseed");
+}
+
+extern "C" int ivrq_kmeans_chain_sums(const float* x, const int64_t* order, const int64_t* offsets, int32_t k,
+                                      int32_t d, const double* init_sums, const int64_t* init_counts,
+                                      const int64_t* total_counts, double* out, int64_t* out_counts, void* stream) {
+  if (k < 1 || d < 1) return fail(IVRQ_EINVAL, "ivrq_kmeans_chain_sums: bad sizes");
+  if ((init_sums == nullptr) != (init_counts == nullptr))
+    return fail(IVRQ_EINVAL, "ivrq_kmeans_chain_sums: init sums and counts go together");
+  chain_sums_kernel<<<k, 128, 0, as_stream(stream)>>>(x, order, offsets, k, d, init_sums, init_counts, total_counts,
+                                                      out, out_counts);
+  return check_launch("ivrq_kmeans_chain_sums");
 }
 
 extern "C" int ivrq_kmeans_update(const float* x, int64_t n, const int64_t* order, const int64_t* offsets, int32_t k,

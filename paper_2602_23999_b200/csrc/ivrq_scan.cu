@@ -1988,6 +1988,17 @@ constexpr int TC_THREADS = 32 * (TC_PROD + 1 + 4);
 constexpr int TCR_EPI = 8;  // tc_refine epilogue warps: 2 per TMEM lane quarter, each half of the group's queries
 constexpr int TCR_THREADS = 32 * (TC_PROD + 1 + TCR_EPI);
 
+#ifdef IVRQ_TC_PROFILE
+// development builds only (-DIVRQ_TC_PROFILE): cycles tc_refine's roles spend waiting, summed over CTAs
+__device__ unsigned long long g_tcr_prof[8];  // 0 MMA wait B, 1 MMA wait accumulator, 2 MMA wait A, 3 MMA total,
+                                              // 4 producer wait empty, 5 epilogue wait full, 6 epilogue busy, 7 tiles
+#define TCR_PROF_T0() const long long _t0 = clock64()
+#define TCR_PROF_ADD(i) atomicAdd(&g_tcr_prof[i], (unsigned long long)(clock64() - _t0))
+#else
+#define TCR_PROF_T0()
+#define TCR_PROF_ADD(i)
+#endif
+
 struct TcArgs {
   CUtensorMap map_a;        // rcodes [N rows x rcode_bytes] (8-bit codes), box 128 B x 128 rows, 128B swizzle
   const int8_t* bslices;    // [nq][nkc][8 rows x 128 B] pre-swizzled digit slices (tc_slices_kernel)
@@ -2081,6 +2092,8 @@ __global__ void __launch_bounds__(TCR_THREADS, 1) tc_refine_kernel(const __grid_
   const uint32_t tbase = *s_taddr;
   const int64_t rb = a.ix.rcode_bytes;
   const uint32_t bq_bytes = (uint32_t)nkc * 1024;  // one query's slices
+  // the two accumulators start at aligned column halves of the allocation
+  const uint32_t acc_stride = tmem_cols(2 * N) / 2;
   uint32_t it_prod = 0, it_mma = 0, tile_mma = 0, tile_epi = 0, grp = 0;
   const int total = a.gpre[a.nlist];
   for (int b = blockIdx.x; b < total; b += gridDim.x, ++grp) {
@@ -2112,9 +2125,15 @@ __global__ void __launch_bounds__(TCR_THREADS, 1) tc_refine_kernel(const __grid_
           for (int t = 0; t < ntile; ++t)
             for (int kc = 0; kc < nkc; ++kc, ++it_prod) {
               const int st = it_prod % NST;
-              tc::mbar_wait(&empty[st], ((it_prod / NST) & 1) ^ 1);
+              {
+                TCR_PROF_T0();
+                tc::mbar_wait(&empty[st], ((it_prod / NST) & 1) ^ 1);
+                TCR_PROF_ADD(4);
+              }
               tc::mbar_expect_tx(&full[st], TCM * TCKC);
-              tc::tma_load_2d(sA + st * TCM * TCKC, &a.map_a, kc * TCKC, (int)(lo + (int64_t)t * TCM), &full[st]);
+              // evict-last: the list's other query groups re-read these rows from L2
+              tc::tma_load_2d_hint(sA + st * TCM * TCKC, &a.map_a, kc * TCKC, (int)(lo + (int64_t)t * TCM), &full[st],
+                                   tc::kL2EvictLast);
             }
         }
       } else {
@@ -2161,30 +2180,53 @@ __global__ void __launch_bounds__(TCR_THREADS, 1) tc_refine_kernel(const __grid_
       // ---- MMA issuer.  N = the group's 8 digit rows per query, rounded to 16 (a list probed by
       // few queries does not pay for a full group)
       const uint32_t idesc = tc::idesc_i8(TCM, 8 * ((nqg + 1) & ~1), false, true);
-      wait1(bfull, grp & 1);
+#ifdef IVRQ_TC_PROFILE
+      const long long _tg = clock64();
+#endif
+      {
+        TCR_PROF_T0();
+        wait1(bfull, grp & 1);
+        if (lane == 0) TCR_PROF_ADD(0);
+      }
       for (int t = 0; t < ntile; ++t, ++tile_mma) {
         const int ab = tile_mma & 1;
-        wait1(&acce[ab], ((tile_mma >> 1) & 1) ^ 1);
+        {
+          TCR_PROF_T0();
+          wait1(&acce[ab], ((tile_mma >> 1) & 1) ^ 1);
+          if (lane == 0) TCR_PROF_ADD(1);
+        }
         tc::fence_after_sync();
         for (int kc = 0; kc < nkc; ++kc, ++it_mma) {
           const int st = it_mma % NST;
-          wait1(&full[st], (it_mma / NST) & 1);
+          {
+            TCR_PROF_T0();
+            wait1(&full[st], (it_mma / NST) & 1);
+            if (lane == 0) TCR_PROF_ADD(2);
+          }
           tc::fence_after_sync();
           if (lane == 0) {
+            TCR_PROF_T0();
             const int ks = min(TCKC, kp - kc * TCKC) / 32;
             for (int s2 = 0; s2 < ks; ++s2) {
               const uint64_t ad = tc::smem_desc_sw128(sA + st * TCM * TCKC + 32 * s2);
               const uint64_t bd = tc::smem_desc_sw128_sbo(sB + kc * 1024 + 32 * s2, bq_bytes);
-              tc::mma_i8(tbase + ab * N, ad, bd, idesc, kc > 0 || s2 > 0);
+              tc::mma_i8(tbase + ab * acc_stride, ad, bd, idesc, kc > 0 || s2 > 0);
             }
             tc::commit(&empty[st]);
             if (kc == nkc - 1) tc::commit(&accf[ab]);
+            TCR_PROF_ADD(5);
           }
           __syncwarp();
         }
       }
       if (lane == 0) tc::commit(bempty);  // sB free once this group's MMAs retire
       __syncwarp();
+#ifdef IVRQ_TC_PROFILE
+      if (lane == 0) {
+        atomicAdd(&g_tcr_prof[3], (unsigned long long)(clock64() - _tg));
+        atomicAdd(&g_tcr_prof[7], (unsigned long long)ntile);
+      }
+#endif
     } else {
       // ---- epilogue: row r of the tile is TMEM lane r (a warp reads lane quarter wid % 4); the two
       // warps of a quarter split the group's queries.  Per-query scalars: lane i holds query j_lo + i.
@@ -2213,9 +2255,12 @@ __global__ void __launch_bounds__(TCR_THREADS, 1) tc_refine_kernel(const __grid_
         if (v < n_c) lf = __ldg(reinterpret_cast<const float2*>(a.ix.long_factors) + lo + v);
         wait1(&accf[ab], (tile_epi >> 1) & 1);
         tc::fence_after_sync();
+#ifdef IVRQ_TC_PROFILE
+        const long long _te = clock64();
+#endif
         for (int j0 = j_lo; j0 < j_hi; j0 += 4) {
           uint32_t d[32];
-          tc::tmem_ld32(tbase + ((uint32_t)(quarter * 32) << 16) + ab * N + 8 * j0, d);
+          tc::tmem_ld32(tbase + ((uint32_t)(quarter * 32) << 16) + ab * acc_stride + 8 * j0, d);
           tc::tmem_ld_wait();
 #pragma unroll
           for (int jj = 0; jj < 4; ++jj) {
@@ -2234,6 +2279,9 @@ __global__ void __launch_bounds__(TCR_THREADS, 1) tc_refine_kernel(const __grid_
             }
           }
         }
+#ifdef IVRQ_TC_PROFILE
+        if (lane == 0 && wid == TC_PROD + 1) atomicAdd(&g_tcr_prof[6], (unsigned long long)(clock64() - _te));
+#endif
         tc::fence_before_sync();
         tc::mbar_arrive(&acce[ab]);
       }
@@ -2608,7 +2656,9 @@ static ScanPolicy scan_policy(const ivrq_index_view& ix, const ivrq_search_param
   // path for 4-bit codes (C2, C4: few survivors, 64-byte rows) and at D = 1536 (C5).
   const int tr = env_flag("IVRQ_TC_REFINE", -1);
   const bool dense = tr >= 0 ? tr != 0 : (!rcode_nibbles(ix.bits) && kpad64(ix.dims) <= 768);
-  sp.rd_path = sp.warp_path && (!refine || (ix.rcodes && dense));
+  // (the epilogue's int32 digit pairs D0 * 128 + D1 stay below 2^31 for kpad <= 960 with 8-bit codes)
+  const bool fits = rcode_nibbles(ix.bits) || kpad64(ix.dims) <= 960;
+  sp.rd_path = sp.warp_path && (!refine || (ix.rcodes && dense && fits));
   sp.first_phase = refine && p.k <= 32 && !chained && env_flag("IVRQ_FIRST_LIST", !sp.warp_path) != 0;
   sp.first_dist = sp.warp_path && !sp.rd_path && refine && !chained && env_flag("IVRQ_FIRST_DIST", 1) != 0;
   // tcgen05 stage 1 for long codes; mma.sync tiles win for short ones (D <= 224)
@@ -2621,6 +2671,12 @@ static ScanPolicy scan_policy(const ivrq_index_view& ix, const ivrq_search_param
 // 2.78 (G = 24, 4 stages), 2.88 (20, 5), 3.19 (16, 6), 3.64 (12, 8))
 static bool tc_refine_shape(int kpad, int& G, int& nst) {
   const size_t cap = 227 * 1024;
+#ifdef TCR_FORCE_G  // development A/B builds only
+  G = TCR_FORCE_G;
+  for (nst = 8; nst >= 2; --nst)
+    if (tc_smem_bytes(kpad, G, nst) <= cap) return true;
+  return false;
+#endif
   for (G = 32; G >= 4; G -= 4) {
     for (nst = 8; nst >= 3; --nst)
       if (tc_smem_bytes(kpad, G, nst) <= cap) return true;
@@ -2890,6 +2946,19 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
             KernelTimer kt("tc_refine_kernel", s);
             scan::tc_refine_kernel<<<(unsigned)sm_count_of_current_device(), scan::TCR_THREADS, tsm, s>>>(ta);
           }
+#ifdef IVRQ_TC_PROFILE
+          {
+            unsigned long long h[8];
+            cudaMemcpyFromSymbolAsync(h, scan::g_tcr_prof, sizeof(h), 0, cudaMemcpyDeviceToHost, s);
+            cudaStreamSynchronize(s);
+            const double tot = (double)h[3];
+            fprintf(stderr, "[tc_refine prof] share of MMA-lane group time: wait B %.3f wait acc %.3f wait A %.3f | "
+                    "producer wait-empty/MMA %.3f | epi wait %.3f busy %.3f (per CTA-warp vs MMA total) tiles %llu\n",
+                    h[0] / tot, h[1] / tot, h[2] / tot, h[4] / tot, h[5] / tot, h[6] / tot, h[7]);
+            static const unsigned long long zero[8] = {};
+            cudaMemcpyToSymbolAsync(scan::g_tcr_prof, zero, sizeof(zero), 0, cudaMemcpyHostToDevice, s);
+          }
+#endif
           return check_launch("ivrq_search_scan(tensor-core refine)");
         };
         a.rdist = rdist;

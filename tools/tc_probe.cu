@@ -44,7 +44,7 @@ __global__ void __launch_bounds__(128) probe(const uint8_t* A, const int8_t* B, 
   const int tid = threadIdx.x, wid = tid >> 5;
   for (int i = tid; i < M * K; i += 128) sa[tc::kmajor_offset(i / K, i % K, M)] = A[i];
   for (int i = tid; i < N * K; i += 128) sb[tc::kmajor_offset(i / K, i % K, N)] = B[i];
-  if (wid == 0) tc::tmem_alloc(&taddr_s, N < 32 ? 32 : N);
+  if (wid == 0) tc::tmem_alloc(&taddr_s, N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : 256);
   if (tid == 0) {
     tc::mbar_init(&bar, 1);
     tc::fence_mbar_init();
@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(128) probe_tma(const __grid_constant__ CUtenso
   __shared__ uint64_t bar, mbar;
   __shared__ uint32_t taddr_s;
   const int tid = threadIdx.x, wid = tid >> 5;
-  if (wid == 0) tc::tmem_alloc(&taddr_s, N < 32 ? 32 : N);
+  if (wid == 0) tc::tmem_alloc(&taddr_s, N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : 256);
   if (tid == 0) {
     tc::mbar_init(&bar, 1);
     tc::mbar_init(&mbar, 1);
@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(128) mma_rate(long long* out, int reps) {
   __shared__ uint32_t taddr_s;
   const int tid = threadIdx.x, wid = tid >> 5;
   for (int i = tid; i < (128 + N) * 128; i += 128) sm[i] = (unsigned char)(i * 7);
-  if (wid == 0) tc::tmem_alloc(&taddr_s, N < 32 ? 32 : N);
+  if (wid == 0) tc::tmem_alloc(&taddr_s, N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : 256);
   if (tid == 0) {
     tc::mbar_init(&bar, 1);
     tc::fence_mbar_init();
@@ -307,7 +307,7 @@ __global__ void __launch_bounds__(128) mma_rate(long long* out, int reps) {
   }
   tc::fence_before_sync();
   __syncthreads();
-  if (wid == 0) tc::tmem_dealloc(taddr_s, N < 32 ? 32 : N);
+  if (wid == 0) tc::tmem_dealloc(taddr_s, N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : 256);
 }
 
 // same, but A cycles through 6 distinct 16 KB stage tiles and B walks 6 distinct 128-byte K chunks
@@ -375,6 +375,67 @@ __global__ void __launch_bounds__(128) mma_rate_stream(long long* out, int reps,
   if (wid == 0) tc::tmem_dealloc(taddr_s, 512);
 }
 
+// MMA rate with the B operand's 8-row atoms spread SBO bytes apart (the refine kernel keeps each
+// query's K chunks together, so one chunk's atoms are nkc KB apart)
+template <int N>
+__global__ void __launch_bounds__(128) mma_rate_sbo(long long* out, int reps, int sbo) {
+  extern __shared__ __align__(1024) unsigned char sm_raw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>(((uintptr_t)sm_raw + 1023) & ~(uintptr_t)1023);
+  unsigned char* sa = sm;            // 3 x 16 KB A stages
+  unsigned char* sb = sm + 3 * 16384;
+  __shared__ uint64_t bar;
+  __shared__ uint32_t taddr_s;
+  const int tid = threadIdx.x, wid = tid >> 5;
+  // pseudo-random operand bytes (rcodes / digit slices look random to the multiplier array)
+  for (int i = tid; i < 3 * 16384 + (N / 8) * sbo; i += 128) {
+    uint32_t h = (uint32_t)i * 2654435761u;
+    h ^= h >> 13;
+    h *= 0x5bd1e995u;
+    sm[i] = (unsigned char)(sbo < 0 ? 0 : (h >> 24));
+  }
+  if (wid == 0) tc::tmem_alloc(&taddr_s, 512);
+  if (tid == 0) {
+    tc::mbar_init(&bar, 1);
+    tc::fence_mbar_init();
+  }
+  tc::fence_smem_async();
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  if (tid == 0) {
+    const uint32_t idesc = tc::idesc_i8(M, N, false, true);
+    const int nkc = sbo / 1024;
+    const long long t0 = clock64();
+    for (int r = 0; r < reps; ++r) {
+      const int kc = r % nkc;
+      for (int s2 = 0; s2 < 4; ++s2)
+        tc::mma_i8(taddr_s + (r & 1) * 256, tc::smem_desc_sw128(sa + (r % 3) * 16384 + 32 * s2),
+                   tc::smem_desc_sw128_sbo(sb + kc * 1024 + 32 * s2, sbo), idesc, r | s2);
+    }
+    tc::commit(&bar);
+    tc::mbar_wait(&bar, 0);
+    out[2 * blockIdx.x + 1] = clock64() - t0;
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (wid == 0) tc::tmem_dealloc(taddr_s, 512);
+}
+
+template <int N>
+void rate_sbo(int sbo) {
+  const int reps = 2000, blocks = 148;
+  long long* d;
+  cudaMalloc(&d, blocks * 16);
+  const int smem = 3 * 16384 + (N / 8) * sbo + 1024;
+  cudaFuncSetAttribute(mma_rate_sbo<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  mma_rate_sbo<N><<<blocks, 128, smem>>>(d, reps, sbo);
+  cudaError_t e = cudaDeviceSynchronize();
+  std::vector<long long> h(2 * blocks);
+  cudaMemcpy(h.data(), d, h.size() * 8, cudaMemcpyDeviceToHost);
+  printf("B atoms %d B apart N=%d: %.1f clk/MMA (%s)\n", sbo, N, h[1] / (4.0 * reps), cudaGetErrorString(e));
+  cudaFree(d);
+}
+
 template <int N>
 void rate_stream(int with_tma) {
   const int reps = 2000, blocks = 148;
@@ -398,7 +459,7 @@ void rate_stream(int with_tma) {
 }
 
 template <int N>
-void rate() {
+double rate() {
   const int reps = 2000, blocks = 148;
   long long* d;
   cudaMalloc(&d, blocks * 16);
@@ -409,9 +470,11 @@ void rate() {
   std::vector<long long> h(2 * blocks);
   cudaMemcpy(h.data(), d, h.size() * 8, cudaMemcpyDeviceToHost);
   const double n_mma = 4.0 * reps;
+  const double mac = 128.0 * N * 32 / (h[1] / n_mma);
   printf("int8 MMA M=128 N=%d K=32: issue %.1f clk/MMA, complete %.1f clk/MMA -> %.0f MAC/clk/SM\n", N,
-         h[0] / n_mma, h[1] / n_mma, 128.0 * N * 32 / (h[1] / n_mma));
+         h[0] / n_mma, h[1] / n_mma, mac);
   cudaFree(d);
+  return mac;
 }
 
 template <int N, int K>
@@ -476,8 +539,26 @@ int main() {
   rate_stream<128>(16);
   rate_stream<128>(2 | 8 | 16);
   rate_stream<64>(0);
+  rate_sbo<224>(1024);
+  rate_sbo<224>(2048);
+  rate_sbo<224>(4096);
+  rate_sbo<224>(6144);
+  rate_sbo<128>(6144);
+  rate_sbo<64>(6144);
+  rate_stream<224>(0);
+  rate_stream<224>(2 | 8 | 16);
   rate<64>();
   rate<128>();
-  rate<256>();
+  rate<224>();
+  const double mac = rate<256>();
+  // dense int8 peak of the part: MAC/clk/SM x 2 x SMs x max SM clock (the resident-operand rate)
+  int dev = 0, sms = 0, khz = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, dev);
+  printf("{\"tops\": %.1f, \"mac_per_clk_per_sm\": %.0f, \"sms\": %d, \"sm_clock_mhz\": %.0f, "
+         "\"how\": \"tools/tc_probe.cu: 148 CTAs x 8000 back-to-back tcgen05.mma.cta_group::1.kind::i8 M=128 N=256 K=32 "
+         "from resident shared-memory operands, clock64 issue-to-commit\"}\n",
+         2.0 * mac * sms * khz * 1e3 / 1e12, mac, sms, khz / 1e3);
   return rc;
 }
