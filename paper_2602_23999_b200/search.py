@@ -19,6 +19,7 @@ threshold trajectory).
 from __future__ import annotations
 
 import math
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -491,16 +492,24 @@ def results_to_lists(res: DeviceResult) -> list[tuple[np.ndarray, np.ndarray]]:
 
 
 # ------------------------------------------------------------------ host pipeline
-_PINNED: dict[tuple[int, str], torch.Tensor] = {}
+_PINNED = threading.local()  # per calling thread: concurrent readers never share staging memory
 
 
 def _pinned(device: torch.device, name: str, nbytes: int) -> torch.Tensor:
-    """A page-locked staging buffer (uint8), grown on demand and kept per device."""
+    """A page-locked staging buffer (uint8), grown on demand, kept per device and per thread.
+
+    The index is immutable and ``search_batch`` may be called from several
+    threads at once (reference index.py:7-8), so each thread stages its queries
+    and results in its own buffers.
+    """
+    bufs = getattr(_PINNED, "bufs", None)
+    if bufs is None:
+        bufs = _PINNED.bufs = {}
     key = (device.index or 0, name)
-    buf = _PINNED.get(key)
+    buf = bufs.get(key)
     if buf is None or buf.numel() < nbytes:
         buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, pin_memory=True)
-        _PINNED[key] = buf
+        bufs[key] = buf
     return buf
 
 
