@@ -16,6 +16,7 @@
 #include <cstdlib>
 #include <functional>
 #include <type_traits>
+#include <vector>
 
 #include "ivrq_common.cuh"
 #include "ivrq_tc.cuh"
@@ -76,8 +77,16 @@ struct Args {
   const int64_t* m_lo;      // [nq * nprobe] first row of the probed list
   const int32_t* m_nc;      // [nq * nprobe] its size, -1 = another shard's list
   const int64_t* m_base;    // [nq * nprobe] (list, query) pair row base in ipbuf / rdist
-  const double* rdist;  // refined distance of every probed (pair, vector) (tc_refine_kernel), or null
-  int rd_prefetch;      // scan_rd_kernel: read every vector's refined distance with its stage-1 inputs
+  // approximate refined distance of every probed (pair, vector) (tc_refine_kernel), or null, and
+  // the per-query radius bounding its distance to the exact value (rd_radius_kernel)
+  const float* rdist;
+  const double* rrad;
+  int32_t* fix_count;        // queries the approximate pass could not certify (rerun exactly), and
+  int32_t* fix_list;         // their ids
+  double* fin_d;             // [nq][32] the approximate pass's queue, for rda_final_kernel
+  int64_t* fin_e;
+  const int32_t* fix_only;   // scan_warp_kernel as the rerun: process only slots < *fix_only_count ...
+  const int32_t* fix_only_count;  // ... of fix_only
 };
 
 __device__ __forceinline__ double dinf() { return __longlong_as_double(0x7ff0000000000000LL); }
@@ -305,17 +314,27 @@ __device__ __forceinline__ void refine_chunk(const Args& a, const QueryCtx& qc, 
 }
 
 // ------------------------------------------------------------ warp top-32 queues
-__device__ __forceinline__ void cmpx(double& d, int64_t& id, int stride, bool take_min) {
+// (dist, id) queues in the 32 lanes of a warp.  `Less` orders two (dist, id) keys: key_less on
+// pids for the exact passes, the row-entry order (EntryLess) for the approximate pass.
+struct PidLess {
+  __device__ __forceinline__ bool operator()(double da, int64_t ia, double db, int64_t ib) const {
+    return key_less(da, ia, db, ib);
+  }
+};
+
+template <class Less>
+__device__ __forceinline__ void cmpx(double& d, int64_t& id, int stride, bool take_min, const Less& lt) {
   const double od = __shfl_xor_sync(FULL, d, stride);
   const int64_t oi = __shfl_xor_sync(FULL, id, stride);
-  const bool other_less = key_less(od, oi, d, id);
-  if (take_min ? other_less : key_less(d, id, od, oi)) {
+  const bool other_less = lt(od, oi, d, id);
+  if (take_min ? other_less : lt(d, id, od, oi)) {
     d = od;
     id = oi;
   }
 }
 
-__device__ __forceinline__ void warp_sort32(double& d, int64_t& id) {
+template <class Less = PidLess>
+__device__ __forceinline__ void warp_sort32(double& d, int64_t& id, const Less& lt = Less()) {
   const int lane = threadIdx.x & 31;
 #pragma unroll
   for (int size = 2; size <= 32; size <<= 1) {
@@ -323,28 +342,33 @@ __device__ __forceinline__ void warp_sort32(double& d, int64_t& id) {
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
       const bool up = (lane & size) == 0;
       const bool lower = (lane & stride) == 0;
-      cmpx(d, id, stride, lower == up);
+      cmpx(d, id, stride, lower == up, lt);
     }
   }
 }
 
 // q (sorted ascending) := 32 smallest of q ∪ b (b sorted ascending), sorted.
-__device__ __forceinline__ void warp_merge32(double& qd, int64_t& qi, double bd, int64_t bi) {
+template <class Less = PidLess>
+__device__ __forceinline__ void warp_merge32(double& qd, int64_t& qi, double bd, int64_t bi, const Less& lt = Less()) {
   const int lane = threadIdx.x & 31;
   const double rd = __shfl_sync(FULL, bd, 31 - lane);
   const int64_t ri = __shfl_sync(FULL, bi, 31 - lane);
-  if (key_less(rd, ri, qd, qi)) {
+  if (lt(rd, ri, qd, qi)) {
     qd = rd;
     qi = ri;
   }
 #pragma unroll
-  for (int stride = 16; stride > 0; stride >>= 1) cmpx(qd, qi, stride, (lane & stride) == 0);
+  for (int stride = 16; stride > 0; stride >>= 1) cmpx(qd, qi, stride, (lane & stride) == 0, lt);
 }
 
 // Fold this warp's candidates (d, id) where `pass` into the sorted queue.
 // Few passers: insert one at a time (position by ballot, shift by shfl_up);
-// many (a filling queue): sort the batch and merge.
-__device__ __forceinline__ void warp_fold(double& qd, int64_t& qi, double d, int64_t id, bool pass, int k) {
+// many (a filling queue): sort the batch and merge.  An insertion past the
+// k-th entry is skipped (the exact passes keep only the top k); the
+// approximate pass folds with k = 32 to keep the 32 smallest.
+template <class Less = PidLess>
+__device__ __forceinline__ void warp_fold(double& qd, int64_t& qi, double d, int64_t id, bool pass, int k,
+                                          const Less& lt = Less()) {
   const int lane = threadIdx.x & 31;
   unsigned m = __ballot_sync(FULL, pass);
   if (__popc(m) > 6) {
@@ -352,8 +376,8 @@ __device__ __forceinline__ void warp_fold(double& qd, int64_t& qi, double d, int
       d = dinf();
       id = NO_ID;
     }
-    warp_sort32(d, id);
-    warp_merge32(qd, qi, d, id);
+    warp_sort32(d, id, lt);
+    warp_merge32(qd, qi, d, id, lt);
     return;
   }
   while (m) {
@@ -363,8 +387,8 @@ __device__ __forceinline__ void warp_fold(double& qd, int64_t& qi, double d, int
     const int64_t xi = __shfl_sync(FULL, id, src);
     const double kd = __shfl_sync(FULL, qd, k - 1);
     const int64_t ki = __shfl_sync(FULL, qi, k - 1);
-    if (!key_less(xd, xi, kd, ki)) continue;  // the queue moved on
-    const int pos = __popc(__ballot_sync(FULL, key_less(qd, qi, xd, xi)));
+    if (!lt(xd, xi, kd, ki)) continue;  // the queue moved on
+    const int pos = __popc(__ballot_sync(FULL, lt(qd, qi, xd, xi)));
     const double ud = __shfl_up_sync(FULL, qd, 1);
     const int64_t ui = __shfl_up_sync(FULL, qi, 1);
     if (lane > pos) {
@@ -793,7 +817,9 @@ __global__ void __launch_bounds__(WQ * 32, MINB) scan_warp_kernel(Args a) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t slot_q = (int64_t)blockIdx.x * WQ + wid;
   if (slot_q >= a.nq) return;  // whole warps only: nothing below synchronises the block
-  const int64_t q = a.qorder ? a.qorder[slot_q] : slot_q;
+  // as the exact rerun of queries the approximate pass listed: only slots < *fix_only_count
+  if (a.fix_only && slot_q >= *a.fix_only_count) return;
+  const int64_t q = a.fix_only ? (int64_t)a.fix_only[slot_q] : a.qorder ? a.qorder[slot_q] : slot_q;
   const int k = a.k, kp = a.kpad;
   const size_t per = ((REFINE ? (size_t)SLICES * (kp + SPAD) : 0) + RING * sizeof(int32_t) + 15) & ~size_t(15);
   unsigned char* wbase = smem + wid * per;
@@ -961,15 +987,31 @@ __global__ void __launch_bounds__(WQ * 32, MINB) scan_warp_kernel(Args a) {
   }
 }
 
-// ------------------------------------------------------------ per-query pass over precomputed distances
-// With the refined distance of every probed (pair, vector) in rdist
-// (tc_refine_kernel) and the stage-1 inner products in ipbuf, a query's pass
-// is a stream: per list in ascending id, the stage-1 estimate and prune
-// (same test as stage1_chunk), then its survivors' refined distances offered
-// to the warp's register queue (the pool).  No shared memory, few registers.
+// ------------------------------------------------------------ per-query passes over precomputed stage-1 inputs
+// With the stage-1 inner products of every probed (pair, vector) in ipbuf
+// (tc_ip_kernel / ip_list_kernel), a query's pass is a stream: per list in
+// ascending id, the stage-1 estimate and prune (same test as stage1_chunk),
+// then its survivors offered to the warp's register queue (the pool).
 constexpr int RDW = 4;    // queries (warps) per CTA
 
-template <bool REFINE, int IPB, int RSUB, int MINB = 1>
+// The float64 prune test lb2 <= T of stage1_chunk for one vector (est2 already computed).
+__device__ __forceinline__ bool stage1_keep64(double est2, double err, double scale, double sq, double ipm, double T) {
+  if (est2 <= T) return true;  // lb2 <= est2 <= T
+  const double margin = dmul(err, sq);
+  if (ipm != 0.0) {  // same decision as stage1_chunk
+    const double sm = dmul(scale, ipm);
+    const double S = dadd(dmul(margin, margin), dmul(sm, sm));
+    const double gap = dsub(est2, T);
+    const double g2 = dmul(gap, gap);
+    if (S >= g2 * (1.0 + 0x1p-38)) return true;
+    if (S <= g2 * (1.0 - 0x1p-38) && gap > T * 0x1p-12) return false;
+    return dmax(dsub(est2, dsqrt(S)), 0.0) <= T;
+  }
+  return dmax(dsub(est2, margin), 0.0) <= T;
+}
+
+// 1-bit indexes: the stage-1 estimate is the distance (search.py:362-366); no refine.
+template <int IPB, int RSUB, int MINB = 1>
 __global__ void __launch_bounds__(RDW * 32, MINB) scan_rd_kernel(Args a) {
   using IPT = typename std::conditional<IPB == 2, int16_t, int32_t>::type;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -993,94 +1035,35 @@ __global__ void __launch_bounds__(RDW * 32, MINB) scan_rd_kernel(Args a) {
     const double d_qc2 = cur.d2;
     const double T_list = a.prune ? T : dinf();
     probed += n_c;
-    const int64_t rowbase = cur.base;
-    const double* rrow = REFINE ? a.rdist + rowbase : nullptr;
-    if (REFINE && T_list == dinf()) {  // nothing can be pruned (lb2 <= +inf): every vector's refined distance
-      surv += n_c;
-      for (int64_t c0 = 0; c0 < n_c; c0 += 32 * RSUB) {
-        double dv[RSUB];
+    const IPT* iprow = reinterpret_cast<const IPT*>(a.ipbuf) + cur.base;
+    const double sq = dsqrt(d_qc2);
+    for (int64_t c0 = 0; c0 < n_c; c0 += 32 * RSUB) {
+      int ipv[RSUB];
+      float fa[RSUB], fs[RSUB], fe[RSUB];
 #pragma unroll
-        for (int u = 0; u < RSUB; ++u) {
-          const int64_t vi = c0 + u * 32 + lane;
-          dv[u] = vi < n_c ? __ldg(rrow + vi) : dinf();
-        }
-#pragma unroll
-        for (int u = 0; u < RSUB; ++u) {
-          const int64_t vi = c0 + u * 32 + lane;
-          if (c0 + u * 32 >= n_c) break;  // warp-uniform
-          warp_offer(a, qd, qi, dv[u], vi < n_c ? (int)vi : -1, lo, k);
-        }
+      for (int u = 0; u < RSUB; ++u) {
+        const int64_t vi = c0 + u * 32 + lane;
+        const bool in = vi < n_c;
+        ipv[u] = in ? (int)__ldg(iprow + vi) : 0;
+        fa[u] = in ? __ldg(a.ix.short_add + lo + vi) : 0.f;
+        fs[u] = in ? __ldg(a.ix.short_scale + lo + vi) : 0.f;
+        fe[u] = in ? __ldg(a.ix.short_err + lo + vi) : 0.f;
       }
-    } else {
-      const IPT* iprow = reinterpret_cast<const IPT*>(a.ipbuf) + rowbase;
-      const double sq = dsqrt(d_qc2);
-      const Stage1F32 f32 = stage1_f32(delta, half_code, ipm, d_qc2, sq, T_list);
-      for (int64_t c0 = 0; c0 < n_c; c0 += 32 * RSUB) {
-        int ipv[RSUB];
-        float fa[RSUB], fs[RSUB], fe[RSUB];
-        double pre[RSUB];  // refined distances fetched with the stage-1 inputs (one round trip per batch)
 #pragma unroll
-        for (int u = 0; u < RSUB; ++u) {
-          const int64_t vi = c0 + u * 32 + lane;
-          const bool in = vi < n_c;
-          pre[u] = (REFINE && a.rd_prefetch && in) ? __ldg(rrow + vi) : 0.0;
-          ipv[u] = in ? (int)__ldg(iprow + vi) : 0;
-          fa[u] = in ? __ldg(a.ix.short_add + lo + vi) : 0.f;
-          fs[u] = in ? __ldg(a.ix.short_scale + lo + vi) : 0.f;
-          fe[u] = in ? __ldg(a.ix.short_err + lo + vi) : 0.f;
+      for (int u = 0; u < RSUB; ++u) {
+        const int64_t vi = c0 + u * 32 + lane;
+        if (c0 + u * 32 >= n_c) break;  // warp-uniform
+        bool keep = false;
+        double est2 = 0.0;
+        if (vi < n_c) {
+          const double scale = (double)fs[u];
+          est2 = dmax(dsub(dadd((double)fa[u], d_qc2), dmul(scale, dsub(dmul(delta, (double)ipv[u]), half_code))), 0.0);
+          keep = stage1_keep64(est2, (double)fe[u], scale, sq, ipm, T_list);
         }
-        bool keep[RSUB];
-        double est[RSUB];
-#pragma unroll
-        for (int u = 0; u < RSUB; ++u) {
-          const int64_t vi = c0 + u * 32 + lane;
-          keep[u] = false;
-          est[u] = 0.0;
-          const int dec = (REFINE && vi < n_c) ? stage1_decide_f32(ipv[u], fa[u], fs[u], fe[u], f32) : -1;
-          if (dec >= 0) {
-            keep[u] = dec != 0;
-          } else if (vi < n_c) {
-            const double ipb = dmul(delta, (double)ipv[u]);
-            const double scale = (double)fs[u];
-            const double est2 = dmax(dsub(dadd((double)fa[u], d_qc2), dmul(scale, dsub(ipb, half_code))), 0.0);
-            est[u] = est2;
-            bool kp;
-            if (est2 <= T_list) {
-              kp = true;  // lb2 <= est2 <= T
-            } else {
-              const double margin = dmul((double)fe[u], sq);
-              if (ipm != 0.0) {  // same decision as stage1_chunk
-                const double sm = dmul(scale, ipm);
-                const double S = dadd(dmul(margin, margin), dmul(sm, sm));
-                const double gap = dsub(est2, T_list);
-                const double g2 = dmul(gap, gap);
-                if (S >= g2 * (1.0 + 0x1p-38)) {
-                  kp = true;
-                } else if (S <= g2 * (1.0 - 0x1p-38) && gap > T_list * 0x1p-12) {
-                  kp = false;
-                } else {
-                  kp = dmax(dsub(est2, dsqrt(S)), 0.0) <= T_list;
-                }
-              } else {
-                kp = dmax(dsub(est2, margin), 0.0) <= T_list;
-              }
-            }
-            keep[u] = kp;
-          }
-        }
-        double dv[RSUB];
-#pragma unroll
-        for (int u = 0; u < RSUB; ++u) {  // survivors' refined distances, loads in flight together
-          const int64_t vi = c0 + u * 32 + lane;
-          dv[u] = keep[u] ? (REFINE ? (a.rd_prefetch ? pre[u] : __ldg(rrow + vi)) : est[u]) : dinf();
-        }
-#pragma unroll
-        for (int u = 0; u < RSUB; ++u) {
-          const unsigned kb = __ballot_sync(FULL, keep[u]);
-          if (!kb) continue;
-          surv += __popc(kb);
-          warp_offer(a, qd, qi, dv[u], keep[u] ? (int)(c0 + u * 32 + lane) : -1, lo, k);
-        }
+        const unsigned kb = __ballot_sync(FULL, keep);
+        if (!kb) continue;
+        surv += __popc(kb);
+        warp_offer(a, qd, qi, keep ? est2 : dinf(), keep ? (int)vi : -1, lo, k);
       }
     }
     const int cnt = __popc(__ballot_sync(FULL, lane < k && qi != NO_ID));
@@ -1097,6 +1080,416 @@ __global__ void __launch_bounds__(RDW * 32, MINB) scan_rd_kernel(Args a) {
       a.stats[2 * q] = probed;
       a.stats[2 * q + 1] = surv;
     }
+  }
+}
+
+// ------------------------------------------------------------ approximate refined distances, certified
+// The refine pass over tc_refine_kernel's approximate distances.  Every stored
+// value s is within rad(s) = rrad[q] + s 2^-23 of the exact refined distance x
+// (refine_chunk's value).  The pass replays the reference's threshold chain
+// with intervals and obtains exact values only where an interval leaves a
+// decision open:
+//  * the queue keeps every candidate that could still be among the k nearest
+//    (s - rad(s) <= s_k + rad(s_k), s_k the queue's k-th value), the 32
+//    smallest by value, so the k-th order statistic of the queue is within
+//    rad(s_k) of the exact threshold T (both are 1-Lipschitz);
+//  * a prune test lb2 <= T is decided by lb2 <= s_k - rad(s_k) (keep) or
+//    lb2 > s_k + rad(s_k) (prune); otherwise the list-start queue (kept in
+//    shared memory) gets exact values for its possible members and T is exact
+//    for the rest of the list;
+//  * at the end the possible members of the top k get exact values and the
+//    queue is re-sorted, so ids, order and distances are the exact pass's.
+// A queue entry is a shard row (bits 0-39) with its probe index (40-59) for the
+// list's d_qc2, EXACT once its value is exact, or a carried-in pool's pid
+// (PIDE).  Should the 32 slots ever fill with possible members (near-ties
+// across > 32 - k vectors), the query is listed for an exact rerun
+// (scan_warp_kernel with fix_only).
+constexpr int64_t E_ROW = (1LL << 40) - 1;
+constexpr int E_PSH = 40;
+constexpr int64_t E_EXACT = 1LL << 60;
+constexpr int64_t E_PIDE = 1LL << 61;  // pid entry (carried-in pool), always exact
+
+__device__ __forceinline__ int64_t entry_pid(const int64_t* pids, int64_t e) {
+  return e == NO_ID ? NO_ID : (e & E_PIDE) ? (e & E_ROW) : pids[e & E_ROW];
+}
+
+// tie of two values: the pids decide (rare; kept out of line so the sort networks stay small)
+__device__ __noinline__ bool entry_tie_less(const int64_t* pids, int64_t ea, int64_t eb) {
+  return entry_pid(pids, ea) < entry_pid(pids, eb);
+}
+
+struct EntryLess {  // (value, pid) order of queue entries
+  const int64_t* pids;
+  __device__ __forceinline__ int64_t pid(int64_t e) const { return entry_pid(pids, e); }
+  __device__ __forceinline__ bool operator()(double da, int64_t ea, double db, int64_t eb) const {
+    return da < db || (da == db && ea != eb && entry_tie_less(pids, ea, eb));
+  }
+};
+
+__device__ __forceinline__ double entry_rad(double d, int64_t e, double rq) {
+  return (e == NO_ID || (e & (E_EXACT | E_PIDE))) ? 0.0 : rq + d * 0x1p-23;
+}
+
+// P <-> K position of the query digit slices (bits 2-3 and 4-5 swapped; see tc_bpairs_kernel)
+__device__ __forceinline__ int slice_pos(int P) { return (P & ~0x3C) | ((P & 0x0C) << 2) | ((P & 0x30) >> 2); }
+
+// What the exact refine of a queue entry needs (kept in local memory by the out-of-line helpers
+// below, which run a few times per query: the hot loop stays small enough for the instruction cache)
+struct ExactCtx {
+  const uint8_t* rcodes;
+  const float2* lf;
+  const double* pd2;     // this query's probe distances
+  const int8_t* qs;      // this query's digit slices
+  int64_t rb;
+  int kp, sexp;
+  double kb, rq;
+  bool nib;
+};
+
+// The query's digits as per-position (high, low) halves in shared memory: position P of an rcode
+// row pairs with hl[P] = (sum_{s<4} D_s 128^(3-s), sum_{s>=4} D_s 128^(7-s)) at slice index slice_pos(P).
+__device__ __noinline__ void load_hl(const ExactCtx& c, int2* hl) {
+  const int kp = c.kp, lane = threadIdx.x & 31;
+  // four consecutive slice positions per lane and load: the eight digit words are independent loads
+  for (int k0 = 4 * lane; k0 < kp; k0 += 128) {
+    uint32_t w[SLICES];
+#pragma unroll
+    for (int s2 = 0; s2 < SLICES; ++s2) w[s2] = __ldg(reinterpret_cast<const uint32_t*>(c.qs + s2 * kp + k0));
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int h = 0, l = 0;
+#pragma unroll
+      for (int s2 = 0; s2 < 4; ++s2) {
+        h = h * 128 + (int)(int8_t)(w[s2] >> (8 * j));
+        l = l * 128 + (int)(int8_t)(w[s2 + 4] >> (8 * j));
+      }
+      hl[slice_pos(k0 + j)] = make_int2(h, l);
+    }
+  }
+  __syncwarp();
+}
+
+// Exact refined distance of queue entry e (refine_chunk's arithmetic), warp-collective.
+__device__ __forceinline__ double exact_value(const ExactCtx& c, const int2* hl, int64_t e) {
+  const int lane = threadIdx.x & 31, kp = c.kp;
+  const int64_t row = e & E_ROW;
+  const int p = (int)((e >> E_PSH) & 0xFFFFF);
+  const uint8_t* rc = c.rcodes + row * c.rb;
+  long long H = 0, L = 0;
+  // lane-strided positions (coalesced row bytes), eight loads in flight
+#pragma unroll 8
+  for (int P = lane; P < kp; P += 32) {
+    int u;
+    if (c.nib) {
+      const uint8_t by = __ldg(rc + (P >> 4) * 8 + ((P >> 3) & 1) * 4 + (P & 3));
+      u = ((P >> 2) & 1) ? (by >> 4) : (by & 15);
+    } else {
+      u = __ldg(rc + P);
+    }
+    const int2 w = hl[P];
+    H += (long long)u * w.x;
+    L += (long long)u * w.y;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    H += __shfl_xor_sync(FULL, H, o);
+    L += __shfl_xor_sync(FULL, L, o);
+  }
+  const double ip = dadd(dmul((double)H, ldexp(1.0, c.sexp - 26)), dmul((double)L, ldexp(1.0, c.sexp - 54)));
+  const float2 lf = __ldg(c.lf + row);
+  return dmax(dsub(dadd((double)lf.x, __ldg(c.pd2 + p)), dmul((double)lf.y, dsub(ip, c.kb))), 0.0);
+}
+
+// Exact values for the queue's possible members of the top k (value - rad <= s_k + rad(s_k)),
+// then the queue re-sorted: its first k entries are then the exact top k, exact.
+__device__ __noinline__ void exactify_top(const ExactCtx& c, const int2* hl, const int64_t* pids, double& qd,
+                                          int64_t& qi, int k) {
+  const double kd = __shfl_sync(FULL, qd, k - 1);
+  const int64_t ke = __shfl_sync(FULL, qi, k - 1);
+  const double lim = kd + entry_rad(kd, ke, c.rq);
+  const bool need = qi != NO_ID && !(qi & (E_EXACT | E_PIDE)) && dsub(qd, entry_rad(qd, qi, c.rq)) <= lim;
+  unsigned m = __ballot_sync(FULL, need);
+  if (!m) return;
+  while (m) {
+    const int src = __ffs(m) - 1;
+    m &= m - 1;
+    const int64_t e = __shfl_sync(FULL, qi, src);
+    const double x = exact_value(c, hl, e);
+    if ((threadIdx.x & 31) == src) {
+      qd = x;
+      qi = e | E_EXACT;
+    }
+  }
+  warp_sort32(qd, qi, EntryLess{pids});
+}
+
+#ifdef IVRQ_RDA_STATS  // development builds only: how often the intervals leave decisions open
+__device__ unsigned long long g_rda_stats[6];  // prune resolutions, exact values, queries, sum rq/T (1e-12), reruns
+#define RDA_STAT(i, v) (((threadIdx.x & 31) == 0) ? (void)atomicAdd(&g_rda_stats[i], (unsigned long long)(v)) : (void)0)
+#else
+#define RDA_STAT(i, v) ((void)0)
+#endif
+
+template <int IPB, int RSUB, int MINB = 1>
+__global__ void __launch_bounds__(RDW * 32, MINB) scan_rda_kernel(Args a) {
+  using IPT = typename std::conditional<IPB == 2, int16_t, int32_t>::type;
+  extern __shared__ __align__(16) unsigned char rda_smem[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t slot_q = (int64_t)blockIdx.x * RDW + wid;
+  if (slot_q >= a.nq) return;  // whole warps only
+  const int64_t q = a.qorder ? a.qorder[slot_q] : slot_q;
+  const int k = a.k, kp = a.kpad;
+  unsigned char* wbase = rda_smem + (size_t)wid * ((size_t)kp * sizeof(int2) + 32 * 16);
+  int2* hl = reinterpret_cast<int2*>(wbase);
+  double* snap_d = reinterpret_cast<double*>(wbase + (size_t)kp * sizeof(int2));
+  int64_t* snap_e = reinterpret_cast<int64_t*>(snap_d + 32);
+  bool hl_ready = false;
+  // The queue is ordered by (value, entry bits): the order of tied approximate values never decides
+  // anything (the threshold is a value; a tie at the 32nd slot is a saturation); the exact top k is
+  // re-sorted by (value, pid) in exactify_top.
+  const PidLess lt;
+  const double* sc = a.scalars + q * IVRQ_QS_COUNT;
+  const double delta = sc[IVRQ_QS_DELTA], half_code = sc[IVRQ_QS_HALF_CODE], ipm = sc[IVRQ_QS_IP_MARGIN];
+  const double rq = a.rrad[q];
+  const int init_n = a.init_counts ? a.init_counts[q] : 0;
+  double qd = lane < init_n ? a.init_dists[q * k + lane] : dinf();
+  int64_t qi = lane < init_n ? (a.init_ids[q * k + lane] | E_PIDE) : NO_ID;
+  double T = init_n >= k ? __shfl_sync(FULL, qd, k - 1) : dinf(), radT = 0.0;
+  bool unsafe = false;
+  long long probed = 0, surv = 0;
+  // offer survivors (value d, entry e; e = NO_ID: none) to the queue
+  auto offer = [&](double d, int64_t e) {
+    const double kd = __shfl_sync(FULL, qd, k - 1);
+    const int64_t ke = __shfl_sync(FULL, qi, k - 1);
+    const bool maybe = e != NO_ID && dsub(d, entry_rad(d, e, rq)) <= kd + entry_rad(kd, ke, rq);
+    if (!__any_sync(FULL, maybe)) return;
+    warp_fold(qd, qi, maybe ? d : dinf(), maybe ? e : NO_ID, maybe, 32, lt);
+    // the 32nd slot a possible member: a candidate pushed out of the queue may have been one
+    const double nk = __shfl_sync(FULL, qd, k - 1);
+    const int64_t nke = __shfl_sync(FULL, qi, k - 1);
+    const double d31 = __shfl_sync(FULL, qd, 31);
+    const int64_t e31 = __shfl_sync(FULL, qi, 31);
+    if (e31 != NO_ID && dsub(d31, entry_rad(d31, e31, rq)) <= nk + entry_rad(nk, nke, rq)) unsafe = true;
+  };
+  ListMeta nxt = list_meta(a, q * a.nprobe);
+  for (int p = 0; p < a.nprobe; ++p) {  // ascending cluster id (search.py:429)
+    const ListMeta cur = nxt;
+    if (p + 1 < a.nprobe) nxt = list_meta(a, q * a.nprobe + p + 1);  // prefetched one list ahead
+    if (cur.nc <= 0) continue;  // another shard's list, or empty
+    const int64_t lo = cur.lo, n_c = cur.nc;
+    const int64_t ebase = lo | ((int64_t)p << E_PSH);
+    const double d_qc2 = cur.d2;
+    double T_list = a.prune ? T : dinf();
+    double rT = a.prune ? radT : 0.0;
+    probed += n_c;
+    const float* rrow = a.rdist + cur.base;
+    if (T_list == dinf()) {  // nothing can be pruned (lb2 <= +inf): every vector's refined distance
+      surv += n_c;
+      for (int64_t c0 = 0; c0 < n_c; c0 += 32 * RSUB) {
+        float dv[RSUB];
+#pragma unroll
+        for (int u = 0; u < RSUB; ++u) {
+          const int64_t vi = c0 + u * 32 + lane;
+          dv[u] = vi < n_c ? __ldg(rrow + vi) : 0.f;
+        }
+#pragma unroll 1
+        for (int u = 0; u < RSUB; ++u) {  // one copy of the queue code (instruction cache); the values
+          const float d0 = dv[0];         // rotate through dv[0] so every index stays static (registers)
+#pragma unroll
+          for (int j = 0; j + 1 < RSUB; ++j) dv[j] = dv[j + 1];
+          const int64_t vi = c0 + u * 32 + lane;
+          if (c0 + u * 32 >= n_c) break;  // warp-uniform
+          offer((double)d0, vi < n_c ? ebase + vi : NO_ID);
+        }
+      }
+    } else {
+      // the list-start queue, for an exact threshold should an interval leave a test open
+      snap_d[lane] = qd;
+      snap_e[lane] = qi;
+      __syncwarp();
+      const IPT* iprow = reinterpret_cast<const IPT*>(a.ipbuf) + cur.base;
+      const double sq = dsqrt(d_qc2);
+      Stage1F32 f32 = stage1_f32(delta, half_code, ipm, d_qc2, sq, T_list);
+      f32.T_lo = __double2float_rd(T_list - rT * (1.0 + 0x1p-40));
+      f32.T_hi = __double2float_ru(T_list + rT * (1.0 + 0x1p-40));
+      for (int64_t c0 = 0; c0 < n_c; c0 += 32 * RSUB) {
+        int ipv[RSUB];
+        float fa[RSUB], fs[RSUB], fe[RSUB], pre[RSUB];
+#pragma unroll
+        for (int u = 0; u < RSUB; ++u) {
+          const int64_t vi = c0 + u * 32 + lane;
+          const bool in = vi < n_c;
+          pre[u] = in ? __ldg(rrow + vi) : 0.f;
+          ipv[u] = in ? (int)__ldg(iprow + vi) : 0;
+          fa[u] = in ? __ldg(a.ix.short_add + lo + vi) : 0.f;
+          fs[u] = in ? __ldg(a.ix.short_scale + lo + vi) : 0.f;
+          fe[u] = in ? __ldg(a.ix.short_err + lo + vi) : 0.f;
+        }
+        int dec[RSUB];
+        bool open = false;
+#pragma unroll
+        for (int u = 0; u < RSUB; ++u) {
+          const int64_t vi = c0 + u * 32 + lane;
+          dec[u] = vi < n_c ? stage1_decide_f32(ipv[u], fa[u], fs[u], fe[u], f32) : 0;
+          if (dec[u] < 0) {
+            const double scale = (double)fs[u];
+            const double est2 =
+                dmax(dsub(dadd((double)fa[u], d_qc2), dmul(scale, dsub(dmul(delta, (double)ipv[u]), half_code))), 0.0);
+            if (stage1_keep64(est2, (double)fe[u], scale, sq, ipm, T_list - rT)) dec[u] = 1;
+            else if (!stage1_keep64(est2, (double)fe[u], scale, sq, ipm, T_list + rT)) dec[u] = 0;
+            open |= dec[u] < 0;
+          }
+        }
+        if (__any_sync(FULL, open)) {
+          // the threshold's interval leaves a test open: exact values for the list-start
+          // queue's possible members give the exact T for the rest of this list
+          // (the context is built here, not held in registers through the stream)
+          ExactCtx ec;
+          ec.rcodes = a.ix.rcodes;
+          ec.lf = reinterpret_cast<const float2*>(a.ix.long_factors);
+          ec.pd2 = a.probe_d2 + q * a.nprobe;
+          ec.qs = a.qslices + q * SLICES * (int64_t)kp;
+          ec.rb = a.ix.rcode_bytes;
+          ec.kp = kp;
+          ec.sexp = (int)sc[IVRQ_QS_SLICE_EXP];
+          ec.kb = sc[IVRQ_QS_KB_SUM];
+          ec.rq = rq;
+          ec.nib = rcode_nibbles(a.ix.bits);
+          if (!hl_ready) {
+            load_hl(ec, hl);
+            hl_ready = true;
+          }
+          RDA_STAT(0, 1);
+          double sd = snap_d[lane];
+          int64_t se = snap_e[lane];
+          exactify_top(ec, hl, a.ix.pids, sd, se, k);
+          T_list = __shfl_sync(FULL, sd, k - 1);
+          rT = 0.0;
+          f32.T_lo = __double2float_rd(T_list);
+          f32.T_hi = __double2float_ru(T_list);
+#pragma unroll
+          for (int u = 0; u < RSUB; ++u) {
+            if (dec[u] < 0) {
+              const double scale = (double)fs[u];
+              const double est2 = dmax(
+                  dsub(dadd((double)fa[u], d_qc2), dmul(scale, dsub(dmul(delta, (double)ipv[u]), half_code))), 0.0);
+              dec[u] = stage1_keep64(est2, (double)fe[u], scale, sq, ipm, T_list) ? 1 : 0;
+            }
+          }
+        }
+        bool keep[RSUB];
+#pragma unroll
+        for (int u = 0; u < RSUB; ++u) keep[u] = dec[u] > 0;
+#pragma unroll 1
+        for (int u = 0; u < RSUB; ++u) {  // one copy of the queue code (instruction cache); values
+          const float d0 = pre[0];        // rotate through slot 0 so every index stays static
+          const bool k0 = keep[0];
+#pragma unroll
+          for (int j = 0; j + 1 < RSUB; ++j) {
+            pre[j] = pre[j + 1];
+            keep[j] = keep[j + 1];
+          }
+          const unsigned kbits = __ballot_sync(FULL, k0);
+          if (!kbits) continue;
+          surv += __popc(kbits);
+          offer((double)d0, k0 ? ebase + c0 + u * 32 + lane : NO_ID);
+        }
+      }
+    }
+    const int cnt = __popc(__ballot_sync(FULL, lane < k && qi != NO_ID));
+    if (cnt >= k) {  // search.py:444-447, as an interval
+      T = __shfl_sync(FULL, qd, k - 1);
+      radT = entry_rad(T, __shfl_sync(FULL, qi, k - 1), rq);
+    }
+  }
+  // the queue (values, entries) for rda_final_kernel, which makes the top k exact
+  a.fin_d[q * 32 + lane] = qd;
+  a.fin_e[q * 32 + lane] = qi;
+  if (lane == 0) {
+    if (a.stats) {
+      a.stats[2 * q] = probed;
+      a.stats[2 * q + 1] = surv;
+    }
+    if (unsafe) a.fix_list[atomicAdd(a.fix_count, 1)] = (int32_t)q;
+  }
+}
+
+// The end of the approximate pass, one CTA (4 warps) per query: exact values for the queue's
+// possible members of the top k (the warps share the query's digit table in shared memory and
+// split the entries), the queue re-sorted by (value, pid), the first k written out.
+constexpr int FIN_W = 4;
+
+__global__ void __launch_bounds__(FIN_W * 32) rda_final_kernel(Args a) {
+  extern __shared__ __align__(16) unsigned char fin_smem[];
+  int2* hl = reinterpret_cast<int2*>(fin_smem);
+  double* sd = reinterpret_cast<double*>(fin_smem + (size_t)a.kpad * sizeof(int2));
+  int64_t* se = reinterpret_cast<int64_t*>(sd + 32);
+  __shared__ int s_need[32];
+  __shared__ int s_nneed;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t q = blockIdx.x;
+  const int k = a.k, kp = a.kpad;
+  const double* sc = a.scalars + q * IVRQ_QS_COUNT;
+  ExactCtx ec;
+  ec.rcodes = a.ix.rcodes;
+  ec.lf = reinterpret_cast<const float2*>(a.ix.long_factors);
+  ec.pd2 = a.probe_d2 + q * a.nprobe;
+  ec.qs = a.qslices + q * SLICES * (int64_t)kp;
+  ec.rb = a.ix.rcode_bytes;
+  ec.kp = kp;
+  ec.sexp = (int)sc[IVRQ_QS_SLICE_EXP];
+  ec.kb = sc[IVRQ_QS_KB_SUM];
+  ec.rq = a.rrad[q];
+  ec.nib = rcode_nibbles(a.ix.bits);
+  // the digit table, all threads: four slice positions per thread and pass
+  for (int k0 = 4 * (int)threadIdx.x; k0 < kp; k0 += 4 * FIN_W * 32) {
+    uint32_t w[SLICES];
+#pragma unroll
+    for (int s2 = 0; s2 < SLICES; ++s2) w[s2] = __ldg(reinterpret_cast<const uint32_t*>(ec.qs + s2 * kp + k0));
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int h = 0, l = 0;
+#pragma unroll
+      for (int s2 = 0; s2 < 4; ++s2) {
+        h = h * 128 + (int)(int8_t)(w[s2] >> (8 * j));
+        l = l * 128 + (int)(int8_t)(w[s2 + 4] >> (8 * j));
+      }
+      hl[slice_pos(k0 + j)] = make_int2(h, l);
+    }
+  }
+  if (wid == 0) {
+    const double qd = a.fin_d[q * 32 + lane];
+    const int64_t qi = a.fin_e[q * 32 + lane];
+    sd[lane] = qd;
+    se[lane] = qi;
+    const double kd = __shfl_sync(FULL, qd, k - 1);
+    const int64_t ke = __shfl_sync(FULL, qi, k - 1);
+    const double lim = kd + entry_rad(kd, ke, ec.rq);
+    const bool need = qi != NO_ID && !(qi & (E_EXACT | E_PIDE)) && dsub(qd, entry_rad(qd, qi, ec.rq)) <= lim;
+    const unsigned m = __ballot_sync(FULL, need);
+    if (need) s_need[__popc(m & ((1u << lane) - 1u))] = lane;
+    if (lane == 0) s_nneed = __popc(m);
+  }
+  __syncthreads();
+  for (int i = wid; i < s_nneed; i += FIN_W) {
+    const int slot = s_need[i];
+    const double x = exact_value(ec, hl, se[slot]);
+    if (lane == 0) {
+      sd[slot] = x;
+      se[slot] |= E_EXACT;
+    }
+  }
+  __syncthreads();
+  if (wid == 0) {
+    double qd = sd[lane];
+    int64_t qi = se[lane];
+    warp_sort32(qd, qi, EntryLess{a.ix.pids});
+    const int pn = __popc(__ballot_sync(FULL, lane < k && qi != NO_ID));
+    if (lane < k) {
+      a.out_ids[q * k + lane] = lane < pn ? entry_pid(a.ix.pids, qi) : -1;
+      a.out_dists[q * k + lane] = lane < pn ? qd : dinf();
+    }
+    if (lane == 0) a.out_counts[q] = pn;
   }
 }
 
@@ -1961,47 +2354,51 @@ __global__ void __launch_bounds__(THREADS, 2) first_dist_kernel(FdArgs a) {
 }
 
 // ------------------------------------------------------------ refine of every probed pair on tcgen05
-// The refined distance (search.py:313-323) of every vector of every probed
-// (list, query) pair, list-major on the 5th-generation tensor cores: for a
-// list c and a group of G queries probing it, D[v][(j, s)] = <u_v, digit_s of
-// q_j> is one int8 GEMM (M = 128 vectors per TMEM tile, N = 8 G digit slices,
-// K = kpad) with the accumulator in TMEM.  The group's digit slices stay
-// resident in shared memory while the list's rcode rows stream past them.
+// A certified approximation of the refined distance (search.py:313-323) of
+// every vector of every probed (list, query) pair, list-major on the
+// 5th-generation tensor cores.  The exact refine (refine_chunk) assembles
+// <u, q_rot> from the query's eight base-128 digits; here only the four most
+// significant digits D0..D3 go through the tensor cores:
+//   hi_v = sum_d u_vd (D0 128^3 + D1 128^2 + D2 128 + D3)_d,  ip ~ hi_v 2^(e-26),
+// the neglected low half being at most U_max kpad 135274560 2^(e-54) in
+// magnitude.  The distance from this ip is stored as float32 together with a
+// per-query radius (rd_radius_kernel) that bounds its distance to the exact
+// value; the per-query pass (scan_rda_kernel) decides with intervals and
+// computes the exact value of the few entries whose decision the radius
+// leaves open, and of its final top k, so results are the exact path's.
+// Halving the digits halves the MMA work and the B operand, so a query group
+// is twice as large (fewer passes over each list's codes) beside a deeper
+// A ring.  For a list c and a group of G queries probing it,
+// D[v][(j, s)] = <u_v, digit_s of q_j> is one int8 GEMM (M = 128 vectors per
+// TMEM tile, N = 4 G digit rows, K = kpad) with the accumulator in TMEM.
 // Warp roles per CTA:
 //   warps 0-3  stage rcode tiles (128 rows x 128 B per stage) into a ring
 //              (one TMA lane for 8-bit codes; all four warps unpack 4-bit codes),
-//   warp 1     also loads the next group's digit slices: one 1-D bulk copy of
-//              nkc KB per query from the pre-swizzled slice array, as soon as
-//              the previous group's MMAs retire (no CTA barrier between groups),
+//   warp 1     also loads the next group's digit rows: one bulk copy per K chunk
+//              from the pre-swizzled pair-ordered array (tc_bpairs_kernel), as soon
+//              as the previous group's MMAs retire (no CTA barrier between groups),
 //   warp 4     issues tcgen05.mma (one elected lane) and commits,
 //   warps 5-12 read the accumulator (tcgen05.ld; two warps per TMEM lane
-//              quarter, each half of the group's queries), assemble each
-//              query's 8 digit dots exactly in int64, round once to float64 and
-//              write the refined distance with refine_chunk's arithmetic.
-// The per-query pass (scan_rd_kernel) then only streams stage-1 inputs and
-// reads the refined distance of its survivors.
+//              quarter, each half of the group's queries), assemble hi_v in int64,
+//              and write the approximate distance as float32.
 constexpr int TCM = 128;     // vectors per tile = TMEM lanes
 constexpr int TCKC = 128;    // K bytes per A stage (4 MMAs of K = 32)
 constexpr int TCST = 6;      // A stages (tc_ip_kernel)
 constexpr int TC_PROD = 4;  // producer warps
 constexpr int TC_THREADS = 32 * (TC_PROD + 1 + 4);
-constexpr int TCR_EPI = 8;  // tc_refine epilogue warps: 2 per TMEM lane quarter, each half of the group's queries
+#ifndef TCR_EPQ
+#define TCR_EPQ 3
+#endif
+constexpr int TCR_EPI = 4 * TCR_EPQ;  // tc_refine epilogue warps: TCR_EPQ per TMEM lane quarter, each a share of the
+                                      // group's queries
 constexpr int TCR_THREADS = 32 * (TC_PROD + 1 + TCR_EPI);
 
-#ifdef IVRQ_TC_PROFILE
-// development builds only (-DIVRQ_TC_PROFILE): cycles tc_refine's roles spend waiting, summed over CTAs
-__device__ unsigned long long g_tcr_prof[8];  // 0 MMA wait B, 1 MMA wait accumulator, 2 MMA wait A, 3 MMA total,
-                                              // 4 producer wait empty, 5 epilogue wait full, 6 epilogue busy, 7 tiles
-#define TCR_PROF_T0() const long long _t0 = clock64()
-#define TCR_PROF_ADD(i) atomicAdd(&g_tcr_prof[i], (unsigned long long)(clock64() - _t0))
-#else
-#define TCR_PROF_T0()
-#define TCR_PROF_ADD(i)
-#endif
+constexpr int TCR_DIG = 4;  // most significant query digits on the tensor cores
 
 struct TcArgs {
   CUtensorMap map_a;        // rcodes [N rows x rcode_bytes] (8-bit codes), box 128 B x 128 rows, 128B swizzle
-  const int8_t* bslices;    // [nq][nkc][8 rows x 128 B] pre-swizzled digit slices (tc_slices_kernel)
+  const int8_t* bslices;    // [nkc][npairs][4 rows x 128 B] pre-swizzled digit rows in pair order (tc_bpairs_kernel)
+  int64_t npairs;
   ivrq_index_view ix;
   int kpad, G, nst, nib;
   const double* scalars;
@@ -2011,7 +2408,7 @@ struct TcArgs {
   const int64_t* poff;      // [nlist + 2]
   const int64_t* pair_base; // [nlist + 1]
   const int32_t* gpre;      // [nlist + 1] prefix of ceil(bucket / G)
-  double* rdist;
+  float* rdist;             // approximate refined distances (radius: rd_radius_kernel)
 };
 
 // byte offset of (row R, byte k < 128) in a 128B-swizzled K-major tile (8-row atoms of 1024 B)
@@ -2019,27 +2416,35 @@ __host__ __device__ inline uint32_t sw128_offset(int R, int k) {
   return (uint32_t)((R >> 3) * 1024 + (R & 7) * 128 + ((((k >> 4) ^ (R & 7)) & 7) << 4) + (k & 15));
 }
 
-// The refine's B operand, laid out for one bulk copy per query: out[q][kc] is the 1 KB
-// 128B-swizzled atom of digit rows s = 0..7, K bytes [128 kc, 128 kc + 128) in rcode
-// byte order P, with qslices' mma.sync fragment order transposed:
-// value(P = 64p + 16t + 4h + j) = qslices[q][s][64p + 16h + 4t + j]; zero past kpad.
-__global__ void tc_slices_kernel(const int8_t* __restrict__ qslices, int64_t nq, int kp, int nkc,
+// The refine's B operand, materialised in pair order so that one bulk copy per K chunk loads a
+// whole query group: out[kc][i] (512 bytes) holds the four digit rows of the query of pair i
+// (list-sorted order), pre-swizzled as rows 4 par .. 4 par + 3 of a 128B-swizzled 8-row atom,
+// par = the pair's slot parity in its list's bucket (groups start at even slots, so consecutive
+// pairs of a group fill one atom), digit d in row 4 par + d, K bytes [128 kc, 128 kc + 128) in
+// rcode byte order P with qslices' mma.sync fragment order transposed:
+// value(P = 64p + 16t + 4h + j) = qslices[q][d][64p + 16h + 4t + j]; zero past kpad.
+__global__ void tc_bpairs_kernel(const int8_t* __restrict__ qslices, const int64_t* __restrict__ porder,
+                                 const int32_t* __restrict__ pslot, int64_t npairs, int nprobe, int kp, int nkc,
                                  int8_t* __restrict__ out) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // one 16-byte group of one row
-  const int64_t ngroups = nq * nkc * 64;
-  if (i >= ngroups) return;
-  const int64_t atom = i >> 6;  // (q, kc)
-  const int w = (int)(i & 63), s = w >> 3, c16 = w & 7;
-  const int64_t q = atom / nkc;
-  const int kc = (int)(atom % nkc);
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // one 16-byte chunk of one row
+  if (t >= npairs * nkc * 32) return;
+  const int w = (int)(t & 31), d = w >> 3, c16 = w & 7;
+  const int64_t blk = t >> 5;  // (kc, i), kc major
+  const int64_t i = blk % npairs;
+  const int kc = (int)(blk / npairs);
+  const int64_t pr = porder[i];
+  const int32_t slot = pslot[pr];
+  if (slot < 0) return;  // not a pair of this shard
+  const int64_t q = pr / nprobe;
   const int P0 = kc * TCKC + 16 * c16;
   uint4 v = make_uint4(0u, 0u, 0u, 0u);
   if (P0 < kp) {
     const int p64 = P0 >> 6, t4 = (P0 >> 4) & 3;
-    const uint32_t* src = reinterpret_cast<const uint32_t*>(qslices + (q * SLICES + s) * kp + 64 * p64 + 4 * t4);
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(qslices + (q * SLICES + d) * kp + 64 * p64 + 4 * t4);
     v = make_uint4(src[0], src[4], src[8], src[12]);
   }
-  *reinterpret_cast<uint4*>(out + atom * 1024 + sw128_offset(s, 16 * c16)) = v;
+  const int R = 4 * (slot & 1) + d;  // row inside the 8-row atom
+  *reinterpret_cast<uint4*>(out + blk * 512 + d * 128 + (((c16 ^ R) & 7) << 4)) = v;
 }
 
 __host__ __device__ inline uint32_t tmem_cols(int n) {  // power of two >= 32 (<= 512)
@@ -2048,16 +2453,27 @@ __host__ __device__ inline uint32_t tmem_cols(int n) {  // power of two >= 32 (<
 
 size_t tc_smem_bytes(int kpad, int G, int nst) {
   const int nkc = (kpad + TCKC - 1) / TCKC;
-  return 1024 + (size_t)nkc * 8 * G * TCKC + (size_t)nst * TCM * TCKC + 256;
+  return 1024 + (size_t)nkc * TCR_DIG * G * TCKC + (size_t)nst * TCM * TCKC + 256 + 2 * 64 * sizeof(double4);
 }
+
+#ifdef IVRQ_TCR_TRACE  // development builds only: timeline of CTA 0's roles (plain stores, no atomics)
+__device__ unsigned long long g_tcr_trace[16 * 4096];
+#define TCR_EV(tag, idx)                                                                       \
+  do {                                                                                         \
+    if (blockIdx.x == 0) g_tcr_trace[((tag) << 12) | ((idx) & 4095)] = (unsigned long long)clock64(); \
+  } while (0)
+#else
+#define TCR_EV(tag, idx) ((void)0)
+#endif
 
 __global__ void __launch_bounds__(TCR_THREADS, 1) tc_refine_kernel(const __grid_constant__ TcArgs a) {
   extern __shared__ __align__(1024) unsigned char tsm_raw[];
   unsigned char* tsm = reinterpret_cast<unsigned char*>(((uintptr_t)tsm_raw + 1023) & ~(uintptr_t)1023);
-  const int G = a.G, N = 8 * G, kp = a.kpad, NST = a.nst;
+  const int G = a.G, kp = a.kpad, NST = a.nst;
   const int nkc = (kp + TCKC - 1) / TCKC;  // 128-byte K chunks
-  int8_t* sB = reinterpret_cast<int8_t*>(tsm);                                   // [G][nkc][8 rows x 128 B]
-  uint8_t* sA = reinterpret_cast<uint8_t*>(tsm + (size_t)nkc * N * TCKC);        // [NST][128 rows x 128 B] swizzled
+  const uint32_t bkc = (uint32_t)(G / 2) * 1024;  // one K chunk of the group's digit rows (G even)
+  int8_t* sB = reinterpret_cast<int8_t*>(tsm);                                   // [nkc][G/2 atoms][1 KB]
+  uint8_t* sA = reinterpret_cast<uint8_t*>(tsm + (size_t)nkc * bkc);             // [NST][128 rows x 128 B] swizzled
   uint64_t* bars = reinterpret_cast<uint64_t*>(sA + (size_t)NST * TCM * TCKC);
   uint64_t* full = bars;                      // [NST]
   uint64_t* empty = bars + NST;               // [NST]
@@ -2066,7 +2482,9 @@ __global__ void __launch_bounds__(TCR_THREADS, 1) tc_refine_kernel(const __grid_
   uint64_t* bfull = bars + 2 * NST + 4;       // [1]
   uint64_t* bempty = bars + 2 * NST + 5;      // [1] the group's MMAs are done with sB
   uint32_t* s_taddr = reinterpret_cast<uint32_t*>(bars + 2 * NST + 6);
+  double4* s_qs = reinterpret_cast<double4*>(bars + 2 * NST + 8);  // [2][64] (dq, kb, hs, row base) per group slot
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int NCOL = TCR_DIG * G;  // accumulator columns of one tile
   // a whole warp waiting on an mbarrier: one lane polls, the warp then re-converges
   auto wait1 = [&](uint64_t* bar, uint32_t parity) {
     if (lane == 0) tc::mbar_wait(bar, parity);
@@ -2085,15 +2503,14 @@ __global__ void __launch_bounds__(TCR_THREADS, 1) tc_refine_kernel(const __grid_
     tc::mbar_init(bempty, 1);
     tc::fence_mbar_init();
   }
-  if (wid == TC_PROD) tc::tmem_alloc(s_taddr, tmem_cols(2 * N));
+  if (wid == TC_PROD) tc::tmem_alloc(s_taddr, tmem_cols(2 * NCOL));
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tbase = *s_taddr;
   const int64_t rb = a.ix.rcode_bytes;
-  const uint32_t bq_bytes = (uint32_t)nkc * 1024;  // one query's slices
   // the two accumulators start at aligned column halves of the allocation
-  const uint32_t acc_stride = tmem_cols(2 * N) / 2;
+  const uint32_t acc_stride = tmem_cols(2 * NCOL) / 2;
   uint32_t it_prod = 0, it_mma = 0, tile_mma = 0, tile_epi = 0, grp = 0;
   const int total = a.gpre[a.nlist];
   for (int b = blockIdx.x; b < total; b += gridDim.x, ++grp) {
@@ -2108,15 +2525,15 @@ __global__ void __launch_bounds__(TCR_THREADS, 1) tc_refine_kernel(const __grid_
     const int nqg = (int)min((int64_t)G, a.poff[c + 1] - ps);
     const int ntile = (int)ceil_div(n_c, TCM);
     if (wid == 1) {
-      // the group operand: each query's digit slices (nkc KB, pre-swizzled) by one bulk copy,
+      // the group operand (its digit rows, pre-swizzled in pair order: one bulk copy per K chunk),
       // issued once the previous group's MMAs no longer read sB
       wait1(bempty, (grp & 1) ^ 1);
-      if (lane == 0) tc::mbar_expect_tx(bfull, (uint32_t)nqg * bq_bytes);
+      if (lane == 0) TCR_EV(7, grp);
+      if (lane == 0) tc::mbar_expect_tx(bfull, (uint32_t)(nqg * nkc * 512));
       __syncwarp();
-      if (lane < nqg) {
-        const int64_t q = a.porder[ps + lane] / a.nprobe;
-        tc::bulk_load(sB + (size_t)lane * bq_bytes, a.bslices + q * bq_bytes, bq_bytes, bfull, tc::kL2EvictLast);
-      }
+      if (lane < nkc)
+        tc::bulk_load(sB + lane * bkc, a.bslices + ((int64_t)lane * a.npairs + ps) * 512, (uint32_t)nqg * 512, bfull,
+                      tc::kL2EvictFirst);
     }
     if (wid < TC_PROD) {
       // ---- producers: rcode tiles -> A ring
@@ -2125,15 +2542,16 @@ __global__ void __launch_bounds__(TCR_THREADS, 1) tc_refine_kernel(const __grid_
           for (int t = 0; t < ntile; ++t)
             for (int kc = 0; kc < nkc; ++kc, ++it_prod) {
               const int st = it_prod % NST;
-              {
-                TCR_PROF_T0();
-                tc::mbar_wait(&empty[st], ((it_prod / NST) & 1) ^ 1);
-                TCR_PROF_ADD(4);
-              }
+              tc::mbar_wait(&empty[st], ((it_prod / NST) & 1) ^ 1);
+              TCR_EV(1, it_prod);
+#ifdef IVRQ_EXP_NOTMA
+              tc::mbar_arrive(&full[st]);
+#else
               tc::mbar_expect_tx(&full[st], TCM * TCKC);
               // evict-last: the list's other query groups re-read these rows from L2
               tc::tma_load_2d_hint(sA + st * TCM * TCKC, &a.map_a, kc * TCKC, (int)(lo + (int64_t)t * TCM), &full[st],
                                    tc::kL2EvictLast);
+#endif
             }
         }
       } else {
@@ -2177,111 +2595,96 @@ __global__ void __launch_bounds__(TCR_THREADS, 1) tc_refine_kernel(const __grid_
         }
       }
     } else if (wid == TC_PROD) {
-      // ---- MMA issuer.  N = the group's 8 digit rows per query, rounded to 16 (a list probed by
+      // ---- MMA issuer.  N = the group's 4 digit rows per query, rounded to 16 (a list probed by
       // few queries does not pay for a full group)
-      const uint32_t idesc = tc::idesc_i8(TCM, 8 * ((nqg + 1) & ~1), false, true);
-#ifdef IVRQ_TC_PROFILE
-      const long long _tg = clock64();
-#endif
-      {
-        TCR_PROF_T0();
-        wait1(bfull, grp & 1);
-        if (lane == 0) TCR_PROF_ADD(0);
-      }
+      const uint32_t idesc = tc::idesc_i8(TCM, TCR_DIG * ((nqg + 3) & ~3), false, true);
+      wait1(bfull, grp & 1);
+      if (lane == 0) TCR_EV(4, grp);
       for (int t = 0; t < ntile; ++t, ++tile_mma) {
         const int ab = tile_mma & 1;
-        {
-          TCR_PROF_T0();
-          wait1(&acce[ab], ((tile_mma >> 1) & 1) ^ 1);
-          if (lane == 0) TCR_PROF_ADD(1);
-        }
+        wait1(&acce[ab], ((tile_mma >> 1) & 1) ^ 1);
+        if (lane == 0) TCR_EV(3, tile_mma);
         tc::fence_after_sync();
         for (int kc = 0; kc < nkc; ++kc, ++it_mma) {
           const int st = it_mma % NST;
-          {
-            TCR_PROF_T0();
-            wait1(&full[st], (it_mma / NST) & 1);
-            if (lane == 0) TCR_PROF_ADD(2);
-          }
+          wait1(&full[st], (it_mma / NST) & 1);
           tc::fence_after_sync();
           if (lane == 0) {
-            TCR_PROF_T0();
+            TCR_EV(2, it_mma);
             const int ks = min(TCKC, kp - kc * TCKC) / 32;
+#ifndef IVRQ_EXP_NOMMA
             for (int s2 = 0; s2 < ks; ++s2) {
               const uint64_t ad = tc::smem_desc_sw128(sA + st * TCM * TCKC + 32 * s2);
-              const uint64_t bd = tc::smem_desc_sw128_sbo(sB + kc * 1024 + 32 * s2, bq_bytes);
+              const uint64_t bd = tc::smem_desc_sw128(sB + kc * bkc + 32 * s2);
               tc::mma_i8(tbase + ab * acc_stride, ad, bd, idesc, kc > 0 || s2 > 0);
             }
+#else
+            (void)ks;
+#endif
+            TCR_EV(8, it_mma);
             tc::commit(&empty[st]);
             if (kc == nkc - 1) tc::commit(&accf[ab]);
-            TCR_PROF_ADD(5);
           }
           __syncwarp();
         }
       }
       if (lane == 0) tc::commit(bempty);  // sB free once this group's MMAs retire
       __syncwarp();
-#ifdef IVRQ_TC_PROFILE
-      if (lane == 0) {
-        atomicAdd(&g_tcr_prof[3], (unsigned long long)(clock64() - _tg));
-        atomicAdd(&g_tcr_prof[7], (unsigned long long)ntile);
-      }
-#endif
     } else {
-      // ---- epilogue: row r of the tile is TMEM lane r (a warp reads lane quarter wid % 4); the two
-      // warps of a quarter split the group's queries.  Per-query scalars: lane i holds query j_lo + i.
-      const int quarter = wid & 3;
+      // ---- epilogue: row r of the tile is TMEM lane r (a warp reads lane quarter wid % 4); the
+      // TCR_EPQ warps of a quarter split the group's queries.  The group's per-query scalars are
+      // staged in shared memory (slot parity = group parity) by the first epilogue warps and read
+      // as broadcasts.
+      const int quarter = wid & 3, part = (wid - (TC_PROD + 1)) >> 2;
       const int r = quarter * 32 + lane;
-      const int jh = ((G >> 1) + 3) & ~3;
-      const int j_lo = ((wid - (TC_PROD + 1)) >> 2) * jh, j_hi = min(nqg, j_lo + jh);
       const int64_t rs = ip_row_stride(n_c);
-      double dq = 0.0, kb = 0.0, hs = 0.0, ls = 0.0;
-      int64_t rowb = 0;
-      if (j_lo + lane < j_hi) {
-        const int64_t pi = ps + j_lo + lane;
+      double4* qs = s_qs + (grp & 1) * 64;
+      const int et = tid - 32 * (TC_PROD + 1);  // 0 .. 32 TCR_EPI - 1
+      if (et < nqg) {
+        const int64_t pi = ps + et;
         const int64_t pr = a.porder[pi];
         const int64_t q = pr / a.nprobe;
-        dq = a.probe_d2[pr];
-        kb = a.scalars[q * IVRQ_QS_COUNT + IVRQ_QS_KB_SUM];
-        const int e = (int)a.scalars[q * IVRQ_QS_COUNT + IVRQ_QS_SLICE_EXP];
-        hs = ldexp(1.0, e - 26);
-        ls = ldexp(1.0, e - 54);
-        rowb = a.pair_base[c] + (pi - a.poff[c]) * rs;
+        qs[et] = make_double4(a.probe_d2[pr], a.scalars[q * IVRQ_QS_COUNT + IVRQ_QS_KB_SUM],
+                              ldexp(1.0, (int)a.scalars[q * IVRQ_QS_COUNT + IVRQ_QS_SLICE_EXP] - 26),
+                              __longlong_as_double(a.pair_base[c] + (pi - a.poff[c]) * rs));
       }
+      // the slots are rewritten two groups later, after every epilogue warp passed this group's
+      // first accumulator wait; all epilogue warps meet here so the writes are visible
+      asm volatile("bar.sync 1, %0;" ::"r"(32 * TCR_EPI) : "memory");
       for (int t = 0; t < ntile; ++t, ++tile_epi) {
         const int ab = tile_epi & 1;
         const int64_t v = (int64_t)t * TCM + r;
         float2 lf = make_float2(0.f, 0.f);
         if (v < n_c) lf = __ldg(reinterpret_cast<const float2*>(a.ix.long_factors) + lo + v);
+        const double lfx = (double)lf.x, lfy = (double)lf.y;
         wait1(&accf[ab], (tile_epi >> 1) & 1);
+        if (lane == 0 && wid == TC_PROD + 1) TCR_EV(5, tile_epi);
         tc::fence_after_sync();
-#ifdef IVRQ_TC_PROFILE
-        const long long _te = clock64();
+#ifdef IVRQ_EXP_NOEPI
+        if (false)
 #endif
-        for (int j0 = j_lo; j0 < j_hi; j0 += 4) {
+        for (int j0 = 8 * part; j0 < nqg; j0 += 8 * TCR_EPQ) {  // 8-query chunks, round robin over the parts
           uint32_t d[32];
-          tc::tmem_ld32(tbase + ((uint32_t)(quarter * 32) << 16) + ab * acc_stride + 8 * j0, d);
+          tc::tmem_ld32(tbase + ((uint32_t)(quarter * 32) << 16) + ab * acc_stride + TCR_DIG * j0, d);
           tc::tmem_ld_wait();
 #pragma unroll
-          for (int jj = 0; jj < 4; ++jj) {
+          for (int jj = 0; jj < 8; ++jj) {
             const int j = j0 + jj;
-            const int src = (j - j_lo) & 31;
-            const double q_dq = __shfl_sync(FULL, dq, src), q_kb = __shfl_sync(FULL, kb, src);
-            const double q_hs = __shfl_sync(FULL, hs, src), q_ls = __shfl_sync(FULL, ls, src);
-            const int64_t q_row = __shfl_sync(FULL, rowb, src);
-            if (j < j_hi && v < n_c) {
-              const int* D = reinterpret_cast<const int*>(d + 8 * jj);
-              const long long hi = (long long)D[0] * 2097152LL + (long long)D[1] * 16384LL + (long long)D[2] * 128LL + D[3];
-              const long long lw = (long long)D[4] * 2097152LL + (long long)D[5] * 16384LL + (long long)D[6] * 128LL + D[7];
-              const double ip = dadd(dmul((double)hi, q_hs), dmul((double)lw, q_ls));
-              // streaming store: written once, read once by scan_rd
-              __stcs(a.rdist + q_row + v, dmax(dsub(dadd((double)lf.x, q_dq), dmul((double)lf.y, dsub(ip, q_kb))), 0.0));
+            if (j < nqg && v < n_c) {
+              const double4 sq = qs[j];
+              const int* D = reinterpret_cast<const int*>(d + TCR_DIG * jj);
+              // hi = (D0 128 + D1) 2^14 + (D2 128 + D3): the int32 pairs cannot overflow (|D_s| <= U 64 kpad,
+              // the dense path's kpad <= 960 for 8-bit codes), hi < 2^47 is exact in float64.  The distance
+              // add + d_qc2 + scale (kb - hi 2^(e-26)) in this order: three roundings of at most 2^-53 M
+              // each, inside rd_radius_kernel's 2^-50 M
+              const double hi = fma((double)(D[0] * 128 + D[1]), 16384.0, (double)(D[2] * 128 + D[3]));
+              const double t = fma(-hi, sq.z, sq.y);
+              // streaming store: written once, read once by the per-query pass
+              __stcs(a.rdist + __double_as_longlong(sq.w) + v, fmaxf((float)fma(lfy, t, lfx + sq.x), 0.f));
             }
           }
         }
-#ifdef IVRQ_TC_PROFILE
-        if (lane == 0 && wid == TC_PROD + 1) atomicAdd(&g_tcr_prof[6], (unsigned long long)(clock64() - _te));
-#endif
+        if (lane == 0 && wid == TC_PROD + 1) TCR_EV(6, tile_epi);
         tc::fence_before_sync();
         tc::mbar_arrive(&acce[ab]);
       }
@@ -2289,7 +2692,53 @@ __global__ void __launch_bounds__(TCR_THREADS, 1) tc_refine_kernel(const __grid_
   }
   tc::fence_before_sync();
   __syncthreads();
-  if (wid == TC_PROD) tc::tmem_dealloc(tbase, tmem_cols(2 * N));
+  if (wid == TC_PROD) tc::tmem_dealloc(tbase, tmem_cols(2 * NCOL));
+}
+
+// Per-query radius of the approximate refined distances written by tc_refine_kernel:
+// |stored - exact| <= rrad[q] + |stored| 2^-23 for every vector of the query's probed lists.
+// With e the query's slice exponent, the neglected digits D4..D7 of each dimension are at most
+// L = 64 (128^3 + 128^2 + 128 + 1) = 135274560 in magnitude, so the neglected part of the inner
+// product is at most U kpad L 2^(e-54) (U = the largest code value, 2^bits - 1); the exact path's own
+// rounding of ip (|ip| <= U kpad 2^e) adds 2^-53 |ip|; through est2 = max(add + d_qc2 - scale (ip - kb), 0)
+// that scales by |scale| <= S, plus the float64 roundings of both evaluations, each at most 2^-52 of
+// M = |add| + d_qc2 + |scale| (|ip| + |kb|) (four operations).  lfmax = (max |add|, max |scale|) over the
+// index, as float bit patterns.  One thread per query.
+__global__ void rd_radius_kernel(const double* __restrict__ scalars, const double* __restrict__ probe_d2,
+                                 const uint32_t* __restrict__ lfmax, int64_t nq, int nprobe, int kp, int umax,
+                                 double* __restrict__ rrad) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nq) return;
+  const double* sc = scalars + q * IVRQ_QS_COUNT;
+  const int e = (int)sc[IVRQ_QS_SLICE_EXP];
+  double dqm = 0.0;
+  for (int p = 0; p < nprobe; ++p) dqm = fmax(dqm, probe_d2[q * nprobe + p]);
+  const double A = (double)__uint_as_float(lfmax[0]), S = (double)__uint_as_float(lfmax[1]);
+  const double U = (double)umax * (double)kp;
+  const double ipmax = ldexp(U, e);
+  const double trunc = S * (U * ldexp(135274560.0, e - 54) + ldexp(ipmax, -53));
+  const double M = A + dqm + S * (ipmax + fabs(sc[IVRQ_QS_KB_SUM]));
+  rrad[q] = (trunc + ldexp(M, -50)) * (1.0 + 0x1p-20);
+}
+
+// lfmax[0] = max |add|, lfmax[1] = max |scale| over the long factors (float bit patterns of
+// non-negative values order like the values, so an integer max is exact); lfmax zeroed by the caller
+__global__ void lf_max_kernel(const float2* __restrict__ lf, int64_t n, uint32_t* __restrict__ lfmax) {
+  uint32_t ma = 0u, ms = 0u;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float2 v = __ldg(lf + i);
+    ma = max(ma, __float_as_uint(fabsf(v.x)));
+    ms = max(ms, __float_as_uint(fabsf(v.y)));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ma = max(ma, __shfl_xor_sync(FULL, ma, o));
+    ms = max(ms, __shfl_xor_sync(FULL, ms, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(lfmax, ma);
+    atomicMax(lfmax + 1, ms);
+  }
 }
 
 // ------------------------------------------------------------ stage-1 inner products on tcgen05
@@ -2572,20 +3021,58 @@ __global__ void merge_topk_kernel(const int64_t* __restrict__ ids, const double*
   out_counts[q] = n;
 }
 
-template <int RS, int MB = 1>
-inline auto rd_kernel_for(bool refine, int ipb) {
-  return refine ? (ipb == 2 ? scan_rd_kernel<true, 2, RS, MB> : scan_rd_kernel<true, 4, RS, MB>)
-                : (ipb == 2 ? scan_rd_kernel<false, 2, RS, MB> : scan_rd_kernel<false, 4, RS, MB>);
-}
+template <bool REFINE, bool NIB>
+int launch_warp(const Args& a, int ipb, cudaStream_t s);
 
 inline int launch_rd(const Args& a, bool refine, int ipb, cudaStream_t s) {
   // 4 sub-chunks of 32 vectors per batch, register budget for 6 resident CTAs (B200 A/B: 1, 6, 8)
-  auto kern = rd_kernel_for<4, 6>(refine, ipb);
-  {
+  if (!refine) {
+    auto kern = ipb == 2 ? scan_rd_kernel<2, 4, 6> : scan_rd_kernel<4, 4, 6>;
     KernelTimer kt("scan_rd_kernel", s);
     kern<<<(unsigned)ceil_div(a.nq, RDW), RDW * 32, 0, s>>>(a);
+    return check_launch("ivrq_search_scan");
   }
-  return check_launch("ivrq_search_scan");
+#ifndef RDA_MINB
+#define RDA_MINB 4
+#endif
+  auto kern = ipb == 2 ? scan_rda_kernel<2, 4, RDA_MINB> : scan_rda_kernel<4, 4, RDA_MINB>;
+  const size_t sm = (size_t)RDW * ((size_t)a.kpad * sizeof(int2) + 32 * 16);
+  if (sm > 48 * 1024 && cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess)
+    return fail(IVRQ_EUNSUP, "ivrq_search_scan: shared memory request too large");
+  // the digit tables are shared memory per warp: ask for the full carveout so the register budget
+  // (6 CTAs per SM), not the L1/shared split, sets the residency
+  cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  {
+    KernelTimer kt("scan_rd_kernel", s);
+    kern<<<(unsigned)ceil_div(a.nq, RDW), RDW * 32, sm, s>>>(a);
+  }
+  IVRQ_TRY(check_launch("ivrq_search_scan"));
+  {
+    const size_t fsm = (size_t)a.kpad * sizeof(int2) + 32 * 16;
+    if (fsm > 48 * 1024 &&
+        cudaFuncSetAttribute(rda_final_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm) != cudaSuccess)
+      return fail(IVRQ_EUNSUP, "ivrq_search_scan: shared memory request too large");
+    rda_final_kernel<<<(unsigned)a.nq, FIN_W * 32, fsm, s>>>(a);
+    IVRQ_TRY(check_launch("ivrq_search_scan(final exact top k)"));
+  }
+#ifdef IVRQ_RDA_STATS
+  {
+    unsigned long long h[6];
+    cudaMemcpyFromSymbolAsync(h, g_rda_stats, sizeof(h), 0, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    fprintf(stderr, "[rda] queries %llu prune-resolutions %llu exact-values %llu mean rq/T %.3g reruns %llu\n", h[2],
+            h[0], h[1], h[2] ? h[3] * 1e-12 / h[2] : 0.0, h[4]);
+    static const unsigned long long zero[6] = {};
+    cudaMemcpyToSymbolAsync(g_rda_stats, zero, sizeof(zero), 0, cudaMemcpyHostToDevice, s);
+  }
+#endif
+  // the exact rerun of the queries the approximate pass could not certify (normally none: the
+  // grid's warps return at once)
+  Args f = a;
+  f.fix_only = a.fix_list;
+  f.fix_only_count = a.fix_count;
+  f.init_ids = a.init_ids;
+  return rcode_nibbles(a.ix.bits) ? launch_warp<true, true>(f, ipb, s) : launch_warp<true, false>(f, ipb, s);
 }
 
 template <bool REFINE, bool NIB>
@@ -2666,19 +3153,21 @@ static ScanPolicy scan_policy(const ivrq_index_view& ix, const ivrq_search_param
   return sp;
 }
 
-// tc_refine group size and A ring depth: the largest query group whose digit slices fit beside
-// a ring of >= 3 A stages (C3, D = 768: G = 28, 3 stages; scan stage measured 2.72 ms against
-// 2.78 (G = 24, 4 stages), 2.88 (20, 5), 3.19 (16, 6), 3.64 (12, 8))
+// tc_refine group size and A ring depth: the largest query group (<= 64: 4 G accumulator columns,
+// double-buffered in 512) whose digit rows fit beside a ring of >= TCR_MIN_ST A stages
+#ifndef TCR_MIN_ST
+#define TCR_MIN_ST 5
+#endif
 static bool tc_refine_shape(int kpad, int& G, int& nst) {
   const size_t cap = 227 * 1024;
 #ifdef TCR_FORCE_G  // development A/B builds only
   G = TCR_FORCE_G;
-  for (nst = 8; nst >= 2; --nst)
+  for (nst = 10; nst >= 2; --nst)
     if (tc_smem_bytes(kpad, G, nst) <= cap) return true;
   return false;
 #endif
-  for (G = 32; G >= 4; G -= 4) {
-    for (nst = 8; nst >= 3; --nst)
+  for (G = 64; G >= 4; G -= 4) {
+    for (nst = 10; nst >= TCR_MIN_ST; --nst)
       if (tc_smem_bytes(kpad, G, nst) <= cap) return true;
   }
   return false;
@@ -2744,7 +3233,6 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
   a.out_counts = out_counts;
   a.stats = stats;
   a.l2_prefetch = 0;  // measured neutral
-  a.rd_prefetch = 1;  // scan_rd: refined distances read with the stage-1 inputs (fewer dependent loads)
   const bool nib = rcode_nibbles(index->bits);
   cudaStream_t s = as_stream(stream);
   const int64_t nl = index->n_clusters;
@@ -2887,7 +3375,7 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
     if (excl == 2) {
       tot[0] = 0;
     } else if (index->max_list > 0 &&
-               npairs * scan::ip_row_stride(index->max_list) * (ipb + (pol.rd_path && refine ? 8 : 0)) <=
+               npairs * scan::ip_row_stride(index->max_list) * (ipb + (pol.rd_path && refine ? 4 : 0)) <=
                    (int64_t(8) << 30)) {
       tot[0] = npairs * scan::ip_row_stride(index->max_list);
     } else if (cudaMemcpyAsync(tot, ptot, sizeof(tot), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
@@ -2905,17 +3393,35 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
         int G = 0, nb = 0;
         if (!scan::tc_refine_shape(a.kpad, G, nb))
           return fail(IVRQ_EUNSUP, "ivrq_search_scan: dims too large for the tensor-core refine");
-        double* rdist = nullptr;
-        int32_t* rgpre = nullptr;
+        float* rdist = nullptr;
+        double* rrad = nullptr;
+        int32_t *rgpre = nullptr, *fix = nullptr;
+        uint32_t* lfmax = nullptr;
         int64_t* rscratch = nullptr;
         int8_t* tcsl = nullptr;
         const int nkc = (a.kpad + scan::TCKC - 1) / scan::TCKC;
         if (!ws.alloc(rdist, (size_t)tot[0]) || !ws.alloc(rgpre, nl + 1) || !ws.alloc(rscratch, nl + 3) ||
-            !ws.alloc(tcsl, (size_t)nq * nkc * 1024))
+            !ws.alloc(tcsl, (size_t)npairs * nkc * 512) || !ws.alloc(rrad, nq) || !ws.alloc(fix, nq + 1) ||
+            !ws.alloc(lfmax, 2))
           return oom("refined-distance buffer allocation failed");
+        if (index->size >= (int64_t(1) << 40) || a.nprobe >= (1 << 20))
+          return fail(IVRQ_EUNSUP, "ivrq_search_scan: index or n_probe too large for the refine pass");
         scan::pair_plan_kernel<<<1, 1024, 0, s>>>(index->offsets, poff, (int)nl, G, rscratch, rgpre, rscratch + nl + 1);
         IVRQ_TRY(check_launch("ivrq_search_scan(refine plan)"));
-        scan::tc_slices_kernel<<<(unsigned)ceil_div(nq * nkc * 64, 256), 256, 0, s>>>(qslices, nq, a.kpad, nkc, tcsl);
+        scan::tc_bpairs_kernel<<<(unsigned)ceil_div(npairs * nkc * 32, 256), 256, 0, s>>>(
+            qslices, porder, pslot, npairs, a.nprobe, a.kpad, nkc, tcsl);
+        cudaMemsetAsync(lfmax, 0, 2 * sizeof(uint32_t), s);
+        cudaMemsetAsync(fix, 0, sizeof(int32_t), s);
+        scan::lf_max_kernel<<<(unsigned)(2 * sm_count_of_current_device()), 256, 0, s>>>(
+            reinterpret_cast<const float2*>(index->long_factors), index->size, lfmax);
+        scan::rd_radius_kernel<<<(unsigned)ceil_div(nq, 128), 128, 0, s>>>(
+            scalars, probe_d2, lfmax, nq, a.nprobe, a.kpad, (1 << index->bits) - 1, rrad);
+        IVRQ_TRY(check_launch("ivrq_search_scan(refine radius)"));
+        a.rrad = rrad;
+        a.fix_count = fix;
+        a.fix_list = fix + 1;
+        if (!ws.alloc(a.fin_d, (size_t)nq * 32) || !ws.alloc(a.fin_e, (size_t)nq * 32))
+          return oom("refined-distance buffer allocation failed");
         scan::TcArgs ta{};
         // A: the rcode rows (8-bit codes; 4-bit indexes are unpacked by the producer warps instead)
         if (!nib && !tc::make_tmap_u8_sw128(&ta.map_a, index->rcodes, (uint64_t)index->rcode_bytes,
@@ -2923,6 +3429,7 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
                                             scan::TCM))
           return fail(IVRQ_ECUDA, "ivrq_search_scan: TMA tensor map encoding failed");
         ta.bslices = tcsl;
+        ta.npairs = npairs;
         ta.ix = *index;
         ta.kpad = a.kpad;
         ta.G = G;
@@ -2946,17 +3453,21 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
             KernelTimer kt("tc_refine_kernel", s);
             scan::tc_refine_kernel<<<(unsigned)sm_count_of_current_device(), scan::TCR_THREADS, tsm, s>>>(ta);
           }
-#ifdef IVRQ_TC_PROFILE
+#ifdef IVRQ_TCR_TRACE
           {
-            unsigned long long h[8];
-            cudaMemcpyFromSymbolAsync(h, scan::g_tcr_prof, sizeof(h), 0, cudaMemcpyDeviceToHost, s);
+            static std::vector<unsigned long long> h(16 * 4096);
+            cudaMemcpyFromSymbolAsync(h.data(), scan::g_tcr_trace, h.size() * 8, 0, cudaMemcpyDeviceToHost, s);
             cudaStreamSynchronize(s);
-            const double tot = (double)h[3];
-            fprintf(stderr, "[tc_refine prof] share of MMA-lane group time: wait B %.3f wait acc %.3f wait A %.3f | "
-                    "producer wait-empty/MMA %.3f | epi wait %.3f busy %.3f (per CTA-warp vs MMA total) tiles %llu\n",
-                    h[0] / tot, h[1] / tot, h[2] / tot, h[4] / tot, h[5] / tot, h[6] / tot, h[7]);
-            static const unsigned long long zero[8] = {};
-            cudaMemcpyToSymbolAsync(scan::g_tcr_prof, zero, sizeof(zero), 0, cudaMemcpyHostToDevice, s);
+            if (const char* path = getenv("IVRQ_TCR_TRACE_OUT")) {
+              if (FILE* f = fopen(path, "wb")) {
+                fwrite(h.data(), 8, h.size(), f);
+                fclose(f);
+              }
+            }
+            cudaMemsetAsync(nullptr, 0, 0, s);
+            void* sym = nullptr;
+            cudaGetSymbolAddress(&sym, scan::g_tcr_trace);
+            cudaMemsetAsync(sym, 0, h.size() * 8, s);
           }
 #endif
           return check_launch("ivrq_search_scan(tensor-core refine)");

@@ -386,10 +386,10 @@ extern "C" int ivrq_prepare_queries(const double* q_rot, int64_t nq, int32_t dim
   if (!params) return fail(IVRQ_EINVAL, "ivrq_prepare_queries: null params");
   if (params->ip_mode == IVRQ_IP_BITWISE && (params->query_bits < 2 || params->query_bits > 8))
     return fail(IVRQ_EINVAL, "query_bits must be in [2, 8]");
+  if (nq == 0) return IVRQ_OK;  // empty batches: the (empty) buffers may be null
   if (params->ip_mode == IVRQ_IP_BITWISE && !planes) return fail(IVRQ_EINVAL, "bitwise mode needs planes");
   if (params->ip_mode == IVRQ_IP_LUT && !luts) return fail(IVRQ_EINVAL, "lut mode needs luts");
   if (params->refine && index_bits >= 2 && !qslices) return fail(IVRQ_EINVAL, "refine needs qslices");
-  if (nq == 0) return IVRQ_OK;
   // rows staged in shared memory (up to 48 KB per block: 4 warps at D <= 1536, fewer beyond)
   int wpb = 4;
   while (wpb > 1 && (size_t)wpb * dims * sizeof(double) > 48 * 1024) --wpb;

@@ -432,3 +432,33 @@ def test_search_batch_short_rows(monkeypatch, chunks):
     for i in range(len(q)):
         np.testing.assert_array_equal(res[i][0], ids[i, : counts[i]])
         np.testing.assert_array_equal(res[i][1], dists[i, : counts[i]])
+
+
+@pytest.mark.parametrize("k,copies,bits", [(10, 40, 8), (30, 6, 8), (10, 12, 4)])
+def test_refine_intervals_near_duplicates(monkeypatch, k, copies, bits):
+    """Near-duplicate vectors (distances apart by ~1e-7 relative, well inside the approximate
+    refine's radius) force every interval decision of scan_rda_kernel open: the exact threshold
+    from the list-start queue, the final exact top k, and (k = 30: more than 32 - k near-ties)
+    the exact rerun.  The dense tcgen05 refine must equal the exact per-query popcount path."""
+    rng = np.random.default_rng(k * 100 + copies)
+    d = 128
+    base = (rng.standard_normal((300, d)) * 2.0).astype(np.float64)
+    x = np.repeat(base, copies, axis=0)
+    x = x * (1.0 + 1e-7 * rng.standard_normal(x.shape))
+    x[::5] = np.repeat(base, copies, axis=0)[::5]  # some exact copies: ties broken by id
+    x = x.astype(np.float32)
+    q = (base[rng.integers(0, 300, 200)] + 0.05 * rng.standard_normal((200, d))).astype(np.float32)
+    ix = iv.build_index(x, iv.BuildParams(n_clusters=8, quant=iv.QuantizationParams(bits=bits), kmeans_iters=3,
+                                          seed=1))
+    sp = iv.SearchParams(k=k, n_probe=4, ip_mode="bitwise", query_bits=4)
+    qd = dev.to_device(q)
+    out = {}
+    for name, env in {"popcount": {"IVRQ_TC_STAGE1": "0"}, "tcgen05": {"IVRQ_TC_IP": "1", "IVRQ_TC_REFINE": "1"}}.items():
+        for key in ("IVRQ_TC_STAGE1", "IVRQ_TC_IP", "IVRQ_TC_REFINE"):
+            monkeypatch.delenv(key, raising=False)
+        for key, val in env.items():
+            monkeypatch.setenv(key, val)
+        r = search_device(qd, ix, sp, with_stats=True)
+        out[name] = [dev.to_host(t) for t in (r.ids, r.dists, r.counts, r.stats)]
+    for a, b in zip(out["popcount"], out["tcgen05"]):
+        np.testing.assert_array_equal(a, b)

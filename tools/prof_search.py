@@ -44,6 +44,14 @@ def main() -> None:
     sp = iv.SearchParams(k=bench.K, n_probe=args.nprobe, ip_mode=args.mode)
     search_device(q, ix, sp)  # warm-up (allocator pools, tensor maps) outside the profiled range
     torch.cuda.synchronize()
+    import ctypes
+    import os
+
+    from paper_2602_23999_b200 import _lib
+
+    timing = os.environ.get("IVRQ_KERNEL_TIMING") == "1"
+    if timing:
+        _lib.call("ivrq_kernel_timing", 1)
     torch.cuda.profiler.start()  # ncu --profile-from-start off: only the searches below are captured
     for _ in range(args.reps):
         ev: dict = {}
@@ -62,6 +70,13 @@ def main() -> None:
         )
     torch.cuda.synchronize()
     torch.cuda.profiler.stop()
+    if timing:
+        _lib.call("ivrq_kernel_timing", 0)
+        for kn in ("tc_refine_kernel", "tc_ip_kernel", "ip_list_kernel", "scan_rd_kernel", "scan_warp_kernel"):
+            tot, n = ctypes.c_double(0.0), ctypes.c_int64(0)
+            _lib.call("ivrq_kernel_time", kn.encode(), ctypes.byref(tot), ctypes.byref(n))
+            if n.value:
+                print(f"{kn} {tot.value / n.value:.4f} ms x{n.value}", file=sys.stderr)
 
 
 if __name__ == "__main__":

@@ -313,16 +313,17 @@ __global__ void __launch_bounds__(128) mma_rate(long long* out, int reps) {
 // same, but A cycles through 6 distinct 16 KB stage tiles and B walks 6 distinct 128-byte K chunks
 // (the refine kernel's smem footprint), optionally with TMA refilling the A stages concurrently
 template <int N>
-__global__ void __launch_bounds__(128) mma_rate_stream(long long* out, int reps, const __grid_constant__ CUtensorMap ma,
+__global__ void __launch_bounds__(384) mma_rate_stream(long long* out, int reps, const __grid_constant__ CUtensorMap ma,
                                                        int with_tma) {
   extern __shared__ __align__(1024) unsigned char sm_raw[];
   unsigned char* sm = reinterpret_cast<unsigned char*>(((uintptr_t)sm_raw + 1023) & ~(uintptr_t)1023);
   unsigned char* sa = sm;                 // 6 x 16 KB
-  unsigned char* sb = sm + 6 * 128 * 128; // 6 x N x 128
+  constexpr int SB = N <= 128 ? 6 : 2;   // B chunks resident (smem budget)
+  unsigned char* sb = sm + 6 * 128 * 128; // SB x N x 128
   __shared__ uint64_t bar, tbar, cbar, tbar2;
   __shared__ uint32_t taddr_s;
   const int tid = threadIdx.x, wid = tid >> 5;
-  for (int i = tid; i < (6 * 128 + 6 * N) * 128; i += 128) sm[i] = (unsigned char)(i * 7);
+  for (int i = tid; i < (6 * 128 + SB * N) * 128; i += blockDim.x) sm[i] = (unsigned char)(i * 7);
   if (wid == 0) tc::tmem_alloc(&taddr_s, 512);
   if (tid == 0) {
     tc::mbar_init(&bar, 1);
@@ -345,7 +346,7 @@ __global__ void __launch_bounds__(128) mma_rate_stream(long long* out, int reps,
       if (with_tma & 16) tc::mbar_wait(&tbar2, 0);  // a (satisfied) barrier wait per stage
       for (int s2 = 0; s2 < 4; ++s2)
         tc::mma_i8(taddr_s, tc::smem_desc_sw128(sa + st * 16384 + 32 * s2),
-                   tc::smem_desc_sw128(sb + st * N * 128 + 32 * s2), idesc, r | s2);
+                   tc::smem_desc_sw128(sb + (st % SB) * N * 128 + 32 * s2), idesc, r | s2);
       if (with_tma & 2) tc::commit(&cbar);  // a commit per stage, as in the refine kernel
     }
     const long long t1 = clock64();
@@ -353,6 +354,22 @@ __global__ void __launch_bounds__(128) mma_rate_stream(long long* out, int reps,
     tc::mbar_wait(&bar, 0);
     out[2 * blockIdx.x] = t1 - t0;
     out[2 * blockIdx.x + 1] = clock64() - t0;
+  } else if (wid >= 2 && (with_tma & 32)) {
+    // epilogue-like load: tcgen05.ld of 32 columns, int64 assembly and float64 arithmetic, global stores
+    const int q4 = wid & 3;
+    double acc = 1.0;
+    for (int r = 0; r < reps / 2; ++r) {
+      uint32_t v[32];
+      tc::tmem_ld32(taddr_s + ((uint32_t)(q4 * 32) << 16) + 256 + (r % 4) * 32, v);
+      tc::tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const long long hi = (long long)(int)v[4 * j] * 2097152LL + (long long)(int)v[4 * j + 1] * 16384LL +
+                             (long long)(int)v[4 * j + 2] * 128LL + (int)v[4 * j + 3];
+        acc = __dadd_rn(__dmul_rn((double)hi, 0x1p-30), __dmul_rn(acc, 0.999));
+      }
+    }
+    if (acc == 12345.0) out[0] = (long long)acc;
   } else if (wid >= 2 && (with_tma & 4)) {
     // concurrent TMEM reads of another accumulator region (the epilogue's tcgen05.ld)
     const int q4 = wid & 3;
@@ -446,9 +463,9 @@ void rate_stream(int with_tma) {
   cudaMemset(src, 1, 4096 * 128);
   CUtensorMap ma;
   tc::make_tmap_u8_sw128(&ma, src, 128, 4096, 128, 128, 128);
-  const int smem = (6 * 128 + 6 * N) * 128 + 1024;
+  const int smem = (6 * 128 + (N <= 128 ? 6 : 2) * N) * 128 + 1024;
   cudaFuncSetAttribute(mma_rate_stream<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  mma_rate_stream<N><<<blocks, 128, smem>>>(d, reps, ma, with_tma);
+  mma_rate_stream<N><<<blocks, (with_tma & 32) ? 384 : 128, smem>>>(d, reps, ma, with_tma);
   cudaError_t e = cudaDeviceSynchronize();
   std::vector<long long> h(2 * blocks);
   cudaMemcpy(h.data(), d, h.size() * 8, cudaMemcpyDeviceToHost);
@@ -547,6 +564,11 @@ int main() {
   rate_sbo<64>(6144);
   rate_stream<224>(0);
   rate_stream<224>(2 | 8 | 16);
+  rate_stream<128>(32);
+  rate_stream<128>(32 | 1);
+  rate_stream<208>(0);
+  rate_stream<208>(32);
+  rate_stream<208>(32 | 1 | 2 | 8 | 16);
   rate<64>();
   rate<128>();
   rate<224>();
