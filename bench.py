@@ -259,9 +259,11 @@ def kernel_roofline(kernel_ms: dict, peaks: dict, probed: int, survivors: int, d
     """Roofline of the scan's dominant kernel (largest CUDA-event time in the timed region).
 
     Algorithmic work per launch:
-      tc_refine_kernel  int8 tensor ops 2 * probed * kpad * 8 (8 digit slices of every probed pair)
+      tc_refine_kernel  int8 tensor ops 2 * probed * kpad * R: R = 4 leading query digits, plus the two
+                        stage-1 sums (u and s8(u) against qhat) when they are fused in (8-bit codes)
       tc_ip/ip_list     int8 tensor ops 2 * probed * 32 ceil(D/32) * 4 (4-bit query planes)
-      scan_rd_kernel    bytes probed * (2 + 12) + survivors * 8 (ip, factors; refined distance)
+      scan_rd_kernel    bytes probed * (2 + 12) + survivors * 4 (ip, factors; float32 refined distance)
+                        (1-bit indexes: probed * 14)
       scan_warp_kernel  bytes probed * (2 + 12) + survivors * (rcode row + 8) (ip, factors; codes, long factors)
     """
     if not kernel_ms:
@@ -273,18 +275,20 @@ def kernel_roofline(kernel_ms: dict, peaks: dict, probed: int, survivors: int, d
     hbm = float(peaks.get("hbm_gbs", 6650.0))
     src = "MEASURED_PEAKS.json" if "_fallback" not in peaks else "fallback"
     if name in ("tc_refine_kernel", "tc_ip_kernel", "ip_list_kernel"):
-        work = 2.0 * probed * (kpad * 8 if name == "tc_refine_kernel" else 32 * g * 4)
+        rows = 4 + (2 if bits == 8 else 0)
+        work = 2.0 * probed * (kpad * rows if name == "tc_refine_kernel" else 32 * g * 4)
         achieved = work / (avg_ms / 1e3) / 1e12
         peak, psrc = int8_peak(peaks)
         out = {"bound": "tensor", "unit": "TFLOP/s", "op": "int8 multiply-add (x2), TOP/s",
                "peak_source": psrc,
-               "work_formula": "2*probed*kpad*8" if name == "tc_refine_kernel" else "2*probed*32*ceil(D/32)*4"}
+               "work_formula": f"2*probed*kpad*{rows}" if name == "tc_refine_kernel" else "2*probed*32*ceil(D/32)*4"}
     else:
-        work = probed * 14.0 + survivors * (8.0 if name == "scan_rd_kernel" else rb + 8.0)
+        per_surv = (4.0 if bits > 1 else 0.0) if name == "scan_rd_kernel" else rb + 8.0
+        work = probed * 14.0 + survivors * per_surv
         achieved = work / (avg_ms / 1e3) / 1e9
         peak = hbm
         out = {"bound": "hbm", "unit": "GB/s", "peak_source": f"{src} hbm_gbs",
-               "work_formula": "probed*14 + survivors*" + ("8" if name == "scan_rd_kernel" else f"({rb}+8)")}
+               "work_formula": f"probed*14 + survivors*{per_surv:g}"}
     out.update({"kernel": name, "achieved": round(achieved, 1), "peak": round(peak, 1),
                 "frac": round(achieved / peak, 4), "work_per_launch": int(work),
                 "kernel_ms_per_launch": round(avg_ms, 4), "launches_timed": launches,

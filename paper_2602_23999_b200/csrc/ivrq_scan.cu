@@ -1223,6 +1223,45 @@ __device__ __noinline__ void exactify_top(const ExactCtx& c, const int2* hl, con
   warp_sort32(qd, qi, EntryLess{pids});
 }
 
+// The float64 prune test (stage1_keep64) against an interval [T_lo, T_hi] of the threshold: 1 keep
+// for every T in it, 0 prune for every T in it, -1 open.
+__device__ __noinline__ int decide64(int ipv, float fa, float fs, float fe, double d_qc2, double delta,
+                                     double half_code, double sq, double ipm, double T_lo, double T_hi) {
+  const double scale = (double)fs;
+  const double est2 = dmax(dsub(dadd((double)fa, d_qc2), dmul(scale, dsub(dmul(delta, (double)ipv), half_code))), 0.0);
+  if (stage1_keep64(est2, (double)fe, scale, sq, ipm, T_lo)) return 1;
+  if (!stage1_keep64(est2, (double)fe, scale, sq, ipm, T_hi)) return 0;
+  return -1;
+}
+
+// The exact threshold of a list: exact values for the list-start queue's possible members
+// (snap_d / snap_e, shared memory), its k-th value after the re-sort.  Warp-collective, out of line.
+__device__ __noinline__ double resolve_threshold(const uint8_t* rcodes, const float* lfac, const double* pd2,
+                                                 const int8_t* qs, const int64_t* pids, int64_t rb, int kp, int sexp,
+                                                 double kb, double rq, bool nib, int2* hl, double* snap_d,
+                                                 int64_t* snap_e, int k) {
+  ExactCtx ec;
+  ec.rcodes = rcodes;
+  ec.lf = reinterpret_cast<const float2*>(lfac);
+  ec.pd2 = pd2;
+  ec.qs = qs;
+  ec.rb = rb;
+  ec.kp = kp;
+  ec.sexp = sexp;
+  ec.kb = kb;
+  ec.rq = rq;
+  ec.nib = nib;
+  load_hl(ec, hl);
+  const int lane = threadIdx.x & 31;
+  double sd = snap_d[lane];
+  int64_t se = snap_e[lane];
+  exactify_top(ec, hl, pids, sd, se, k);
+  snap_d[lane] = sd;  // the list-start queue, now exact where it matters (a second open test reuses it)
+  snap_e[lane] = se;
+  __syncwarp();
+  return __shfl_sync(FULL, sd, k - 1);
+}
+
 #ifdef IVRQ_RDA_STATS  // development builds only: how often the intervals leave decisions open
 __device__ unsigned long long g_rda_stats[6];  // prune resolutions, exact values, queries, sum rq/T (1e-12), reruns
 #define RDA_STAT(i, v) (((threadIdx.x & 31) == 0) ? (void)atomicAdd(&g_rda_stats[i], (unsigned long long)(v)) : (void)0)
@@ -1264,7 +1303,11 @@ __global__ void __launch_bounds__(RDW * 32, MINB) scan_rda_kernel(Args a) {
     const bool maybe = e != NO_ID && dsub(d, entry_rad(d, e, rq)) <= kd + entry_rad(kd, ke, rq);
     if (!__any_sync(FULL, maybe)) return;
     warp_fold(qd, qi, maybe ? d : dinf(), maybe ? e : NO_ID, maybe, 32, lt);
-    // the 32nd slot a possible member: a candidate pushed out of the queue may have been one
+  };
+  // The 32nd slot a possible member: a candidate pushed out of the queue may have been one.  Checked
+  // once per list: pushed-out values are >= the final 32nd value, s - rad(s) increases with s and
+  // the k-th value only decreases, so a 32nd slot that is not a possible member now never was.
+  auto check_saturation = [&]() {
     const double nk = __shfl_sync(FULL, qd, k - 1);
     const int64_t nke = __shfl_sync(FULL, qi, k - 1);
     const double d31 = __shfl_sync(FULL, qd, 31);
@@ -1331,51 +1374,26 @@ __global__ void __launch_bounds__(RDW * 32, MINB) scan_rda_kernel(Args a) {
         for (int u = 0; u < RSUB; ++u) {
           const int64_t vi = c0 + u * 32 + lane;
           dec[u] = vi < n_c ? stage1_decide_f32(ipv[u], fa[u], fs[u], fe[u], f32) : 0;
-          if (dec[u] < 0) {
-            const double scale = (double)fs[u];
-            const double est2 =
-                dmax(dsub(dadd((double)fa[u], d_qc2), dmul(scale, dsub(dmul(delta, (double)ipv[u]), half_code))), 0.0);
-            if (stage1_keep64(est2, (double)fe[u], scale, sq, ipm, T_list - rT)) dec[u] = 1;
-            else if (!stage1_keep64(est2, (double)fe[u], scale, sq, ipm, T_list + rT)) dec[u] = 0;
-            open |= dec[u] < 0;
-          }
+          // the float64 test inside the float32 band (about 1e-5 of the vectors), out of line
+          if (dec[u] < 0)
+            dec[u] = decide64(ipv[u], fa[u], fs[u], fe[u], d_qc2, delta, half_code, sq, ipm, T_list - rT, T_list + rT);
+          open |= dec[u] < 0;
         }
         if (__any_sync(FULL, open)) {
           // the threshold's interval leaves a test open: exact values for the list-start
           // queue's possible members give the exact T for the rest of this list
-          // (the context is built here, not held in registers through the stream)
-          ExactCtx ec;
-          ec.rcodes = a.ix.rcodes;
-          ec.lf = reinterpret_cast<const float2*>(a.ix.long_factors);
-          ec.pd2 = a.probe_d2 + q * a.nprobe;
-          ec.qs = a.qslices + q * SLICES * (int64_t)kp;
-          ec.rb = a.ix.rcode_bytes;
-          ec.kp = kp;
-          ec.sexp = (int)sc[IVRQ_QS_SLICE_EXP];
-          ec.kb = sc[IVRQ_QS_KB_SUM];
-          ec.rq = rq;
-          ec.nib = rcode_nibbles(a.ix.bits);
-          if (!hl_ready) {
-            load_hl(ec, hl);
-            hl_ready = true;
-          }
-          RDA_STAT(0, 1);
-          double sd = snap_d[lane];
-          int64_t se = snap_e[lane];
-          exactify_top(ec, hl, a.ix.pids, sd, se, k);
-          T_list = __shfl_sync(FULL, sd, k - 1);
+          if (!hl_ready) hl_ready = true;
+          T_list = resolve_threshold(a.ix.rcodes, a.ix.long_factors, a.probe_d2 + q * a.nprobe,
+                                     a.qslices + q * SLICES * (int64_t)kp, a.ix.pids, a.ix.rcode_bytes, kp,
+                                     (int)sc[IVRQ_QS_SLICE_EXP], sc[IVRQ_QS_KB_SUM], rq, rcode_nibbles(a.ix.bits), hl,
+                                     snap_d, snap_e, k);
           rT = 0.0;
           f32.T_lo = __double2float_rd(T_list);
           f32.T_hi = __double2float_ru(T_list);
 #pragma unroll
-          for (int u = 0; u < RSUB; ++u) {
-            if (dec[u] < 0) {
-              const double scale = (double)fs[u];
-              const double est2 = dmax(
-                  dsub(dadd((double)fa[u], d_qc2), dmul(scale, dsub(dmul(delta, (double)ipv[u]), half_code))), 0.0);
-              dec[u] = stage1_keep64(est2, (double)fe[u], scale, sq, ipm, T_list) ? 1 : 0;
-            }
-          }
+          for (int u = 0; u < RSUB; ++u)
+            if (dec[u] < 0)
+              dec[u] = decide64(ipv[u], fa[u], fs[u], fe[u], d_qc2, delta, half_code, sq, ipm, T_list, T_list);
         }
         bool keep[RSUB];
 #pragma unroll
@@ -1396,6 +1414,7 @@ __global__ void __launch_bounds__(RDW * 32, MINB) scan_rda_kernel(Args a) {
         }
       }
     }
+    check_saturation();
     const int cnt = __popc(__ballot_sync(FULL, lane < k && qi != NO_ID));
     if (cnt >= k) {  // search.py:444-447, as an interval
       T = __shfl_sync(FULL, qd, k - 1);
@@ -2409,6 +2428,11 @@ struct TcArgs {
   const int64_t* pair_base; // [nlist + 1]
   const int32_t* gpre;      // [nlist + 1] prefix of ceil(bucket / G)
   float* rdist;             // approximate refined distances (radius: rd_radius_kernel)
+  // fused stage 1 (8-bit codes): the binary inner products <msb(u), qhat> from the same rcode tiles,
+  // as (sum u qhat - sum s8(u) qhat) / 256 with u read as unsigned and as signed bytes
+  const int8_t* bqhat;      // [nkc][npairs][128 B] (tc_qpairs_kernel), or null
+  void* ipbuf;
+  int ip32;
 };
 
 // byte offset of (row R, byte k < 128) in a 128B-swizzled K-major tile (8-row atoms of 1024 B)
@@ -2447,14 +2471,42 @@ __global__ void tc_bpairs_kernel(const int8_t* __restrict__ qslices, const int64
   *reinterpret_cast<uint4*>(out + blk * 512 + d * 128 + (((c16 ^ R) & 7) << 4)) = v;
 }
 
+// The fused stage 1's B operand: out[kc][i] (128 bytes) = the quantized query row (qhat_kernel) of
+// pair i, K bytes [128 kc, 128 kc + 128) in dimension order (the rcode byte order of 8-bit codes),
+// pre-swizzled as row (slot & 7) of a 128B-swizzled 8-row atom; zero past the row.
+__global__ void tc_qpairs_kernel(const int8_t* __restrict__ qhat, const int64_t* __restrict__ porder,
+                                 const int32_t* __restrict__ pslot, int64_t npairs, int nprobe, int rowb, int nkc,
+                                 int8_t* __restrict__ out) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // one 16-byte chunk
+  if (t >= npairs * nkc * 8) return;
+  const int c16 = (int)(t & 7);
+  const int64_t blk = t >> 3;  // (kc, i), kc major
+  const int64_t i = blk % npairs;
+  const int kc = (int)(blk / npairs);
+  const int64_t pr = porder[i];
+  const int32_t slot = pslot[pr];
+  if (slot < 0) return;
+  const int P0 = kc * TCKC + 16 * c16;
+  uint4 v = make_uint4(0u, 0u, 0u, 0u);
+  if (P0 < rowb) v = *reinterpret_cast<const uint4*>(qhat + (pr / nprobe) * (int64_t)rowb + P0);
+  const int R = slot & 7;
+  *reinterpret_cast<uint4*>(out + blk * 128 + (((c16 ^ R) & 7) << 4)) = v;
+}
+
 __host__ __device__ inline uint32_t tmem_cols(int n) {  // power of two >= 32 (<= 512)
   return n <= 32 ? 32u : n <= 64 ? 64u : n <= 128 ? 128u : n <= 256 ? 256u : 512u;
 }
 
-size_t tc_smem_bytes(int kpad, int G, int nst) {
+__host__ __device__ inline int round16(int n) { return (n + 15) & ~15; }
+
+size_t tc_smem_bytes(int kpad, int G, int nst, bool fused) {
   const int nkc = (kpad + TCKC - 1) / TCKC;
-  return 1024 + (size_t)nkc * TCR_DIG * G * TCKC + (size_t)nst * TCM * TCKC + 256 + 2 * 64 * sizeof(double4);
+  return 1024 + (size_t)nkc * (TCR_DIG * G + (fused ? round16(G) : 0)) * TCKC + (size_t)nst * TCM * TCKC + 256 +
+         2 * 64 * sizeof(double4);
 }
+
+// accumulator columns of one tile: 4 digit columns per query, and the fused stage 1's two sums
+__host__ __device__ inline int tc_ncol(int G, bool fused) { return TCR_DIG * G + (fused ? 2 * round16(G) : 0); }
 
 #ifdef IVRQ_TCR_TRACE  // development builds only: timeline of CTA 0's roles (plain stores, no atomics)
 __device__ unsigned long long g_tcr_trace[16 * 4096];
@@ -2471,9 +2523,13 @@ __global__ void __launch_bounds__(TCR_THREADS, 1) tc_refine_kernel(const __grid_
   unsigned char* tsm = reinterpret_cast<unsigned char*>(((uintptr_t)tsm_raw + 1023) & ~(uintptr_t)1023);
   const int G = a.G, kp = a.kpad, NST = a.nst;
   const int nkc = (kp + TCKC - 1) / TCKC;  // 128-byte K chunks
-  const uint32_t bkc = (uint32_t)(G / 2) * 1024;  // one K chunk of the group's digit rows (G even)
-  int8_t* sB = reinterpret_cast<int8_t*>(tsm);                                   // [nkc][G/2 atoms][1 KB]
-  uint8_t* sA = reinterpret_cast<uint8_t*>(tsm + (size_t)nkc * bkc);             // [NST][128 rows x 128 B] swizzled
+  const bool fused = a.bqhat != nullptr;
+  const int G16 = round16(G);
+  // one K chunk of the group's B rows: the digit rows (G/2 atoms; G even), then (fused) the qhat rows
+  // (G16/8 atoms), placed right after the group's own digit rows so one MMA covers both
+  const uint32_t bkc = (uint32_t)(G / 2) * 1024 + (fused ? (uint32_t)(G16 / 8) * 1024 : 0u);
+  int8_t* sB = reinterpret_cast<int8_t*>(tsm);                                   // [nkc][bkc]
+  uint8_t* sA = reinterpret_cast<uint8_t*>(sB + (size_t)nkc * bkc);             // [NST][128 rows x 128 B] swizzled
   uint64_t* bars = reinterpret_cast<uint64_t*>(sA + (size_t)NST * TCM * TCKC);
   uint64_t* full = bars;                      // [NST]
   uint64_t* empty = bars + NST;               // [NST]
@@ -2484,7 +2540,7 @@ __global__ void __launch_bounds__(TCR_THREADS, 1) tc_refine_kernel(const __grid_
   uint32_t* s_taddr = reinterpret_cast<uint32_t*>(bars + 2 * NST + 6);
   double4* s_qs = reinterpret_cast<double4*>(bars + 2 * NST + 8);  // [2][64] (dq, kb, hs, row base) per group slot
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int NCOL = TCR_DIG * G;  // accumulator columns of one tile
+  const int NCOL = tc_ncol(G, fused);  // accumulator columns of one tile
   // a whole warp waiting on an mbarrier: one lane polls, the warp then re-converges
   auto wait1 = [&](uint64_t* bar, uint32_t parity) {
     if (lane == 0) tc::mbar_wait(bar, parity);
@@ -2529,10 +2585,14 @@ __global__ void __launch_bounds__(TCR_THREADS, 1) tc_refine_kernel(const __grid_
       // issued once the previous group's MMAs no longer read sB
       wait1(bempty, (grp & 1) ^ 1);
       if (lane == 0) TCR_EV(7, grp);
-      if (lane == 0) tc::mbar_expect_tx(bfull, (uint32_t)(nqg * nkc * 512));
+      if (lane == 0) tc::mbar_expect_tx(bfull, (uint32_t)(nqg * nkc * (fused ? 640 : 512)));
       __syncwarp();
       if (lane < nkc)
         tc::bulk_load(sB + lane * bkc, a.bslices + ((int64_t)lane * a.npairs + ps) * 512, (uint32_t)nqg * 512, bfull,
+                      tc::kL2EvictFirst);
+      else if (fused && lane < 2 * nkc)  // after the group's 4 ((nqg + 3) & ~3) digit rows
+        tc::bulk_load(sB + (lane - nkc) * bkc + (((nqg + 3) & ~3) >> 1) * 1024,
+                      a.bqhat + ((int64_t)(lane - nkc) * a.npairs + ps) * 128, (uint32_t)nqg * 128, bfull,
                       tc::kL2EvictFirst);
     }
     if (wid < TC_PROD) {
@@ -2597,7 +2657,10 @@ __global__ void __launch_bounds__(TCR_THREADS, 1) tc_refine_kernel(const __grid_
     } else if (wid == TC_PROD) {
       // ---- MMA issuer.  N = the group's 4 digit rows per query, rounded to 16 (a list probed by
       // few queries does not pay for a full group)
-      const uint32_t idesc = tc::idesc_i8(TCM, TCR_DIG * ((nqg + 3) & ~3), false, true);
+      // one MMA for the digit rows (and the qhat rows after them: sum u qhat), one for sum s8(u) qhat
+      const int ndig = TCR_DIG * ((nqg + 3) & ~3);
+      const uint32_t idesc = tc::idesc_i8(TCM, ndig + (fused ? round16(nqg) : 0), false, true);
+      const uint32_t idq_s = tc::idesc_i8(TCM, round16(nqg), true, true);
       wait1(bfull, grp & 1);
       if (lane == 0) TCR_EV(4, grp);
       for (int t = 0; t < ntile; ++t, ++tile_mma) {
@@ -2617,6 +2680,10 @@ __global__ void __launch_bounds__(TCR_THREADS, 1) tc_refine_kernel(const __grid_
               const uint64_t ad = tc::smem_desc_sw128(sA + st * TCM * TCKC + 32 * s2);
               const uint64_t bd = tc::smem_desc_sw128(sB + kc * bkc + 32 * s2);
               tc::mma_i8(tbase + ab * acc_stride, ad, bd, idesc, kc > 0 || s2 > 0);
+              if (fused) {
+                const uint64_t qd = tc::smem_desc_sw128(sB + kc * bkc + (ndig >> 3) * 1024 + 32 * s2);
+                tc::mma_i8(tbase + ab * acc_stride + TCR_DIG * G + G16, ad, qd, idq_s, kc > 0 || s2 > 0);
+              }
             }
 #else
             (void)ks;
@@ -2665,7 +2732,25 @@ __global__ void __launch_bounds__(TCR_THREADS, 1) tc_refine_kernel(const __grid_
 #endif
         for (int j0 = 8 * part; j0 < nqg; j0 += 8 * TCR_EPQ) {  // 8-query chunks, round robin over the parts
           uint32_t d[32];
-          tc::tmem_ld32(tbase + ((uint32_t)(quarter * 32) << 16) + ab * acc_stride + TCR_DIG * j0, d);
+          const uint32_t trow = tbase + ((uint32_t)(quarter * 32) << 16) + ab * acc_stride;
+          tc::tmem_ld32(trow + TCR_DIG * j0, d);
+          if (fused) {
+            uint32_t du[8], ds[8];
+            tc::tmem_ld8(trow + TCR_DIG * ((nqg + 3) & ~3) + j0, du);
+            tc::tmem_ld8(trow + TCR_DIG * G + G16 + j0, ds);
+            tc::tmem_ld_wait();
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj) {
+              const int j = j0 + jj;
+              if (j < nqg && v < n_c) {
+                // sum u qhat - sum s8(u) qhat = 256 sum msb(u) qhat, exactly
+                const int ip = ((int)du[jj] - (int)ds[jj]) >> 8;
+                const int64_t at = __double_as_longlong(qs[j].w) + v;
+                if (a.ip32) __stcs(reinterpret_cast<int32_t*>(a.ipbuf) + at, ip);
+                else __stcs(reinterpret_cast<int16_t*>(a.ipbuf) + at, (int16_t)ip);
+              }
+            }
+          }
           tc::tmem_ld_wait();
 #pragma unroll
           for (int jj = 0; jj < 8; ++jj) {
@@ -3035,7 +3120,10 @@ inline int launch_rd(const Args& a, bool refine, int ipb, cudaStream_t s) {
 #ifndef RDA_MINB
 #define RDA_MINB 4
 #endif
-  auto kern = ipb == 2 ? scan_rda_kernel<2, 4, RDA_MINB> : scan_rda_kernel<4, 4, RDA_MINB>;
+#ifndef RDA_RSUB
+#define RDA_RSUB 4
+#endif
+  auto kern = ipb == 2 ? scan_rda_kernel<2, RDA_RSUB, RDA_MINB> : scan_rda_kernel<4, RDA_RSUB, RDA_MINB>;
   const size_t sm = (size_t)RDW * ((size_t)a.kpad * sizeof(int2) + 32 * 16);
   if (sm > 48 * 1024 && cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess)
     return fail(IVRQ_EUNSUP, "ivrq_search_scan: shared memory request too large");
@@ -3156,19 +3244,28 @@ static ScanPolicy scan_policy(const ivrq_index_view& ix, const ivrq_search_param
 // tc_refine group size and A ring depth: the largest query group (<= 64: 4 G accumulator columns,
 // double-buffered in 512) whose digit rows fit beside a ring of >= TCR_MIN_ST A stages
 #ifndef TCR_MIN_ST
-#define TCR_MIN_ST 5
+#define TCR_MIN_ST 4
 #endif
-static bool tc_refine_shape(int kpad, int& G, int& nst) {
+// (fused stage 1: G a multiple of 8, so every group starts an 8-row atom of qhat rows, and the two
+// extra sums per query within the 512 columns)
+static bool tc_refine_shape(int kpad, bool fused, int& G, int& nst) {
   const size_t cap = 227 * 1024;
+  const int step = fused ? 8 : 4;
 #ifdef TCR_FORCE_G  // development A/B builds only
   G = TCR_FORCE_G;
   for (nst = 10; nst >= 2; --nst)
-    if (tc_smem_bytes(kpad, G, nst) <= cap) return true;
+    if (tc_smem_bytes(kpad, G, nst, fused) <= cap && 2 * tc_ncol(G, fused) <= 512) return true;
   return false;
 #endif
-  for (G = 64; G >= 4; G -= 4) {
+  for (G = 64; G >= step; G -= step) {
+    if (2 * tc_ncol(G, fused) > 512) continue;
     for (nst = 10; nst >= TCR_MIN_ST; --nst)
-      if (tc_smem_bytes(kpad, G, nst) <= cap) return true;
+      if (tc_smem_bytes(kpad, G, nst, fused) <= cap) return true;
+  }
+  for (G = 64; G >= step; G -= step) {  // very wide rows: a shallower ring
+    if (2 * tc_ncol(G, fused) > 512) continue;
+    for (nst = TCR_MIN_ST - 1; nst >= 2; --nst)
+      if (tc_smem_bytes(kpad, G, nst, fused) <= cap) return true;
   }
   return false;
 }
@@ -3387,11 +3484,14 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
       int8_t* qhat = nullptr;
       if (!ws.alloc(ipbuf, (size_t)tot[0] * ipb) || !ws.alloc(qhat, (size_t)nq * 32 * a.g))
         return oom("inner-product buffer allocation failed");
+      // 8-bit codes: the stage-1 inner products come out of the refine's own MMAs (no separate pass;
+      // msb(u) = u >> 7 is what the signed reading of the byte subtracts)
+      const bool fused = pol.rd_path && refine && index->bits == 8;
       if (pol.rd_path && refine) {
         // refined distance of every probed pair on tcgen05 (concurrent with the inner products):
         // one work item per (list, group of G queries probing it)
         int G = 0, nb = 0;
-        if (!scan::tc_refine_shape(a.kpad, G, nb))
+        if (!scan::tc_refine_shape(a.kpad, fused, G, nb))
           return fail(IVRQ_EUNSUP, "ivrq_search_scan: dims too large for the tensor-core refine");
         float* rdist = nullptr;
         double* rrad = nullptr;
@@ -3444,7 +3544,18 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
         ta.pair_base = pbase;
         ta.gpre = rgpre;
         ta.rdist = rdist;
-        const size_t tsm = scan::tc_smem_bytes(a.kpad, G, nb);
+        if (fused) {
+          int8_t* qpairs4 = nullptr;
+          if (!ws.alloc(qpairs4, (size_t)npairs * nkc * 128)) return oom("workspace allocation failed");
+          scan::qhat_kernel<<<(unsigned)ceil_div(nq * a.g, 256), 256, 0, s>>>(planes, nq, a.g, a.qbits, qhat);
+          scan::tc_qpairs_kernel<<<(unsigned)ceil_div(npairs * nkc * 8, 256), 256, 0, s>>>(
+              qhat, porder, pslot, npairs, a.nprobe, 32 * a.g, nkc, qpairs4);
+          IVRQ_TRY(check_launch("ivrq_search_scan(fused stage-1 operand)"));
+          ta.bqhat = qpairs4;
+          ta.ipbuf = ipbuf;
+          ta.ip32 = ipb == 4 ? 1 : 0;
+        }
+        const size_t tsm = scan::tc_smem_bytes(a.kpad, G, nb, fused);
         if (cudaFuncSetAttribute(scan::tc_refine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm) !=
             cudaSuccess)
           return fail(IVRQ_EUNSUP, "ivrq_search_scan: dims too large for the tensor-core refine");
@@ -3474,6 +3585,10 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
         };
         a.rdist = rdist;
       }
+      if (fused) {
+        IVRQ_TRY(refine_launch());  // writes the stage-1 inner products as well
+        refine_launch = nullptr;
+      } else
       {
         // fork: the stage-1 inner products on the side stream, the refine on s; both only read
         // the index and the prepared queries.  The fork joins on every return path.
