@@ -104,6 +104,7 @@ enum {
   IVRQ_QS_KB_SUM = 4,     /* k_b * sum_q used by the refine (search.py:323)    */
   IVRQ_QS_HALF_CODE = 5,  /* 0.5 * code_sum_q (search.py:281)                  */
   IVRQ_QS_SLICE_EXP = 6,  /* e: q_rot ~ sum_s slice_s * 128^(7-s) * 2^(e-55)   */
+  IVRQ_QS_L1 = 7,         /* sum |q_rot| (bounds of the certified LUT stage 1)   */
   IVRQ_QS_COUNT = 8
 };
 

@@ -488,7 +488,8 @@ __global__ void __launch_bounds__(THREADS, 4) scan_kernel(Args a) {
   __shared__ int s_pool_n;
   __shared__ long long s_probed, s_surv;
   if (blockIdx.x >= a.nq) return;
-  const int64_t q = a.qorder ? a.qorder[blockIdx.x] : (int64_t)blockIdx.x;
+  if (a.fix_only && (int)blockIdx.x >= *a.fix_only_count) return;  // as the exact rerun of listed queries
+  const int64_t q = a.fix_only ? (int64_t)a.fix_only[blockIdx.x] : a.qorder ? a.qorder[blockIdx.x] : (int64_t)blockIdx.x;
   const int k = a.k;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const Smem s = carve<MODE, REFINE>(a, smem, false);
@@ -665,11 +666,20 @@ __device__ __forceinline__ Stage1F32 stage1_f32(double delta, double half_code, 
   return f;
 }
 
+__device__ __forceinline__ int stage1_decide_f32x(float t1, float add, float scale, float err, const Stage1F32& f,
+                                                  float extra);
+
 __device__ __forceinline__ int stage1_decide_f32(int ip, float add, float scale, float err, const Stage1F32& f) {
-  const float t1 = f.delta * (float)ip;
+  return stage1_decide_f32x(f.delta * (float)ip, add, scale, err, f, 0.f);
+}
+
+// The same test from t1 = delta * ip given directly, with `extra` (>= 0) added to the inner product's
+// error (the certified LUT estimate's bound, scan_rda_kernel<LUT>).
+__device__ __forceinline__ int stage1_decide_f32x(float t1, float add, float scale, float err, const Stage1F32& f,
+                                                  float extra) {
   const float e = (add + f.dqc) - scale * (t1 - f.half);
   const float M = fabsf(add) + f.dqc + fabsf(scale) * (fabsf(t1) + f.ahalf);
-  const float E = M * 0x1p-19f;
+  const float E = M * 0x1p-19f + fabsf(scale) * extra;
   const float dk = (e + E) - f.T_lo;  // >= est2 - T
   if (dk <= 0.f) return 1;
   const float mg = err * f.sq, sm = scale * f.ipm;
@@ -1225,10 +1235,33 @@ __device__ __noinline__ void exactify_top(const ExactCtx& c, const int2* hl, con
 
 // The float64 prune test (stage1_keep64) against an interval [T_lo, T_hi] of the threshold: 1 keep
 // for every T in it, 0 prune for every T in it, -1 open.
-__device__ __noinline__ int decide64(int ipv, float fa, float fs, float fe, double d_qc2, double delta,
-                                     double half_code, double sq, double ipm, double T_lo, double T_hi) {
+__device__ __noinline__ int decide64(int ipv, float fa, float fs, float fe, double d_qc2, const double* sc,
+                                     double T_lo, double T_hi) {
+  const double delta = sc[IVRQ_QS_DELTA], half_code = sc[IVRQ_QS_HALF_CODE], ipm = sc[IVRQ_QS_IP_MARGIN];
+  const double sq = dsqrt(d_qc2);
   const double scale = (double)fs;
   const double est2 = dmax(dsub(dadd((double)fa, d_qc2), dmul(scale, dsub(dmul(delta, (double)ipv), half_code))), 0.0);
+  if (stage1_keep64(est2, (double)fe, scale, sq, ipm, T_lo)) return 1;
+  if (!stage1_keep64(est2, (double)fe, scale, sq, ipm, T_hi)) return 0;
+  return -1;
+}
+
+// LUT mode: the exact stage-1 inner product (the reference's table sum, scan_kernel's order) of row
+// vi of a list, then the float64 test against [T_lo, T_hi] as decide64.  Out of line: it runs only where
+// the certified estimate leaves the float32 test open.
+__device__ __noinline__ int decide64_lut(const uint32_t* words, int64_t n_c, int64_t vi, int g, const float* lut,
+                                         float fa, float fs, float fe, double d_qc2, const double* sc, double T_lo,
+                                         double T_hi) {
+  double acc = 0.0;
+  for (int gi = 0; gi < g; ++gi) {
+    const uint32_t w = __ldg(words + (int64_t)gi * n_c + vi);
+    const float* lrow = lut + gi * 8 * 16;
+#pragma unroll
+    for (int s2 = 0; s2 < 8; ++s2) acc = dadd(acc, (double)lrow[s2 * 16 + ((w >> (4 * s2)) & 15u)]);
+  }
+  const double half_code = sc[IVRQ_QS_HALF_CODE], ipm = sc[IVRQ_QS_IP_MARGIN];
+  const double sq = dsqrt(d_qc2), scale = (double)fs;
+  const double est2 = dmax(dsub(dadd((double)fa, d_qc2), dmul(scale, dsub(acc, half_code))), 0.0);
   if (stage1_keep64(est2, (double)fe, scale, sq, ipm, T_lo)) return 1;
   if (!stage1_keep64(est2, (double)fe, scale, sq, ipm, T_hi)) return 0;
   return -1;
@@ -1271,7 +1304,9 @@ __device__ unsigned long long g_rda_stats[6];  // prune resolutions, exact value
 
 template <int IPB, int RSUB, int MINB = 1>
 __global__ void __launch_bounds__(RDW * 32, MINB) scan_rda_kernel(Args a) {
-  using IPT = typename std::conditional<IPB == 2, int16_t, int32_t>::type;
+  // IPB 2 / 4: exact integer stage-1 inner products (bitwise); 0: certified float32 LUT estimates
+  constexpr bool LUT = IPB == 0;
+  using IPT = typename std::conditional<IPB == 2, int16_t, typename std::conditional<LUT, float, int32_t>::type>::type;
   extern __shared__ __align__(16) unsigned char rda_smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t slot_q = (int64_t)blockIdx.x * RDW + wid;
@@ -1282,20 +1317,23 @@ __global__ void __launch_bounds__(RDW * 32, MINB) scan_rda_kernel(Args a) {
   int2* hl = reinterpret_cast<int2*>(wbase);
   double* snap_d = reinterpret_cast<double*>(wbase + (size_t)kp * sizeof(int2));
   int64_t* snap_e = reinterpret_cast<int64_t*>(snap_d + 32);
-  bool hl_ready = false;
   // The queue is ordered by (value, entry bits): the order of tied approximate values never decides
   // anything (the threshold is a value; a tie at the 32nd slot is a saturation); the exact top k is
   // re-sorted by (value, pid) in exactify_top.
   const PidLess lt;
   const double* sc = a.scalars + q * IVRQ_QS_COUNT;
-  const double delta = sc[IVRQ_QS_DELTA], half_code = sc[IVRQ_QS_HALF_CODE], ipm = sc[IVRQ_QS_IP_MARGIN];
   const double rq = a.rrad[q];
+  // LUT: |estimate - table sum| <= eq + |estimate| 2^-23: the tables' float32 rounding (2^-24 sum|q|),
+  // their float64 sums, and the neglected query digits (kpad 135274560 2^(e-54)); float, rounded up
+  float eq = 0.f;
+  if (LUT)
+    eq = __double2float_ru((sc[IVRQ_QS_L1] * (0x1p-24 + 0x1p-44) +
+                            (double)kp * ldexp(135274560.0, (int)sc[IVRQ_QS_SLICE_EXP] - 54)) * (1.0 + 0x1p-20));
   const int init_n = a.init_counts ? a.init_counts[q] : 0;
   double qd = lane < init_n ? a.init_dists[q * k + lane] : dinf();
   int64_t qi = lane < init_n ? (a.init_ids[q * k + lane] | E_PIDE) : NO_ID;
-  double T = init_n >= k ? __shfl_sync(FULL, qd, k - 1) : dinf(), radT = 0.0;
   bool unsafe = false;
-  long long probed = 0, surv = 0;
+  int probed = 0, surv = 0;
   // offer survivors (value d, entry e; e = NO_ID: none) to the queue
   auto offer = [&](double d, int64_t e) {
     const double kd = __shfl_sync(FULL, qd, k - 1);
@@ -1320,14 +1358,18 @@ __global__ void __launch_bounds__(RDW * 32, MINB) scan_rda_kernel(Args a) {
     if (p + 1 < a.nprobe) nxt = list_meta(a, q * a.nprobe + p + 1);  // prefetched one list ahead
     if (cur.nc <= 0) continue;  // another shard's list, or empty
     const int64_t lo = cur.lo, n_c = cur.nc;
-    const int64_t ebase = lo | ((int64_t)p << E_PSH);
     const double d_qc2 = cur.d2;
-    double T_list = a.prune ? T : dinf();
-    double rT = a.prune ? radT : 0.0;
-    probed += n_c;
+    // the threshold before this list (search.py:444-447) as an interval: the queue's k-th value
+    // and its radius (the threshold state lives in the queue, not in registers across lists)
+    double T_list = dinf(), rT = 0.0;
+    if (a.prune && __popc(__ballot_sync(FULL, lane < k && qi != NO_ID)) >= k) {
+      T_list = __shfl_sync(FULL, qd, k - 1);
+      rT = entry_rad(T_list, __shfl_sync(FULL, qi, k - 1), rq);
+    }
+    probed += (int)n_c;
     const float* rrow = a.rdist + cur.base;
     if (T_list == dinf()) {  // nothing can be pruned (lb2 <= +inf): every vector's refined distance
-      surv += n_c;
+      surv += (int)n_c;
       for (int64_t c0 = 0; c0 < n_c; c0 += 32 * RSUB) {
         float dv[RSUB];
 #pragma unroll
@@ -1342,7 +1384,7 @@ __global__ void __launch_bounds__(RDW * 32, MINB) scan_rda_kernel(Args a) {
           for (int j = 0; j + 1 < RSUB; ++j) dv[j] = dv[j + 1];
           const int64_t vi = c0 + u * 32 + lane;
           if (c0 + u * 32 >= n_c) break;  // warp-uniform
-          offer((double)d0, vi < n_c ? ebase + vi : NO_ID);
+          offer((double)d0, vi < n_c ? ((lo + vi) | ((int64_t)p << E_PSH)) : NO_ID);
         }
       }
     } else {
@@ -1351,8 +1393,8 @@ __global__ void __launch_bounds__(RDW * 32, MINB) scan_rda_kernel(Args a) {
       snap_e[lane] = qi;
       __syncwarp();
       const IPT* iprow = reinterpret_cast<const IPT*>(a.ipbuf) + cur.base;
-      const double sq = dsqrt(d_qc2);
-      Stage1F32 f32 = stage1_f32(delta, half_code, ipm, d_qc2, sq, T_list);
+      Stage1F32 f32 = stage1_f32(sc[IVRQ_QS_DELTA], sc[IVRQ_QS_HALF_CODE], sc[IVRQ_QS_IP_MARGIN], d_qc2, dsqrt(d_qc2),
+                                 T_list);
       f32.T_lo = __double2float_rd(T_list - rT * (1.0 + 0x1p-40));
       f32.T_hi = __double2float_ru(T_list + rT * (1.0 + 0x1p-40));
       for (int64_t c0 = 0; c0 < n_c; c0 += 32 * RSUB) {
@@ -1362,8 +1404,10 @@ __global__ void __launch_bounds__(RDW * 32, MINB) scan_rda_kernel(Args a) {
         for (int u = 0; u < RSUB; ++u) {
           const int64_t vi = c0 + u * 32 + lane;
           const bool in = vi < n_c;
+#ifndef RDA_NOPRE
           pre[u] = in ? __ldg(rrow + vi) : 0.f;
-          ipv[u] = in ? (int)__ldg(iprow + vi) : 0;
+#endif
+          ipv[u] = in ? (LUT ? __float_as_int((float)__ldg(iprow + vi)) : (int)__ldg(iprow + vi)) : 0;
           fa[u] = in ? __ldg(a.ix.short_add + lo + vi) : 0.f;
           fs[u] = in ? __ldg(a.ix.short_scale + lo + vi) : 0.f;
           fe[u] = in ? __ldg(a.ix.short_err + lo + vi) : 0.f;
@@ -1373,16 +1417,23 @@ __global__ void __launch_bounds__(RDW * 32, MINB) scan_rda_kernel(Args a) {
 #pragma unroll
         for (int u = 0; u < RSUB; ++u) {
           const int64_t vi = c0 + u * 32 + lane;
-          dec[u] = vi < n_c ? stage1_decide_f32(ipv[u], fa[u], fs[u], fe[u], f32) : 0;
-          // the float64 test inside the float32 band (about 1e-5 of the vectors), out of line
-          if (dec[u] < 0)
-            dec[u] = decide64(ipv[u], fa[u], fs[u], fe[u], d_qc2, delta, half_code, sq, ipm, T_list - rT, T_list + rT);
+          if (LUT) {
+            const float t1 = __int_as_float(ipv[u]);
+            dec[u] = vi < n_c ? stage1_decide_f32x(t1, fa[u], fs[u], fe[u], f32, eq + fabsf(t1) * 0x1p-23f) : 0;
+            if (dec[u] < 0)  // the exact table sum, out of line
+              dec[u] = decide64_lut(a.ix.packed_msb + (int64_t)a.g * lo, n_c, vi, a.g, a.luts + q * 8 * a.g * 16,
+                                    fa[u], fs[u], fe[u], d_qc2, sc, T_list - rT, T_list + rT);
+          } else {
+            dec[u] = vi < n_c ? stage1_decide_f32(ipv[u], fa[u], fs[u], fe[u], f32) : 0;
+            // the float64 test inside the float32 band (about 1e-5 of the vectors), out of line
+            if (dec[u] < 0)
+              dec[u] = decide64(ipv[u], fa[u], fs[u], fe[u], d_qc2, sc, T_list - rT, T_list + rT);
+          }
           open |= dec[u] < 0;
         }
         if (__any_sync(FULL, open)) {
           // the threshold's interval leaves a test open: exact values for the list-start
           // queue's possible members give the exact T for the rest of this list
-          if (!hl_ready) hl_ready = true;
           T_list = resolve_threshold(a.ix.rcodes, a.ix.long_factors, a.probe_d2 + q * a.nprobe,
                                      a.qslices + q * SLICES * (int64_t)kp, a.ix.pids, a.ix.rcode_bytes, kp,
                                      (int)sc[IVRQ_QS_SLICE_EXP], sc[IVRQ_QS_KB_SUM], rq, rcode_nibbles(a.ix.bits), hl,
@@ -1393,11 +1444,17 @@ __global__ void __launch_bounds__(RDW * 32, MINB) scan_rda_kernel(Args a) {
 #pragma unroll
           for (int u = 0; u < RSUB; ++u)
             if (dec[u] < 0)
-              dec[u] = decide64(ipv[u], fa[u], fs[u], fe[u], d_qc2, delta, half_code, sq, ipm, T_list, T_list);
+              dec[u] = LUT ? decide64_lut(a.ix.packed_msb + (int64_t)a.g * lo, n_c, c0 + u * 32 + lane, a.g,
+                                          a.luts + q * 8 * a.g * 16, fa[u], fs[u], fe[u], d_qc2, sc, T_list, T_list)
+                           : decide64(ipv[u], fa[u], fs[u], fe[u], d_qc2, sc, T_list, T_list);
         }
         bool keep[RSUB];
 #pragma unroll
         for (int u = 0; u < RSUB; ++u) keep[u] = dec[u] > 0;
+#ifdef RDA_NOPRE
+#pragma unroll
+        for (int u = 0; u < RSUB; ++u) pre[u] = keep[u] ? __ldg(rrow + c0 + u * 32 + lane) : 0.f;
+#endif
 #pragma unroll 1
         for (int u = 0; u < RSUB; ++u) {  // one copy of the queue code (instruction cache); values
           const float d0 = pre[0];        // rotate through slot 0 so every index stays static
@@ -1410,16 +1467,11 @@ __global__ void __launch_bounds__(RDW * 32, MINB) scan_rda_kernel(Args a) {
           const unsigned kbits = __ballot_sync(FULL, k0);
           if (!kbits) continue;
           surv += __popc(kbits);
-          offer((double)d0, k0 ? ebase + c0 + u * 32 + lane : NO_ID);
+          offer((double)d0, k0 ? ((lo + c0 + u * 32 + lane) | ((int64_t)p << E_PSH)) : NO_ID);
         }
       }
     }
     check_saturation();
-    const int cnt = __popc(__ballot_sync(FULL, lane < k && qi != NO_ID));
-    if (cnt >= k) {  // search.py:444-447, as an interval
-      T = __shfl_sync(FULL, qd, k - 1);
-      radT = entry_rad(T, __shfl_sync(FULL, qi, k - 1), rq);
-    }
   }
   // the queue (values, entries) for rda_final_kernel, which makes the top k exact
   a.fin_d[q * 32 + lane] = qd;
@@ -2433,6 +2485,9 @@ struct TcArgs {
   const int8_t* bqhat;      // [nkc][npairs][128 B] (tc_qpairs_kernel), or null
   void* ipbuf;
   int ip32;
+  // LUT mode (8-bit codes): the stage-1 estimate <msb(u), q> from the digit rows read both ways,
+  // written as float32 (a certified approximation of the LUT sum, see scan_rda_kernel)
+  int lut;
 };
 
 // byte offset of (row R, byte k < 128) in a 128B-swizzled K-major tile (8-row atoms of 1024 B)
@@ -2499,14 +2554,17 @@ __host__ __device__ inline uint32_t tmem_cols(int n) {  // power of two >= 32 (<
 
 __host__ __device__ inline int round16(int n) { return (n + 15) & ~15; }
 
-size_t tc_smem_bytes(int kpad, int G, int nst, bool fused) {
+// stage-1 fusion of the refine: 0 none, 1 bitwise (qhat rows), 2 LUT (the digit rows read as signed too)
+size_t tc_smem_bytes(int kpad, int G, int nst, int fusion) {
   const int nkc = (kpad + TCKC - 1) / TCKC;
-  return 1024 + (size_t)nkc * (TCR_DIG * G + (fused ? round16(G) : 0)) * TCKC + (size_t)nst * TCM * TCKC + 256 +
-         2 * 64 * sizeof(double4);
+  return 1024 + (size_t)nkc * (TCR_DIG * G + (fusion == 1 ? round16(G) : 0)) * TCKC + (size_t)nst * TCM * TCKC +
+         256 + 2 * 64 * sizeof(double4);
 }
 
-// accumulator columns of one tile: 4 digit columns per query, and the fused stage 1's two sums
-__host__ __device__ inline int tc_ncol(int G, bool fused) { return TCR_DIG * G + (fused ? 2 * round16(G) : 0); }
+// accumulator columns of one tile: 4 digit columns per query, and the fused stage 1's sums
+__host__ __device__ inline int tc_ncol(int G, int fusion) {
+  return TCR_DIG * G + (fusion == 1 ? 2 * round16(G) : fusion == 2 ? TCR_DIG * G : 0);
+}
 
 #ifdef IVRQ_TCR_TRACE  // development builds only: timeline of CTA 0's roles (plain stores, no atomics)
 __device__ unsigned long long g_tcr_trace[16 * 4096];
@@ -2524,6 +2582,7 @@ __global__ void __launch_bounds__(TCR_THREADS, 1) tc_refine_kernel(const __grid_
   const int G = a.G, kp = a.kpad, NST = a.nst;
   const int nkc = (kp + TCKC - 1) / TCKC;  // 128-byte K chunks
   const bool fused = a.bqhat != nullptr;
+  const bool lutf = a.lut != 0;
   const int G16 = round16(G);
   // one K chunk of the group's B rows: the digit rows (G/2 atoms; G even), then (fused) the qhat rows
   // (G16/8 atoms), placed right after the group's own digit rows so one MMA covers both
@@ -2540,7 +2599,7 @@ __global__ void __launch_bounds__(TCR_THREADS, 1) tc_refine_kernel(const __grid_
   uint32_t* s_taddr = reinterpret_cast<uint32_t*>(bars + 2 * NST + 6);
   double4* s_qs = reinterpret_cast<double4*>(bars + 2 * NST + 8);  // [2][64] (dq, kb, hs, row base) per group slot
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int NCOL = tc_ncol(G, fused);  // accumulator columns of one tile
+  const int NCOL = tc_ncol(G, fused ? 1 : lutf ? 2 : 0);  // accumulator columns of one tile
   // a whole warp waiting on an mbarrier: one lane polls, the warp then re-converges
   auto wait1 = [&](uint64_t* bar, uint32_t parity) {
     if (lane == 0) tc::mbar_wait(bar, parity);
@@ -2661,6 +2720,7 @@ __global__ void __launch_bounds__(TCR_THREADS, 1) tc_refine_kernel(const __grid_
       const int ndig = TCR_DIG * ((nqg + 3) & ~3);
       const uint32_t idesc = tc::idesc_i8(TCM, ndig + (fused ? round16(nqg) : 0), false, true);
       const uint32_t idq_s = tc::idesc_i8(TCM, round16(nqg), true, true);
+      const uint32_t idd_s = tc::idesc_i8(TCM, ndig, true, true);
       wait1(bfull, grp & 1);
       if (lane == 0) TCR_EV(4, grp);
       for (int t = 0; t < ntile; ++t, ++tile_mma) {
@@ -2683,6 +2743,8 @@ __global__ void __launch_bounds__(TCR_THREADS, 1) tc_refine_kernel(const __grid_
               if (fused) {
                 const uint64_t qd = tc::smem_desc_sw128(sB + kc * bkc + (ndig >> 3) * 1024 + 32 * s2);
                 tc::mma_i8(tbase + ab * acc_stride + TCR_DIG * G + G16, ad, qd, idq_s, kc > 0 || s2 > 0);
+              } else if (lutf) {  // the digit rows against u read as signed bytes
+                tc::mma_i8(tbase + ab * acc_stride + TCR_DIG * G, ad, bd, idd_s, kc > 0 || s2 > 0);
               }
             }
 #else
@@ -2748,6 +2810,24 @@ __global__ void __launch_bounds__(TCR_THREADS, 1) tc_refine_kernel(const __grid_
                 const int64_t at = __double_as_longlong(qs[j].w) + v;
                 if (a.ip32) __stcs(reinterpret_cast<int32_t*>(a.ipbuf) + at, ip);
                 else __stcs(reinterpret_cast<int16_t*>(a.ipbuf) + at, (int16_t)ip);
+              }
+            }
+          }
+          if (lutf) {
+            uint32_t ds[32];
+            tc::tmem_ld32(trow + TCR_DIG * G + TCR_DIG * j0, ds);
+            tc::tmem_ld_wait();
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj) {
+              const int j = j0 + jj;
+              if (j < nqg && v < n_c) {
+                // sum_d msb(u) D_d = (sum u D_d - sum s8(u) D_d) / 256, exactly; <msb, q> up to the neglected
+                // digits (|.| <= kpad L 2^(e-54)), then rounded to float32
+                int m[4];
+#pragma unroll
+                for (int dd = 0; dd < 4; ++dd) m[dd] = ((int)d[TCR_DIG * jj + dd] - (int)ds[TCR_DIG * jj + dd]) >> 8;
+                const double hm = fma((double)(m[0] * 128 + m[1]), 16384.0, (double)(m[2] * 128 + m[3]));
+                __stcs(reinterpret_cast<float*>(a.ipbuf) + __double_as_longlong(qs[j].w) + v, (float)(hm * qs[j].z));
               }
             }
           }
@@ -3108,6 +3188,8 @@ __global__ void merge_topk_kernel(const int64_t* __restrict__ ids, const double*
 
 template <bool REFINE, bool NIB>
 int launch_warp(const Args& a, int ipb, cudaStream_t s);
+template <int MODE>
+int launch_mode(const Args& a, bool refine, bool nib, int ipb, cudaStream_t s);
 
 inline int launch_rd(const Args& a, bool refine, int ipb, cudaStream_t s) {
   // 4 sub-chunks of 32 vectors per batch, register budget for 6 resident CTAs (B200 A/B: 1, 6, 8)
@@ -3123,7 +3205,9 @@ inline int launch_rd(const Args& a, bool refine, int ipb, cudaStream_t s) {
 #ifndef RDA_RSUB
 #define RDA_RSUB 4
 #endif
-  auto kern = ipb == 2 ? scan_rda_kernel<2, RDA_RSUB, RDA_MINB> : scan_rda_kernel<4, RDA_RSUB, RDA_MINB>;
+  auto kern = ipb == 2   ? scan_rda_kernel<2, RDA_RSUB, RDA_MINB>
+              : ipb == 0 ? scan_rda_kernel<0, RDA_RSUB, RDA_MINB>
+                         : scan_rda_kernel<4, RDA_RSUB, RDA_MINB>;
   const size_t sm = (size_t)RDW * ((size_t)a.kpad * sizeof(int2) + 32 * 16);
   if (sm > 48 * 1024 && cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess)
     return fail(IVRQ_EUNSUP, "ivrq_search_scan: shared memory request too large");
@@ -3160,6 +3244,10 @@ inline int launch_rd(const Args& a, bool refine, int ipb, cudaStream_t s) {
   f.fix_only = a.fix_list;
   f.fix_only_count = a.fix_count;
   f.init_ids = a.init_ids;
+  if (ipb == 0) {  // LUT mode: the per-query LUT scan (stage 1 from the tables), exact throughout
+    f.ipbuf = nullptr;
+    return launch_mode<IVRQ_IP_LUT>(f, true, rcode_nibbles(a.ix.bits), 0, s);
+  }
   return rcode_nibbles(a.ix.bits) ? launch_warp<true, true>(f, ipb, s) : launch_warp<true, false>(f, ipb, s);
 }
 
@@ -3211,6 +3299,7 @@ int launch_mode(const Args& a, bool refine, bool nib, int ipb, cudaStream_t s) {
 // environment variables only force a path, for those equivalence tests.
 struct ScanPolicy {
   bool tc_path, warp_path, rd_path, first_phase, first_dist, tc_ip;
+  bool lut_rd;  // LUT mode through the certified list-major path
 };
 
 static int env_flag(const char* name, int dflt) {
@@ -3234,6 +3323,13 @@ static ScanPolicy scan_policy(const ivrq_index_view& ix, const ivrq_search_param
   // (the epilogue's int32 digit pairs D0 * 128 + D1 stay below 2^31 for kpad <= 960 with 8-bit codes)
   const bool fits = rcode_nibbles(ix.bits) || kpad64(ix.dims) <= 960;
   sp.rd_path = sp.warp_path && (!refine || (ix.rcodes && dense && fits));
+  // LUT mode on the same list-major path for 8-bit codes: the refine's digit rows read as signed bytes
+  // give a certified approximation of the LUT stage 1 (scan_rda_kernel<LUT>)
+  if (p.ip_mode == IVRQ_IP_LUT && p.k <= 32 && refine && ix.bits == 8 && ix.rcodes && dense && fits && nl >= 1 &&
+      env_flag("IVRQ_TC_STAGE1", 1) != 0 && env_flag("IVRQ_LUT_RD", 1) != 0) {
+    sp.tc_path = sp.warp_path = sp.rd_path = true;
+    sp.lut_rd = true;
+  }
   sp.first_phase = refine && p.k <= 32 && !chained && env_flag("IVRQ_FIRST_LIST", !sp.warp_path) != 0;
   sp.first_dist = sp.warp_path && !sp.rd_path && refine && !chained && env_flag("IVRQ_FIRST_DIST", 1) != 0;
   // tcgen05 stage 1 for long codes; mma.sync tiles win for short ones (D <= 224)
@@ -3246,26 +3342,26 @@ static ScanPolicy scan_policy(const ivrq_index_view& ix, const ivrq_search_param
 #ifndef TCR_MIN_ST
 #define TCR_MIN_ST 4
 #endif
-// (fused stage 1: G a multiple of 8, so every group starts an 8-row atom of qhat rows, and the two
-// extra sums per query within the 512 columns)
-static bool tc_refine_shape(int kpad, bool fused, int& G, int& nst) {
+// (bitwise fusion: G a multiple of 8, so every group starts an 8-row atom of qhat rows; every fusion:
+// its extra sums within the 512 columns)
+static bool tc_refine_shape(int kpad, int fusion, int& G, int& nst) {
   const size_t cap = 227 * 1024;
-  const int step = fused ? 8 : 4;
+  const int step = fusion == 1 ? 8 : 4;
 #ifdef TCR_FORCE_G  // development A/B builds only
   G = TCR_FORCE_G;
   for (nst = 10; nst >= 2; --nst)
-    if (tc_smem_bytes(kpad, G, nst, fused) <= cap && 2 * tc_ncol(G, fused) <= 512) return true;
+    if (tc_smem_bytes(kpad, G, nst, fusion) <= cap && 2 * tc_ncol(G, fusion) <= 512) return true;
   return false;
 #endif
   for (G = 64; G >= step; G -= step) {
-    if (2 * tc_ncol(G, fused) > 512) continue;
+    if (2 * tc_ncol(G, fusion) > 512) continue;
     for (nst = 10; nst >= TCR_MIN_ST; --nst)
-      if (tc_smem_bytes(kpad, G, nst, fused) <= cap) return true;
+      if (tc_smem_bytes(kpad, G, nst, fusion) <= cap) return true;
   }
   for (G = 64; G >= step; G -= step) {  // very wide rows: a shallower ring
-    if (2 * tc_ncol(G, fused) > 512) continue;
+    if (2 * tc_ncol(G, fusion) > 512) continue;
     for (nst = TCR_MIN_ST - 1; nst >= 2; --nst)
-      if (tc_smem_bytes(kpad, G, nst, fused) <= cap) return true;
+      if (tc_smem_bytes(kpad, G, nst, fusion) <= cap) return true;
   }
   return false;
 }
@@ -3447,7 +3543,7 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
   int ipb = 0;
   const int64_t ipmax = (int64_t)words_per_vector(index->dims) * 32 << (params->query_bits - 1);
   if (pol.tc_path) {
-    ipb = ipmax <= 32768 ? 2 : 4;
+    ipb = pol.lut_rd ? 4 : ipmax <= 32768 ? 2 : 4;  // LUT: float32 stage-1 estimates
     const int64_t npairs = nq * a.nprobe;
     const int excl = pol.rd_path     ? 0
                      : pol.warp_path ? (refine && !a.prune ? 2 : (refine && !init_counts ? 1 : 0))
@@ -3486,12 +3582,13 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
         return oom("inner-product buffer allocation failed");
       // 8-bit codes: the stage-1 inner products come out of the refine's own MMAs (no separate pass;
       // msb(u) = u >> 7 is what the signed reading of the byte subtracts)
-      const bool fused = pol.rd_path && refine && index->bits == 8;
+      const bool fused = pol.rd_path && refine && index->bits == 8 && !pol.lut_rd;
+      const int fusion = fused ? 1 : pol.lut_rd ? 2 : 0;
       if (pol.rd_path && refine) {
         // refined distance of every probed pair on tcgen05 (concurrent with the inner products):
         // one work item per (list, group of G queries probing it)
         int G = 0, nb = 0;
-        if (!scan::tc_refine_shape(a.kpad, fused, G, nb))
+        if (!scan::tc_refine_shape(a.kpad, fusion, G, nb))
           return fail(IVRQ_EUNSUP, "ivrq_search_scan: dims too large for the tensor-core refine");
         float* rdist = nullptr;
         double* rrad = nullptr;
@@ -3555,7 +3652,11 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
           ta.ipbuf = ipbuf;
           ta.ip32 = ipb == 4 ? 1 : 0;
         }
-        const size_t tsm = scan::tc_smem_bytes(a.kpad, G, nb, fused);
+        if (pol.lut_rd) {
+          ta.lut = 1;
+          ta.ipbuf = ipbuf;
+        }
+        const size_t tsm = scan::tc_smem_bytes(a.kpad, G, nb, fusion);
         if (cudaFuncSetAttribute(scan::tc_refine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm) !=
             cudaSuccess)
           return fail(IVRQ_EUNSUP, "ivrq_search_scan: dims too large for the tensor-core refine");
@@ -3585,8 +3686,8 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
         };
         a.rdist = rdist;
       }
-      if (fused) {
-        IVRQ_TRY(refine_launch());  // writes the stage-1 inner products as well
+      if (fusion) {
+        IVRQ_TRY(refine_launch());  // writes the stage-1 inner products (or LUT estimates) as well
         refine_launch = nullptr;
       } else
       {
@@ -3676,6 +3777,7 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
     if (pol.rd_path && a.ipbuf) return scan::launch_rd(a, refine, ipb, s);
     return scan::launch_mode<IVRQ_IP_BITWISE>(a, refine, nib, pol.warp_path ? -ipb : ipb, s);
   }
+  if (pol.lut_rd && a.ipbuf) return scan::launch_rd(a, refine, 0, s);  // ipb 0: float32 LUT estimates
   return scan::launch_mode<IVRQ_IP_LUT>(a, refine, nib, 0, s);
 }
 

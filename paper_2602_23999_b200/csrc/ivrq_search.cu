@@ -180,6 +180,13 @@ __global__ void prepare_kernel(const double* __restrict__ q_rot, int64_t nq, int
   double sum_q = 0.0;
   if (lane == 0) sum_q = pairwise_sum_seq(x, d);
   sum_q = __shfl_sync(0xffffffffu, sum_q, 0);
+  {
+    double l1 = 0.0;  // an upper bound of sum |q| (every partial sum rounded up)
+    for (int i = lane; i < d; i += 32) l1 = __dadd_ru(l1, fabs(x[i]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) l1 = __dadd_ru(l1, __shfl_xor_sync(0xffffffffu, l1, o));
+    if (lane == 0) scalars[q * IVRQ_QS_COUNT + IVRQ_QS_L1] = l1;
+  }
   const double k_b = ((double)((1 << index_bits) - 1)) / 2.0;
   double* sc = scalars + q * IVRQ_QS_COUNT;
   if (qslices) {

@@ -462,3 +462,20 @@ def test_refine_intervals_near_duplicates(monkeypatch, k, copies, bits):
         out[name] = [dev.to_host(t) for t in (r.ids, r.dists, r.counts, r.stats)]
     for a, b in zip(out["popcount"], out["tcgen05"]):
         np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("n,d,nlist,nprobe,k", [(12000, 300, 32, 6, 10), (8000, 768, 16, 5, 10), (6000, 128, 24, 24, 32)])
+def test_lut_list_major_path_matches_per_query_lut_scan(monkeypatch, n, d, nlist, nprobe, k):
+    """LUT mode (the reference's default ip_mode) on 8-bit indexes: the list-major path with the
+    certified LUT estimate (tc_refine's digit rows read as signed bytes, exact table sums where the
+    estimate leaves a test open) == the per-query LUT scan: ids, dists, counts and survivor stats."""
+    ix, q = _synthetic_index(n, d, nlist, 8, seed=d + 1)
+    sp = iv.SearchParams(k=k, n_probe=nprobe, ip_mode="lut")
+    qd = dev.to_device(q)
+    out = {}
+    for name, val in (("per_query", "0"), ("list_major", "1")):
+        monkeypatch.setenv("IVRQ_LUT_RD", val)
+        r = search_device(qd, ix, sp, with_stats=True)
+        out[name] = [dev.to_host(t) for t in (r.ids, r.dists, r.counts, r.stats)]
+    for a, b in zip(out["per_query"], out["list_major"]):
+        np.testing.assert_array_equal(a, b)
