@@ -255,12 +255,14 @@ def ncu_traffic(cfg_name: str, nprobe: int, kernel: str | None = None):
     return None
 
 
-def kernel_roofline(kernel_ms: dict, peaks: dict, probed: int, survivors: int, d: int, bits: int) -> dict:
+def kernel_roofline(kernel_ms: dict, peaks: dict, probed: int, survivors: int, d: int, bits: int,
+                    mode: str = "bitwise") -> dict:
     """Roofline of the scan's dominant kernel (largest CUDA-event time in the timed region).
 
     Algorithmic work per launch:
-      tc_refine_kernel  int8 tensor ops 2 * probed * kpad * R: R = 4 leading query digits, plus the two
-                        stage-1 sums (u and s8(u) against qhat) when they are fused in (8-bit codes)
+      tc_refine_kernel  int8 tensor ops 2 * probed * kpad * R: R = 4 leading query digits, plus the fused
+                        stage 1 for 8-bit codes: 2 qhat rows (bitwise) or the 4 digit rows again read as
+                        signed bytes (LUT)
       tc_ip/ip_list     int8 tensor ops 2 * probed * 32 ceil(D/32) * 4 (4-bit query planes)
       scan_rd_kernel    bytes probed * (2 + 12) + survivors * 4 (ip, factors; float32 refined distance)
                         (1-bit indexes: probed * 14)
@@ -275,7 +277,7 @@ def kernel_roofline(kernel_ms: dict, peaks: dict, probed: int, survivors: int, d
     hbm = float(peaks.get("hbm_gbs", 6650.0))
     src = "MEASURED_PEAKS.json" if "_fallback" not in peaks else "fallback"
     if name in ("tc_refine_kernel", "tc_ip_kernel", "ip_list_kernel"):
-        rows = 4 + (2 if bits == 8 else 0)
+        rows = 4 + ((4 if mode == "lut" else 2) if bits == 8 else 0)
         work = 2.0 * probed * (kpad * rows if name == "tc_refine_kernel" else 32 * g * 4)
         achieved = work / (avg_ms / 1e3) / 1e12
         peak, psrc = int8_peak(peaks)
@@ -434,7 +436,7 @@ def run_ours(args, cfg_name: str) -> dict:
     scan_mean_ms = float(np.mean(scan_ms))
     peaks = measured_peaks()
     hbm = float(peaks.get("hbm_gbs", 6650.0))
-    roofline = kernel_roofline(kernel_ms, peaks, probed=probed, survivors=survivors, d=d, bits=bits)
+    roofline = kernel_roofline(kernel_ms, peaks, probed=probed, survivors=survivors, d=d, bits=bits, mode=args.mode)
     traffic = ncu_traffic(cfg_name, nprobe, roofline.get("kernel"))
     roofline["traffic"] = traffic
     g = (d + 31) // 32

@@ -1334,13 +1334,22 @@ __global__ void __launch_bounds__(RDW * 32, MINB) scan_rda_kernel(Args a) {
   int64_t qi = lane < init_n ? (a.init_ids[q * k + lane] | E_PIDE) : NO_ID;
   bool unsafe = false;
   int probed = 0, surv = 0;
-  // offer survivors (value d, entry e; e = NO_ID: none) to the queue
-  auto offer = [&](double d, int64_t e) {
+  // Offer survivors (float32 value d, entry e; e = NO_ID: none) to the queue.  A new entry is a
+  // possible member iff d - rad(d) <= s_k + rad(s_k), i.e. d <= (s_k + rad(s_k) + rq) / (1 - 2^-23):
+  // that bound is kept as a float rounded up (a looser filter only lets more candidates into the
+  // fold) and recomputed when the queue changes.
+  auto member_bound = [&]() {
     const double kd = __shfl_sync(FULL, qd, k - 1);
     const int64_t ke = __shfl_sync(FULL, qi, k - 1);
-    const bool maybe = e != NO_ID && dsub(d, entry_rad(d, e, rq)) <= kd + entry_rad(kd, ke, rq);
+    return kd == dinf() ? __int_as_float(0x7f800000)
+                        : __double2float_ru((kd + entry_rad(kd, ke, rq) + rq) * (1.0 + 0x1p-22));
+  };
+  float lim = member_bound();
+  auto offer = [&](float d, int64_t e) {
+    const bool maybe = e != NO_ID && d <= lim;
     if (!__any_sync(FULL, maybe)) return;
-    warp_fold(qd, qi, maybe ? d : dinf(), maybe ? e : NO_ID, maybe, 32, lt);
+    warp_fold(qd, qi, maybe ? (double)d : dinf(), maybe ? e : NO_ID, maybe, 32, lt);
+    lim = member_bound();
   };
   // The 32nd slot a possible member: a candidate pushed out of the queue may have been one.  Checked
   // once per list: pushed-out values are >= the final 32nd value, s - rad(s) increases with s and
@@ -1384,7 +1393,7 @@ __global__ void __launch_bounds__(RDW * 32, MINB) scan_rda_kernel(Args a) {
           for (int j = 0; j + 1 < RSUB; ++j) dv[j] = dv[j + 1];
           const int64_t vi = c0 + u * 32 + lane;
           if (c0 + u * 32 >= n_c) break;  // warp-uniform
-          offer((double)d0, vi < n_c ? ((lo + vi) | ((int64_t)p << E_PSH)) : NO_ID);
+          offer(d0, vi < n_c ? ((lo + vi) | ((int64_t)p << E_PSH)) : NO_ID);
         }
       }
     } else {
@@ -1467,7 +1476,7 @@ __global__ void __launch_bounds__(RDW * 32, MINB) scan_rda_kernel(Args a) {
           const unsigned kbits = __ballot_sync(FULL, k0);
           if (!kbits) continue;
           surv += __popc(kbits);
-          offer((double)d0, k0 ? ((lo + c0 + u * 32 + lane) | ((int64_t)p << E_PSH)) : NO_ID);
+          offer(d0, k0 ? ((lo + c0 + u * 32 + lane) | ((int64_t)p << E_PSH)) : NO_ID);
         }
       }
     }
@@ -2576,13 +2585,14 @@ __device__ unsigned long long g_tcr_trace[16 * 4096];
 #define TCR_EV(tag, idx) ((void)0)
 #endif
 
+template <int FUSION>  // 0 none, 1 bitwise stage 1 (qhat rows), 2 LUT estimate (digit rows read as signed)
 __global__ void __launch_bounds__(TCR_THREADS, 1) tc_refine_kernel(const __grid_constant__ TcArgs a) {
   extern __shared__ __align__(1024) unsigned char tsm_raw[];
   unsigned char* tsm = reinterpret_cast<unsigned char*>(((uintptr_t)tsm_raw + 1023) & ~(uintptr_t)1023);
   const int G = a.G, kp = a.kpad, NST = a.nst;
   const int nkc = (kp + TCKC - 1) / TCKC;  // 128-byte K chunks
-  const bool fused = a.bqhat != nullptr;
-  const bool lutf = a.lut != 0;
+  constexpr bool fused = FUSION == 1;
+  constexpr bool lutf = FUSION == 2;
   const int G16 = round16(G);
   // one K chunk of the group's B rows: the digit rows (G/2 atoms; G even), then (fused) the qhat rows
   // (G16/8 atoms), placed right after the group's own digit rows so one MMA covers both
@@ -3657,13 +3667,14 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
           ta.ipbuf = ipbuf;
         }
         const size_t tsm = scan::tc_smem_bytes(a.kpad, G, nb, fusion);
-        if (cudaFuncSetAttribute(scan::tc_refine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm) !=
-            cudaSuccess)
+        auto rk = fusion == 1 ? scan::tc_refine_kernel<1> : fusion == 2 ? scan::tc_refine_kernel<2>
+                                                                        : scan::tc_refine_kernel<0>;
+        if (cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm) != cudaSuccess)
           return fail(IVRQ_EUNSUP, "ivrq_search_scan: dims too large for the tensor-core refine");
-        refine_launch = [ta, tsm, s]() {
+        refine_launch = [ta, tsm, s, rk]() {
           {
             KernelTimer kt("tc_refine_kernel", s);
-            scan::tc_refine_kernel<<<(unsigned)sm_count_of_current_device(), scan::TCR_THREADS, tsm, s>>>(ta);
+            rk<<<(unsigned)sm_count_of_current_device(), scan::TCR_THREADS, tsm, s>>>(ta);
           }
 #ifdef IVRQ_TCR_TRACE
           {

@@ -11,7 +11,7 @@ import csv
 import json
 import sys
 
-SCAN = ("scan_", "first_", "ip_", "tc_", "pair_", "qhat", "cs_", "group_prefix")
+SCAN = ("scan_", "first_", "ip_", "tc_", "pair_", "qhat", "cs_", "group_prefix", "rda_", "lf_max", "rd_radius")
 
 
 def main(path, cfg, nprobe):
