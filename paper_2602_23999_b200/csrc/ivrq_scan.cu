@@ -83,6 +83,7 @@ struct Args {
   const double* rrad;
   int32_t* fix_count;        // queries the approximate pass could not certify (rerun exactly), and
   int32_t* fix_list;         // their ids
+  const float4* sf4;         // (add, scale, err, 0) per vector: one 16-byte load (pack_short_kernel), or null
   double* fin_d;             // [nq][32] the approximate pass's queue, for rda_final_kernel
   int64_t* fin_e;
   const int32_t* fix_only;   // scan_warp_kernel as the rerun: process only slots < *fix_only_count ...
@@ -1304,9 +1305,12 @@ __device__ unsigned long long g_rda_stats[6];  // prune resolutions, exact value
 
 template <int IPB, int RSUB, int MINB = 1>
 __global__ void __launch_bounds__(RDW * 32, MINB) scan_rda_kernel(Args a) {
-  // IPB 2 / 4: exact integer stage-1 inner products (bitwise); 0: certified float32 LUT estimates
+  // IPB 2 / 4: exact integer stage-1 inner products in ipbuf (int16 / int32) beside float32 distances;
+  // 1 / 0: (distance, stage-1 value) float pairs from the fused refine, the value an exact integer (1)
+  // or the certified LUT estimate (0), with the short factors packed as float4
   constexpr bool LUT = IPB == 0;
-  using IPT = typename std::conditional<IPB == 2, int16_t, typename std::conditional<LUT, float, int32_t>::type>::type;
+  constexpr bool PK = IPB < 2;
+  using IPT = typename std::conditional<IPB == 2, int16_t, int32_t>::type;
   extern __shared__ __align__(16) unsigned char rda_smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t slot_q = (int64_t)blockIdx.x * RDW + wid;
@@ -1376,7 +1380,7 @@ __global__ void __launch_bounds__(RDW * 32, MINB) scan_rda_kernel(Args a) {
       rT = entry_rad(T_list, __shfl_sync(FULL, qi, k - 1), rq);
     }
     probed += (int)n_c;
-    const float* rrow = a.rdist + cur.base;
+    const float* rrow = a.rdist + (PK ? 2 : 1) * cur.base;
     if (T_list == dinf()) {  // nothing can be pruned (lb2 <= +inf): every vector's refined distance
       surv += (int)n_c;
       for (int64_t c0 = 0; c0 < n_c; c0 += 32 * RSUB) {
@@ -1384,7 +1388,7 @@ __global__ void __launch_bounds__(RDW * 32, MINB) scan_rda_kernel(Args a) {
 #pragma unroll
         for (int u = 0; u < RSUB; ++u) {
           const int64_t vi = c0 + u * 32 + lane;
-          dv[u] = vi < n_c ? __ldg(rrow + vi) : 0.f;
+          dv[u] = vi < n_c ? __ldg(rrow + (PK ? 2 : 1) * vi) : 0.f;
         }
 #pragma unroll 1
         for (int u = 0; u < RSUB; ++u) {  // one copy of the queue code (instruction cache); the values
@@ -1401,7 +1405,7 @@ __global__ void __launch_bounds__(RDW * 32, MINB) scan_rda_kernel(Args a) {
       snap_d[lane] = qd;
       snap_e[lane] = qi;
       __syncwarp();
-      const IPT* iprow = reinterpret_cast<const IPT*>(a.ipbuf) + cur.base;
+      const IPT* iprow = PK ? nullptr : reinterpret_cast<const IPT*>(a.ipbuf) + cur.base;
       Stage1F32 f32 = stage1_f32(sc[IVRQ_QS_DELTA], sc[IVRQ_QS_HALF_CODE], sc[IVRQ_QS_IP_MARGIN], d_qc2, dsqrt(d_qc2),
                                  T_list);
       f32.T_lo = __double2float_rd(T_list - rT * (1.0 + 0x1p-40));
@@ -1413,13 +1417,21 @@ __global__ void __launch_bounds__(RDW * 32, MINB) scan_rda_kernel(Args a) {
         for (int u = 0; u < RSUB; ++u) {
           const int64_t vi = c0 + u * 32 + lane;
           const bool in = vi < n_c;
-#ifndef RDA_NOPRE
-          pre[u] = in ? __ldg(rrow + vi) : 0.f;
-#endif
-          ipv[u] = in ? (LUT ? __float_as_int((float)__ldg(iprow + vi)) : (int)__ldg(iprow + vi)) : 0;
-          fa[u] = in ? __ldg(a.ix.short_add + lo + vi) : 0.f;
-          fs[u] = in ? __ldg(a.ix.short_scale + lo + vi) : 0.f;
-          fe[u] = in ? __ldg(a.ix.short_err + lo + vi) : 0.f;
+          if (PK) {
+            const float2 r = in ? __ldg(reinterpret_cast<const float2*>(rrow) + vi) : make_float2(0.f, 0.f);
+            pre[u] = r.x;
+            ipv[u] = LUT ? __float_as_int(r.y) : (int)r.y;
+            const float4 f = in ? __ldg(a.sf4 + lo + vi) : make_float4(0.f, 0.f, 0.f, 0.f);
+            fa[u] = f.x;
+            fs[u] = f.y;
+            fe[u] = f.z;
+          } else {
+            pre[u] = in ? __ldg(rrow + vi) : 0.f;
+            ipv[u] = in ? (int)__ldg(iprow + vi) : 0;
+            fa[u] = in ? __ldg(a.ix.short_add + lo + vi) : 0.f;
+            fs[u] = in ? __ldg(a.ix.short_scale + lo + vi) : 0.f;
+            fe[u] = in ? __ldg(a.ix.short_err + lo + vi) : 0.f;
+          }
         }
         int dec[RSUB];
         bool open = false;
@@ -1460,10 +1472,6 @@ __global__ void __launch_bounds__(RDW * 32, MINB) scan_rda_kernel(Args a) {
         bool keep[RSUB];
 #pragma unroll
         for (int u = 0; u < RSUB; ++u) keep[u] = dec[u] > 0;
-#ifdef RDA_NOPRE
-#pragma unroll
-        for (int u = 0; u < RSUB; ++u) pre[u] = keep[u] ? __ldg(rrow + c0 + u * 32 + lane) : 0.f;
-#endif
 #pragma unroll 1
         for (int u = 0; u < RSUB; ++u) {  // one copy of the queue code (instruction cache); values
           const float d0 = pre[0];        // rotate through slot 0 so every index stays static
@@ -2806,41 +2814,12 @@ __global__ void __launch_bounds__(TCR_THREADS, 1) tc_refine_kernel(const __grid_
           uint32_t d[32];
           const uint32_t trow = tbase + ((uint32_t)(quarter * 32) << 16) + ab * acc_stride;
           tc::tmem_ld32(trow + TCR_DIG * j0, d);
+          uint32_t du[8], ds8[8], ds[32];
           if (fused) {
-            uint32_t du[8], ds[8];
             tc::tmem_ld8(trow + TCR_DIG * ((nqg + 3) & ~3) + j0, du);
-            tc::tmem_ld8(trow + TCR_DIG * G + G16 + j0, ds);
-            tc::tmem_ld_wait();
-#pragma unroll
-            for (int jj = 0; jj < 8; ++jj) {
-              const int j = j0 + jj;
-              if (j < nqg && v < n_c) {
-                // sum u qhat - sum s8(u) qhat = 256 sum msb(u) qhat, exactly
-                const int ip = ((int)du[jj] - (int)ds[jj]) >> 8;
-                const int64_t at = __double_as_longlong(qs[j].w) + v;
-                if (a.ip32) __stcs(reinterpret_cast<int32_t*>(a.ipbuf) + at, ip);
-                else __stcs(reinterpret_cast<int16_t*>(a.ipbuf) + at, (int16_t)ip);
-              }
-            }
+            tc::tmem_ld8(trow + TCR_DIG * G + G16 + j0, ds8);
           }
-          if (lutf) {
-            uint32_t ds[32];
-            tc::tmem_ld32(trow + TCR_DIG * G + TCR_DIG * j0, ds);
-            tc::tmem_ld_wait();
-#pragma unroll
-            for (int jj = 0; jj < 8; ++jj) {
-              const int j = j0 + jj;
-              if (j < nqg && v < n_c) {
-                // sum_d msb(u) D_d = (sum u D_d - sum s8(u) D_d) / 256, exactly; <msb, q> up to the neglected
-                // digits (|.| <= kpad L 2^(e-54)), then rounded to float32
-                int m[4];
-#pragma unroll
-                for (int dd = 0; dd < 4; ++dd) m[dd] = ((int)d[TCR_DIG * jj + dd] - (int)ds[TCR_DIG * jj + dd]) >> 8;
-                const double hm = fma((double)(m[0] * 128 + m[1]), 16384.0, (double)(m[2] * 128 + m[3]));
-                __stcs(reinterpret_cast<float*>(a.ipbuf) + __double_as_longlong(qs[j].w) + v, (float)(hm * qs[j].z));
-              }
-            }
-          }
+          if (lutf) tc::tmem_ld32(trow + TCR_DIG * G + TCR_DIG * j0, ds);
           tc::tmem_ld_wait();
 #pragma unroll
           for (int jj = 0; jj < 8; ++jj) {
@@ -2854,8 +2833,26 @@ __global__ void __launch_bounds__(TCR_THREADS, 1) tc_refine_kernel(const __grid_
               // each, inside rd_radius_kernel's 2^-50 M
               const double hi = fma((double)(D[0] * 128 + D[1]), 16384.0, (double)(D[2] * 128 + D[3]));
               const double t = fma(-hi, sq.z, sq.y);
-              // streaming store: written once, read once by the per-query pass
-              __stcs(a.rdist + __double_as_longlong(sq.w) + v, fmaxf((float)fma(lfy, t, lfx + sq.x), 0.f));
+              const float rd = fmaxf((float)fma(lfy, t, lfx + sq.x), 0.f);
+              const int64_t at = __double_as_longlong(sq.w) + v;
+              if (FUSION == 0) {
+                __stcs(a.rdist + at, rd);  // streaming store: written once, read once by the per-query pass
+              } else {
+                float ipf;
+                if (fused) {
+                  // sum u qhat - sum s8(u) qhat = 256 sum msb(u) qhat, exactly (an integer below 2^24)
+                  ipf = (float)(((int)du[jj] - (int)ds8[jj]) >> 8);
+                } else {
+                  // sum_d msb(u) D_d = (sum u D_d - sum s8(u) D_d) / 256, exactly; <msb, q> up to the
+                  // neglected digits (|.| <= kpad L 2^(e-54)), then rounded to float32
+                  int m[4];
+#pragma unroll
+                  for (int dd = 0; dd < 4; ++dd) m[dd] = ((int)D[dd] - (int)ds[TCR_DIG * jj + dd]) >> 8;
+                  ipf = (float)(fma((double)(m[0] * 128 + m[1]), 16384.0, (double)(m[2] * 128 + m[3])) * sq.z);
+                }
+                // (distance, stage-1 value) side by side: one 8-byte load per vector in the per-query pass
+                __stcs(reinterpret_cast<float2*>(a.rdist) + at, make_float2(rd, ipf));
+              }
             }
           }
         }
@@ -2894,6 +2891,13 @@ __global__ void rd_radius_kernel(const double* __restrict__ scalars, const doubl
   const double trunc = S * (U * ldexp(135274560.0, e - 54) + ldexp(ipmax, -53));
   const double M = A + dqm + S * (ipmax + fabs(sc[IVRQ_QS_KB_SUM]));
   rrad[q] = (trunc + ldexp(M, -50)) * (1.0 + 0x1p-20);
+}
+
+// (add, scale, err) of every vector packed for one 16-byte load in the per-query pass
+__global__ void pack_short_kernel(const float* __restrict__ add, const float* __restrict__ scale,
+                                  const float* __restrict__ err, int64_t n, float4* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = make_float4(__ldg(add + i), __ldg(scale + i), __ldg(err + i), 0.f);
 }
 
 // lfmax[0] = max |add|, lfmax[1] = max |scale| over the long factors (float bit patterns of
@@ -3215,9 +3219,8 @@ inline int launch_rd(const Args& a, bool refine, int ipb, cudaStream_t s) {
 #ifndef RDA_RSUB
 #define RDA_RSUB 4
 #endif
-  auto kern = ipb == 2   ? scan_rda_kernel<2, RDA_RSUB, RDA_MINB>
-              : ipb == 0 ? scan_rda_kernel<0, RDA_RSUB, RDA_MINB>
-                         : scan_rda_kernel<4, RDA_RSUB, RDA_MINB>;
+  auto kern = a.sf4 ? (ipb == 0 ? scan_rda_kernel<0, RDA_RSUB, RDA_MINB> : scan_rda_kernel<1, RDA_RSUB, RDA_MINB>)
+                     : (ipb == 2 ? scan_rda_kernel<2, RDA_RSUB, RDA_MINB> : scan_rda_kernel<4, RDA_RSUB, RDA_MINB>);
   const size_t sm = (size_t)RDW * ((size_t)a.kpad * sizeof(int2) + 32 * 16);
   if (sm > 48 * 1024 && cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess)
     return fail(IVRQ_EUNSUP, "ivrq_search_scan: shared memory request too large");
@@ -3254,9 +3257,11 @@ inline int launch_rd(const Args& a, bool refine, int ipb, cudaStream_t s) {
   f.fix_only = a.fix_list;
   f.fix_only_count = a.fix_count;
   f.init_ids = a.init_ids;
-  if (ipb == 0) {  // LUT mode: the per-query LUT scan (stage 1 from the tables), exact throughout
-    f.ipbuf = nullptr;
-    return launch_mode<IVRQ_IP_LUT>(f, true, rcode_nibbles(a.ix.bits), 0, s);
+  if (a.sf4) {  // fused stage 1 (no inner products in ipbuf): the per-query scan, stage 1 from the
+    f.ipbuf = nullptr;  // planes or tables, exact throughout
+    f.sf4 = nullptr;
+    return ipb == 0 ? launch_mode<IVRQ_IP_LUT>(f, true, rcode_nibbles(a.ix.bits), 0, s)
+                    : launch_mode<IVRQ_IP_BITWISE>(f, true, rcode_nibbles(a.ix.bits), 0, s);
   }
   return rcode_nibbles(a.ix.bits) ? launch_warp<true, true>(f, ipb, s) : launch_warp<true, false>(f, ipb, s);
 }
@@ -3607,7 +3612,8 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
         int64_t* rscratch = nullptr;
         int8_t* tcsl = nullptr;
         const int nkc = (a.kpad + scan::TCKC - 1) / scan::TCKC;
-        if (!ws.alloc(rdist, (size_t)tot[0]) || !ws.alloc(rgpre, nl + 1) || !ws.alloc(rscratch, nl + 3) ||
+        if (!ws.alloc(rdist, (size_t)tot[0] * (fusion ? 2 : 1)) || !ws.alloc(rgpre, nl + 1) ||
+            !ws.alloc(rscratch, nl + 3) ||
             !ws.alloc(tcsl, (size_t)npairs * nkc * 512) || !ws.alloc(rrad, nq) || !ws.alloc(fix, nq + 1) ||
             !ws.alloc(lfmax, 2))
           return oom("refined-distance buffer allocation failed");
@@ -3627,6 +3633,13 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
         a.rrad = rrad;
         a.fix_count = fix;
         a.fix_list = fix + 1;
+        if (fusion) {  // the per-query pass reads (distance, stage-1 value) pairs and packed short factors
+          float4* sf4 = nullptr;
+          if (!ws.alloc(sf4, (size_t)index->size)) return oom("workspace allocation failed");
+          scan::pack_short_kernel<<<(unsigned)(4 * sm_count_of_current_device()), 256, 0, s>>>(
+              index->short_add, index->short_scale, index->short_err, index->size, sf4);
+          a.sf4 = sf4;
+        }
         if (!ws.alloc(a.fin_d, (size_t)nq * 32) || !ws.alloc(a.fin_e, (size_t)nq * 32))
           return oom("refined-distance buffer allocation failed");
         scan::TcArgs ta{};

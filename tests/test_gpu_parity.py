@@ -434,8 +434,9 @@ def test_search_batch_short_rows(monkeypatch, chunks):
         np.testing.assert_array_equal(res[i][1], dists[i, : counts[i]])
 
 
-@pytest.mark.parametrize("k,copies,bits", [(10, 40, 8), (30, 6, 8), (10, 12, 4)])
-def test_refine_intervals_near_duplicates(monkeypatch, k, copies, bits):
+@pytest.mark.parametrize("k,copies,bits,mode", [(10, 40, 8, "bitwise"), (30, 6, 8, "bitwise"), (10, 12, 4, "bitwise"),
+                                                (10, 40, 8, "lut"), (30, 6, 8, "lut")])
+def test_refine_intervals_near_duplicates(monkeypatch, k, copies, bits, mode):
     """Near-duplicate vectors (distances apart by ~1e-7 relative, well inside the approximate
     refine's radius) force every interval decision of scan_rda_kernel open: the exact threshold
     from the list-start queue, the final exact top k, and (k = 30: more than 32 - k near-ties)
@@ -450,7 +451,7 @@ def test_refine_intervals_near_duplicates(monkeypatch, k, copies, bits):
     q = (base[rng.integers(0, 300, 200)] + 0.05 * rng.standard_normal((200, d))).astype(np.float32)
     ix = iv.build_index(x, iv.BuildParams(n_clusters=8, quant=iv.QuantizationParams(bits=bits), kmeans_iters=3,
                                           seed=1))
-    sp = iv.SearchParams(k=k, n_probe=4, ip_mode="bitwise", query_bits=4)
+    sp = iv.SearchParams(k=k, n_probe=4, ip_mode=mode, query_bits=4)
     qd = dev.to_device(q)
     out = {}
     for name, env in {"popcount": {"IVRQ_TC_STAGE1": "0"}, "tcgen05": {"IVRQ_TC_IP": "1", "IVRQ_TC_REFINE": "1"}}.items():
