@@ -488,9 +488,10 @@ __global__ void __launch_bounds__(THREADS, 4) scan_kernel(Args a) {
   __shared__ double s_T;
   __shared__ int s_pool_n;
   __shared__ long long s_probed, s_surv;
-  if (blockIdx.x >= a.nq) return;
-  if (a.fix_only && (int)blockIdx.x >= *a.fix_only_count) return;  // as the exact rerun of listed queries
-  const int64_t q = a.fix_only ? (int64_t)a.fix_only[blockIdx.x] : a.qorder ? a.qorder[blockIdx.x] : (int64_t)blockIdx.x;
+  // one query per CTA; as the exact rerun of listed queries (fix_only) a small grid strides the list
+  const int64_t nslot = a.fix_only ? (int64_t)*a.fix_only_count : a.nq;
+  for (int64_t slot = blockIdx.x; slot < nslot; slot += gridDim.x) {
+  const int64_t q = a.fix_only ? (int64_t)a.fix_only[slot] : a.qorder ? a.qorder[slot] : slot;
   const int k = a.k;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const Smem s = carve<MODE, REFINE>(a, smem, false);
@@ -604,6 +605,8 @@ __global__ void __launch_bounds__(THREADS, 4) scan_kernel(Args a) {
       a.stats[2 * q] = s_probed;
       a.stats[2 * q + 1] = s_surv;
     }
+  }
+  __syncthreads();  // the CTA's shared state is reused by the next slot
   }
 }
 
@@ -3297,7 +3300,7 @@ int launch_t(const Args& a, int ipb, cudaStream_t s) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return fail(IVRQ_EUNSUP, "ivrq_search_scan: shared memory request too large");
   }
-  kern<<<(unsigned)a.nq, THREADS, sm, s>>>(a);
+  kern<<<(unsigned)(a.fix_only ? std::min<int64_t>(a.nq, 2 * sm_count_of_current_device()) : a.nq), THREADS, sm, s>>>(a);
   return check_launch("ivrq_search_scan");
 }
 
