@@ -2684,14 +2684,10 @@ __global__ void __launch_bounds__(TCR_THREADS, 1) tc_refine_kernel(const __grid_
               const int st = it_prod % NST;
               tc::mbar_wait(&empty[st], ((it_prod / NST) & 1) ^ 1);
               TCR_EV(1, it_prod);
-#ifdef IVRQ_EXP_NOTMA
-              tc::mbar_arrive(&full[st]);
-#else
               tc::mbar_expect_tx(&full[st], TCM * TCKC);
               // evict-last: the list's other query groups re-read these rows from L2
               tc::tma_load_2d_hint(sA + st * TCM * TCKC, &a.map_a, kc * TCKC, (int)(lo + (int64_t)t * TCM), &full[st],
                                    tc::kL2EvictLast);
-#endif
             }
         }
       } else {
@@ -2756,7 +2752,6 @@ __global__ void __launch_bounds__(TCR_THREADS, 1) tc_refine_kernel(const __grid_
           if (lane == 0) {
             TCR_EV(2, it_mma);
             const int ks = min(TCKC, kp - kc * TCKC) / 32;
-#ifndef IVRQ_EXP_NOMMA
             for (int s2 = 0; s2 < ks; ++s2) {
               const uint64_t ad = tc::smem_desc_sw128(sA + st * TCM * TCKC + 32 * s2);
               const uint64_t bd = tc::smem_desc_sw128(sB + kc * bkc + 32 * s2);
@@ -2768,9 +2763,6 @@ __global__ void __launch_bounds__(TCR_THREADS, 1) tc_refine_kernel(const __grid_
                 tc::mma_i8(tbase + ab * acc_stride + TCR_DIG * G, ad, bd, idd_s, kc > 0 || s2 > 0);
               }
             }
-#else
-            (void)ks;
-#endif
             TCR_EV(8, it_mma);
             tc::commit(&empty[st]);
             if (kc == nkc - 1) tc::commit(&accf[ab]);
@@ -2810,9 +2802,6 @@ __global__ void __launch_bounds__(TCR_THREADS, 1) tc_refine_kernel(const __grid_
         wait1(&accf[ab], (tile_epi >> 1) & 1);
         if (lane == 0 && wid == TC_PROD + 1) TCR_EV(5, tile_epi);
         tc::fence_after_sync();
-#ifdef IVRQ_EXP_NOEPI
-        if (false)
-#endif
         for (int j0 = 8 * part; j0 < nqg; j0 += 8 * TCR_EPQ) {  // 8-query chunks, round robin over the parts
           uint32_t d[32];
           const uint32_t trow = tbase + ((uint32_t)(quarter * 32) << 16) + ab * acc_stride;
