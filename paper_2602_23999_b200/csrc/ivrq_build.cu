@@ -1061,7 +1061,7 @@ extern "C" int ivrq_counting_sort(const int32_t* labels, int64_t n, int32_t k, i
     return check_launch("ivrq_counting_sort");
   }
   if ((size_t)k * 4 > 200 * 1024) return fail(IVRQ_EUNSUP, "ivrq_counting_sort: too many clusters");
-  int64_t tile = 2048;
+  int64_t tile = 256;  // short serial walks per CTA (one warp per tile): the search's pair sorts are small
   // tiles x labels stays within max(n, 2^20) entries: the per-label passes over
   // the tile counts (cs_counts, cs_base) are then no larger than the rows
   while (ceil_div(n, tile) * (int64_t)k > std::max(n, (int64_t)1 << 20) && tile < (int64_t)1 << 16) tile *= 2;
