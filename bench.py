@@ -690,6 +690,89 @@ def run_reference(args, cfg_name: str) -> dict:
     }
 
 
+def run_sharded(args, cfg_name: str) -> dict:
+    """`--sharded`: the north star's list-sharded design, strong scaling.  The dataset's rows are split
+    in ascending blocks over the ranks, `build_sharded` trains shared centroids (data-parallel Lloyd)
+    and leaves each rank a contiguous cluster-id range; every step searches ONE shared 10K-query batch
+    with `search_sharded` (the exact ascending-id chain for B >= 2, the all-gather merge otherwise)."""
+    import torch
+    import torch.distributed as tdist
+
+    import paper_2602_23999_b200 as iv
+    from paper_2602_23999_b200.distributed import build_sharded, search_sharded
+    from paper_2602_23999_b200.linalg import exact_knn_device
+
+    world, rank, local = dist_setup()
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    for key, val in (("MASTER_ADDR", "127.0.0.1"), ("MASTER_PORT", "29533"), ("RANK", "0"), ("WORLD_SIZE", "1")):
+        os.environ.setdefault(key, val)  # a one-rank NCCL group when not launched by torchrun
+    tdist.init_process_group("nccl", device_id=device)
+    cfg = CONFIGS[cfg_name]
+    n, d, nlist, bits = cfg["n"], cfg["d"], cfg["nlist"], cfg["bits"]
+    x, queries = make_dataset_gpu(n, NQ, d, device, seed=20260810 + 0)
+    lo, hi = n * rank // world, n * (rank + 1) // world
+    x_local = x[lo:hi].contiguous()
+    params = iv.BuildParams(n_clusters=nlist, quant=iv.QuantizationParams(bits=bits), kmeans_iters=25,
+                            train_fraction=train_fraction(n, nlist), seed=0)
+    tdist.barrier()
+    torch.cuda.synchronize()
+    tb = time.perf_counter()
+    sidx = build_sharded(x_local, params)
+    torch.cuda.synchronize()
+    tdist.barrier()
+    build_s = time.perf_counter() - tb
+    sp = iv.SearchParams(k=K, n_probe=cfg["nprobe"], ip_mode=args.mode)
+    n_gt = min(NQ, 1000)
+    gt = exact_knn_device(x, queries[:n_gt].to(torch.float64), K)[0].cpu().numpy() if rank == 0 else None
+    del x
+    for _ in range(args.warmup):
+        ids, dists, counts = search_sharded(queries, sidx, sp)
+    torch.cuda.synchronize()
+    tdist.barrier()
+    stream = torch.cuda.current_stream(device)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        ids, dists, counts = search_sharded(queries, sidx, sp)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=device)
+    if world > 1:
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+    ms = float(t.item()) / args.steps
+    # end to end: host queries in, host ids out, every step
+    q_host = queries.cpu().numpy()
+    tdist.barrier()
+    te = time.perf_counter()
+    for _ in range(args.steps):
+        qd = torch.from_numpy(q_host).to(device, non_blocking=False)
+        ids_e, _, _ = search_sharded(qd, sidx, sp)
+        ids_e = ids_e.cpu()
+    e2e_s = (time.perf_counter() - te) / args.steps
+    te_t = torch.tensor([e2e_s], dtype=torch.float64, device=device)
+    if world > 1:
+        tdist.all_reduce(te_t, op=tdist.ReduceOp.MAX)
+    e2e_s = float(te_t.item())
+    out = None
+    if rank == 0:
+        got = ids[:n_gt].cpu().numpy()
+        out = {
+            "metric": "search QPS @ recall@10~0.95 (10K-query batch)", "value": round(NQ / (ms / 1e3), 1),
+            "unit": "queries/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64 estimator / int popcount / u8 codes", "data": DATA_NOTE,
+            "config": dict(config_dict(cfg_name, args.mode), parallelism=f"list-sharded x{world}",
+                           search_protocol="chain" if bits > 1 and sp.prune else "merge"),
+            "quality": {"recall_at_10": recall_at_k(got, gt, K), "recall_queries": n_gt},
+            "build": {"seconds": round(build_s, 3), "note": "build_sharded, device-resident rows"},
+            "e2e": {"value": round(NQ / e2e_s, 1), "unit": "queries/s", "h2d_bytes_per_step": int(q_host.nbytes),
+                    "d2h_bytes_per_step": int(NQ * K * 8)},
+        }
+    tdist.destroy_process_group()
+    return out
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -704,10 +787,14 @@ def main() -> None:
     ap.add_argument("--gt-queries", type=int, default=2000, help="queries with exact ground truth (0 = all)")
     ap.add_argument("--gt-check", type=int, default=100, help="ground-truth rows checked against the oracle")
     ap.add_argument("--build-breakdown", action="store_true", help="rebuild once with per-stage timings")
+    ap.add_argument("--sharded", action="store_true",
+                    help="list-sharded build + search of one shared batch (strong scaling) instead of replicas")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         out = run_reference(args, args.config)
+    elif args.sharded:
+        out = run_sharded(args, args.config)
     else:
         out = run_ours(args, args.config)
     if out:

@@ -401,6 +401,7 @@ __device__ K radix_kth(int n, int k, int total_bits, int32_t* hist, Get get, int
 constexpr int SMEM_ROW = 16384;  // upper bounds staged in shared memory up to this many centroids
 __host__ __device__ inline bool rs_fast_tau(int nlist, int nprobe) {
   // short rows: the radix select over shared memory is already cheaper than the register pass
+  // (measured at C3, nlist 1024: the register pass made the probe 0.45 ms against 0.39)
   return nlist >= 4096 && nlist <= RS_REG * RS_THREADS && nprobe <= RS_THREADS;
 }
 

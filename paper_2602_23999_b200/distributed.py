@@ -482,8 +482,12 @@ def _merge_gpu(stacked: Pools, parts: int, k: int) -> Pools:
 
 
 def search_sharded(q: torch.Tensor, sidx: ShardedIndex, params, group=None, mode: str = "auto",
-                   n_micro: int = 4) -> Pools:
-    """Search a list-sharded index; every rank returns the final (ids, dists, counts)."""
+                   n_micro: int | None = None) -> Pools:
+    """Search a list-sharded index; every rank returns the final (ids, dists, counts).
+
+    ``n_micro`` (chain mode) defaults to the number of ranks: enough micro-batches to keep every
+    rank busy once the chain is full, and no more (each micro-batch streams the rank's lists again).
+    """
     from paper_2602_23999_b200.search import _probe_device, prepare_queries_device, rotate_queries_device
 
     shard = sidx.local
@@ -519,5 +523,7 @@ def search_sharded(q: torch.Tensor, sidx: ShardedIndex, params, group=None, mode
     if mode == "merge":
         return merge_protocol(scan(slice(0, nq), None), k, group, _merge_gpu)
     if mode == "chain":
+        if n_micro is None:
+            n_micro = tdist.get_world_size(group) if tdist.is_initialized() else 1
         return chain_protocol(scan, nq, k, group, n_micro=n_micro, device=q.device)
     raise ValueError(f"unknown mode {mode!r}")
