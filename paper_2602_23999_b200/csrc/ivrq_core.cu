@@ -3,6 +3,7 @@
 
 #include <atomic>
 #include <cstdlib>
+#include <algorithm>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -46,9 +47,13 @@ cudaMemPool_t library_pool() {
       cudaGetLastError();
       return nullptr;
     }
-    // keep up to 4 GiB of freed workspace mapped (a C3 search uses ~1.3 GB per call)
+    // keep up to min(16 GiB, 1/8 of the device) of freed workspace mapped: a search's buffers (C3
+    // ~2.5 GB, C4 ~5 GB) are then reused across calls instead of being unmapped and mapped again
+    // at every call; ivrq_release_memory trims the pool on demand
     const char* env = getenv("IVRQ_POOL_KEEP_BYTES");
-    uint64_t keep = env ? strtoull(env, nullptr, 10) : (uint64_t(4) << 30);
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    uint64_t keep = env ? strtoull(env, nullptr, 10) : std::min<uint64_t>(uint64_t(16) << 30, total_b / 8);
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
     pools[dev] = pool;
   }

@@ -3323,10 +3323,11 @@ static ScanPolicy scan_policy(const ivrq_index_view& ix, const ivrq_search_param
   sp.warp_path = sp.tc_path && env_flag("IVRQ_WARP_SCAN", 1) != 0;
   // every probed pair refined list-major on tcgen05 (then a streaming per-query pass): dense
   // refine costs (probed vectors) x kpad MACs against (survivors) x kpad gathered by the in-warp
-  // refine; measured on the B200: dense wins for 8-bit codes at D <= 768 (C3), the survivor-only
-  // path for 4-bit codes (C2, C4: few survivors, 64-byte rows) and at D = 1536 (C5).
+  // refine.  Measured on the B200 with the certified 4-digit refine (round 2): dense wins at D <= 768
+  // for every code width (C3; C2 3.08 vs 3.37 ms per step, C4 9.65 vs 10.5); at D = 1536 (C5) the
+  // survivor-only path.
   const int tr = env_flag("IVRQ_TC_REFINE", -1);
-  const bool dense = tr >= 0 ? tr != 0 : (!rcode_nibbles(ix.bits) && kpad64(ix.dims) <= 768);
+  const bool dense = tr >= 0 ? tr != 0 : kpad64(ix.dims) <= 768;
   // (the epilogue's int32 digit pairs D0 * 128 + D1 stay below 2^31 for kpad <= 960 with 8-bit codes)
   const bool fits = rcode_nibbles(ix.bits) || kpad64(ix.dims) <= 960;
   sp.rd_path = sp.warp_path && (!refine || (ix.rcodes && dense && fits));
@@ -3585,7 +3586,9 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
     if (tot[0] > 0) {
       uint8_t* ipbuf = nullptr;
       int8_t* qhat = nullptr;
-      if (!ws.alloc(ipbuf, (size_t)tot[0] * ipb) || !ws.alloc(qhat, (size_t)nq * 32 * a.g))
+      // (the fused refine writes the stage-1 values beside its distances: no separate buffer)
+      const bool fused_stage1 = pol.rd_path && refine && index->bits == 8;
+      if (!ws.alloc(ipbuf, fused_stage1 ? 16 : (size_t)tot[0] * ipb) || !ws.alloc(qhat, (size_t)nq * 32 * a.g))
         return oom("inner-product buffer allocation failed");
       // 8-bit codes: the stage-1 inner products come out of the refine's own MMAs (no separate pass;
       // msb(u) = u >> 7 is what the signed reading of the byte subtracts)
