@@ -2508,6 +2508,7 @@ struct TcArgs {
   // LUT mode (8-bit codes): the stage-1 estimate <msb(u), q> from the digit rows read both ways,
   // written as float32 (a certified approximation of the LUT sum, see scan_rda_kernel)
   int lut;
+  int nib_hi;               // 4-bit codes unpacked as 16 u (the fused stage 1 reads the MSB as the sign bit)
 };
 
 // byte offset of (row R, byte k < 128) in a 128B-swizzled K-major tile (8-row atoms of 1024 B)
@@ -2551,7 +2552,7 @@ __global__ void tc_bpairs_kernel(const int8_t* __restrict__ qslices, const int64
 // pre-swizzled as row (slot & 7) of a 128B-swizzled 8-row atom; zero past the row.
 __global__ void tc_qpairs_kernel(const int8_t* __restrict__ qhat, const int64_t* __restrict__ porder,
                                  const int32_t* __restrict__ pslot, int64_t npairs, int nprobe, int rowb, int nkc,
-                                 int8_t* __restrict__ out) {
+                                 int nib, int8_t* __restrict__ out) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // one 16-byte chunk
   if (t >= npairs * nkc * 8) return;
   const int c16 = (int)(t & 7);
@@ -2563,7 +2564,21 @@ __global__ void tc_qpairs_kernel(const int8_t* __restrict__ qhat, const int64_t*
   if (slot < 0) return;
   const int P0 = kc * TCKC + 16 * c16;
   uint4 v = make_uint4(0u, 0u, 0u, 0u);
-  if (P0 < rowb) v = *reinterpret_cast<const uint4*>(qhat + (pr / nprobe) * (int64_t)rowb + P0);
+  const int8_t* row = qhat + (pr / nprobe) * (int64_t)rowb;
+  if (!nib) {
+    if (P0 < rowb) v = *reinterpret_cast<const uint4*>(row + P0);
+  } else {  // 4-bit codes: element P of the unpacked tile holds dimension refine_kdim(slice_pos(P))
+    uint32_t w[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const int P = P0 + e;
+      const int kk = (P & ~0x3C) | ((P & 0x0C) << 2) | ((P & 0x30) >> 2);
+      const int dim = refine_kdim(kk, true);
+      const uint32_t b = dim < rowb ? (uint32_t)(uint8_t)row[dim] : 0u;
+      w[e >> 2] |= b << (8 * (e & 3));
+    }
+    v = make_uint4(w[0], w[1], w[2], w[3]);
+  }
   const int R = slot & 7;
   *reinterpret_cast<uint4*>(out + blk * 128 + (((c16 ^ R) & 7) << 4)) = v;
 }
@@ -2723,8 +2738,12 @@ __global__ void __launch_bounds__(TCR_THREADS, 1) tc_refine_kernel(const __grid_
             const int i = pl + e * 32 * TC_PROD;
             const int r = i / (TCKC / 16), pc = 16 * (i % (TCKC / 16));
             const uint2 x = xc[e];
+            // fused stage 1: the code in the byte's high half (16 u), so its MSB is the byte's sign bit
             *reinterpret_cast<uint4*>(dst + sw128_offset(r, pc)) =
-                make_uint4(x.x & 0x0F0F0F0Fu, (x.x >> 4) & 0x0F0F0F0Fu, x.y & 0x0F0F0F0Fu, (x.y >> 4) & 0x0F0F0F0Fu);
+                a.nib_hi ? make_uint4((x.x << 4) & 0xF0F0F0F0u, x.x & 0xF0F0F0F0u, (x.y << 4) & 0xF0F0F0F0u,
+                                      x.y & 0xF0F0F0F0u)
+                         : make_uint4(x.x & 0x0F0F0F0Fu, (x.x >> 4) & 0x0F0F0F0Fu, x.y & 0x0F0F0F0Fu,
+                                      (x.y >> 4) & 0x0F0F0F0Fu);
           }
           tc::fence_smem_async();
           tc::mbar_arrive(&full[st]);
@@ -2823,7 +2842,10 @@ __global__ void __launch_bounds__(TCR_THREADS, 1) tc_refine_kernel(const __grid_
               // the dense path's kpad <= 960 for 8-bit codes), hi < 2^47 is exact in float64.  The distance
               // add + d_qc2 + scale (kb - hi 2^(e-26)) in this order: three roundings of at most 2^-53 M
               // each, inside rd_radius_kernel's 2^-50 M
-              const double hi = fma((double)(D[0] * 128 + D[1]), 16384.0, (double)(D[2] * 128 + D[3]));
+              // (4-bit codes with the fused stage 1 come in as 16 u: the digit sums are exact multiples of 16)
+              const int sh = a.nib_hi ? 4 : 0;
+              const double hi = fma((double)((D[0] >> sh) * 128 + (D[1] >> sh)), 16384.0,
+                                    (double)((D[2] >> sh) * 128 + (D[3] >> sh)));
               const double t = fma(-hi, sq.z, sq.y);
               const float rd = fmaxf((float)fma(lfy, t, lfx + sq.x), 0.f);
               const int64_t at = __double_as_longlong(sq.w) + v;
@@ -3333,7 +3355,8 @@ static ScanPolicy scan_policy(const ivrq_index_view& ix, const ivrq_search_param
   sp.rd_path = sp.warp_path && (!refine || (ix.rcodes && dense && fits));
   // LUT mode on the same list-major path for 8-bit codes: the refine's digit rows read as signed bytes
   // give a certified approximation of the LUT stage 1 (scan_rda_kernel<LUT>)
-  if (p.ip_mode == IVRQ_IP_LUT && p.k <= 32 && refine && ix.bits == 8 && ix.rcodes && dense && fits && nl >= 1 &&
+  if (p.ip_mode == IVRQ_IP_LUT && p.k <= 32 && refine && (ix.bits == 8 || rcode_nibbles(ix.bits)) && ix.rcodes &&
+      dense && fits && nl >= 1 &&
       env_flag("IVRQ_TC_STAGE1", 1) != 0 && env_flag("IVRQ_LUT_RD", 1) != 0) {
     sp.tc_path = sp.warp_path = sp.rd_path = true;
     sp.lut_rd = true;
@@ -3587,12 +3610,12 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
       uint8_t* ipbuf = nullptr;
       int8_t* qhat = nullptr;
       // (the fused refine writes the stage-1 values beside its distances: no separate buffer)
-      const bool fused_stage1 = pol.rd_path && refine && index->bits == 8;
+      const bool fused_stage1 = pol.rd_path && refine && (index->bits == 8 || nib);
       if (!ws.alloc(ipbuf, fused_stage1 ? 16 : (size_t)tot[0] * ipb) || !ws.alloc(qhat, (size_t)nq * 32 * a.g))
         return oom("inner-product buffer allocation failed");
       // 8-bit codes: the stage-1 inner products come out of the refine's own MMAs (no separate pass;
       // msb(u) = u >> 7 is what the signed reading of the byte subtracts)
-      const bool fused = pol.rd_path && refine && index->bits == 8 && !pol.lut_rd;
+      const bool fused = pol.rd_path && refine && (index->bits == 8 || nib) && !pol.lut_rd;
       const int fusion = fused ? 1 : pol.lut_rd ? 2 : 0;
       if (pol.rd_path && refine) {
         // refined distance of every probed pair on tcgen05 (concurrent with the inner products):
@@ -3664,7 +3687,7 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
           if (!ws.alloc(qpairs4, (size_t)npairs * nkc * 128)) return oom("workspace allocation failed");
           scan::qhat_kernel<<<(unsigned)ceil_div(nq * a.g, 256), 256, 0, s>>>(planes, nq, a.g, a.qbits, qhat);
           scan::tc_qpairs_kernel<<<(unsigned)ceil_div(npairs * nkc * 8, 256), 256, 0, s>>>(
-              qhat, porder, pslot, npairs, a.nprobe, 32 * a.g, nkc, qpairs4);
+              qhat, porder, pslot, npairs, a.nprobe, 32 * a.g, nkc, nib ? 1 : 0, qpairs4);
           IVRQ_TRY(check_launch("ivrq_search_scan(fused stage-1 operand)"));
           ta.bqhat = qpairs4;
           ta.ipbuf = ipbuf;
@@ -3674,6 +3697,7 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
           ta.lut = 1;
           ta.ipbuf = ipbuf;
         }
+        ta.nib_hi = (nib && fusion) ? 1 : 0;
         const size_t tsm = scan::tc_smem_bytes(a.kpad, G, nb, fusion);
         auto rk = fusion == 1 ? scan::tc_refine_kernel<1> : fusion == 2 ? scan::tc_refine_kernel<2>
                                                                         : scan::tc_refine_kernel<0>;
