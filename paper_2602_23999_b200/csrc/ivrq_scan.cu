@@ -2508,7 +2508,8 @@ struct TcArgs {
   // LUT mode (8-bit codes): the stage-1 estimate <msb(u), q> from the digit rows read both ways,
   // written as float32 (a certified approximation of the LUT sum, see scan_rda_kernel)
   int lut;
-  int nib_hi;               // 4-bit codes unpacked as 16 u (the fused stage 1 reads the MSB as the sign bit)
+  int nib_hi;               // codes of <= 4 bits unpacked as u << nib_hi, nib_hi = 8 - bits (the fused stage 1
+                            // reads the code's MSB as the sign bit), else 0
 };
 
 // byte offset of (row R, byte k < 128) in a 128B-swizzled K-major tile (8-row atoms of 1024 B)
@@ -2738,12 +2739,11 @@ __global__ void __launch_bounds__(TCR_THREADS, 1) tc_refine_kernel(const __grid_
             const int i = pl + e * 32 * TC_PROD;
             const int r = i / (TCKC / 16), pc = 16 * (i % (TCKC / 16));
             const uint2 x = xc[e];
-            // fused stage 1: the code in the byte's high half (16 u), so its MSB is the byte's sign bit
+            // fused stage 1: u << (8 - bits), so the code's MSB is the byte's sign bit (a.nib_hi = 8 - bits)
+            const int sh = a.nib_hi;
             *reinterpret_cast<uint4*>(dst + sw128_offset(r, pc)) =
-                a.nib_hi ? make_uint4((x.x << 4) & 0xF0F0F0F0u, x.x & 0xF0F0F0F0u, (x.y << 4) & 0xF0F0F0F0u,
-                                      x.y & 0xF0F0F0F0u)
-                         : make_uint4(x.x & 0x0F0F0F0Fu, (x.x >> 4) & 0x0F0F0F0Fu, x.y & 0x0F0F0F0Fu,
-                                      (x.y >> 4) & 0x0F0F0F0Fu);
+                make_uint4((x.x & 0x0F0F0F0Fu) << sh, ((x.x >> 4) & 0x0F0F0F0Fu) << sh, (x.y & 0x0F0F0F0Fu) << sh,
+                           ((x.y >> 4) & 0x0F0F0F0Fu) << sh);
           }
           tc::fence_smem_async();
           tc::mbar_arrive(&full[st]);
@@ -2842,8 +2842,8 @@ __global__ void __launch_bounds__(TCR_THREADS, 1) tc_refine_kernel(const __grid_
               // the dense path's kpad <= 960 for 8-bit codes), hi < 2^47 is exact in float64.  The distance
               // add + d_qc2 + scale (kb - hi 2^(e-26)) in this order: three roundings of at most 2^-53 M
               // each, inside rd_radius_kernel's 2^-50 M
-              // (4-bit codes with the fused stage 1 come in as 16 u: the digit sums are exact multiples of 16)
-              const int sh = a.nib_hi ? 4 : 0;
+              // (codes of <= 4 bits with the fused stage 1 come in as u 2^(8 - bits): exact multiples)
+              const int sh = a.nib_hi;
               const double hi = fma((double)((D[0] >> sh) * 128 + (D[1] >> sh)), 16384.0,
                                     (double)((D[2] >> sh) * 128 + (D[3] >> sh)));
               const double t = fma(-hi, sq.z, sq.y);
@@ -3697,7 +3697,7 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
           ta.lut = 1;
           ta.ipbuf = ipbuf;
         }
-        ta.nib_hi = (nib && fusion) ? 1 : 0;
+        ta.nib_hi = (nib && fusion) ? 8 - index->bits : 0;
         const size_t tsm = scan::tc_smem_bytes(a.kpad, G, nb, fusion);
         auto rk = fusion == 1 ? scan::tc_refine_kernel<1> : fusion == 2 ? scan::tc_refine_kernel<2>
                                                                         : scan::tc_refine_kernel<0>;
