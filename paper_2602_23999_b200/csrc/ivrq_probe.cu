@@ -603,6 +603,7 @@ int probe_tc(const double* q_rot, int64_t nq, int32_t dims, const float* centroi
   int32_t *qe = nullptr, *ce = nullptr;
   double *ql1 = nullptr, *cl1 = nullptr;
   float* bounds = nullptr;
+  // (bound rows in 256 MB chunks; 64 / 100 MB chunks measured slower at C4: probe 2.08 / 1.99 vs 1.78 ms)
   const int64_t rows = std::max<int64_t>(128, std::min<int64_t>(nq, ((int64_t)256 << 20) / ((int64_t)n_clusters * 8)));
   Workspace ws(s);
   if (!ws.alloc(qd, (size_t)4 * nq * kp) || !ws.alloc(cd, (size_t)4 * n_clusters * kp) || !ws.alloc(qe, nq) ||
