@@ -120,6 +120,24 @@ IVRQ_API int ivrq_device_sm_count(int device, int* out);
  * process-wide default CUDA pool is never reconfigured. */
 IVRQ_API int ivrq_release_memory(void* stream);
 
+/* Enqueue on `stream` a wait until *flag >= value (cuStreamWaitValue32, GEQ).  `flag` is a
+ * word of page-locked host memory that the host raises once it has staged a piece of a
+ * query batch; search_batch enqueues the whole search first and publishes the pieces as
+ * they are copied (host-side pipeline of reference search.py:390-454).  IVRQ_EUNSUP when
+ * the driver has no stream memory operations (the caller then stages before enqueueing). */
+IVRQ_API int ivrq_stream_wait_flag(const uint32_t* flag, uint32_t value, void* stream);
+
+/* Copy `rows` rows of `row_bytes` from host `src` into page-locked `dst` on `nthreads` native
+ * threads, in `npieces` row pieces: thread t copies part t of each piece in piece order, then
+ * atomically increments flags[p] (page-locked, npieces words, zeroed here).  Piece p is staged
+ * once flags[p] == nthreads: a stream waits for it with ivrq_stream_wait_flag(flags + p,
+ * nthreads), the host with ivrq_stage_wait.  Returns at once; ivrq_stage_join(*handle) joins
+ * the threads (call it exactly once, after which src may be released). */
+IVRQ_API int ivrq_stage_rows(void* dst, const void* src, int64_t rows, int64_t row_bytes, int32_t npieces,
+                             int32_t nthreads, uint32_t* flags, void** handle);
+IVRQ_API int ivrq_stage_wait(const uint32_t* flags, int32_t piece, int32_t nthreads);
+IVRQ_API int ivrq_stage_join(void* handle);
+
 /* Bytes per vector of the rcodes layout (0 for bits == 1). */
 IVRQ_API int64_t ivrq_rcode_row_bytes(int32_t dims, int32_t bits);
 

@@ -73,6 +73,10 @@ _SIGNATURES: dict[str, tuple[object, list[object]]] = {
     "ivrq_last_error": (ctypes.c_char_p, []),
     "ivrq_device_sm_count": (c_int, [c_int, POINTER(c_int)]),
     "ivrq_release_memory": (c_int, [P]),
+    "ivrq_stream_wait_flag": (c_int, [P, ctypes.c_uint32, P]),
+    "ivrq_stage_rows": (c_int, [P, P, c_int64, c_int64, c_int32, c_int32, P, POINTER(c_void_p)]),
+    "ivrq_stage_wait": (c_int, [P, c_int32, c_int32]),
+    "ivrq_stage_join": (c_int, [P]),
     "ivrq_row_sqnorms": (c_int, [P, c_int, c_int64, c_int32, P, P]),
     "ivrq_matmul_nt": (c_int, [P, c_int, P, c_int, c_int64, c_int64, c_int32, P, P]),
     "ivrq_rotate_queries": (c_int, [P, c_int, c_int64, c_int32, P, P, P]),

@@ -4,7 +4,14 @@
 #include <atomic>
 #include <cstdlib>
 #include <algorithm>
+#include <condition_variable>
+#if defined(__x86_64__)
+#include <emmintrin.h>
+#endif
+#include <cstring>
+#include <deque>
 #include <mutex>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -194,6 +201,167 @@ extern "C" int ivrq_release_memory(void* stream) {
   if (!pool) return IVRQ_OK;
   if (cudaStreamSynchronize(as_stream(stream)) != cudaSuccess || cudaMemPoolTrimTo(pool, 0) != cudaSuccess)
     return fail(IVRQ_ECUDA, "ivrq_release_memory: pool trim failed");
+  return IVRQ_OK;
+}
+
+extern "C" int ivrq_stream_wait_flag(const uint32_t* flag, uint32_t value, void* stream) {
+  // cuStreamWaitValue32(GEQ) on a page-locked host word: work enqueued after it on `stream`
+  // (the H2D copy of a piece of a host batch) starts only once the host has published the
+  // piece, so a whole search is enqueued before its queries are staged (search.py pipeline)
+  using WaitFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+  static WaitFn wait = nullptr;
+  if (!wait) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return fail(IVRQ_EUNSUP, "ivrq_stream_wait_flag: cuStreamWaitValue32 unavailable");
+    wait = reinterpret_cast<WaitFn>(fn);
+  }
+  if (!flag) return fail(IVRQ_EINVAL, "ivrq_stream_wait_flag: null flag");
+  void* dptr = nullptr;
+  if (cudaHostGetDevicePointer(&dptr, const_cast<uint32_t*>(flag), 0) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(IVRQ_EINVAL, "ivrq_stream_wait_flag: flag is not in page-locked host memory");
+  }
+  if (wait(reinterpret_cast<CUstream>(as_stream(stream)), reinterpret_cast<CUdeviceptr>(dptr), value,
+           CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+    return fail(IVRQ_EUNSUP, "ivrq_stream_wait_flag: stream wait rejected by the driver");
+  return IVRQ_OK;
+}
+
+namespace {
+// A host batch copied into page-locked memory by native threads, piece by piece.  The batch is cut
+// into (piece, part) tasks queued piece-major on a persistent worker pool; a task copies its rows
+// and then raises its piece's flag word by one (release), so flags[p] == nparts once piece p is
+// staged.  No Python (and no GIL) is on the publish path: a stream waiting on the flags can never
+// wait on the interpreter.  The workers live for the process (threads that exit per call unmap
+// their stacks, and the TLB shootdowns measurably slowed the DMA reading the staged rows).
+// Copy with non-temporal stores, then drain them.  The DMA that reads the staged rows must not find
+// them dirty in the cores' private caches (snooping them back ran the H2D copy of the last-staged
+// rows at ~1/3 of the rate of rows already written back).
+void stream_copy(char* dst, const char* src, size_t bytes) {
+#if defined(__x86_64__)
+  size_t head = (16 - (reinterpret_cast<uintptr_t>(dst) & 15)) & 15;
+  if (head > bytes) head = bytes;
+  if (head) std::memcpy(dst, src, head);
+  dst += head;
+  src += head;
+  bytes -= head;
+  size_t i = 0;
+  for (; i + 64 <= bytes; i += 64) {
+    const __m128i a = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i));
+    const __m128i b = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 16));
+    const __m128i c = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 32));
+    const __m128i e = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 48));
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i), a);
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 16), b);
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 32), c);
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 48), e);
+  }
+  if (i < bytes) std::memcpy(dst + i, src + i, bytes - i);
+  _mm_sfence();
+#else
+  std::memcpy(dst, src, bytes);
+#endif
+}
+
+struct StageJob {
+  std::atomic<int64_t> left{0};
+  std::mutex mu;
+  std::condition_variable cv;
+};
+struct StageTask {
+  StageJob* job;
+  char* dst;
+  const char* src;
+  size_t bytes;
+  uint32_t* flag;
+};
+struct StagePool {
+  std::mutex mu;
+  std::condition_variable cv;
+  std::deque<StageTask> q;
+  int workers = 0;
+  void grow(int n) {  // under mu
+    for (; workers < n; ++workers) {
+      std::thread([this]() { run(); }).detach();
+    }
+  }
+  void run() {
+    for (;;) {
+      StageTask t;
+      {
+        std::unique_lock<std::mutex> lk(mu);
+        cv.wait(lk, [this]() { return !q.empty(); });
+        t = q.front();
+        q.pop_front();
+      }
+      if (t.bytes) stream_copy(t.dst, t.src, t.bytes);
+      __atomic_fetch_add(t.flag, 1u, __ATOMIC_SEQ_CST);
+      {  // under the job's lock: ivrq_stage_join frees the job as soon as it sees left == 0
+        std::lock_guard<std::mutex> lk(t.job->mu);
+        if (t.job->left.fetch_sub(1) == 1) t.job->cv.notify_all();
+      }
+    }
+  }
+};
+StagePool& stage_pool() {
+  static StagePool* pool = new StagePool();  // never destroyed: the detached workers outlive main()
+  return *pool;
+}
+}  // namespace
+
+extern "C" int ivrq_stage_rows(void* dst, const void* src, int64_t rows, int64_t row_bytes, int32_t npieces,
+                               int32_t nthreads, uint32_t* flags, void** handle) {
+  if (!handle) return fail(IVRQ_EINVAL, "ivrq_stage_rows: null handle");
+  *handle = nullptr;
+  if (rows < 0 || row_bytes <= 0 || npieces < 1 || nthreads < 1 || nthreads > 256 || !flags ||
+      (rows > 0 && (!dst || !src)))
+    return fail(IVRQ_EINVAL, "ivrq_stage_rows: bad arguments");
+  for (int p = 0; p < npieces; ++p) __atomic_store_n(flags + p, 0u, __ATOMIC_RELEASE);
+  auto* job = new StageJob();
+  job->left = (int64_t)npieces * nthreads;
+  char* d = static_cast<char*>(dst);
+  const char* sp = static_cast<const char*>(src);
+  StagePool& pool = stage_pool();
+  {
+    std::lock_guard<std::mutex> lk(pool.mu);
+    try {
+      pool.grow(nthreads);
+    } catch (...) {
+      if (pool.workers == 0) {
+        delete job;
+        return fail(IVRQ_ECUDA, "ivrq_stage_rows: could not start the staging threads");
+      }
+    }
+    for (int p = 0; p < npieces; ++p) {
+      const int64_t x = rows * p / npieces, y = rows * (p + 1) / npieces;
+      for (int t = 0; t < nthreads; ++t) {
+        const int64_t u = x + (y - x) * t / nthreads, v = x + (y - x) * (t + 1) / nthreads;
+        pool.q.push_back({job, d + u * row_bytes, sp + u * row_bytes, (size_t)((v - u) * row_bytes), flags + p});
+      }
+    }
+  }
+  pool.cv.notify_all();
+  *handle = job;
+  return IVRQ_OK;
+}
+
+extern "C" int ivrq_stage_wait(const uint32_t* flags, int32_t piece, int32_t nthreads) {
+  // host-side wait for one piece (used when the driver has no stream memory operations)
+  while (__atomic_load_n(flags + piece, __ATOMIC_ACQUIRE) < (uint32_t)nthreads) std::this_thread::yield();
+  return IVRQ_OK;
+}
+
+extern "C" int ivrq_stage_join(void* handle) {
+  auto* job = static_cast<StageJob*>(handle);
+  if (!job) return IVRQ_OK;
+  {
+    std::unique_lock<std::mutex> lk(job->mu);
+    job->cv.wait(lk, [job]() { return job->left.load() == 0; });
+  }
+  delete job;
   return IVRQ_OK;
 }
 

@@ -19,6 +19,7 @@ threshold trajectory).
 from __future__ import annotations
 
 import math
+import os
 import threading
 from dataclasses import dataclass
 
@@ -341,14 +342,19 @@ def cluster_local_search(
     return dev.to_host(out_i[:m]).copy(), dev.to_host(out_d[:m]).copy()
 
 
-def _probe_device(q_rot: torch.Tensor, cent: torch.Tensor, c_sq: torch.Tensor, n_probe: int, order_by_id: bool):
+def _probe_device(q_rot: torch.Tensor, cent: torch.Tensor, c_sq: torch.Tensor, n_probe: int, order_by_id: bool,
+                  out: tuple[torch.Tensor, torch.Tensor] | None = None, ws: torch.Tensor | None = None):
     nq, d = q_rot.shape
     nlist = cent.shape[0]
-    ids = torch.empty((nq, n_probe), dtype=torch.int64, device=q_rot.device)
-    d2 = torch.empty((nq, n_probe), dtype=torch.float64, device=q_rot.device)
+    if out is None:
+        ids = torch.empty((nq, n_probe), dtype=torch.int64, device=q_rot.device)
+        d2 = torch.empty((nq, n_probe), dtype=torch.float64, device=q_rot.device)
+    else:
+        ids, d2 = out
     lib = _lib.load()
     ws_bytes = int(lib.ivrq_select_clusters_workspace(nq, nlist))
-    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=q_rot.device)
+    if ws is None or ws.numel() < ws_bytes:
+        ws = torch.empty(ws_bytes, dtype=torch.uint8, device=q_rot.device)
     _lib.call(
         "ivrq_select_clusters_ordered",
         dev.ptr(q_rot), nq, d, dev.ptr(cent), dev.ptr(c_sq), nlist, n_probe, 1 if order_by_id else 0,
@@ -404,19 +410,27 @@ def rotate_queries_device(q: torch.Tensor, index: IvfRabitqIndex, out: torch.Ten
     return q_rot
 
 
-def prepare_queries_device(q_rot: torch.Tensor, index: IvfRabitqIndex, params: SearchParams):
-    """QueryState scalars + planes/LUTs for every query (device tensors)."""
-    nq, d = q_rot.shape
+def _query_state_buffers(nq: int, d: int, index: IvfRabitqIndex, params: SearchParams, device):
+    """scalars, planes, luts, qslices as ivrq_prepare_queries writes them (None when unused)."""
     g = (d + 31) // 32
-    scalars = torch.empty((nq, _lib.QS_COUNT), dtype=torch.float64, device=q_rot.device)
+    scalars = torch.empty((nq, _lib.QS_COUNT), dtype=torch.float64, device=device)
     planes = luts = qslices = None
     if params.refine and index.bits >= 2:
         kpad = (d + 63) // 64 * 64
-        qslices = torch.empty((nq, 8, kpad), dtype=torch.int8, device=q_rot.device)
+        qslices = torch.empty((nq, 8, kpad), dtype=torch.int8, device=device)
     if params.ip_mode == "bitwise":
-        planes = torch.empty((nq, params.query_bits, g), dtype=torch.int32, device=q_rot.device)
+        planes = torch.empty((nq, params.query_bits, g), dtype=torch.int32, device=device)
     else:
-        luts = torch.empty((nq, 8 * g, 16), dtype=torch.float32, device=q_rot.device)
+        luts = torch.empty((nq, 8 * g, 16), dtype=torch.float32, device=device)
+    return scalars, planes, luts, qslices
+
+
+def prepare_queries_device(q_rot: torch.Tensor, index: IvfRabitqIndex, params: SearchParams, out=None):
+    """QueryState scalars + planes/LUTs for every query (device tensors); ``out`` = row slices
+    of buffers from _query_state_buffers."""
+    nq, d = q_rot.shape
+    scalars, planes, luts, qslices = out if out is not None else _query_state_buffers(nq, d, index, params,
+                                                                                      q_rot.device)
     cp = params.to_c()
     _lib.call(
         "ivrq_prepare_queries",
@@ -459,6 +473,16 @@ def search_device(
     mark("probed")
     scalars, planes, luts, qslices = prepare_queries_device(q_rot, index, params)
     mark("prepared")
+    res = _scan_device(q_rot, index, params, probe_ids, probe_d2, (scalars, planes, luts, qslices), with_stats)
+    mark("scanned")
+    return res
+
+
+def _scan_device(q_rot, index: IvfRabitqIndex, params: SearchParams, probe_ids, probe_d2, state,
+                 with_stats: bool = False) -> DeviceResult:
+    """ivrq_search_scan over the whole batch (the per-query loop, search.py:425-448)."""
+    nq = q_rot.shape[0]
+    scalars, planes, luts, qslices = state
     k = params.k
     out_ids = torch.empty((nq, k), dtype=torch.int64, device=q_rot.device)
     out_d = torch.empty((nq, k), dtype=torch.float64, device=q_rot.device)
@@ -471,7 +495,6 @@ def search_device(
         dev.ptr(luts), dev.ptr(qslices), nq, cp, dev.ptr(out_ids), dev.ptr(out_d), dev.ptr(counts), dev.ptr(stats),
         dev.stream_ptr(),
     )
-    mark("scanned")
     return DeviceResult(ids=out_ids, dists=out_d, counts=counts, stats=stats)
 
 
@@ -513,9 +536,19 @@ def _pinned(device: torch.device, name: str, nbytes: int) -> torch.Tensor:
     return buf
 
 
-_STAGE_THREADS = 4
-_STAGE_PIECES = 4  # host->device pieces of a single-batch search (copy / transfer / rotation overlap)
+def _env_int(name: str, default: int) -> int:
+    v = os.environ.get(name)
+    return int(v) if v else default
+
+
+_STAGE_THREADS = max(1, _env_int("IVRQ_STAGE_THREADS", min(8, os.cpu_count() or 4)))
 _POOL = None
+
+
+def _stage_pieces(nq: int) -> int:
+    """Host->device pieces of a single-batch search (copy / transfer / rotation overlap):
+    pieces of >= 1024 queries keep every rotation GEMM at least a wave of tiles."""
+    return max(1, min(_env_int("IVRQ_STAGE_PIECES", 4), nq // 1024))
 
 
 def _stage_pool():
@@ -542,6 +575,102 @@ def _chunk_bounds(nq: int) -> list[int]:
     n = int(env) if env else 1  # each chunk re-streams the index (list-major kernels): one batch
     n = max(1, min(n, nq))
     return [nq * i // n for i in range(n + 1)]
+
+
+_WAIT_OK: bool | None = None
+
+
+def _stream_wait_supported(flag_ptr: int) -> bool:
+    """Whether the driver takes stream waits on a host flag (probed once, value 0 always holds)."""
+    global _WAIT_OK
+    if _WAIT_OK is None:
+        if os.environ.get("IVRQ_STREAM_WAIT", "1") == "0":
+            _WAIT_OK = False
+        else:
+            try:
+                _lib.call("ivrq_stream_wait_flag", flag_ptr, 0, dev.stream_ptr())
+                _WAIT_OK = True
+            except Exception:
+                _WAIT_OK = False
+    return _WAIT_OK
+
+
+def _copy_stream(device) -> torch.cuda.Stream:
+    """The calling thread's host->device copy stream on ``device``."""
+    streams = getattr(_PINNED, "copy_streams", None)
+    if streams is None:
+        streams = _PINNED.copy_streams = {}
+    key = device.index or 0
+    if key not in streams:
+        streams[key] = torch.cuda.Stream(device)
+    return streams[key]
+
+
+class _PieceStager:
+    """Host copy of a query batch into pinned memory, in row pieces, on native threads.
+
+    ivrq_stage_rows splits every piece over all threads, which copy the pieces in
+    order and raise one page-locked flag word per piece; piece 0 is staged after 1/P
+    of the copy.  When the driver supports stream memory operations the stream waits
+    on the piece's flag (ivrq_stream_wait_flag), so the whole search is enqueued while
+    the copy runs; otherwise ``wait(p)`` blocks the host on piece p.  Nothing on the
+    publish path needs the interpreter: a GPU-synchronising call made while the GIL is
+    held (an allocation, say) cannot deadlock against the staging.
+    """
+
+    def __init__(self, q: np.ndarray, pin_np: np.ndarray, device) -> None:
+        import ctypes
+
+        nq = q.shape[0]
+        npieces = _stage_pieces(nq)
+        edges = [nq * p // npieces for p in range(npieces + 1)]  # the same split as ivrq_stage_rows
+        self.pieces = list(zip(edges[:-1], edges[1:]))
+        self.max_piece = max(y - x for x, y in self.pieces)
+        self.nthreads = _STAGE_THREADS
+        flags_t = _pinned(device, "flag", 4 * npieces)[: 4 * npieces]
+        self.flags_ptr = flags_t.data_ptr()
+        self.stream_wait = _stream_wait_supported(self.flags_ptr)
+        self._q = q  # kept alive until the threads are joined
+        self._handle = ctypes.c_void_p()
+        _lib.call("ivrq_stage_rows", pin_np.ctypes.data, q.ctypes.data, nq, q.strides[0], npieces, self.nthreads,
+                  self.flags_ptr, ctypes.byref(self._handle))
+
+    def wait(self, p: int) -> None:
+        if self.stream_wait:
+            _lib.call("ivrq_stream_wait_flag", self.flags_ptr + 4 * p, self.nthreads, dev.stream_ptr())
+        else:
+            _lib.call("ivrq_stage_wait", self.flags_ptr, p, self.nthreads)
+
+    def finish(self) -> None:
+        """Join the copy threads (every flag then holds its final value: no wait stays pending)."""
+        if self._handle:
+            _lib.call("ivrq_stage_join", self._handle)
+            self._handle = None
+
+
+class _Front:
+    """Rotation, probe and query state for row pieces of one batch, into whole-batch buffers."""
+
+    def __init__(self, nq: int, d: int, index: IvfRabitqIndex, params: SearchParams, device, max_piece: int):
+        self.index, self.params = index, params
+        t = index.device
+        self.cent, self.c_sq = t["centroids"], t["centroid_sqnorms"]
+        self.q_rot = torch.empty((nq, d), dtype=torch.float64, device=device)
+        self.probe_ids = torch.empty((nq, params.n_probe), dtype=torch.int64, device=device)
+        self.probe_d2 = torch.empty((nq, params.n_probe), dtype=torch.float64, device=device)
+        self.state = _query_state_buffers(nq, d, index, params, device)
+        ws_bytes = int(_lib.load().ivrq_select_clusters_workspace(max_piece, self.cent.shape[0]))
+        self.ws = torch.empty(ws_bytes, dtype=torch.uint8, device=device)
+
+    def run(self, qd: torch.Tensor, x: int, y: int) -> None:
+        if y <= x:
+            return
+        q_rot = self.q_rot[x:y]
+        rotate_queries_device(qd, self.index, out=q_rot)
+        _probe_device(q_rot, self.cent, self.c_sq, self.params.n_probe, True,
+                      out=(self.probe_ids[x:y], self.probe_d2[x:y]), ws=self.ws)
+        prepare_queries_device(q_rot, self.index, self.params,
+                               out=tuple(None if b is None else b[x:y] for b in self.state))
 
 
 def _search_pipelined(q: np.ndarray, index: IvfRabitqIndex, params: SearchParams):
@@ -589,33 +718,51 @@ def _search_pipelined(q: np.ndarray, index: IvfRabitqIndex, params: SearchParams
         pool = _stage_pool()
         return [pool.submit(np.copyto, pin_q_np[x:y], q[x:y]) for x, y in zip(parts[:-1], parts[1:]) if y > x]
 
-    def stage_rotate(a: int, b: int, q_rot: torch.Tensor) -> None:
-        # pieces: host copy of piece p+1 runs while piece p is transferred and rotated
-        pieces = np.linspace(a, b, _STAGE_PIECES + 1).astype(np.int64)
-        pool = _stage_pool()
-        futs = [pool.submit(np.copyto, pin_q_np[x:y], q[x:y]) for x, y in zip(pieces[:-1], pieces[1:])]
-        for (x, y), f in zip(zip(pieces[:-1], pieces[1:]), futs):
-            f.result()
-            if y > x:
-                qd[x:y].copy_(pin_q_t[x:y], non_blocking=True)
-                rotate_queries_device(qd[x:y], index, out=q_rot[x - a : y - a])
-
-    if len(bounds) == 2:  # one batch: staging, transfer and rotation overlap piecewise
-        import os
+    if len(bounds) == 2:  # one batch: staging, transfer, rotation, probe and prep overlap piecewise
         import time
 
         trace = os.environ.get("IVRQ_E2E_TRACE")
         t0 = time.perf_counter()
         with torch.cuda.stream(stream):
-            q_rot = torch.empty((nq, d), dtype=torch.float64, device=device)
-            stage_rotate(0, nq, q_rot)
-            t1 = time.perf_counter()
-            res = search_device(None, index, params, q_rot=q_rot)
-            ids_t.copy_(res.ids, non_blocking=True)
-            dists_t.copy_(res.dists, non_blocking=True)
-            counts_t.copy_(res.counts, non_blocking=True)
-            ev = torch.cuda.Event()
-            ev.record(stream)
+            stager = _PieceStager(q, pin_q_np, device)
+            try:
+                front = _Front(nq, d, index, params, device, stager.max_piece)
+                tev = []
+
+                def tmark(name):
+                    if trace:
+                        e = torch.cuda.Event(enable_timing=True)
+                        e.record(stream)
+                        tev.append((name, e))
+
+                tmark("start")
+                # H2D copies on a copy stream (each behind its piece's flag), so the transfer of
+                # piece p+1 overlaps the rotation / probe / prep of piece p on the compute stream
+                cstream = _copy_stream(device)
+                ready = torch.cuda.Event()
+                ready.record(stream)  # qd's memory is free on the compute stream from here
+                cstream.wait_event(ready)
+                qd.record_stream(cstream)
+                for p, (x, y) in enumerate(stager.pieces):
+                    with torch.cuda.stream(cstream):
+                        stager.wait(p)  # a stream wait on the published flag (or a host wait)
+                        qd[x:y].copy_(pin_q_t[x:y], non_blocking=True)
+                        landed = torch.cuda.Event()
+                        landed.record(cstream)
+                    stream.wait_event(landed)
+                    tmark(f"h{p}")
+                    front.run(qd[x:y], x, y)
+                    tmark(f"f{p}")
+                t1 = time.perf_counter()
+                res = _scan_device(front.q_rot, index, params, front.probe_ids, front.probe_d2, front.state)
+                tmark("scan")
+                ids_t.copy_(res.ids, non_blocking=True)
+                dists_t.copy_(res.dists, non_blocking=True)
+                counts_t.copy_(res.counts, non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(stream)
+            finally:
+                stager.finish()  # every piece published (releases the stream on any error), copies joined
             t2 = time.perf_counter()
             # the per-query row views are made while the GPU searches; the results are copied
             # into the viewed arrays once the event fires, short rows (count < k) re-cut after
@@ -634,8 +781,11 @@ def _search_pipelined(q: np.ndarray, index: IvfRabitqIndex, params: SearchParams
         if trace:
             import sys
 
-            print(f"[e2e] staged+rotate-enqueued {1e3*(t1-t0):.2f} enqueue {1e3*(t2-t1):.2f} "
-                  f"row views + gpu-wait {1e3*(t3-t2):.2f} copy-out {1e3*(t4-t3):.2f} ms", file=sys.stderr)
+            print(f"[e2e] front enqueued {1e3*(t1-t0):.2f} scan enqueued + staged {1e3*(t2-t1):.2f} "
+                  f"row views + gpu-wait {1e3*(t3-t2):.2f} copy-out {1e3*(t4-t3):.2f} ms "
+                  f"(stream wait {'on' if stager.stream_wait else 'off'})", file=sys.stderr)
+            print("[e2e] gpu timeline ms: " + " ".join(f"{n} {tev[0][1].elapsed_time(e):.2f}" for n, e in tev[1:]),
+                  file=sys.stderr)
         return results
 
     with torch.cuda.stream(stream):

@@ -381,6 +381,44 @@ def test_search_batch_pipeline_chunks_identical(monkeypatch):
         np.testing.assert_array_equal(got, ids)
 
 
+@pytest.mark.parametrize("stream_wait", [True, False])
+@pytest.mark.parametrize("pieces", ["1", "3", "8"])
+def test_search_batch_published_pieces_identical(monkeypatch, stream_wait, pieces):
+    """search_batch's single-batch pipeline (pieces staged by the host threads, published through a
+    page-locked flag the stream waits on, or host waits when stream_wait is off; rotation, probe and
+    query prep per piece) returns exactly the device search of the whole batch; two threads searching
+    at once get their own results."""
+    import threading
+
+    from paper_2602_23999_b200 import search as S
+
+    ix, q = _synthetic_index(20000, 64, 40, 4, seed=3)
+    q = np.concatenate([q] * 7)  # 4900 queries: up to 4 pieces of >= 1024 rows
+    sp = iv.SearchParams(k=10, n_probe=5, ip_mode="bitwise")
+    r = search_device(dev.to_device(q), ix, sp)
+    ids = dev.to_host(r.ids)
+    monkeypatch.setenv("IVRQ_STAGE_PIECES", pieces)
+    monkeypatch.setattr(S, "_WAIT_OK", None if stream_wait else False)
+    res = iv.search_batch(q, ix, sp)
+    if stream_wait:
+        assert S._WAIT_OK is True  # the driver takes the stream wait on a B200
+    np.testing.assert_array_equal(np.stack([a for a, _ in res]), ids)
+    q2 = np.ascontiguousarray(q[::-1])
+    out = {}
+
+    def worker(name, qq):
+        for _ in range(3):
+            out[name] = iv.search_batch(qq, ix, sp)
+
+    th = [threading.Thread(target=worker, args=("a", q)), threading.Thread(target=worker, args=("b", q2))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    np.testing.assert_array_equal(np.stack([a for a, _ in out["a"]]), ids)
+    np.testing.assert_array_equal(np.stack([a for a, _ in out["b"]]), ids[::-1])
+
+
 def test_kmeanspp_parallel_exact_matches_sequential_walk(monkeypatch):
     """k-means++ sampling decided by the double-double prefix + rounding band equals
     NumPy's sequential cumsum walk (searchsorted(cumsum(d2), r * total)) step for step."""

@@ -258,3 +258,26 @@ def test_fvecs_ivecs_round_trip_and_errors(tmp_path):
     empty = tmp_path / "e.fvecs"
     empty.write_bytes(b"")
     assert iv.read_fvecs(str(empty)).shape == (0, 0)
+
+
+@pytest.mark.parametrize("rows,pieces,threads", [(10000, 8, 8), (7, 3, 4), (0, 1, 2), (4900, 4, 16)])
+def test_native_staging_copies_pieces_and_raises_flags(rows, pieces, threads):
+    """ivrq_stage_rows (search_batch's host staging, no interpreter on the publish path): every row
+    copied, every piece's flag == the thread count, host waits return, join is clean."""
+    import ctypes
+
+    rng = np.random.default_rng(rows)
+    q = rng.standard_normal((rows, 96)).astype(np.float32)
+    dst = np.zeros_like(q)
+    flags = np.full(pieces, 77, dtype=np.uint32)  # zeroed by the call
+    h = ctypes.c_void_p()
+    _lib.call("ivrq_stage_rows", dst.ctypes.data, q.ctypes.data, rows, 96 * 4, pieces, threads,
+              flags.ctypes.data, ctypes.byref(h))
+    for p in range(pieces):
+        _lib.call("ivrq_stage_wait", flags.ctypes.data, p, threads)
+    _lib.call("ivrq_stage_join", h)
+    np.testing.assert_array_equal(dst, q)
+    assert (flags == threads).all()
+    with pytest.raises(ValueError):
+        _lib.call("ivrq_stage_rows", dst.ctypes.data, q.ctypes.data, rows, 0, pieces, threads,
+                  flags.ctypes.data, ctypes.byref(h))
