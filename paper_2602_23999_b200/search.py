@@ -469,9 +469,14 @@ def search_device(
         q_rot = rotate_queries_device(q, index)
     mark("rotated")
     t = index.device
-    probe_ids, probe_d2 = _probe_device(q_rot, t["centroids"], t["centroid_sqnorms"], params.n_probe, True)
+    # query prep on the side stream beside the probe (both only read q_rot); the "probed"
+    # stage mark therefore covers both, "prepared" follows it at once
+    state = _query_state_buffers(nq, q_rot.shape[1], index, params, q_rot.device)
+    with _forked() as side:
+        with torch.cuda.stream(side):
+            scalars, planes, luts, qslices = prepare_queries_device(q_rot, index, params, out=state)
+        probe_ids, probe_d2 = _probe_device(q_rot, t["centroids"], t["centroid_sqnorms"], params.n_probe, True)
     mark("probed")
-    scalars, planes, luts, qslices = prepare_queries_device(q_rot, index, params)
     mark("prepared")
     res = _scan_device(q_rot, index, params, probe_ids, probe_d2, (scalars, planes, luts, qslices), with_stats)
     mark("scanned")
@@ -606,6 +611,29 @@ def _copy_stream(device) -> torch.cuda.Stream:
     return streams[key]
 
 
+class _forked:
+    """Fork the current stream into the calling thread's side stream and join it back on exit.
+
+    Buffers used on the side stream must be allocated before the fork (they are then
+    free on the current stream's timeline, which the side stream joins first)."""
+
+    def __enter__(self) -> torch.cuda.Stream:
+        self.main = torch.cuda.current_stream()
+        dev_ = self.main.device
+        streams = getattr(_PINNED, "side_streams", None)
+        if streams is None:
+            streams = _PINNED.side_streams = {}
+        key = dev_.index or 0
+        if key not in streams:
+            streams[key] = torch.cuda.Stream(dev_)
+        self.side = streams[key]
+        self.side.wait_stream(self.main)
+        return self.side
+
+    def __exit__(self, *exc) -> None:
+        self.main.wait_stream(self.side)
+
+
 class _PieceStager:
     """Host copy of a query batch into pinned memory, in row pieces, on native threads.
 
@@ -667,10 +695,12 @@ class _Front:
             return
         q_rot = self.q_rot[x:y]
         rotate_queries_device(qd, self.index, out=q_rot)
-        _probe_device(q_rot, self.cent, self.c_sq, self.params.n_probe, True,
-                      out=(self.probe_ids[x:y], self.probe_d2[x:y]), ws=self.ws)
-        prepare_queries_device(q_rot, self.index, self.params,
-                               out=tuple(None if b is None else b[x:y] for b in self.state))
+        with _forked() as side:  # query prep beside the probe (both only read q_rot)
+            with torch.cuda.stream(side):
+                prepare_queries_device(q_rot, self.index, self.params,
+                                       out=tuple(None if b is None else b[x:y] for b in self.state))
+            _probe_device(q_rot, self.cent, self.c_sq, self.params.n_probe, True,
+                          out=(self.probe_ids[x:y], self.probe_d2[x:y]), ws=self.ws)
 
 
 def _search_pipelined(q: np.ndarray, index: IvfRabitqIndex, params: SearchParams):

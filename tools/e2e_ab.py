@@ -70,6 +70,16 @@ def main() -> None:
             torch.cuda.synchronize()
             iv.search_batch(q_host, ix, sp)
             os.environ.pop("IVRQ_E2E_TRACE")
+            if os.environ.get("E2E_CPROFILE") and pc == 4:
+                import cProfile
+                import pstats
+
+                pr = cProfile.Profile()
+                pr.enable()
+                for _ in range(5):
+                    iv.search_batch(q_host, ix, sp)
+                pr.disable()
+                pstats.Stats(pr, stream=sys.stderr).sort_stats("tottime").print_stats(18)
             print(f"threads {th:2d} pieces {pc:2d}: mean {1e3*np.mean(ts):.2f} ms  median {1e3*np.median(ts):.2f} ms "
                   f"-> {bench.NQ/np.mean(ts)/1e6:.3f}M QPS  same={same}", file=sys.stderr)
 
