@@ -88,6 +88,7 @@ struct Args {
   int64_t* fin_e;
   const int32_t* fix_only;   // scan_warp_kernel as the rerun: process only slots < *fix_only_count ...
   const int32_t* fix_only_count;  // ... of fix_only
+  int32_t* rda_next;         // scan_rda_kernel's query-slot counter (zeroed), or null: one slot per warp
 };
 
 __device__ __forceinline__ double dinf() { return __longlong_as_double(0x7ff0000000000000LL); }
@@ -1316,7 +1317,16 @@ __global__ void __launch_bounds__(RDW * 32, MINB) scan_rda_kernel(Args a) {
   using IPT = typename std::conditional<IPB == 2, int16_t, int32_t>::type;
   extern __shared__ __align__(16) unsigned char rda_smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int64_t slot_q = (int64_t)blockIdx.x * RDW + wid;
+  for (int it = 0;; ++it) {  // persistent warps: one query slot per iteration
+  int64_t slot_q;
+  if (a.rda_next) {  // the next slot from a counter (no tail of partial waves, uneven queries balance)
+    int v = 0;
+    if (lane == 0) v = atomicAdd(a.rda_next, 1);
+    slot_q = __shfl_sync(FULL, v, 0);
+  } else {
+    if (it) return;
+    slot_q = (int64_t)blockIdx.x * RDW + wid;
+  }
   if (slot_q >= a.nq) return;  // whole warps only
   const int64_t q = a.qorder ? a.qorder[slot_q] : slot_q;
   const int k = a.k, kp = a.kpad;
@@ -1503,6 +1513,7 @@ __global__ void __launch_bounds__(RDW * 32, MINB) scan_rda_kernel(Args a) {
     }
     if (unsafe) a.fix_list[atomicAdd(a.fix_count, 1)] = (int32_t)q;
   }
+  }  // query slots
 }
 
 // The end of the approximate pass, one CTA (4 warps) per query: exact values for the queue's
@@ -3243,7 +3254,10 @@ inline int launch_rd(const Args& a, bool refine, int ipb, cudaStream_t s) {
   cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   {
     KernelTimer kt("scan_rd_kernel", s);
-    kern<<<(unsigned)ceil_div(a.nq, RDW), RDW * 32, sm, s>>>(a);
+    // persistent: RDA_MINB CTAs per SM take query slots from a.rda_next
+    const int64_t blocks = a.rda_next ? std::min<int64_t>(ceil_div(a.nq, RDW), (int64_t)RDA_MINB * sm_count_of_current_device())
+                                      : ceil_div(a.nq, RDW);
+    kern<<<(unsigned)blocks, RDW * 32, sm, s>>>(a);
   }
   IVRQ_TRY(check_launch("ivrq_search_scan"));
   {
@@ -3632,7 +3646,7 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
         const int nkc = (a.kpad + scan::TCKC - 1) / scan::TCKC;
         if (!ws.alloc(rdist, (size_t)tot[0] * (fusion ? 2 : 1)) || !ws.alloc(rgpre, nl + 1) ||
             !ws.alloc(rscratch, nl + 3) ||
-            !ws.alloc(tcsl, (size_t)npairs * nkc * 512) || !ws.alloc(rrad, nq) || !ws.alloc(fix, nq + 1) ||
+            !ws.alloc(tcsl, (size_t)npairs * nkc * 512) || !ws.alloc(rrad, nq) || !ws.alloc(fix, nq + 2) ||
             !ws.alloc(lfmax, 2))
           return oom("refined-distance buffer allocation failed");
         if (index->size >= (int64_t(1) << 40) || a.nprobe >= (1 << 20))
@@ -3643,6 +3657,7 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
             qslices, porder, pslot, npairs, a.nprobe, a.kpad, nkc, tcsl);
         cudaMemsetAsync(lfmax, 0, 2 * sizeof(uint32_t), s);
         cudaMemsetAsync(fix, 0, sizeof(int32_t), s);
+        cudaMemsetAsync(fix + nq + 1, 0, sizeof(int32_t), s);
         scan::lf_max_kernel<<<(unsigned)(2 * sm_count_of_current_device()), 256, 0, s>>>(
             reinterpret_cast<const float2*>(index->long_factors), index->size, lfmax);
         scan::rd_radius_kernel<<<(unsigned)ceil_div(nq, 128), 128, 0, s>>>(
@@ -3651,6 +3666,7 @@ extern "C" int ivrq_search_scan_shard(const ivrq_index_view* index, int64_t list
         a.rrad = rrad;
         a.fix_count = fix;
         a.fix_list = fix + 1;
+        a.rda_next = fix + nq + 1;
         if (fusion) {  // the per-query pass reads (distance, stage-1 value) pairs and packed short factors
           float4* sf4 = nullptr;
           if (!ws.alloc(sf4, (size_t)index->size)) return oom("workspace allocation failed");
