@@ -405,7 +405,12 @@ __host__ __device__ inline bool rs_fast_tau(int nlist, int nprobe) {
   return nlist >= 4096 && nlist <= RS_REG * RS_THREADS && nprobe <= RS_THREADS;
 }
 
-__global__ void __launch_bounds__(RS_THREADS) probe_rescore_kernel(float* __restrict__ bnd, int64_t q0, int nlist,
+// FAST: the register-held tau path is compiled in (nlist 4096..16384, 64 bounds per thread in registers,
+// one CTA per SM by registers); otherwise the radix path alone, under a 64-register budget so that four
+// CTAs (1024 threads) share an SM: the kernel is latency-bound (long-scoreboard and barrier stalls at
+// 37% occupancy with 79 registers, C3 ncu)
+template <bool FAST>
+__global__ void __launch_bounds__(RS_THREADS, FAST ? 1 : 4) probe_rescore_kernel(float* __restrict__ bnd, int64_t q0, int nlist,
                                                                    int nprobe, int order_by_id,
                                                                    const double* __restrict__ q_rot,
                                                                    const float* __restrict__ cent, int d,
@@ -443,7 +448,7 @@ __global__ void __launch_bounds__(RS_THREADS) probe_rescore_kernel(float* __rest
     s_have = 0;
   }
   __syncthreads();
-  const bool fast_tau = rs_fast_tau(nlist, nprobe);
+  const bool fast_tau = FAST && rs_fast_tau(nlist, nprobe);
   if (fast_tau) {
     float u[RS_REG];
     float m = __int_as_float(0x7f800000);  // +inf
@@ -635,9 +640,12 @@ int probe_tc(const double* q_rot, int64_t nq, int32_t dims, const float* centroi
   const size_t sm = tp_smem_bytes();
   auto tk = tc_probe_kernel<ndig>;
   if (cudaFuncSetAttribute(tk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess ||
-      cudaFuncSetAttribute(probe_rescore_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ROW * 4) !=
+      cudaFuncSetAttribute(probe_rescore_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ROW * 4) !=
+          cudaSuccess ||
+      cudaFuncSetAttribute(probe_rescore_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ROW * 4) !=
           cudaSuccess)
     return fail(IVRQ_EUNSUP, "ivrq_select_clusters: tensor-core probe shared memory");
+  cudaFuncSetAttribute(probe_rescore_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   for (int64_t r0 = 0; r0 < nq; r0 += rows) {
     const int64_t rn = std::min(rows, nq - r0);
     ta.q0 = r0;
@@ -648,7 +656,8 @@ int probe_tc(const double* q_rot, int64_t nq, int32_t dims, const float* centroi
     IVRQ_TRY(check_launch("ivrq_select_clusters(tc bounds)"));
     const size_t rsm =
         n_clusters <= SMEM_ROW && !rs_fast_tau(n_clusters, n_probe) ? (size_t)n_clusters * sizeof(float) : 0;
-    probe_rescore_kernel<<<(unsigned)rn, RS_THREADS, rsm, s>>>(bounds, r0, n_clusters, n_probe, order_by_id, q_rot,
+    auto rk = rs_fast_tau(n_clusters, n_probe) ? probe_rescore_kernel<true> : probe_rescore_kernel<false>;
+    rk<<<(unsigned)rn, RS_THREADS, rsm, s>>>(bounds, r0, n_clusters, n_probe, order_by_id, q_rot,
                                                                centroids, dims, q_sq, centroid_sqnorms, ids, d2, nullptr);
     IVRQ_TRY(check_launch("ivrq_select_clusters(rescore)"));
   }
