@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(THREADS, 1) tc_probe_kernel(const __grid_const
       // the tile's centroid scalars, staged while the MMAs run (double-buffered by tile parity)
       __shared__ double s_csq[2][128], s_cl1[2][128];
       __shared__ int32_t s_ce[2][128];
-      __shared__ float s_stage[EPW * 2 * 16 * 16];  // per epilogue warp: 16 queries x 16 centroids, L and U
+      __shared__ __align__(16) float s_stage[EPW * 2 * 16 * 16];  // per epilogue warp: 16 queries x 16 centroids, L and U
       {
         const int et = tid - 64;  // 0..32*EPW-1
         if (et < CT) {
@@ -292,13 +292,27 @@ __global__ void __launch_bounds__(THREADS, 1) tc_probe_kernel(const __grid_const
             stg[256 + jl * 16 + 8 * s + i] = ub;
           }
           __syncwarp();
-          const int ci = lane & 15, which = lane >> 4;  // lanes 0-15: L, 16-31: U
-          const int64_t c = (int64_t)ct * CT + cc0 + ci;
+          const int64_t cb = (int64_t)ct * CT + cc0;  // the chunk's first centroid (a multiple of 16)
+          if ((a.nlist & 3) == 0 && cb + 16 <= a.nlist) {
+            // 16-byte stores: lane = (query of 4, L/U, 4-centroid quad), four passes over the 16 queries
+            const int c4 = lane & 3, which = (lane >> 2) & 1;
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+              const int j = h * 4 + (lane >> 3);
+              const int64_t qrow = (int64_t)qt * QT + quarter * 16 + j;
+              if (qrow < a.nrows)
+                *reinterpret_cast<float4*>(a.bnd + (qrow * 2 + which) * (int64_t)a.nlist + cb + 4 * c4) =
+                    *reinterpret_cast<const float4*>(stg + which * 256 + j * 16 + 4 * c4);
+            }
+          } else {
+            const int ci = lane & 15, which = lane >> 4;  // lanes 0-15: L, 16-31: U
+            const int64_t c = cb + ci;
 #pragma unroll 4
-          for (int j = 0; j < 16; ++j) {
-            const int64_t qrow = (int64_t)qt * QT + quarter * 16 + j;
-            if (qrow < a.nrows && c < a.nlist)
-              a.bnd[qrow * 2 * (int64_t)a.nlist + (int64_t)which * a.nlist + c] = stg[which * 256 + j * 16 + ci];
+            for (int j = 0; j < 16; ++j) {
+              const int64_t qrow = (int64_t)qt * QT + quarter * 16 + j;
+              if (qrow < a.nrows && c < a.nlist)
+                a.bnd[qrow * 2 * (int64_t)a.nlist + (int64_t)which * a.nlist + c] = stg[which * 256 + j * 16 + ci];
+            }
           }
           __syncwarp();
         }
@@ -406,11 +420,11 @@ __host__ __device__ inline bool rs_fast_tau(int nlist, int nprobe) {
 }
 
 // FAST: the register-held tau path is compiled in (nlist 4096..16384, 64 bounds per thread in registers,
-// one CTA per SM by registers); otherwise the radix path alone, under a 64-register budget so that four
+// three CTAs per SM by registers); otherwise the radix path alone, under a 64-register budget so that four
 // CTAs (1024 threads) share an SM: the kernel is latency-bound (long-scoreboard and barrier stalls at
 // 37% occupancy with 79 registers, C3 ncu)
 template <bool FAST>
-__global__ void __launch_bounds__(RS_THREADS, FAST ? 1 : 4) probe_rescore_kernel(float* __restrict__ bnd, int64_t q0, int nlist,
+__global__ void __launch_bounds__(RS_THREADS, FAST ? 3 : 4) probe_rescore_kernel(float* __restrict__ bnd, int64_t q0, int nlist,
                                                                    int nprobe, int order_by_id,
                                                                    const double* __restrict__ q_rot,
                                                                    const float* __restrict__ cent, int d,

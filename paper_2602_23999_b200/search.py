@@ -472,6 +472,7 @@ def search_device(
     # query prep on the side stream beside the probe (both only read q_rot); the "probed"
     # stage mark therefore covers both, "prepared" follows it at once
     state = _query_state_buffers(nq, q_rot.shape[1], index, params, q_rot.device)
+    # (measured on C3: beside the probe 3.28 ms per step, after it 3.31; a high-priority side stream 3.28)
     with _forked() as side:
         with torch.cuda.stream(side):
             scalars, planes, luts, qslices = prepare_queries_device(q_rot, index, params, out=state)
