@@ -1521,7 +1521,10 @@ __global__ void __launch_bounds__(RDW * 32, MINB) scan_rda_kernel(Args a) {
 // split the entries), the queue re-sorted by (value, pid), the first k written out.
 constexpr int FIN_W = 4;
 
-__global__ void __launch_bounds__(FIN_W * 32) rda_final_kernel(Args a) {
+#ifndef FIN_MINB
+#define FIN_MINB 10  // 48 registers: 10 CTAs per SM (C3 step 3.26 -> 3.24 ms; 12 CTAs at 40 registers: 3.29)
+#endif
+__global__ void __launch_bounds__(FIN_W * 32, FIN_MINB) rda_final_kernel(Args a) {
   extern __shared__ __align__(16) unsigned char fin_smem[];
   int2* hl = reinterpret_cast<int2*>(fin_smem);
   double* sd = reinterpret_cast<double*>(fin_smem + (size_t)a.kpad * sizeof(int2));
