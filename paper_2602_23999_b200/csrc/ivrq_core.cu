@@ -10,6 +10,7 @@
 #endif
 #include <cstring>
 #include <deque>
+#include <pthread.h>
 #include <mutex>
 #include <thread>
 #include <string>
@@ -306,9 +307,15 @@ struct StagePool {
     }
   }
 };
+StagePool* g_stage_pool = nullptr;
+void stage_pool_after_fork() { g_stage_pool = new StagePool(); }  // the child has none of the workers
 StagePool& stage_pool() {
-  static StagePool* pool = new StagePool();  // never destroyed: the detached workers outlive main()
-  return *pool;
+  static std::once_flag once;
+  std::call_once(once, []() {
+    g_stage_pool = new StagePool();  // never destroyed: the detached workers outlive main()
+    pthread_atfork(nullptr, nullptr, stage_pool_after_fork);
+  });
+  return *g_stage_pool;
 }
 }  // namespace
 

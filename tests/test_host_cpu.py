@@ -281,3 +281,41 @@ def test_native_staging_copies_pieces_and_raises_flags(rows, pieces, threads):
     with pytest.raises(ValueError):
         _lib.call("ivrq_stage_rows", dst.ctypes.data, q.ctypes.data, rows, 0, pieces, threads,
                   flags.ctypes.data, ctypes.byref(h))
+
+
+def test_native_staging_after_fork():
+    """The staging pool is rebuilt in a forked child (its workers are not inherited): a copy there
+    completes instead of waiting on threads that do not exist."""
+    import ctypes
+    import os
+
+    q = np.arange(4096 * 8, dtype=np.float32).reshape(4096, 8)
+    dst = np.zeros_like(q)
+    flags = np.zeros(2, dtype=np.uint32)
+    h = ctypes.c_void_p()
+    _lib.call("ivrq_stage_rows", dst.ctypes.data, q.ctypes.data, 4096, 32, 2, 4, flags.ctypes.data, ctypes.byref(h))
+    _lib.call("ivrq_stage_join", h)  # the parent's pool has started its workers
+    pid = os.fork()
+    if pid == 0:  # child: copy again through the library, exit 0 on success
+        code = 1
+        try:
+            d2 = np.zeros_like(q)
+            h2 = ctypes.c_void_p()
+            _lib.call("ivrq_stage_rows", d2.ctypes.data, q.ctypes.data, 4096, 32, 2, 4, flags.ctypes.data,
+                      ctypes.byref(h2))
+            _lib.call("ivrq_stage_join", h2)
+            code = 0 if np.array_equal(d2, q) else 2
+        finally:
+            os._exit(code)
+    import time
+
+    deadline = time.time() + 60
+    while time.time() < deadline:
+        done, status = os.waitpid(pid, os.WNOHANG)
+        if done:
+            assert os.waitstatus_to_exitcode(status) == 0
+            return
+        time.sleep(0.05)
+    os.kill(pid, 9)
+    os.waitpid(pid, 0)
+    raise AssertionError("staging in the forked child did not complete")
