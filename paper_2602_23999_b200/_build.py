@@ -68,6 +68,12 @@ def build(force: bool = False, verbose: bool = False, extra_flags: list[str] | N
     flags = ARCH_FLAGS + NVCC_FLAGS + list(extra_flags or [])
     srcs = _sources()
     hdr_m = max((p.stat().st_mtime for p in _headers()), default=0.0)
+    # cached objects are reused only when they were compiled with these exact flags (a variant
+    # build with -D switches must never leave its objects behind for the next default build)
+    stamp = BUILD_DIR / "flags.txt"
+    if not stamp.exists() or stamp.read_text() != " ".join(flags):
+        force = True
+        stamp.unlink(missing_ok=True)  # rewritten once every object has been compiled with these flags
 
     def compile_one(src: Path) -> Path:
         obj = BUILD_DIR / (src.stem + ".o")
@@ -90,6 +96,7 @@ def build(force: bool = False, verbose: bool = False, extra_flags: list[str] | N
     workers = max(1, min(len(srcs), os.cpu_count() or 1))
     with concurrent.futures.ThreadPoolExecutor(max_workers=workers) as ex:
         objs = list(ex.map(compile_one, srcs))
+    stamp.write_text(" ".join(flags))
     tmp = LIB_PATH.with_suffix(".so.tmp")
     cmd = [nvcc, *ARCH_FLAGS, "-shared", "-cudart", "static", "-o", str(tmp), *map(str, objs)]
     res = subprocess.run(cmd, capture_output=True, text=True)

@@ -214,7 +214,12 @@ __global__ void __launch_bounds__(THREADS, 1) tc_probe_kernel(const __grid_const
         const int sc = qe + s_ce[ab][cl] - 2 * (7 * NDIG - 1);  // s_q s_c
         const double csq = s_csq[ab][cl];
         const double p2 = pow2(sc);
-        const double dot = dadd(dmul(dot_scaled_hi, pow2(sc + shift_hi)), dmul(dot_scaled_lo, p2));
+        double dot;
+        if constexpr (NDIG == 2) {  // the whole sum is the low part (hi == 0): the same value, fewer ops
+          dot = dmul(dot_scaled_lo, p2);
+        } else {
+          dot = dadd(dmul(dot_scaled_hi, pow2(sc + shift_hi)), dmul(dot_scaled_lo, p2));
+        }
         const double dist = dsub(dadd(qsq, csq), dmul(2.0, dot));
         const double rep = dmul(ql1 + s_cl1[ab][cl] + 0.5 * a.d, p2);  // 2 (s_q s_c / 2)(|Q|_1+|C|_1+K/2)
         const double slack = (qsq + csq + 2.0 * fabs(dot)) * 0x1p-40;
