@@ -818,14 +818,21 @@ def main() -> None:
                     help="list-sharded build + search of one shared batch (strong scaling) instead of replicas")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    # stdout carries exactly the one JSON line: everything else written to fd 1 while the bench runs
+    # (NCCL's version banner, library chatter) goes to stderr
+    sys.stdout.flush()
+    json_fd = os.dup(1)
+    os.dup2(2, 1)
     if args.impl == "reference":
         out = run_reference(args, args.config)
     elif args.sharded:
         out = run_sharded(args, args.config)
     else:
         out = run_ours(args, args.config)
+    sys.stdout.flush()
     if out:
-        print(json.dumps(out), flush=True)
+        os.write(json_fd, (json.dumps(out) + "\n").encode())
+    os.close(json_fd)
 
 
 if __name__ == "__main__":
