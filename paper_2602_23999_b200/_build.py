@@ -51,9 +51,12 @@ def _headers() -> list[Path]:
     return sorted(CSRC.glob("*.cuh")) + sorted(INCLUDE.glob("*.h"))
 
 
-def needs_build() -> bool:
+def needs_build(extra_flags: list[str] | None = None) -> bool:
     if not LIB_PATH.exists():
         return True
+    stamp = BUILD_DIR / "flags.txt"
+    if stamp.exists() and stamp.read_text() != " ".join(ARCH_FLAGS + NVCC_FLAGS + list(extra_flags or [])):
+        return True  # the library was last linked from objects built with other flags
     lib_m = LIB_PATH.stat().st_mtime
     deps = _sources() + _headers() + [Path(__file__)]
     return any(p.stat().st_mtime > lib_m for p in deps)
@@ -61,7 +64,7 @@ def needs_build() -> bool:
 
 def build(force: bool = False, verbose: bool = False, extra_flags: list[str] | None = None) -> Path:
     """Compile every ``csrc/*.cu`` for sm_100a and link ``libivrq_b200.so``."""
-    if not force and not needs_build():
+    if not force and not needs_build(extra_flags):
         return LIB_PATH
     nvcc = _nvcc()
     BUILD_DIR.mkdir(exist_ok=True)

@@ -117,12 +117,14 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* mbar) {
 
 __device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t parity) {
   const uint32_t a = (uint32_t)__cvta_generic_to_shared(mbar);
+  // with a suspend-time hint: a waiting thread sleeps in the barrier instead of re-polling
+  // (C3 tc_refine 1.021 -> 1.006 ms: its spinning producer / MMA / epilogue warps issue less)
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
       "@!P1 bra WAIT_%=;\n\t}" ::"r"(a),
-      "r"(parity)
+      "r"(parity), "r"(0x989680u)
       : "memory");
 }
 
