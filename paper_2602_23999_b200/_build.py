@@ -51,12 +51,29 @@ def _headers() -> list[Path]:
     return sorted(CSRC.glob("*.cuh")) + sorted(INCLUDE.glob("*.h"))
 
 
+BUILDINFO = LIB_PATH.with_name(LIB_PATH.name + ".buildinfo")  # travels with the library
+
+
+def _source_digest(extra_flags: list[str] | None = None) -> str:
+    """sha256 of the nvcc flags and every source, header and this script: what the library is built from."""
+    import hashlib
+
+    h = hashlib.sha256(" ".join(ARCH_FLAGS + NVCC_FLAGS + list(extra_flags or [])).encode())
+    for p in _sources() + _headers() + [Path(__file__)]:
+        h.update(p.name.encode())
+        h.update(p.read_bytes())
+    return h.hexdigest()
+
+
 def needs_build(extra_flags: list[str] | None = None) -> bool:
+    """Whether libivrq_b200.so is missing or was built from other sources / flags.
+
+    Decided by content (the digest recorded beside the library), not by file times: a
+    snapshot of the repo copied to another machine may not keep the files' mtimes."""
     if not LIB_PATH.exists():
         return True
-    stamp = BUILD_DIR / "flags.txt"
-    if stamp.exists() and stamp.read_text() != " ".join(ARCH_FLAGS + NVCC_FLAGS + list(extra_flags or [])):
-        return True  # the library was last linked from objects built with other flags
+    if BUILDINFO.exists():
+        return BUILDINFO.read_text().strip() != _source_digest(extra_flags)
     lib_m = LIB_PATH.stat().st_mtime
     deps = _sources() + _headers() + [Path(__file__)]
     return any(p.stat().st_mtime > lib_m for p in deps)
@@ -106,6 +123,7 @@ def build(force: bool = False, verbose: bool = False, extra_flags: list[str] | N
     if res.returncode != 0:
         raise RuntimeError(f"nvcc link failed:\n{res.stderr}")
     os.replace(tmp, LIB_PATH)
+    BUILDINFO.write_text(_source_digest(extra_flags) + "\n")
     return LIB_PATH
 
 
