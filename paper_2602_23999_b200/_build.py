@@ -58,7 +58,8 @@ def _source_digest(extra_flags: list[str] | None = None) -> str:
     """sha256 of the nvcc flags and every source, header and this script: what the library is built from."""
     import hashlib
 
-    h = hashlib.sha256(" ".join(ARCH_FLAGS + NVCC_FLAGS + list(extra_flags or [])).encode())
+    flags = [f.replace(str(INCLUDE), "<include>") for f in ARCH_FLAGS + NVCC_FLAGS + list(extra_flags or [])]
+    h = hashlib.sha256(" ".join(flags).encode())  # location independent: the repo root differs per machine
     for p in _sources() + _headers() + [Path(__file__)]:
         h.update(p.name.encode())
         h.update(p.read_bytes())
